@@ -1,0 +1,195 @@
+/*
+ * fp8flow.h -- C ABI of libfp8flow: the data-parallel hot path of FP8-Flow-MoE
+ * ("FP8-Flow-MoE: A Casting-Free FP8 Recipe without Double Quantization Error", arXiv 2511.02302)
+ * as hand-written CUDA kernels for NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = line n of the paper's LaTeX source.  Readings of ambiguous passages are the
+ * numbered readings R1..R28 of DESIGN.md §3.
+ *
+ * ------------------------------------------------------------------------------------------
+ * Numeric contract (every entry point)
+ *   E4M3 code   1 sign | 4 exponent (bias 7) | 3 mantissa bits, MSB first; max 448;
+ *               Eq. 10.  Rounding: round-to-nearest, ties to even (R8);
+ *               finite overflow saturates to +-448 (R9); the sign of zero is kept (R10).
+ *   UE8M0 scale one byte b per 1x128 tile, value 2^(b-127).  b = T + 127 where
+ *               T is the least integer with max|x| <= 448 * 2^T over the tile (Eq. 2, read
+ *               with a power-of-two scale rounded up, R3), clamped to [-127, 127] (R13); an
+ *               all-zero tile gets b = 0 (R11).
+ *   Row-wise FP8 tensor: codes q[rows][cols] row-major (cols % 128 == 0) and scales
+ *               s[cols/128][ld_s] "MN-major": one contiguous run of ld_s >= rows bytes per
+ *               128-wide column tile; s[j][i] is the scale of row i, columns 128j..128j+127.
+ *   Segments    an expert's rows [o_e, o_e + m_e) of a permuted buffer; device int32 offsets
+ *               seg_offsets[0..num_segs], non-decreasing, every m_e % 16 == 0 and every
+ *               o_e % 16 == 0.
+ *
+ * Memory and execution
+ *   All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA storage) unless stated.
+ *   The caller owns every buffer, including workspaces (size queries provided).  The library
+ *   never allocates, frees, synchronises or keeps state between calls; it is reentrant.
+ *   `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is asynchronous on
+ *   that stream; data-dependent sizes (padded rows, segment sizes) stay on the device, so every
+ *   call is CUDA-graph capturable.
+ *
+ * Errors
+ *   Arguments are validated synchronously; on error a status is returned and nothing is
+ *   launched.  A failed launch returns FP8FLOW_ERR_CUDA and fp8flow_last_cuda_error() gives the
+ *   cudaError_t.  Device faults surface at the caller's next synchronisation.  Non-finite
+ *   inputs are a precondition violation (not checked on device).  There is no CPU fallback: on
+ *   a device that is not sm_100 every compute entry point returns FP8FLOW_ERR_ARCH.
+ * ------------------------------------------------------------------------------------------
+ */
+#ifndef FP8FLOW_H_
+#define FP8FLOW_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FP8FLOW_API __attribute__((visibility("default")))
+#else
+#define FP8FLOW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FP8FLOW_OK = 0,
+  FP8FLOW_ERR_NULL = 1,      /* a required pointer is NULL                                        */
+  FP8FLOW_ERR_SHAPE = 2,     /* negative size, cols % 128 != 0, rows % 16 != 0 where required     */
+  FP8FLOW_ERR_ALIGN = 3,     /* a pointer or leading dimension is not 16-byte aligned              */
+  FP8FLOW_ERR_ARG = 4,       /* top_k / expert range / align / num_segs out of range               */
+  FP8FLOW_ERR_WORKSPACE = 5, /* workspace too small                                                */
+  FP8FLOW_ERR_ARCH = 6,      /* current device is not sm_100 (B200); no fallback exists            */
+  FP8FLOW_ERR_CUDA = 7       /* a CUDA runtime call or launch failed; see fp8flow_last_cuda_error() */
+} fp8flow_status_t;
+
+/* Human-readable name of a status code (static storage). */
+FP8FLOW_API const char* fp8flow_status_string(int status);
+/* cudaError_t of the last FP8FLOW_ERR_CUDA returned on the calling thread (0 if none). */
+FP8FLOW_API int fp8flow_last_cuda_error(void);
+/* Library version (major*10000 + minor*100 + patch) and the compiled target ("sm_100a"). */
+FP8FLOW_API int fp8flow_version(void);
+FP8FLOW_API const char* fp8flow_build_target(void);
+/* FP8FLOW_OK if the current CUDA device is sm_100, else FP8FLOW_ERR_ARCH / FP8FLOW_ERR_CUDA. */
+FP8FLOW_API int fp8flow_device_check(void);
+
+/* ==========================================================================================
+ * A1  Entry quantization, BF16 -> E4M3 with 1x128 power-of-two scales.
+ *     Eq. 2, Eq. 3, s = 2^T; the single forward cast at the entry
+ *     point and its backward twin on dY ("from 12 to 2" P:28; R27).
+ *   x_bf16  [rows][cols] BF16, row-major, 16-byte aligned             (read)
+ *   q       [rows][cols] E4M3 codes, 16-byte aligned                  (written)
+ *   s       [cols/128][ld_s] UE8M0 scale bytes, MN-major; ld_s >= rows, ld_s % 16 == 0 (written
+ *           for rows [0, rows) of every tile column; bytes rows..ld_s-1 untouched)
+ *   rows >= 0 (0 = no-op), cols > 0 and cols % 128 == 0.
+ *   Result: q[i][j] = E4M3_RNE(x[i][j] * 2^-T[i][j/128]) (the product is exact; |.| <= 448).
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_quantize_rowwise(const void* x_bf16, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s, int64_t ld_s,
+                             void* stream);
+
+/* ==========================================================================================
+ * A2  Scaling-aware FP8 transpose (Algorithm 1; derivation P:173-200).
+ *     Row-wise FP8 -> column-wise FP8 for the wgrad GEMM without dequantization:
+ *     for each segment e and each block (ib, jb) of rows o_e+128ib.. (the last block of a
+ *     segment may be partial, R14; blocks never straddle segments, R15) x columns 128jb..+127:
+ *        T_max = max over the block's rows of T[i][jb]                 (R6)
+ *        sT_e[ib][j] = T_max for all 128 columns j of the block
+ *        qT_e[j][i - o_e] = E4M3_RNE(decode(q[i][j]) * 2^-(T_max - T[i][jb]))   (R5, R7)
+ *     i.e. the exponent field is lowered by k = T_max - T_row; codes that leave the normal range
+ *     are re-rounded into the subnormal grid (the only loss, "provided that no overflow or
+ *     underflow occurs").
+ *   q, s, ld_s   row-wise input [rows][cols] + MN-major scales (ld_s % 16 == 0, ld_s >= rows)
+ *   rows % 16 == 0, cols % 128 == 0
+ *   seg_offsets  device int32 [num_segs + 1], or NULL = one segment [0, rows); 1 <= num_segs <= 1024
+ *   qT           output codes; segment e occupies bytes [cols*o_e, cols*(o_e + m_e)) as a
+ *                row-major [cols][m_e] matrix (physically transposed, R23).  16-byte aligned.
+ *   sT           output scales; segment e occupies rows [P_e, P_e + ceil(m_e/128)) of a
+ *                [*][cols] byte matrix, P_e = sum_{e'<e} ceil(m_e'/128).  Capacity needed:
+ *                cols * (rows/128 + num_segs) bytes.  16-byte aligned.
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                                    const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
+                                    void* stream);
+
+/* Naive comparator: dequantize to BF16 -> transpose -> column-wise requantize with
+ * fresh pow2 scales per (column, 128-row block of a segment).  Same arguments and output layout as
+ * A2 plus a device workspace of fp8flow_naive_workspace_bytes() bytes.  Benchmark comparator
+ * only: it exhibits the second rounding the paper calls double quantization error (Eq. 9). */
+FP8FLOW_API size_t fp8flow_naive_workspace_bytes(int64_t rows, int64_t cols, int32_t num_segs);
+FP8FLOW_API int fp8flow_naive_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                            const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* ==========================================================================================
+ * A3  Fused permute + padding: plan, then move.
+ *
+ * fp8flow_permute_plan -- routing plan for the local experts [expert_begin, expert_begin + E_loc):
+ *   topk_idx        device int32 [num_tokens][top_k] global expert ids, distinct per token
+ *   align           padding multiple, 16 in the paper; any value in [1, 1024]
+ *   row_map         device int32 [num_tokens][top_k] (written): output row of pair (t, k), or -1
+ *                   when topk_idx[t][k] is not a local expert
+ *   src_of_row      device int32 [max_rows] (written for rows < expert_offsets[E_loc]): source
+ *                   token of each output row, -1 for PAD rows
+ *   expert_offsets  device int32 [E_loc + 1] (written): expert e's rows are
+ *                   [offsets[e], offsets[e+1]), count_e real rows in ascending token order then
+ *                   ceil(count_e/align)*align - count_e PAD rows (R16)
+ *   max_rows        capacity; num_tokens*top_k + E_loc*(align-1) always suffices.  If the padded
+ *                   total exceeds it, rows beyond are dropped (row_map = -1) and the workspace's
+ *                   first int32 is set to 1 (else 0) -- readable by the caller after sync.
+ *   ws              device workspace of fp8flow_permute_workspace_bytes() bytes
+ *   1 <= top_k <= 16, 1 <= E_loc <= 1024, num_tokens >= 0.  Deterministic: the plan depends only
+ *   on topk_idx (no atomics decide an order).
+ * ========================================================================================== */
+FP8FLOW_API size_t fp8flow_permute_workspace_bytes(int64_t num_tokens, int32_t top_k, int32_t num_local_experts);
+FP8FLOW_API int fp8flow_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int32_t top_k, int32_t expert_begin,
+                         int32_t num_local_experts, int32_t align, int32_t* row_map, int32_t* src_of_row,
+                         int64_t max_rows, int32_t* expert_offsets, void* ws, size_t ws_bytes, void* stream);
+
+/* fp8flow_permute_pad -- move row-wise FP8 tokens into the padded expert-major buffer in one pass:
+ *   q_out[r] = q_tok[src_of_row[r]], s_out[j][r] = s_tok[j][src_of_row[r]] for r < R =
+ *   expert_offsets[E_loc]; PAD rows get code 0x00 and scale byte 0x00 (R17, R11).
+ *   q_tok [num_tokens][hidden] + s_tok [hidden/128][ld_s_tok]  (row-wise FP8, as from A1)
+ *   q_out [max_rows][hidden], s_out [hidden/128][max_rows]       (rows >= R untouched)
+ *   hidden % 128 == 0; q_tok, q_out 16-byte aligned; max_rows % 16 == 0. */
+FP8FLOW_API int fp8flow_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t num_tokens,
+                        int64_t hidden, const int32_t* src_of_row, const int32_t* expert_offsets,
+                        int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out, void* stream);
+
+/* ==========================================================================================
+ * A4  Fused unpermute + unpadding, BF16 at the second boundary (R22):
+ *     y[t][h] = BF16_RNE( sum over k = 0..top_k-1 with row_map[t][k] >= 0 of
+ *                         probs[t][k] * x[row_map[t][k]][h] )
+ *     accumulated in fp32 as acc = fmaf(p, x, acc) from +0 in k order (acc + x when probs is
+ *     NULL); PAD rows are never read; tokens without a local expert get +0 (R21).
+ *   x_bf16 [*][hidden] BF16 expert-major rows; row_map [num_tokens][top_k]; probs fp32
+ *   [num_tokens][top_k] or NULL; y_bf16 [num_tokens][hidden].  hidden % 8 == 0, 16-byte aligned
+ *   x and y, 1 <= top_k <= 16.
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_unpermute_unpad(const void* x_bf16, int64_t hidden, const int32_t* row_map, const float* probs,
+                            int64_t num_tokens, int32_t top_k, void* y_bf16, void* stream);
+
+/* ==========================================================================================
+ * A5  Fused SwiGLU + quantization: from the BF16 fc1 output (R19)
+ *     y = silu(a) * b = a*b / (1 + e^-a), a = h[:, :ffn] (gate), b = h[:, ffn:] (R18), then A1's
+ *     1x128 quantization along ffn.  Reference value: fp64 evaluation rounded once to fp32 (R20);
+ *     acceptance: codes within 1 E4M3 ULP on <= 1e-4 of elements, scale bytes identical.
+ *   h_bf16  [rows_max][2*ffn] BF16, 16-byte aligned
+ *   rows_dev device int32 holding the actual row count (e.g. &expert_offsets[E_loc]), or NULL
+ *           for rows_max rows; must be <= rows_max
+ *   q       [rows_max][ffn] E4M3 codes; s [ffn/128][ld_s] MN-major, ld_s >= rows_max, % 16 == 0
+ *   ffn % 128 == 0.
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_swiglu_quant(const void* h_bf16, int64_t rows_max, const int32_t* rows_dev, int64_t ffn, uint8_t* q,
+                         uint8_t* s, int64_t ld_s, void* stream);
+
+/* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
+ * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */
+FP8FLOW_API int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FP8FLOW_H_ */

@@ -1,0 +1,207 @@
+// api.cu -- the extern "C" boundary of libfp8flow (include/fp8flow.h): argument validation,
+// architecture check, status codes, and dispatch to the sm_100a kernels.  No compute happens on
+// the host and there is no fallback path.
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/fp8flow.h"
+#include "kernels.h"
+
+using namespace fp8flow;
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+constexpr int kMaxDevices = 64;
+int g_dev_ok[kMaxDevices];   // 0 = unknown, 1 = sm_100, 2 = other
+int g_dev_sms[kMaxDevices];
+
+int fail_cuda(cudaError_t e) {
+  g_last_cuda_error = static_cast<int>(e);
+  return FP8FLOW_ERR_CUDA;
+}
+
+// resolves the current device; returns OK / ERR_ARCH / ERR_CUDA and the SM count
+int device(int* num_sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail_cuda(e);
+  if (dev < 0 || dev >= kMaxDevices) return FP8FLOW_ERR_ARCH;
+  if (g_dev_ok[dev] == 0) {
+    int major = 0, minor = 0, sms = 0;
+    if ((e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+      return fail_cuda(e);
+    g_dev_sms[dev] = sms;
+    g_dev_ok[dev] = (major == 10 && minor == 0) ? 1 : 2;
+  }
+  if (g_dev_ok[dev] != 1) return FP8FLOW_ERR_ARCH;
+  *num_sms = g_dev_sms[dev];
+  return FP8FLOW_OK;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int launched(cudaError_t e) { return e == cudaSuccess ? FP8FLOW_OK : fail_cuda(e); }
+
+}  // namespace
+
+extern "C" {
+
+const char* fp8flow_status_string(int status) {
+  switch (status) {
+    case FP8FLOW_OK: return "FP8FLOW_OK";
+    case FP8FLOW_ERR_NULL: return "FP8FLOW_ERR_NULL";
+    case FP8FLOW_ERR_SHAPE: return "FP8FLOW_ERR_SHAPE";
+    case FP8FLOW_ERR_ALIGN: return "FP8FLOW_ERR_ALIGN";
+    case FP8FLOW_ERR_ARG: return "FP8FLOW_ERR_ARG";
+    case FP8FLOW_ERR_WORKSPACE: return "FP8FLOW_ERR_WORKSPACE";
+    case FP8FLOW_ERR_ARCH: return "FP8FLOW_ERR_ARCH";
+    case FP8FLOW_ERR_CUDA: return "FP8FLOW_ERR_CUDA";
+    default: return "FP8FLOW_UNKNOWN_STATUS";
+  }
+}
+
+int fp8flow_last_cuda_error(void) { return g_last_cuda_error; }
+int fp8flow_version(void) { return 100; }  // 0.1.0
+const char* fp8flow_build_target(void) { return "sm_100a"; }
+
+int fp8flow_device_check(void) {
+  int sms = 0;
+  return device(&sms);
+}
+
+int fp8flow_quantize_rowwise(const void* x_bf16, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s, int64_t ld_s,
+                             void* stream) {
+  if (rows < 0 || cols <= 0 || cols % 128 != 0) return FP8FLOW_ERR_SHAPE;
+  if (ld_s < rows || ld_s % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (rows == 0) return FP8FLOW_OK;
+  if (!x_bf16 || !q || !s) return FP8FLOW_ERR_NULL;
+  if (!aligned16(x_bf16) || !aligned16(q)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_quantize_rowwise(x_bf16, rows, cols, q, s, ld_s, static_cast<cudaStream_t>(stream), sms));
+}
+
+static int check_transpose_args(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                                const int32_t* seg_offsets, int32_t num_segs, const uint8_t* qT, const uint8_t* sT) {
+  if (rows < 0 || cols <= 0 || cols % 128 != 0 || rows % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (rows > INT32_MAX - 128) return FP8FLOW_ERR_SHAPE;
+  if (ld_s < rows || ld_s % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (seg_offsets && (num_segs < 1 || num_segs > 1024)) return FP8FLOW_ERR_ARG;
+  if (!q || !s || !qT || !sT) return FP8FLOW_ERR_NULL;
+  if (!aligned16(q) || !aligned16(s) || !aligned16(qT) || !aligned16(sT)) return FP8FLOW_ERR_ALIGN;
+  return FP8FLOW_OK;
+}
+
+int fp8flow_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                                    const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
+                                    void* stream) {
+  if (rows == 0 && !seg_offsets) return FP8FLOW_OK;
+  int st = check_transpose_args(q, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
+  if (st != FP8FLOW_OK) return st;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_scaling_aware_transpose(q, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT,
+                                                 static_cast<cudaStream_t>(stream), sms));
+}
+
+size_t fp8flow_naive_workspace_bytes(int64_t rows, int64_t cols, int32_t num_segs) {
+  if (rows < 0 || cols < 0 || num_segs < 0) return 0;
+  return naive_workspace_bytes(rows, cols, num_segs < 1 ? 1 : num_segs);
+}
+
+int fp8flow_naive_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                            const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (rows == 0 && !seg_offsets) return FP8FLOW_OK;
+  int st = check_transpose_args(q, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
+  if (st != FP8FLOW_OK) return st;
+  if (!ws) return FP8FLOW_ERR_NULL;
+  if (!aligned16(ws)) return FP8FLOW_ERR_ALIGN;
+  if (ws_bytes < naive_workspace_bytes(rows, cols, seg_offsets ? num_segs : 1)) return FP8FLOW_ERR_WORKSPACE;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_naive_transpose(q, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, ws,
+                                         static_cast<cudaStream_t>(stream), sms));
+}
+
+size_t fp8flow_permute_workspace_bytes(int64_t num_tokens, int32_t top_k, int32_t num_local_experts) {
+  (void)top_k;
+  if (num_tokens < 0 || num_local_experts < 1) return 0;
+  return permute_workspace_bytes(num_tokens, num_local_experts);
+}
+
+int fp8flow_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int32_t top_k, int32_t expert_begin,
+                         int32_t num_local_experts, int32_t align, int32_t* row_map, int32_t* src_of_row,
+                         int64_t max_rows, int32_t* expert_offsets, void* ws, size_t ws_bytes, void* stream) {
+  if (num_tokens < 0 || max_rows < 0) return FP8FLOW_ERR_SHAPE;
+  if (top_k < 1 || top_k > 16 || num_local_experts < 1 || num_local_experts > 1024 || align < 1 || align > 1024 ||
+      expert_begin < 0)
+    return FP8FLOW_ERR_ARG;
+  if (num_tokens > INT32_MAX / 16 || max_rows > INT32_MAX) return FP8FLOW_ERR_SHAPE;
+  if (!expert_offsets || !ws || (num_tokens > 0 && (!topk_idx || !row_map)) || (max_rows > 0 && !src_of_row))
+    return FP8FLOW_ERR_NULL;
+  if (ws_bytes < permute_workspace_bytes(num_tokens, num_local_experts)) return FP8FLOW_ERR_WORKSPACE;
+  if (!aligned16(ws)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_permute_plan(topk_idx, num_tokens, top_k, expert_begin, num_local_experts, align, row_map,
+                                      src_of_row, max_rows, expert_offsets, ws, static_cast<cudaStream_t>(stream)));
+}
+
+int fp8flow_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t num_tokens,
+                        int64_t hidden, const int32_t* src_of_row, const int32_t* expert_offsets,
+                        int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out, void* stream) {
+  if (num_tokens < 0 || hidden <= 0 || hidden % 128 != 0 || max_rows < 0 || max_rows % 16 != 0)
+    return FP8FLOW_ERR_SHAPE;
+  if (ld_s_tok < num_tokens) return FP8FLOW_ERR_SHAPE;
+  if (num_local_experts < 1 || num_local_experts > 1024) return FP8FLOW_ERR_ARG;
+  if (max_rows == 0) return FP8FLOW_OK;
+  if (!src_of_row || !expert_offsets || !q_out || !s_out || (num_tokens > 0 && (!q_tok || !s_tok)))
+    return FP8FLOW_ERR_NULL;
+  if ((q_tok && !aligned16(q_tok)) || !aligned16(q_out)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_permute_pad(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts,
+                                     max_rows, q_out, s_out, static_cast<cudaStream_t>(stream), sms));
+}
+
+int fp8flow_unpermute_unpad(const void* x_bf16, int64_t hidden, const int32_t* row_map, const float* probs,
+                            int64_t num_tokens, int32_t top_k, void* y_bf16, void* stream) {
+  if (num_tokens < 0 || hidden <= 0 || hidden % 8 != 0) return FP8FLOW_ERR_SHAPE;
+  if (top_k < 1 || top_k > 16) return FP8FLOW_ERR_ARG;
+  if (num_tokens == 0) return FP8FLOW_OK;
+  if (!x_bf16 || !row_map || !y_bf16) return FP8FLOW_ERR_NULL;
+  if (!aligned16(x_bf16) || !aligned16(y_bf16) || (hidden * 2) % 16 != 0) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_unpermute_unpad(x_bf16, hidden, row_map, probs, num_tokens, top_k, y_bf16,
+                                         static_cast<cudaStream_t>(stream), sms));
+}
+
+int fp8flow_swiglu_quant(const void* h_bf16, int64_t rows_max, const int32_t* rows_dev, int64_t ffn, uint8_t* q,
+                         uint8_t* s, int64_t ld_s, void* stream) {
+  if (rows_max < 0 || ffn <= 0 || ffn % 128 != 0) return FP8FLOW_ERR_SHAPE;
+  if (ld_s < rows_max || ld_s % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (rows_max == 0) return FP8FLOW_OK;
+  if (!h_bf16 || !q || !s) return FP8FLOW_ERR_NULL;
+  if (!aligned16(h_bf16) || !aligned16(q)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(
+      launch_swiglu_quant(h_bf16, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<cudaStream_t>(stream), sms));
+}
+
+int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream) {
+  if (nbytes < 0) return FP8FLOW_ERR_SHAPE;
+  if (!out_dev || (nbytes > 0 && !buf)) return FP8FLOW_ERR_NULL;
+  if (nbytes > 0 && !aligned16(buf)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_checksum64(buf, nbytes, out_dev, static_cast<cudaStream_t>(stream), sms));
+}
+
+}  // extern "C"

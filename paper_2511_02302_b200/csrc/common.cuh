@@ -1,0 +1,128 @@
+// common.cuh -- device helpers shared by the sm_100a kernels of libfp8flow.
+//
+// Numeric contract (readings R3/R8-R13): E4M3 codes with RNE + satfinite + signed
+// zero (the hardware cvt.rn.satfinite behaviour); UE8M0 scale bytes = T + 127 where T is the
+// least integer with amax <= 448 * 2^T, clamped to [-127, 127]; amax = 0 -> byte 0.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace fp8flow {
+
+constexpr int kTile = 128;  // 1x128 scaling tiles and 128x128 transpose blocks
+
+// ------------------------------------------------------------------------------------------
+// E4M3 conversions (PTX cvt; SASS F2FP).  In the e4m3x2 packing the first-listed source lands in
+// the UPPER byte, so (lo, hi) are swapped on the way in to keep memory order = element order.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cvt_e4m3x2_f32(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_f16x2_from_e4m3x2(uint32_t two_codes) {
+  uint32_t r;
+  uint16_t v = static_cast<uint16_t>(two_codes);
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_e4m3x2_from_f16x2(uint32_t h2) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f16x2 %0, %1;" : "=h"(r) : "r"(h2));
+  return r;
+}
+
+// UE8M0 scale byte from the bit pattern of a non-negative amax.
+//   BF16 amax (15-bit magnitude):  byte = expfield - 8 + [mant7 > 0x60], clamped at 0
+//   fp32 amax (31-bit magnitude):  byte = expfield - 8 + [mant23 > 0x600000], clamped at 0
+// (T = e - 8 + [m > 0.75]: amax <= 1.75 * 2^e = 448 * 2^(e-8); zero/subnormal -> T = -127.)
+__device__ __forceinline__ uint32_t scale_byte_from_bf16_mag(uint32_t mag) {
+  int ef = static_cast<int>(mag >> 7);
+  int b = ef - 8 + ((mag & 0x7Fu) > 0x60u ? 1 : 0);
+  b = ef == 0 ? 0 : b;
+  return static_cast<uint32_t>(b < 0 ? 0 : b);
+}
+__device__ __forceinline__ uint32_t scale_byte_from_f32_mag(uint32_t mag) {
+  int ef = static_cast<int>(mag >> 23);
+  int b = ef - 8 + ((mag & 0x7FFFFFu) > 0x600000u ? 1 : 0);
+  b = ef == 0 ? 0 : b;
+  b = b > 254 ? 254 : b;
+  return static_cast<uint32_t>(b < 0 ? 0 : b);
+}
+// 2^-T as fp32 for a scale byte (T = byte - 127); exact for bytes 0..253.
+__device__ __forceinline__ float inv_scale_from_byte(uint32_t byte) {
+  return __uint_as_float((254u - byte) << 23);
+}
+// 2^T as fp32 for a scale byte; byte 0 (T = -127) is the fp32 subnormal 2^-127.
+__device__ __forceinline__ float scale_from_byte(uint32_t byte) {
+  return byte == 0 ? __uint_as_float(0x00400000u) : __uint_as_float(byte << 23);
+}
+
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// half-warp (16 lanes) max reduction; every lane of the half receives the result
+__device__ __forceinline__ uint32_t halfwarp_max_u32(uint32_t v) {
+  v = max(v, __shfl_xor_sync(0xffffffffu, v, 8));
+  v = max(v, __shfl_xor_sync(0xffffffffu, v, 4));
+  v = max(v, __shfl_xor_sync(0xffffffffu, v, 2));
+  v = max(v, __shfl_xor_sync(0xffffffffu, v, 1));
+  return v;
+}
+
+// ------------------------------------------------------------------------------------------
+// Exponent shift of 4 packed codes by the same k >= 0 (derivation after Eq. 11):
+// result = E4M3_RNE(decode(c) * 2^-k).  Fast path: every nonzero code stays normal (E > k), so
+// the result is the exponent-field edit c - (k << 3) per byte.  Otherwise: exact f16 route --
+// e4m3 -> f16 (exact), multiply by 2^-min(k,24) in f16 (exact unless the product is < 2^-24,
+// in which case the E4M3 result is +-0 either way), then one RNE cvt back to E4M3.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t f16_pow2_neg(uint32_t k) {
+  // f16 bit pattern of 2^-k for k in [0, 24]
+  return k <= 14u ? ((15u - k) << 10) : (1u << (24u - k));
+}
+static __device__ __noinline__ uint32_t shift4_slow(uint32_t w, uint32_t k) {
+  uint32_t kk = k > 24u ? 24u : k;
+  uint32_t m = f16_pow2_neg(kk);
+  __half2 mul = __halves2half2(__ushort_as_half(static_cast<unsigned short>(m)),
+                               __ushort_as_half(static_cast<unsigned short>(m)));
+  uint32_t lo = cvt_f16x2_from_e4m3x2(w & 0xFFFFu);
+  uint32_t hi = cvt_f16x2_from_e4m3x2(w >> 16);
+  __half2 l2 = __hmul2(*reinterpret_cast<__half2*>(&lo), mul);
+  __half2 h2 = __hmul2(*reinterpret_cast<__half2*>(&hi), mul);
+  uint32_t rl = cvt_e4m3x2_from_f16x2(*reinterpret_cast<uint32_t*>(&l2));
+  uint32_t rh = cvt_e4m3x2_from_f16x2(*reinterpret_cast<uint32_t*>(&h2));
+  return (rl & 0xFFFFu) | (rh << 16);
+}
+__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t k) {
+  uint32_t e4 = (w >> 3) & 0x0F0F0F0Fu;
+  uint32_t gt = __vcmpgtu4(e4, k * 0x01010101u);           // 0xFF where E > k (k <= 255)
+  uint32_t nz = __vcmpne4(w & 0x7F7F7F7Fu, 0u);             // 0xFF where the code is not +-0
+  if ((nz & ~gt) == 0u) return w - (((k & 31u) << 3) * 0x01010101u & gt);
+  return shift4_slow(w, k);
+}
+
+// ------------------------------------------------------------------------------------------
+// memory helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_v2(void* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+
+__device__ __forceinline__ float bf16lo_to_f32(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi_to_f32(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+}  // namespace fp8flow

@@ -1,0 +1,477 @@
+// transpose.cu -- A2: scaling-aware FP8 transpose (Algorithm 1), plus the naive
+// dequantize -> transpose -> requantize comparator used only for benchmarking.
+//
+// A2 semantics (R5-R7, R14, R15, R23): per segment e = [o, o+m) (an expert's rows,
+// m a multiple of 16) and per block (ib, jb) = rows o+128ib.. (partial last block) x columns
+// 128jb..128jb+127:
+//     T_max = max_i T[i][jb];  sT_e[ib][j] = T_max;  qT_e[j][i-o] = shift(q[i][j], T_max - T[i][jb])
+//
+// Kernel design (sm_100a, HBM-bound, 2.016 B/element):
+//   * persistent CTAs (2 per SM), static round-robin over the 128x128 tiles of all segments; the
+//     tile -> (segment, row block) map is a prefix sum over ceil(m_e/128) computed in shared memory
+//     from the DEVICE segment offsets (no host sync: CUDA-graph capturable).
+//   * the 16 KB input tile arrives by TMA (cp.async.bulk.tensor.2d, mbarrier complete_tx) into a
+//     4-stage ring, so 3 tiles are in flight while one is transposed.
+//   * thread (g, c) owns rows 4g..4g+3 x bytes 16c..16c+15: 4 conflict-free LDS.128 (8 threads of
+//     a quarter-warp read one full 128-byte row), the per-row exponent shift is applied to whole
+//     32-bit words (4 codes of one row share k), then 4x4 byte blocks are transposed with PRMT.
+//   * the transposed words go to a second 16 KB buffer with a 16-byte-chunk XOR swizzle
+//     (chunk ^= j/16) that makes both the 32-bit writes and the 128-bit read-out conflict-free, and
+//     leave as coalesced 128-bit stores (each output row's 128 bytes = one full line).
+//   * T_max per block: 4 scale bytes per thread (one 32-bit load of the MN-major scale run),
+//     redux.sync max per warp, 8-entry smem combine.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fp8flow {
+
+constexpr int kTStages = 4;
+constexpr int kTThreads = 256;
+constexpr int kMaxSegs = 1024;
+constexpr int kTileBytes = kTile * kTile;
+
+struct TransposeSmem {
+  uint8_t in[kTStages][kTileBytes];
+  uint32_t out[kTile * kTile / 4];
+  uint64_t full_bar[kTStages];
+  uint32_t red[kTThreads / 32];
+  int32_t seg_off[kMaxSegs + 1];
+  int32_t blk_prefix[kMaxSegs + 1];
+  int32_t total_rb;
+};
+
+// ---------------------------------------------------------------------------------------------
+// PTX wrappers: mbarrier + TMA
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// block-wide exclusive scan of one value per thread (blockDim.x == kTThreads); returns the
+// exclusive prefix and writes the block total to *total (visible after the trailing sync).
+__device__ __forceinline__ int block_exclusive_scan(int v, uint32_t* warp_tmp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int n = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += n;
+  }
+  if (lane == 31) warp_tmp[warp] = static_cast<uint32_t>(incl);
+  __syncthreads();
+  int base = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kTThreads / 32; ++w) {
+    int t = static_cast<int>(warp_tmp[w]);
+    base += (w < warp) ? t : 0;
+    all += t;
+  }
+  if (threadIdx.x == 0) *total = all;
+  __syncthreads();
+  return base + incl - v;
+}
+
+// Loads the segment offsets and builds blk_prefix[e] = sum_{e'<e} ceil(m_e'/128) in smem.
+__device__ __forceinline__ void load_segments(TransposeSmem& sm, const int32_t* seg_offsets, int32_t num_segs,
+                                              int64_t rows) {
+  const int tid = threadIdx.x;
+  if (seg_offsets == nullptr) {
+    if (tid == 0) {
+      sm.seg_off[0] = 0;
+      sm.seg_off[1] = static_cast<int32_t>(rows);
+    }
+  } else {
+    for (int i = tid; i <= num_segs; i += kTThreads) sm.seg_off[i] = seg_offsets[i];
+  }
+  __syncthreads();
+  // 4 consecutive segments per thread (num_segs <= 1024)
+  int nb[4], tsum = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = tid * 4 + i;
+    nb[i] = e < num_segs ? (sm.seg_off[e + 1] - sm.seg_off[e] + kTile - 1) / kTile : 0;
+    tsum += nb[i];
+  }
+  int run = block_exclusive_scan(tsum, sm.red, &sm.total_rb);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = tid * 4 + i;
+    if (e <= num_segs) sm.blk_prefix[e] = run;
+    run += nb[i];
+  }
+  __syncthreads();
+}
+
+// largest e in [0, num_segs) with blk_prefix[e] <= rb  (the segment that owns row block rb)
+__device__ __forceinline__ int find_segment(const int32_t* blk_prefix, int num_segs, int rb) {
+  int lo = 0, hi = num_segs;  // invariant: blk_prefix[lo] <= rb < blk_prefix[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (blk_prefix[mid] <= rb) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kTThreads, 2)
+    scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q, const uint8_t* __restrict__ s,
+                                   int64_t ld_s, int64_t rows, int64_t cols, const int32_t* __restrict__ seg_offsets,
+                                   int32_t num_segs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  TransposeSmem& sm = *reinterpret_cast<TransposeSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
+
+  if (tid == 0) {
+    for (int i = 0; i < kTStages; ++i) mbar_init(&sm.full_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)) : "memory");
+  }
+  load_segments(sm, seg_offsets, nsegs, rows);
+
+  const int n_jb = static_cast<int>(cols / kTile);
+  const int64_t total_tiles = static_cast<int64_t>(sm.total_rb) * n_jb;
+  const int64_t first = blockIdx.x;
+  const int64_t stride = gridDim.x;
+  const int64_t n_local = first < total_tiles ? (total_tiles - first + stride - 1) / stride : 0;
+
+  auto issue = [&](int64_t i) {
+    const int64_t t = first + i * stride;
+    const int rb = static_cast<int>(t / n_jb);
+    const int jb = static_cast<int>(t - static_cast<int64_t>(rb) * n_jb);
+    const int e = find_segment(sm.blk_prefix, nsegs, rb);
+    const int r0 = sm.seg_off[e] + (rb - sm.blk_prefix[e]) * kTile;
+    const int st = static_cast<int>(i % kTStages);
+    mbar_expect_tx(&sm.full_bar[st], kTileBytes);
+    tma_load_2d(sm.in[st], &tmap_q, &sm.full_bar[st], jb * kTile, r0);
+  };
+
+  if (tid == 0) {
+    for (int64_t i = 0; i < n_local && i < kTStages; ++i) issue(i);
+  }
+
+  const int g = tid >> 3;  // row quad 0..31
+  const int c = tid & 7;   // 16-byte column chunk 0..7
+
+  for (int64_t i = 0; i < n_local; ++i) {
+    const int64_t t = first + i * stride;
+    const int rb = static_cast<int>(t / n_jb);
+    const int jb = static_cast<int>(t - static_cast<int64_t>(rb) * n_jb);
+    const int e = find_segment(sm.blk_prefix, nsegs, rb);
+    const int o = sm.seg_off[e];
+    const int m = sm.seg_off[e + 1] - o;
+    const int ib = rb - sm.blk_prefix[e];
+    const int r0 = o + ib * kTile;
+    const int rows_valid = min(kTile, m - ib * kTile);  // multiple of 16
+
+    // ---- block scale max (Algorithm 1: S_max = max_i S_i^row) -------------------------------
+    uint32_t sw = 0;
+    if (4 * g < rows_valid) sw = *reinterpret_cast<const uint32_t*>(s + jb * ld_s + r0 + 4 * g);
+    uint32_t mx = max(max(sw & 0xFFu, (sw >> 8) & 0xFFu), max((sw >> 16) & 0xFFu, sw >> 24));
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) sm.red[warp] = mx;
+    __syncthreads();  // S1
+    uint32_t tmax = sm.red[0];
+#pragma unroll
+    for (int w = 1; w < kTThreads / 32; ++w) tmax = max(tmax, sm.red[w]);
+
+    // ---- wait for the tile, shift rows, transpose 4x4 byte blocks ------------------------------
+    const int st = static_cast<int>(i % kTStages);
+    mbar_wait(&sm.full_bar[st], static_cast<uint32_t>((i / kTStages) & 1));
+    uint4 rv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      rv[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
+      const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
+      if (k != 0u) {
+        rv[r].x = shift4(rv[r].x, k);
+        rv[r].y = shift4(rv[r].y, k);
+        rv[r].z = shift4(rv[r].z, k);
+        rv[r].w = shift4(rv[r].w, k);
+      }
+    }
+    const uint32_t R[4][4] = {{rv[0].x, rv[0].y, rv[0].z, rv[0].w},
+                              {rv[1].x, rv[1].y, rv[1].z, rv[1].w},
+                              {rv[2].x, rv[2].y, rv[2].z, rv[2].w},
+                              {rv[3].x, rv[3].y, rv[3].z, rv[3].w}};
+    const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
+      const uint32_t t1 = __byte_perm(R[0][w], R[1][w], 0x7362);
+      const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
+      const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
+      const int j0 = 16 * c + 4 * w;
+      sm.out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
+      sm.out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
+      sm.out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
+      sm.out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
+    }
+    __syncthreads();  // S2: tile consumed, out buffer complete
+
+    if (tid == 0 && i + kTStages < n_local) issue(i + kTStages);
+
+    // ---- coalesced 128-bit read-out: 8 threads per output row --------------------------------
+    uint8_t* qTe = qT + cols * static_cast<int64_t>(o);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int j = (tid >> 3) + 32 * it;
+      if (16 * c < rows_valid) {
+        const int phys = c ^ ((j >> 4) & 7);
+        const uint4 v = *reinterpret_cast<const uint4*>(&sm.out[j * 32 + 4 * phys]);
+        st_v4(qTe + (static_cast<int64_t>(jb) * kTile + j) * m + ib * kTile + 16 * c, v);
+      }
+    }
+    if (tid < 8) {
+      const uint32_t b4 = tmax * 0x01010101u;
+      st_v4(sT + static_cast<int64_t>(rb) * cols + jb * kTile + 16 * tid, make_uint4(b4, b4, b4, b4));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side: tensor map + launch
+// ---------------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+static int transpose_blocks_per_sm() {
+  static int occ = 0;
+  if (occ == 0) {
+    cudaFuncSetAttribute(scaling_aware_transpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(TransposeSmem)));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scaling_aware_transpose_kernel, kTThreads,
+                                                      sizeof(TransposeSmem)) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+  }
+  return occ;
+}
+
+cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows,
+                                           int64_t cols, const int32_t* seg_offsets, int32_t num_segs,
+                                           uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
+  PFN_encodeTiled encode = get_encode_fn();
+  if (!encode) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(cols)};
+  const cuuint32_t box[2] = {kTile, kTile};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(q), gdim, gstride, box, estride,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
+  int64_t grid = static_cast<int64_t>(num_sms) * transpose_blocks_per_sm();
+  if (grid > ub_tiles) grid = ub_tiles;
+  if (grid < 1) grid = 1;
+  scaling_aware_transpose_kernel<<<static_cast<unsigned>(grid), kTThreads, sizeof(TransposeSmem), stream>>>(
+      map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
+  return cudaGetLastError();
+}
+
+// =============================================================================================
+// Naive comparator: dequantize (E4M3 x 2^T -> BF16) -> BF16 transpose per segment ->
+// column-wise 1x128 requantization with fresh scales.  Three plain kernels + a segment prefix.
+// =============================================================================================
+__global__ void seg_prefix_kernel(const int32_t* __restrict__ seg_offsets, int32_t num_segs, int64_t rows,
+                                  int32_t* __restrict__ seg_out, int32_t* __restrict__ blk_prefix) {
+  __shared__ int32_t so[kMaxSegs + 1];
+  __shared__ uint32_t red[kTThreads / 32];
+  __shared__ int total;
+  const int tid = threadIdx.x;
+  const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
+  if (seg_offsets == nullptr) {
+    if (tid == 0) {
+      so[0] = 0;
+      so[1] = static_cast<int32_t>(rows);
+    }
+  } else {
+    for (int i = tid; i <= nsegs; i += kTThreads) so[i] = seg_offsets[i];
+  }
+  __syncthreads();
+  int nb[4], tsum = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = tid * 4 + i;
+    nb[i] = e < nsegs ? (so[e + 1] - so[e] + kTile - 1) / kTile : 0;
+    tsum += nb[i];
+  }
+  int run = block_exclusive_scan(tsum, red, &total);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = tid * 4 + i;
+    if (e <= nsegs) {
+      blk_prefix[e] = run;
+      seg_out[e] = so[e];
+    }
+    run += nb[i];
+  }
+}
+
+__global__ void naive_dequant_kernel(const uint8_t* __restrict__ q, const uint8_t* __restrict__ s, int64_t ld_s,
+                                     int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ xd) {
+  const int64_t n16 = rows * cols / 16;
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n16;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e0 = v * 16, r = e0 / cols, cc = e0 - r * cols;
+    const uint4 w = ld_nc_v4(q + e0);
+    const float sc = scale_from_byte(s[(cc / kTile) * ld_s + r]);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t lo = cvt_f16x2_from_e4m3x2(ws[k] & 0xFFFFu), hi = cvt_f16x2_from_e4m3x2(ws[k] >> 16);
+      float2 a = __half22float2(*reinterpret_cast<__half2*>(&lo));
+      float2 b = __half22float2(*reinterpret_cast<__half2*>(&hi));
+      __nv_bfloat162 pa = __floats2bfloat162_rn(a.x * sc, a.y * sc);
+      __nv_bfloat162 pb = __floats2bfloat162_rn(b.x * sc, b.y * sc);
+      o[2 * k] = *reinterpret_cast<uint32_t*>(&pa);
+      o[2 * k + 1] = *reinterpret_cast<uint32_t*>(&pb);
+    }
+    st_v4(xd + e0, make_uint4(o[0], o[1], o[2], o[3]));
+    st_v4(xd + e0 + 8, make_uint4(o[4], o[5], o[6], o[7]));
+  }
+}
+
+// per segment: xT_e[j][i] = xd[o + i][j]; block = 16 rows (never straddles a segment) x 128 cols
+__global__ void naive_transpose_bf16_kernel(const __nv_bfloat16* __restrict__ xd, int64_t cols,
+                                            const int32_t* __restrict__ seg_off, int32_t nsegs,
+                                            __nv_bfloat16* __restrict__ xT) {
+  __shared__ uint16_t tile[16][128 + 2];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 16;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 128;
+  if (r0 >= seg_off[nsegs]) return;
+  int lo = 0, hi = nsegs;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (seg_off[mid] <= r0) lo = mid;
+    else hi = mid;
+  }
+  const int64_t o = seg_off[lo], m = seg_off[lo + 1] - o;
+  const uint16_t* src = reinterpret_cast<const uint16_t*>(xd);
+  for (int idx = threadIdx.x; idx < 16 * 128; idx += blockDim.x) {
+    const int r = idx / 128, cc = idx % 128;
+    tile[r][cc] = src[(r0 + r) * cols + c0 + cc];
+  }
+  __syncthreads();
+  uint16_t* dst = reinterpret_cast<uint16_t*>(xT) + cols * o;
+  for (int idx = threadIdx.x; idx < 16 * 128; idx += blockDim.x) {
+    const int j = idx / 16, r = idx % 16;
+    dst[(c0 + j) * m + (r0 - o) + r] = tile[r][j];
+  }
+}
+
+// column-wise requantization: rows j of xT_e (length m_e), 1x128 tiles along i (ragged last tile)
+__global__ void naive_colquant_kernel(const __nv_bfloat16* __restrict__ xT, int64_t cols,
+                                      const int32_t* __restrict__ seg_off, const int32_t* __restrict__ blk_prefix,
+                                      int32_t nsegs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t jgroups = cols / 32;
+  const int64_t total = static_cast<int64_t>(blk_prefix[nsegs]) * jgroups;
+  if (warp >= total) return;
+  const int rb = static_cast<int>(warp / jgroups);
+  const int64_t j0 = (warp - static_cast<int64_t>(rb) * jgroups) * 32;
+  const int e = find_segment(blk_prefix, nsegs, rb);
+  const int64_t o = seg_off[e], m = seg_off[e + 1] - o;
+  const int ib = rb - blk_prefix[e];
+  const int valid = static_cast<int>(min64(kTile, m - ib * kTile));
+  uint32_t keep = 0;
+  for (int jj = 0; jj < 32; jj += 2) {
+    const int64_t j = j0 + jj + half;
+    const int i0 = ib * kTile + sub * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (sub * 8 < valid) v = ld_nc_v4(xT + cols * o + j * m + i0);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t mag = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mag = max(mag, max(w[k] & 0x7FFFu, (w[k] >> 16) & 0x7FFFu));
+    mag = halfwarp_max_u32(mag);
+    const uint32_t sb = scale_byte_from_bf16_mag(mag);
+    const float inv = inv_scale_from_byte(sb);
+    uint32_t cc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cc[k] = cvt_e4m3x2_f32(bf16lo_to_f32(w[k]) * inv, bf16hi_to_f32(w[k]) * inv);
+    if (sub * 8 < valid) st_v2(qT + cols * o + j * m + i0, cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
+    const uint32_t a = __shfl_sync(0xffffffffu, sb, 0), b = __shfl_sync(0xffffffffu, sb, 16);
+    if (lane == jj) keep = a;
+    if (lane == jj + 1) keep = b;
+  }
+  sT[static_cast<int64_t>(rb) * cols + j0 + lane] = static_cast<uint8_t>(keep);
+}
+
+size_t naive_workspace_bytes(int64_t rows, int64_t cols, int32_t num_segs) {
+  return 256 + 2 * 4 * static_cast<size_t>(num_segs + 1) + 256 + 4 * static_cast<size_t>(rows) * cols;
+}
+
+cudaError_t launch_naive_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                                   const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
+                                   void* ws, cudaStream_t stream, int num_sms) {
+  const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  int32_t* seg_out = reinterpret_cast<int32_t*>(base);
+  int32_t* blk_prefix = seg_out + (nsegs + 1);
+  size_t off = (2 * 4 * static_cast<size_t>(nsegs + 1) + 255) / 256 * 256;
+  __nv_bfloat16* xd = reinterpret_cast<__nv_bfloat16*>(base + off);
+  __nv_bfloat16* xT = xd + rows * cols;
+  seg_prefix_kernel<<<1, kTThreads, 0, stream>>>(seg_offsets, num_segs, rows, seg_out, blk_prefix);
+  const int64_t n16 = rows * cols / 16;
+  int64_t g1 = (n16 + 255) / 256;
+  if (g1 > static_cast<int64_t>(num_sms) * 16) g1 = static_cast<int64_t>(num_sms) * 16;
+  naive_dequant_kernel<<<static_cast<unsigned>(g1 < 1 ? 1 : g1), 256, 0, stream>>>(q, s, ld_s, rows, cols, xd);
+  dim3 g2(static_cast<unsigned>(cols / 128), static_cast<unsigned>((rows + 15) / 16));
+  naive_transpose_bf16_kernel<<<g2, 256, 0, stream>>>(xd, cols, seg_out, nsegs, xT);
+  const int64_t warps = (rows / kTile + nsegs) * (cols / 32);
+  naive_colquant_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, stream>>>(xT, cols, seg_out, blk_prefix,
+                                                                                      nsegs, qT, sT);
+  return cudaGetLastError();
+}
+
+}  // namespace fp8flow

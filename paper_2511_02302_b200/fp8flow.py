@@ -1,0 +1,198 @@
+"""Thin Python binding of libfp8flow (include/fp8flow.h).
+
+Argument marshalling only: every function has the name of the C entry point it calls, takes
+torch CUDA tensors (device memory owned by the caller) and passes their pointers, sizes and the
+current CUDA stream to the library.  No compute happens here and there is no fallback: if the
+shared library is missing or the device is not sm_100, calls raise.
+
+Layouts (see include/fp8flow.h): BF16 tensors are torch.bfloat16; E4M3 codes and UE8M0 scale
+bytes are torch.uint8; scales are MN-major [cols/128, ld_s].
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfp8flow.so")
+_lib = None
+
+STATUS = {
+    0: "FP8FLOW_OK", 1: "FP8FLOW_ERR_NULL", 2: "FP8FLOW_ERR_SHAPE", 3: "FP8FLOW_ERR_ALIGN",
+    4: "FP8FLOW_ERR_ARG", 5: "FP8FLOW_ERR_WORKSPACE", 6: "FP8FLOW_ERR_ARCH", 7: "FP8FLOW_ERR_CUDA",
+}
+
+# exported symbols and their C signatures (restype, argtypes)
+_P, _I64, _I32, _SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+SIGNATURES = {
+    "fp8flow_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "fp8flow_last_cuda_error": (ctypes.c_int, []),
+    "fp8flow_version": (ctypes.c_int, []),
+    "fp8flow_build_target": (ctypes.c_char_p, []),
+    "fp8flow_device_check": (ctypes.c_int, []),
+    "fp8flow_quantize_rowwise": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _I64, _P]),
+    "fp8flow_scaling_aware_transpose": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P]),
+    "fp8flow_naive_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
+    "fp8flow_naive_transpose": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _SZ, _P]),
+    "fp8flow_permute_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "fp8flow_permute_plan": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _I64, _P, _P, _SZ, _P]),
+    "fp8flow_permute_pad": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _P, _I32, _I64, _P, _P, _P]),
+    "fp8flow_unpermute_unpad": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _I32, _P, _P]),
+    "fp8flow_swiglu_quant": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _P]),
+    "fp8flow_checksum64": (ctypes.c_int, [_P, _I64, _P, _P]),
+}
+
+
+class Fp8FlowError(RuntimeError):
+    pass
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libfp8flow.so (built in-tree by __graft_entry__.build()).  Raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise Fp8FlowError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str) -> None:
+    if status != 0:
+        msg = f"{what} failed: {STATUS.get(status, status)}"
+        if status == 7:
+            msg += f" (cudaError {lib().fp8flow_last_cuda_error()})"
+        raise Fp8FlowError(msg)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise Fp8FlowError("libfp8flow takes device tensors only (no CPU fallback)")
+    if not t.is_contiguous():
+        raise Fp8FlowError("tensors must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _u8(t):
+    assert t.dtype == torch.uint8, t.dtype
+    return t
+
+
+# ----------------------------------------------------------------------------------- misc
+def fp8flow_device_check() -> None:
+    _check(lib().fp8flow_device_check(), "fp8flow_device_check")
+
+
+def fp8flow_version() -> int:
+    return lib().fp8flow_version()
+
+
+def fp8flow_build_target() -> str:
+    return lib().fp8flow_build_target().decode()
+
+
+# ----------------------------------------------------------------------------------- A1
+def fp8flow_quantize_rowwise(x: torch.Tensor, q: torch.Tensor, s: torch.Tensor, stream=None) -> None:
+    """x bf16 [rows, cols] -> q uint8 [rows, cols], s uint8 [cols/128, ld_s]."""
+    assert x.dtype == torch.bfloat16 and x.dim() == 2
+    rows, cols = x.shape
+    _check(lib().fp8flow_quantize_rowwise(_ptr(x), rows, cols, _ptr(_u8(q)), _ptr(_u8(s)), s.shape[1],
+                                          _stream(stream)), "fp8flow_quantize_rowwise")
+
+
+# ----------------------------------------------------------------------------------- A2
+def fp8flow_scaling_aware_transpose(q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor, sT: torch.Tensor,
+                                    seg_offsets: torch.Tensor | None = None, stream=None) -> None:
+    """q uint8 [rows, cols] + s [cols/128, ld_s] -> qT (flat, segment-major), sT [tiles, cols]."""
+    rows, cols = q.shape
+    nseg = 0 if seg_offsets is None else seg_offsets.numel() - 1
+    if seg_offsets is not None:
+        assert seg_offsets.dtype == torch.int32
+    _check(lib().fp8flow_scaling_aware_transpose(_ptr(_u8(q)), _ptr(_u8(s)), s.shape[1], rows, cols,
+                                                 _ptr(seg_offsets), nseg, _ptr(_u8(qT)), _ptr(_u8(sT)),
+                                                 _stream(stream)), "fp8flow_scaling_aware_transpose")
+
+
+def fp8flow_naive_workspace_bytes(rows: int, cols: int, num_segs: int) -> int:
+    return lib().fp8flow_naive_workspace_bytes(rows, cols, num_segs)
+
+
+def fp8flow_naive_transpose(q, s, qT, sT, ws: torch.Tensor, seg_offsets=None, stream=None) -> None:
+    rows, cols = q.shape
+    nseg = 0 if seg_offsets is None else seg_offsets.numel() - 1
+    _check(lib().fp8flow_naive_transpose(_ptr(_u8(q)), _ptr(_u8(s)), s.shape[1], rows, cols, _ptr(seg_offsets), nseg,
+                                         _ptr(_u8(qT)), _ptr(_u8(sT)), _ptr(ws), ws.numel() * ws.element_size(),
+                                         _stream(stream)), "fp8flow_naive_transpose")
+
+
+# ----------------------------------------------------------------------------------- A3
+def fp8flow_permute_workspace_bytes(num_tokens: int, top_k: int, num_local_experts: int) -> int:
+    return lib().fp8flow_permute_workspace_bytes(num_tokens, top_k, num_local_experts)
+
+
+def fp8flow_permute_plan(topk_idx: torch.Tensor, expert_begin: int, num_local_experts: int, align: int,
+                         row_map: torch.Tensor, src_of_row: torch.Tensor, expert_offsets: torch.Tensor,
+                         ws: torch.Tensor, stream=None) -> None:
+    assert topk_idx.dtype == torch.int32 and topk_idx.dim() == 2
+    T, K = topk_idx.shape
+    _check(lib().fp8flow_permute_plan(_ptr(topk_idx), T, K, expert_begin, num_local_experts, align, _ptr(row_map),
+                                      _ptr(src_of_row), src_of_row.numel(), _ptr(expert_offsets), _ptr(ws),
+                                      ws.numel() * ws.element_size(), _stream(stream)), "fp8flow_permute_plan")
+
+
+def fp8flow_permute_pad(q_tok, s_tok, src_of_row, expert_offsets, q_out, s_out, stream=None) -> None:
+    T, H = q_tok.shape
+    _check(lib().fp8flow_permute_pad(_ptr(_u8(q_tok)), _ptr(_u8(s_tok)), s_tok.shape[1], T, H, _ptr(src_of_row),
+                                     _ptr(expert_offsets), expert_offsets.numel() - 1, q_out.shape[0],
+                                     _ptr(_u8(q_out)), _ptr(_u8(s_out)), _stream(stream)), "fp8flow_permute_pad")
+
+
+# ----------------------------------------------------------------------------------- A4
+def fp8flow_unpermute_unpad(x: torch.Tensor, row_map: torch.Tensor, probs: torch.Tensor | None, y: torch.Tensor,
+                            stream=None) -> None:
+    assert x.dtype == torch.bfloat16 and y.dtype == torch.bfloat16
+    T, K = row_map.shape
+    _check(lib().fp8flow_unpermute_unpad(_ptr(x), x.shape[1], _ptr(row_map), _ptr(probs), T, K, _ptr(y),
+                                         _stream(stream)), "fp8flow_unpermute_unpad")
+
+
+# ----------------------------------------------------------------------------------- A5
+def fp8flow_swiglu_quant(h: torch.Tensor, q: torch.Tensor, s: torch.Tensor, rows_dev: torch.Tensor | None = None,
+                         stream=None) -> None:
+    assert h.dtype == torch.bfloat16 and h.dim() == 2
+    rows_max, F2 = h.shape
+    _check(lib().fp8flow_swiglu_quant(_ptr(h), rows_max, _ptr(rows_dev), F2 // 2, _ptr(_u8(q)), _ptr(_u8(s)),
+                                      s.shape[1], _stream(stream)), "fp8flow_swiglu_quant")
+
+
+def fp8flow_checksum64(buf: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+    """out: int64 CUDA tensor of one element (holds the uint64 bit pattern)."""
+    _check(lib().fp8flow_checksum64(_ptr(buf), buf.numel() * buf.element_size(), _ptr(out), _stream(stream)),
+           "fp8flow_checksum64")
+
+
+# ----------------------------------------------------------------------------------- sizes
+def transpose_out_shapes(rows: int, cols: int, num_segs: int = 1):
+    """Capacity of qT (bytes) and sT (tile rows) for fp8flow_scaling_aware_transpose."""
+    return rows * cols, rows // 128 + num_segs
+
+
+def permute_max_rows(num_tokens: int, top_k: int, num_local_experts: int, align: int = 16) -> int:
+    r = num_tokens * top_k + num_local_experts * (align - 1)
+    return (r + 15) // 16 * 16

@@ -1,0 +1,116 @@
+"""CPU checks of the C-ABI library: it builds, loads, exports exactly what include/fp8flow.h declares,
+and validates arguments synchronously (these paths return before any CUDA call, so they run
+without a GPU).  No compute is launched here."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fp8flow.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2511_02302_b200 import build, fp8flow
+
+    build.build_library()
+    return fp8flow.lib()
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"FP8FLOW_API\s+[\w\s\*]+?\b(fp8flow_\w+)\s*\(", txt)))
+
+
+def test_exports_match_header(L):
+    from paper_2511_02302_b200 import fp8flow
+
+    declared = header_symbols()
+    assert len(declared) >= 14
+    out = subprocess.check_output(["nm", "-D", "--defined-only", fp8flow.LIB_PATH]).decode()
+    exported = sorted(set(re.findall(r"\b(fp8flow_\w+)\b", out)))
+    assert exported == declared
+    assert sorted(fp8flow.SIGNATURES) == declared          # the binding covers every entry point
+    for name in declared:
+        assert hasattr(L, name)
+
+
+def test_build_target_is_sm100a(L):
+    from paper_2511_02302_b200 import fp8flow
+
+    assert L.fp8flow_build_target() == b"sm_100a"
+    sass = subprocess.run(["cuobjdump", "--list-elf", fp8flow.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass
+
+
+def test_tma_and_no_legacy_tensor_path_in_sass():
+    """The transpose kernel issues TMA (UTMALDG); none of the kernels uses tensor-core MMA (HBM-bound ops)."""
+    from paper_2511_02302_b200 import fp8flow
+
+    sass = subprocess.run(["cuobjdump", "-sass", fp8flow.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass
+    assert "HMMA" not in sass
+
+
+def test_status_strings(L):
+    assert L.fp8flow_status_string(0) == b"FP8FLOW_OK"
+    assert L.fp8flow_status_string(6) == b"FP8FLOW_ERR_ARCH"
+
+
+def test_validation_before_any_cuda_call(L):
+    # bad shapes / args are rejected synchronously (no device needed)
+    assert L.fp8flow_quantize_rowwise(None, 4, 100, None, None, 16, None) == 2            # cols % 128
+    assert L.fp8flow_quantize_rowwise(None, 4, 128, None, None, 2, None) == 2              # ld_s < rows
+    assert L.fp8flow_quantize_rowwise(None, 0, 128, None, None, 16, None) == 0             # empty: no-op
+    assert L.fp8flow_quantize_rowwise(None, 4, 128, None, None, 16, None) == 1             # NULL
+    assert L.fp8flow_quantize_rowwise(ctypes.c_void_p(8), 4, 128, ctypes.c_void_p(16), ctypes.c_void_p(16), 16,
+                                      None) == 3                                            # alignment
+    assert L.fp8flow_scaling_aware_transpose(None, None, 32, 24, 128, None, 0, None, None, None) == 2  # rows % 16
+    assert L.fp8flow_scaling_aware_transpose(ctypes.c_void_p(16), ctypes.c_void_p(16), 32, 32, 128,
+                                             ctypes.c_void_p(16), 2000, ctypes.c_void_p(16), ctypes.c_void_p(16),
+                                             None) == 4                                     # num_segs
+    assert L.fp8flow_permute_plan(None, 10, 0, 0, 8, 16, None, None, 100, None, None, 0, None) == 4   # top_k
+    assert L.fp8flow_permute_plan(None, 10, 8, 0, 0, 16, None, None, 100, None, None, 0, None) == 4   # E_loc
+    ws_need = L.fp8flow_permute_workspace_bytes(10, 8, 4)
+    assert ws_need > 0
+    assert L.fp8flow_permute_plan(ctypes.c_void_p(16), 10, 8, 0, 4, 16, ctypes.c_void_p(16), ctypes.c_void_p(16),
+                                  100, ctypes.c_void_p(16), ctypes.c_void_p(16), ws_need - 1, None) == 5
+    assert L.fp8flow_unpermute_unpad(None, 7168, None, None, 4, 17, None, None) == 4       # top_k > 16
+    assert L.fp8flow_swiglu_quant(None, 4, None, 100, None, None, 16, None) == 2            # ffn % 128
+    assert L.fp8flow_naive_transpose(ctypes.c_void_p(16), ctypes.c_void_p(16), 32, 32, 128, None, 0,
+                                     ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16), 10, None) == 5
+
+
+def test_no_device_means_error_not_fallback(L):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    # valid arguments, but no usable device: a CUDA/arch error, never a silent CPU path
+    st = L.fp8flow_quantize_rowwise(ctypes.c_void_p(16), 4, 128, ctypes.c_void_p(16), ctypes.c_void_p(16), 16, None)
+    assert st in (6, 7)
+
+
+def test_binding_refuses_cpu_tensors(L):
+    import torch
+
+    from paper_2511_02302_b200 import fp8flow
+
+    x = torch.zeros(4, 128, dtype=torch.bfloat16)
+    q = torch.zeros(4, 128, dtype=torch.uint8)
+    s = torch.zeros(1, 16, dtype=torch.uint8)
+    with pytest.raises(fp8flow.Fp8FlowError):
+        fp8flow.fp8flow_quantize_rowwise(x, q, s)
+
+
+def test_product_package_never_imports_oracle():
+    """The product path (package + CUDA sources) neither imports, links nor calls the oracle."""
+    pkg = os.path.join(ROOT, "paper_2511_02302_b200")
+    bad = re.compile(r"^\s*(import\s+oracle|from\s+oracle\b)|liboracle|\borc_\w+\(|fp8flow_oracle", re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                assert not bad.search(open(os.path.join(dirpath, f)).read()), f

@@ -1,0 +1,334 @@
+"""GPU parity: every op of the hot path through the C ABI (libfp8flow via its binding) against the
+CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): bit-exact codes and scales for quantize (A1), transpose (A2),
+permute plan + move (A3) and unpermute (A4, BF16 bytes); SwiGLU+quant (A5) codes within 1 E4M3
+ULP on <= 1e-4 of elements with byte-identical scales.  Sizes span several tiles with ragged
+tails, plus the BASELINE.json full sizes (configs 1-4) and the edge cases of each method.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_02302_b200 import fp8flow
+
+    fp8flow.fp8flow_device_check()  # raises on anything but sm_100
+    return fp8flow
+
+
+def dev(a):
+    t = torch.from_numpy(np.ascontiguousarray(a)) if isinstance(a, np.ndarray) else a
+    return t.cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def bf16_dev(x_bits):
+    return torch.from_numpy(np.ascontiguousarray(x_bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def e4m3_ulp_dist(a, b):
+    def ordv(c):
+        c = c.astype(np.int32)
+        return np.where(c < 0x80, c & 0x7F, -(c & 0x7F))
+    return np.abs(ordv(a) - ordv(b))
+
+
+# =========================================================================================== A1
+def run_quantize(F, x_bf16, ld_s=None):
+    rows, cols = x_bf16.shape
+    ld_s = ld_s or ((rows + 15) // 16 * 16)
+    q = torch.empty(rows, cols, dtype=torch.uint8, device="cuda")
+    s = torch.full((cols // 128, ld_s), 0xAB, dtype=torch.uint8, device="cuda")
+    F.fp8flow_quantize_rowwise(x_bf16, q, s)
+    torch.cuda.synchronize()
+    return host(q), host(s)
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (1, 128), (33, 384), (1000, 1152), (4096, 7168)])
+def test_quantize_parity(F, orc, rows, cols):
+    x = synth.activations_bf16(rows, cols, 100 + rows)
+    q, s = run_quantize(F, x.cuda())
+    ld = s.shape[1]
+    q_ref, s_ref = orc.quantize_rowwise_bf16(synth.bf16_bits(x), ld_s=ld)
+    assert np.array_equal(q, q_ref)
+    assert np.array_equal(s[:, :rows], s_ref[:, :rows])
+    assert np.all(s[:, rows:] == 0xAB)                                  # padding bytes untouched
+
+
+def test_quantize_edge_values(F, orc):
+    """amax exactly 448*2^T and its BF16 successor, zeros, subnormal BF16, huge values, -0."""
+    rows, cols = 64, 256
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal((rows, cols)) * 0.3).astype(np.float32)
+    for i in range(rows):
+        T = int(rng.integers(-30, 30))
+        x[i, 5] = 448.0 * 2.0 ** T                                       # exactly on the boundary
+        if i % 2:
+            x[i, 6] = np.nextafter(np.float32(448.0 * 2.0 ** T), np.float32(np.inf))  # rounds up in bf16
+    x[3] = 0.0                                                           # zero tile -> byte 0
+    x[4, :128] = -0.0
+    x[5, :] = 1e-40                                                      # bf16 subnormal
+    x[6, 0] = 3.0e38                                                     # near bf16 max
+    xb = torch.from_numpy(x).to(torch.bfloat16)
+    q, s = run_quantize(F, xb.cuda())
+    q_ref, s_ref = orc.quantize_rowwise_bf16(synth.bf16_bits(xb), ld_s=s.shape[1])
+    assert np.array_equal(q, q_ref) and np.array_equal(s[:, :rows], s_ref[:, :rows])
+
+
+def test_quantize_deterministic(F):
+    x = synth.activations_bf16(512, 2048, 7).cuda()
+    a = run_quantize(F, x)
+    b = run_quantize(F, x)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# =========================================================================================== A2
+def run_transpose(F, q, s, seg=None, naive=False):
+    rows, cols = q.shape
+    nseg = 1 if seg is None else len(seg) - 1
+    nbytes, ntiles = F.transpose_out_shapes(rows, cols, nseg)
+    qT = torch.full((max(nbytes, 16),), 0xCD, dtype=torch.uint8, device="cuda")
+    sT = torch.full((ntiles, cols), 0xCD, dtype=torch.uint8, device="cuda")
+    seg_t = None if seg is None else dev(np.asarray(seg, np.int32))
+    qd, sd = dev(q), dev(s)
+    if naive:
+        ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, nseg), dtype=torch.uint8, device="cuda")
+        F.fp8flow_naive_transpose(qd, sd, qT, sT, ws, seg_offsets=seg_t)
+    else:
+        F.fp8flow_scaling_aware_transpose(qd, sd, qT, sT, seg_offsets=seg_t)
+    torch.cuda.synchronize()
+    return host(qT), host(sT)
+
+
+def check_transpose(F, orc, q, s, seg=None, naive=False):
+    qT, sT = run_transpose(F, q, s, seg, naive)
+    fn = orc.naive_transpose if naive else orc.scaling_aware_transpose
+    qT_ref, sT_ref = fn(q, s, seg)
+    n = qT_ref.size
+    assert np.array_equal(qT[:n], qT_ref), np.argwhere(qT[:n] != qT_ref)[:5]
+    assert np.array_equal(sT[:sT_ref.shape[0]], sT_ref)
+
+
+def constructed_rowwise(rows, cols, seed, k_max=40):
+    """Row-wise FP8 built directly: all 254 non-NaN codes appear in every row block and the block's
+    row scales span k = 0..k_max (the adversarial all-codes x all-k suite)."""
+    rng = np.random.default_rng(seed)
+    codes = np.array([c for c in range(256) if c not in (0x7F, 0xFF)], np.uint8)
+    q = codes[rng.integers(0, codes.size, (rows, cols))]
+    q[:, :254] = codes[None, :]
+    T = 100 - (np.arange(rows) % (k_max + 1))                            # block max 100 -> k = 0..k_max
+    s = np.tile(T.astype(np.uint8), (cols // 128, 1))
+    s = np.ascontiguousarray(np.roll(s, 3, axis=1))
+    return q, s
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (128, 128), (384, 640), (4096, 7168)])
+def test_transpose_parity_quantized(F, orc, rows, cols):
+    x = synth.activations_bf16(rows, cols, 200 + rows)
+    q, s = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
+    check_transpose(F, orc, q, s)
+
+
+def test_transpose_all_codes_all_k(F, orc):
+    q, s = constructed_rowwise(512, 384, 1)
+    check_transpose(F, orc, q, s)
+
+
+def test_transpose_ragged_segments(F, orc):
+    # per-expert token counts {0,1,15,16,17,127,128,129} padded to 16, plus larger ones
+    m = [0, 16, 16, 16, 32, 128, 128, 144, 0, 256, 272, 16]
+    seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
+    rows, cols = int(seg[-1]), 512
+    q, s = constructed_rowwise(rows, cols, 2, k_max=24)
+    check_transpose(F, orc, q, s, seg)
+    x = synth.activations_bf16(rows, cols, 3)
+    q, s = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
+    check_transpose(F, orc, q, s, seg)
+
+
+def test_transpose_involution_on_gpu(F, orc):
+    """R24 on the device path: T∘T∘T == T bitwise."""
+    q, s = constructed_rowwise(256, 256, 4, k_max=12)
+    q1, s1 = run_transpose(F, q, s)
+    q2, s2 = run_transpose(F, q1[: 256 * 256].reshape(256, 256), s1)
+    q3, s3 = run_transpose(F, q2[: 256 * 256].reshape(256, 256), s2)
+    assert np.array_equal(q3, q1) and np.array_equal(s3, s1)
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (1024, 1024)])
+def test_naive_transpose_parity(F, orc, rows, cols):
+    x = synth.activations_bf16(rows, cols, 300 + rows)
+    q, s = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
+    check_transpose(F, orc, q, s, naive=True)
+    m = [16, 128, 144, 0, rows - 288]
+    seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
+    check_transpose(F, orc, q, s, seg, naive=True)
+
+
+# =========================================================================================== A3
+def run_plan(F, topk_idx, e0, E_loc, align=16, max_rows=None):
+    T, K = topk_idx.shape
+    max_rows = max_rows or F.permute_max_rows(T, K, E_loc, align)
+    row_map = torch.empty(T, K, dtype=torch.int32, device="cuda")
+    src = torch.full((max_rows,), -7, dtype=torch.int32, device="cuda")
+    off = torch.empty(E_loc + 1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(F.fp8flow_permute_workspace_bytes(T, K, E_loc), dtype=torch.uint8, device="cuda")
+    F.fp8flow_permute_plan(dev(topk_idx), e0, E_loc, align, row_map, src, off, ws)
+    torch.cuda.synchronize()
+    return host(row_map), host(src), host(off), int(host(ws[:4].view(torch.int32))[0])
+
+
+@pytest.mark.parametrize("T,E,K,group,ngroups,align", [
+    (16384, 256, 8, 0, 8, 16), (16384, 256, 8, 5, 8, 16), (3000, 64, 6, 0, 1, 16), (777, 32, 4, 1, 4, 128),
+    (5, 8, 2, 0, 2, 16)])
+def test_permute_plan_parity(F, orc, T, E, K, group, ngroups, align):
+    idx, _ = synth.routing(T, 400 + T, num_experts=E, top_k=K, num_groups=min(8, E // 4), topk_groups=2)
+    per = E // ngroups
+    e0 = group * per
+    rm, src, off, status = run_plan(F, idx.numpy(), e0, per, align)
+    rm_ref, src_ref, off_ref = orc.permute_plan(idx.numpy(), e0, per, align=align, max_rows=len(src))
+    assert status == 0
+    assert np.array_equal(off, off_ref) and np.array_equal(rm, rm_ref)
+    assert np.array_equal(src[: off[-1]], src_ref[: off[-1]])
+
+
+def test_permute_plan_no_tokens_for_some_experts(F, orc):
+    idx = np.array([[0, 3], [3, 1], [1, 0], [0, 1]], np.int32)
+    rm, src, off, _ = run_plan(F, idx, 0, 6)
+    rm_ref, src_ref, off_ref = orc.permute_plan(idx, 0, 6, max_rows=len(src))
+    assert np.array_equal(off, off_ref) and np.array_equal(rm, rm_ref)
+    assert np.array_equal(src[: off[-1]], src_ref[: off[-1]])
+
+
+def test_permute_plan_overflow_status(F):
+    idx = np.zeros((64, 1), np.int32)
+    rm, src, off, status = run_plan(F, idx, 0, 1, 16, max_rows=32)
+    assert status == 1 and off[-1] == 64 and np.all(rm[32:] == -1) and np.all(rm[:32, 0] == np.arange(32))
+
+
+def run_move(F, q_tok, s_tok, src, off, max_rows):
+    T, H = q_tok.shape
+    q_out = torch.full((max_rows, H), 0xEE, dtype=torch.uint8, device="cuda")
+    s_out = torch.full((H // 128, max_rows), 0xEE, dtype=torch.uint8, device="cuda")
+    F.fp8flow_permute_pad(dev(q_tok), dev(s_tok), dev(src), dev(off), q_out, s_out)
+    torch.cuda.synchronize()
+    return host(q_out), host(s_out)
+
+
+@pytest.mark.parametrize("T,H,group", [(16384, 7168, 3), (1000, 1024, 0)])
+def test_permute_pad_parity(F, orc, T, H, group):
+    x = synth.activations_bf16(T, H, 500 + T)
+    q_tok, s_tok = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
+    idx, _ = synth.routing(T, 501 + T)
+    sh = synth.expert_shard(idx, torch.zeros(idx.shape), group, 8)
+    q_recv = np.ascontiguousarray(q_tok[sh.recv_tokens])
+    s_recv = np.ascontiguousarray(s_tok[:, sh.recv_tokens])
+    rm, src, off = orc.permute_plan(sh.topk_idx, sh.expert_begin, sh.num_local_experts)
+    max_rows = (len(src) + 15) // 16 * 16
+    src_p = np.full(max_rows, -1, np.int32)
+    src_p[: len(src)] = src
+    qo, so = run_move(F, q_recv, s_recv, src_p, off, max_rows)
+    qo_ref, so_ref = orc.permute_pad(q_recv, s_recv, src_p, off, max_rows=max_rows)
+    R = int(off[-1])
+    assert np.array_equal(qo[:R], qo_ref[:R]) and np.array_equal(so[:, :R], so_ref[:, :R])
+    assert np.all(qo[R:] == 0xEE)                                        # rows >= R untouched
+
+
+# =========================================================================================== A4
+@pytest.mark.parametrize("with_probs", [True, False])
+@pytest.mark.parametrize("T,H,K,E_loc", [(2000, 7168, 8, 32), (300, 256, 4, 16), (64, 1024, 16, 64)])
+def test_unpermute_parity(F, orc, T, H, K, E_loc, with_probs):
+    idx, probs = synth.routing(T, 600 + T, num_experts=max(E_loc * 2, K * 2), top_k=K,
+                               num_groups=4, topk_groups=4)
+    rm, src, off = orc.permute_plan(idx.numpy(), 0, E_loc)
+    R = int(off[-1])
+    xb = synth.bf16_bits(synth.normal_bf16(max(R, 1), H, 601))
+    p = probs.numpy() if with_probs else None
+    y_ref = orc.unpermute(xb, rm, p)
+    y = torch.empty(T, H, dtype=torch.bfloat16, device="cuda")
+    F.fp8flow_unpermute_unpad(bf16_dev(xb), dev(rm), dev(p) if with_probs else None, y)
+    torch.cuda.synchronize()
+    assert np.array_equal(host(y.view(torch.int16)).view(np.uint16), y_ref)
+
+
+# =========================================================================================== A5
+def run_swiglu(F, h_bits, rows_dev=None, ld_s=None):
+    rows, F2 = h_bits.shape
+    ld_s = ld_s or ((rows + 15) // 16 * 16)
+    q = torch.empty(rows, F2 // 2, dtype=torch.uint8, device="cuda")
+    s = torch.full((F2 // 256, ld_s), 0xAB, dtype=torch.uint8, device="cuda")
+    F.fp8flow_swiglu_quant(bf16_dev(h_bits), q, s, rows_dev=None if rows_dev is None else dev(rows_dev))
+    torch.cuda.synchronize()
+    return host(q), host(s)
+
+
+def check_swiglu(q, s, q_ref, s_ref, rows):
+    assert np.array_equal(s[:, :rows], s_ref[:, :rows])                  # identical scales
+    d = e4m3_ulp_dist(q[:rows], q_ref[:rows])
+    assert d.max(initial=0) <= 1
+    assert np.mean(d > 0) <= 1e-4
+
+
+@pytest.mark.parametrize("rows,ffn,sigma", [(256, 256, 1.5), (100, 2048, 1.5), (2048, 2048, 4.0),
+                                            (16640, 2048, 1.5)])
+def test_swiglu_quant_parity(F, orc, rows, ffn, sigma):
+    hb = synth.bf16_bits(synth.normal_bf16(rows, 2 * ffn, 700 + rows, sigma=sigma))
+    q, s = run_swiglu(F, hb)
+    q_ref, s_ref = orc.swiglu_quant(hb, ld_s=s.shape[1])
+    check_swiglu(q, s, q_ref, s_ref, rows)
+
+
+def test_swiglu_quant_near_boundaries_and_wild(F, orc):
+    """Tiles whose SwiGLU amax sits at 448*2^T within a few ulp, huge |a| (exp overflow range),
+    tiny products (subnormal range), zeros and PAD rows."""
+    rows, ffn = 64, 256
+    rng = np.random.default_rng(5)
+    a = rng.normal(0, 1.5, (rows, ffn)).astype(np.float32)
+    b = rng.normal(0, 1.5, (rows, ffn)).astype(np.float32)
+    # a = 20: silu(a) = a (1 - 2e-9); b chosen so that a*b lands near 448*2^T * (1 +- eps)
+    for i in range(0, 32):
+        T = int(rng.integers(-6, 6))
+        a[i, 7] = 20.0
+        b[i, 7] = 448.0 * 2.0 ** T / 20.0 * (1 + (i - 16) * 2.0 ** -8)
+    a[40, :] = -100.0
+    a[41, :] = 90.0
+    a[42, :], b[42, :] = 1e-20, 1e-20
+    a[43, :], b[43, :] = 0.0, 0.0
+    h = np.concatenate([a, b], axis=1)
+    hb = synth.bf16_bits(torch.from_numpy(h).to(torch.bfloat16))
+    q, s = run_swiglu(F, hb)
+    q_ref, s_ref = orc.swiglu_quant(hb, ld_s=s.shape[1])
+    check_swiglu(q, s, q_ref, s_ref, rows)
+
+
+def test_swiglu_quant_rows_dev(F, orc):
+    rows_max, ffn, rows = 256, 512, 176
+    hb = synth.bf16_bits(synth.normal_bf16(rows_max, 2 * ffn, 9, sigma=1.5))
+    q, s = run_swiglu(F, hb, rows_dev=np.array([rows], np.int32))
+    q_ref, s_ref = orc.swiglu_quant(hb[:rows], ld_s=s.shape[1])
+    check_swiglu(q, s, q_ref, s_ref, rows)
+    assert np.all(s[:, rows:] == 0xAB)
+
+
+# =========================================================================================== checksum
+def test_checksum_matches_oracle(F, orc):
+    rng = np.random.default_rng(1)
+    for n in (16, 1000 * 16, 12345 * 16 + 16):
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        F.fp8flow_checksum64(dev(b), out)
+        torch.cuda.synchronize()
+        got = int(np.array(out.cpu().numpy()).view(np.uint64)[0])
+        assert got == orc.checksum64(b)
