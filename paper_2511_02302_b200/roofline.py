@@ -1,0 +1,65 @@
+"""Algorithmic byte counts per launch of each hot-path op.
+
+These are the bytes the method must move (inputs read once, outputs written once), not what a
+particular kernel happens to move; achieved GB/s = these bytes / measured kernel time, and the
+roofline fraction divides by the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+Scales are UE8M0: one byte per 128 elements.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+
+def quantize_bytes(rows: int, cols: int) -> int:
+    """A1: BF16 read (2 B) + E4M3 write (1 B) + one scale byte per 1x128 tile."""
+    return rows * cols * 3 + rows * (cols // 128)
+
+
+def transpose_bytes(seg_lengths, cols: int) -> int:
+    """A2: codes + row scales read for the rows inside segments, codes written once, one output
+    scale byte per (128-row block, column) of each segment."""
+    m = sum(seg_lengths)
+    blocks = sum((x + 127) // 128 for x in seg_lengths)
+    return m * cols + m * (cols // 128) + m * cols + blocks * cols
+
+
+def naive_transpose_actual_bytes(seg_lengths, cols: int) -> int:
+    """The comparator's own traffic: dequant (1 + 1/128 -> 2), BF16 transpose (2 -> 2),
+    column-wise quantize (2 -> 1 + scales)."""
+    m = sum(seg_lengths)
+    blocks = sum((x + 127) // 128 for x in seg_lengths)
+    return m * cols * (1 + 2) + m * (cols // 128) + m * cols * (2 + 2) + m * cols * (2 + 1) + blocks * cols
+
+
+def permute_plan_bytes(num_tokens: int, top_k: int, padded_rows: int) -> int:
+    """A3 plan: topk_idx read, row_map written, src_of_row written (int32 each)."""
+    return num_tokens * top_k * 4 * 2 + padded_rows * 4
+
+
+def permute_move_bytes(unique_src_rows: int, padded_rows: int, hidden: int) -> int:
+    """A3 move: each source token's codes + scales read once, every output row (incl. PAD) written,
+    src_of_row read."""
+    row = hidden + hidden // 128
+    return unique_src_rows * row + padded_rows * row + padded_rows * 4
+
+
+def unpermute_bytes(valid_rows: int, num_tokens: int, top_k: int, hidden: int, with_probs: bool = True) -> int:
+    """A4: every non-PAD BF16 row read once, every token's BF16 output written, row_map (+ probs)."""
+    return valid_rows * hidden * 2 + num_tokens * hidden * 2 + num_tokens * top_k * (4 + (4 if with_probs else 0))
+
+
+def swiglu_quant_bytes(rows: int, ffn: int) -> int:
+    """A5: BF16 [rows, 2F] read, E4M3 [rows, F] written, one scale byte per 1x128 output tile."""
+    return rows * (4 * ffn + ffn + ffn // 128)
+
+
+def measured_peaks(root: str) -> dict:
+    """HBM copy bandwidth to use as the roofline denominator: the driver-measured figure when
+    MEASURED_PEAKS.json exists, else the profiling guide's fallback (6650 GB/s)."""
+    path = os.path.join(root, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}

@@ -172,7 +172,7 @@ def test_naive_transpose_parity(F, orc, rows, cols):
     x = synth.activations_bf16(rows, cols, 300 + rows)
     q, s = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
     check_transpose(F, orc, q, s, naive=True)
-    m = [16, 128, 144, 0, rows - 288]
+    m = [16, 128, 0, rows - 144]
     seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
     check_transpose(F, orc, q, s, seg, naive=True)
 
