@@ -1,0 +1,555 @@
+#!/usr/bin/env python
+"""bench.py -- FP8-Flow-MoE hot path on B200: scaling-aware transpose + quantize GB/s.
+
+One STEP = one pass of the whole hot path for one expert-parallel
+rank of a DeepSeek-V3 MoE layer (16384 tokens, top-8 of 256 experts, hidden 7168, expert FFN
+2x2048; the rank owns expert group g = rank mod 8, i.e. 32 experts, the EP8 partition):
+
+    A1  quantize the rank's 2048-token BF16 shard (forward entry cast)
+    A3  permute plan (3 kernels) + fused permute/pad move of the received FP8 tokens
+    A5  fused SwiGLU + quant of the fc1 output [R, 4096]
+    A4  fused unpermute + unpad of the fc2 output [R, 7168] with gate probs
+    A1  quantize the rank's 2048-token BF16 output gradient dY (backward entry cast)
+    A2  scaling-aware transpose of X_perm [R, 7168] and of A [R, 2048], segments = experts (Alg. 1)
+
+Inputs are synthetic (synth/, seeded) and resident in HBM; the L2 is flushed (256 MiB write)
+before every step, outside the timed events.  All kernels of a step are enqueued while the
+stream is held by a short spin kernel, so the events measure back-to-back GPU execution.
+value = algorithmic bytes of all ranks' steps / max-over-ranks time (GB/s); weak scaling (every
+rank owns one expert group).  N > 1: launch under torchrun (one process per GPU, NCCL used only
+after timing).  `--impl reference` times the CPU oracle on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2511_02302_b200 import dist as D  # noqa: E402
+from paper_2511_02302_b200 import roofline as RL  # noqa: E402
+
+METRIC = "scaling-aware transpose + quantize GB/s and % of HBM peak at 1/2/4/8 B200"
+T_GLOBAL, HIDDEN, FFN, N_EXPERTS, TOP_K, ALIGN = 16384, synth.HIDDEN, synth.FFN, synth.NUM_EXPERTS, synth.TOP_K, 16
+KERNELS_PER_STEP = 10   # A1, plan x3, move, A5, A4, A1(dY), A2 x2
+OPS = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
+       "A2_transpose_xperm", "A2_transpose_a"]
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# =============================================================================================
+# workload (host side, seeded)
+# =============================================================================================
+class HostWorkload:
+    """Everything one rank's step consumes, on the host (numpy / CPU torch)."""
+
+    def __init__(self, group: int):
+        t0 = time.time()
+        self.group = group
+        idx, probs = synth.routing(T_GLOBAL, synth.BASE_SEED)
+        sh = synth.expert_shard(idx, probs, group, D.NUM_GROUPS)
+        self.e0, self.E_loc = sh.expert_begin, sh.num_local_experts
+        self.recv = sh.recv_tokens
+        self.topk_idx = sh.topk_idx                      # [T_recv, 8] int32
+        self.probs = sh.probs                            # [T_recv, 8] fp32
+        self.T_recv = len(self.recv)
+        # the layer's input activations; the received tokens are what dispatch would deliver
+        x_full = synth.activations_bf16(T_GLOBAL, HIDDEN, synth.BASE_SEED + 1)
+        tok0 = (T_GLOBAL // D.NUM_GROUPS) * group
+        self.x_shard = x_full[tok0: tok0 + T_GLOBAL // D.NUM_GROUPS].contiguous()
+        self.x_recv = x_full[torch.from_numpy(self.recv)].contiguous()
+        del x_full
+        self.dy_shard = synth.activations_bf16(T_GLOBAL // D.NUM_GROUPS, HIDDEN, synth.BASE_SEED + 2 + group)
+        counts = np.array([np.sum(self.topk_idx == self.e0 + e) for e in range(self.E_loc)])
+        self.counts = counts
+        self.padded = (counts + ALIGN - 1) // ALIGN * ALIGN
+        self.R = int(self.padded.sum())                  # padded rows of this rank
+        self.valid_rows = int(counts.sum())
+        self.h = synth.normal_bf16(self.R, 2 * FFN, synth.BASE_SEED + 3 + group, sigma=1.5)
+        self.y = synth.normal_bf16(self.R, HIDDEN, synth.BASE_SEED + 4 + group)
+        log(f"[bench] group {group}: T_recv={self.T_recv} R={self.R} valid={self.valid_rows} "
+            f"(host inputs in {time.time() - t0:.1f}s)")
+
+    def zero_pad_rows(self, src_of_row: np.ndarray) -> None:
+        """fc1/fc2 outputs of PAD rows are GEMM outputs of zero rows: zero them."""
+        pad = torch.from_numpy(src_of_row[: self.R] < 0)
+        self.h[pad] = 0
+        self.y[pad] = 0
+
+    def op_bytes(self) -> dict:
+        seg = [int(x) for x in self.padded]
+        n_shard = T_GLOBAL // D.NUM_GROUPS
+        return {
+            "A1_quantize_x": RL.quantize_bytes(n_shard, HIDDEN),
+            "A3_plan": RL.permute_plan_bytes(self.T_recv, TOP_K, self.R),
+            "A3_move": RL.permute_move_bytes(self.T_recv, self.R, HIDDEN),
+            "A5_swiglu_quant": RL.swiglu_quant_bytes(self.R, FFN),
+            "A4_unpermute": RL.unpermute_bytes(self.valid_rows, self.T_recv, TOP_K, HIDDEN, True),
+            "A1_quantize_dy": RL.quantize_bytes(n_shard, HIDDEN),
+            "A2_transpose_xperm": RL.transpose_bytes(seg, HIDDEN),
+            "A2_transpose_a": RL.transpose_bytes(seg, FFN),
+        }
+
+
+# =============================================================================================
+# device side
+# =============================================================================================
+class DeviceStep:
+    def __init__(self, hw: HostWorkload, device: torch.device):
+        from paper_2511_02302_b200 import fp8flow as F
+
+        self.F, self.hw, self.dev = F, hw, device
+        F.fp8flow_device_check()
+        T, R, E = hw.T_recv, hw.R, hw.E_loc
+        n_shard = T_GLOBAL // D.NUM_GROUPS
+        u8, i32 = torch.uint8, torch.int32
+        z = lambda *s, dt=u8: torch.empty(*s, dtype=dt, device=device)  # noqa: E731
+        # inputs (resident)
+        self.x_shard = hw.x_shard.to(device)
+        self.dy_shard = hw.dy_shard.to(device)
+        self.topk = torch.from_numpy(hw.topk_idx).to(device)
+        self.probs = torch.from_numpy(hw.probs).to(device)
+        x_recv = hw.x_recv.to(device)
+        self.q_recv = z(T, HIDDEN)
+        self.s_recv = z(HIDDEN // 128, (T + 15) // 16 * 16)
+        F.fp8flow_quantize_rowwise(x_recv, self.q_recv, self.s_recv)   # setup: dispatch payload
+        del x_recv
+        # outputs
+        self.q_x, self.s_x = z(n_shard, HIDDEN), z(HIDDEN // 128, n_shard)
+        self.q_dy, self.s_dy = z(n_shard, HIDDEN), z(HIDDEN // 128, n_shard)
+        self.row_map, self.src, self.off = z(T, TOP_K, dt=i32), z(R, dt=i32), z(E + 1, dt=i32)
+        self.ws = z(F.fp8flow_permute_workspace_bytes(T, TOP_K, E))
+        self.x_perm, self.s_perm = z(R, HIDDEN), z(HIDDEN // 128, R)
+        self.q_a, self.s_a = z(R, FFN), z(FFN // 128, R)
+        self.y_tok = z(T, HIDDEN, dt=torch.bfloat16)
+        self.xT, self.sxT = z(R * HIDDEN), z(R // 128 + E, HIDDEN)
+        self.aT, self.saT = z(R * FFN), z(R // 128 + E, FFN)
+        # plan once at setup to zero the PAD rows of the synthetic GEMM outputs
+        F.fp8flow_permute_plan(self.topk, hw.e0, E, ALIGN, self.row_map, self.src, self.off, self.ws)
+        torch.cuda.synchronize(device)
+        assert int(self.off[-1].item()) == R and int(self.ws[:4].view(torch.int32).item()) == 0
+        hw.zero_pad_rows(self.src.cpu().numpy())
+        self.h = hw.h.to(device)
+        self.y = hw.y.to(device)
+        self.l2_flush = torch.empty(256 << 20, dtype=u8, device=device)
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(len(OPS) + 1)]
+
+    def launch_ops(self, record: bool) -> None:
+        F, hw, ev = self.F, self.hw, self.events
+        if record:
+            ev[0].record()
+        F.fp8flow_quantize_rowwise(self.x_shard, self.q_x, self.s_x)
+        if record:
+            ev[1].record()
+        F.fp8flow_permute_plan(self.topk, hw.e0, hw.E_loc, ALIGN, self.row_map, self.src, self.off, self.ws)
+        if record:
+            ev[2].record()
+        F.fp8flow_permute_pad(self.q_recv, self.s_recv, self.src, self.off, self.x_perm, self.s_perm)
+        if record:
+            ev[3].record()
+        F.fp8flow_swiglu_quant(self.h, self.q_a, self.s_a, rows_dev=self.off[hw.E_loc:])
+        if record:
+            ev[4].record()
+        F.fp8flow_unpermute_unpad(self.y, self.row_map, self.probs, self.y_tok)
+        if record:
+            ev[5].record()
+        F.fp8flow_quantize_rowwise(self.dy_shard, self.q_dy, self.s_dy)
+        if record:
+            ev[6].record()
+        F.fp8flow_scaling_aware_transpose(self.x_perm, self.s_perm, self.xT, self.sxT, seg_offsets=self.off)
+        if record:
+            ev[7].record()
+        F.fp8flow_scaling_aware_transpose(self.q_a, self.s_a, self.aT, self.saT, seg_offsets=self.off)
+        if record:
+            ev[8].record()
+
+    def timed_step(self) -> list[float]:
+        """L2 flush, hold the stream, enqueue the step with events, release; returns per-op ms."""
+        self.l2_flush.zero_()
+        torch.cuda._sleep(2_000_000)   # ~1 ms spin: the whole step is enqueued before it runs
+        self.launch_ops(record=True)
+        self.events[-1].synchronize()
+        return [self.events[i].elapsed_time(self.events[i + 1]) for i in range(len(OPS))]
+
+    def outputs(self) -> dict:
+        return {"q_x": self.q_x, "s_x": self.s_x, "x_perm": self.x_perm, "s_perm": self.s_perm, "q_a": self.q_a,
+                "s_a": self.s_a, "y_tok": self.y_tok, "q_dy": self.q_dy, "s_dy": self.s_dy, "xT": self.xT,
+                "sxT": self.sxT, "aT": self.aT, "saT": self.saT}
+
+    def checksums(self) -> list[int]:
+        out = torch.zeros(len(self.outputs()), dtype=torch.int64, device=self.dev)
+        for i, t in enumerate(self.outputs().values()):
+            self.F.fp8flow_checksum64(t, out[i:i + 1])
+        return [int(v) & ((1 << 64) - 1) for v in out.cpu().tolist()]
+
+
+# =============================================================================================
+# end to end through the C ABI with host buffers
+# =============================================================================================
+def run_e2e(ds: DeviceStep, steps: int) -> dict:
+    """Per step: H2D of every input from pinned host memory, the step, output checksums, D2H of
+    the checksums (the step's verification result).  Timed with CUDA events on the stream."""
+    hw = ds.hw
+    host_in = {
+        "x_shard": hw.x_shard, "dy_shard": hw.dy_shard, "topk": torch.from_numpy(hw.topk_idx),
+        "probs": torch.from_numpy(hw.probs), "q_recv": ds.q_recv.cpu(), "s_recv": ds.s_recv.cpu(),
+        "h": hw.h, "y": hw.y,
+    }
+    pinned = {k: v.contiguous().pin_memory() for k, v in host_in.items()}
+    dev_in = {"x_shard": ds.x_shard, "dy_shard": ds.dy_shard, "topk": ds.topk, "probs": ds.probs,
+              "q_recv": ds.q_recv, "s_recv": ds.s_recv, "h": ds.h, "y": ds.y}
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    n_out = len(ds.outputs())
+    res_dev = torch.zeros(n_out, dtype=torch.int64, device=ds.dev)
+    res_host = torch.zeros(n_out, dtype=torch.int64).pin_memory()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for it in range(steps + 1):
+        ds.l2_flush.zero_()
+        torch.cuda.synchronize(ds.dev)
+        s.record()
+        for k, t in pinned.items():
+            dev_in[k].copy_(t, non_blocking=True)
+        ds.launch_ops(record=False)
+        for i, t in enumerate(ds.outputs().values()):
+            ds.F.fp8flow_checksum64(t, res_dev[i:i + 1])
+        res_host.copy_(res_dev, non_blocking=True)
+        e.record()
+        e.synchronize()
+        if it > 0:
+            times.append(s.elapsed_time(e))
+    ms = statistics.mean(times)
+    return {"ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": n_out * 8}
+
+
+# =============================================================================================
+# parity of the timed outputs against the oracle (sampled; after timing)
+# =============================================================================================
+def verify(ds: DeviceStep) -> dict:
+    import oracle as O
+
+    hw, res = ds.hw, {}
+    host = lambda t: t.cpu().numpy()  # noqa: E731
+    bits = synth.bf16_bits
+    rows = np.r_[0:64, len(hw.x_shard) - 64:len(hw.x_shard)]
+    for name, x, q, s in (("A1_quantize_x", hw.x_shard, ds.q_x, ds.s_x), ("A1_quantize_dy", hw.dy_shard, ds.q_dy, ds.s_dy)):
+        qr, sr = O.quantize_rowwise_bf16(bits(x)[rows])
+        res[name] = bool(np.array_equal(host(q)[rows], qr) and np.array_equal(host(s)[:, rows], sr))
+    rm, src, off = O.permute_plan(hw.topk_idx, hw.e0, hw.E_loc, max_rows=hw.R)
+    res["A3_plan"] = bool(np.array_equal(host(ds.row_map), rm) and np.array_equal(host(ds.off), off)
+                          and np.array_equal(host(ds.src), src))
+    q_recv, s_recv = host(ds.q_recv), host(ds.s_recv)
+    qo, so = O.permute_pad(q_recv, s_recv, src, off, max_rows=hw.R)
+    res["A3_move"] = bool(np.array_equal(host(ds.x_perm), qo) and np.array_equal(host(ds.s_perm), so))
+    sample = np.r_[0:256, hw.R - 256:hw.R]
+    qa, sa = O.swiglu_quant(bits(hw.h)[sample])
+    q_a, s_a = host(ds.q_a)[sample], host(ds.s_a)[:, sample]
+    ulp = lambda c: np.where(c < 0x80, c & 0x7F, -(c.astype(np.int32) & 0x7F))  # noqa: E731
+    d = np.abs(ulp(q_a.astype(np.int32)) - ulp(qa.astype(np.int32)))
+    res["A5_swiglu_quant"] = bool(np.array_equal(s_a, sa) and d.max() <= 1 and np.mean(d > 0) <= 1e-4)
+    toks = np.r_[0:128, hw.T_recv - 128:hw.T_recv]
+    y_ref = O.unpermute(bits(hw.y), rm[toks], hw.probs[toks])
+    res["A4_unpermute"] = bool(np.array_equal(host(ds.y_tok.view(torch.int16))[toks].view(np.uint16), y_ref))
+    # A2 on three experts (first, middle, last), each checked as its own segment
+    for name, qsrc, ssrc, qT, sT, cols in (("A2_transpose_xperm", qo, so, ds.xT, ds.sxT, HIDDEN),
+                                           ("A2_transpose_a", host(ds.q_a), host(ds.s_a), ds.aT, ds.saT, FFN)):
+        ok = True
+        qT_h, sT_h = host(qT), host(sT)
+        tiles = np.concatenate([[0], np.cumsum((np.diff(off) + 127) // 128)])
+        for e in (0, hw.E_loc // 2, hw.E_loc - 1):
+            o, m = int(off[e]), int(off[e + 1] - off[e])
+            if m == 0:
+                continue
+            qr, sr = O.scaling_aware_transpose(np.ascontiguousarray(qsrc[o:o + m]), np.ascontiguousarray(ssrc[:, o:o + m]))
+            ok &= np.array_equal(qT_h[cols * o: cols * (o + m)], qr)
+            ok &= np.array_equal(sT_h[tiles[e]: tiles[e + 1]], sr)
+        res[name] = bool(ok)
+    return res
+
+
+# =============================================================================================
+# CPU oracle timing (cpu_baseline and the reference arm)
+# =============================================================================================
+def oracle_sample(hw: HostWorkload, frac: float, threads: int | None) -> tuple[float, float, str]:
+    """Runs the oracle on a bounded sample (fraction `frac` of every op's rows) of this rank's step.
+    Returns (algorithmic bytes of the sample, seconds, description)."""
+    import oracle as O
+
+    bits = synth.bf16_bits
+    n_sh = max(16, int(len(hw.x_shard) * frac) // 16 * 16)
+    n_tok = max(16, int(hw.T_recv * frac))
+    n_rows = max(128, int(hw.R * frac) // 16 * 16)
+    xs, dys = bits(hw.x_shard[:n_sh]), bits(hw.dy_shard[:n_sh])
+    hs, ys = bits(hw.h[:n_rows]), bits(hw.y)
+    x_recv_bits = bits(hw.x_recv[:n_tok])
+    q_tok, s_tok = O.quantize_rowwise_bf16(x_recv_bits)                     # setup (untimed)
+    idx_s = hw.topk_idx[:n_tok]
+    counts = np.array([np.sum(idx_s == hw.e0 + e) for e in range(hw.E_loc)])
+    padded = (counts + ALIGN - 1) // ALIGN * ALIGN
+    R_s = int(padded.sum())
+    t0 = time.perf_counter()
+    O.quantize_rowwise_bf16(xs, threads=threads)
+    rm, src, off = O.permute_plan(idx_s, hw.e0, hw.E_loc, max_rows=R_s)
+    qo, so = O.permute_pad(q_tok, s_tok, src, off, max_rows=R_s, threads=threads)
+    qa, sa = O.swiglu_quant(hs, threads=threads)
+    O.unpermute(ys, rm, hw.probs[:n_tok], threads=threads)
+    O.quantize_rowwise_bf16(dys, threads=threads)
+    O.scaling_aware_transpose(qo, so, off, threads=threads)
+    seg_a = np.array([0, n_rows], np.int32)
+    O.scaling_aware_transpose(qa, sa, seg_a, threads=threads)
+    dt = time.perf_counter() - t0
+    nbytes = (2 * RL.quantize_bytes(n_sh, HIDDEN) + RL.permute_plan_bytes(n_tok, TOP_K, R_s)
+              + RL.permute_move_bytes(n_tok, R_s, HIDDEN) + RL.swiglu_quant_bytes(n_rows, FFN)
+              + RL.unpermute_bytes(int(counts.sum()), n_tok, TOP_K, HIDDEN, True)
+              + RL.transpose_bytes([int(p) for p in padded], HIDDEN) + RL.transpose_bytes([n_rows], FFN))
+    desc = (f"oracle (plain C, fp64) on {frac:.4g} of rank-0's step: A1 {n_sh}x{HIDDEN} x2, A3 plan+move "
+            f"{n_tok} tokens -> {R_s} rows, A5 {n_rows}x{2 * FFN}, A4 {n_tok} tokens, A2 {R_s}x{HIDDEN} + "
+            f"{n_rows}x{FFN}")
+    return nbytes, dt, desc
+
+
+def cpu_cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+# =============================================================================================
+# clocks
+# =============================================================================================
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx, self.proc, self.path = gpu_index, None, f"/tmp/fp8flow_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                try:
+                    rows.append((float(p[1]), float(p[2]), p[5:9]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        load = [r[0] for r in rows if r[0] > 500] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# =============================================================================================
+# config-2 sub-measurement (4096 x 7168, one expert): A1, A2 and the naive comparator
+# =============================================================================================
+def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
+    from paper_2511_02302_b200 import fp8flow as F
+
+    rows, cols = 4096, HIDDEN
+    x = synth.activations_bf16(rows, cols, synth.BASE_SEED + 9).to(device)
+    q = torch.empty(rows, cols, dtype=torch.uint8, device=device)
+    s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=device)
+    qT = torch.empty(rows * cols, dtype=torch.uint8, device=device)
+    sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
+    ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, 1), dtype=torch.uint8, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ops = {"A1_quantize": (lambda: F.fp8flow_quantize_rowwise(x, q, s), RL.quantize_bytes(rows, cols)),
+           "A2_transpose": (lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT), RL.transpose_bytes([rows], cols)),
+           "naive_dequant_transpose_requant": (lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws),
+                                               RL.transpose_bytes([rows], cols))}
+    out = {"shape": [rows, cols], "l2": "flushed before each launch"}
+    for name, (fn, nbytes) in ops.items():
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            torch.cuda._sleep(1_000_000)
+            ev[0].record()
+            fn()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        ms = statistics.median(ts)
+        out[name] = {"us": round(ms * 1e3, 2), "gbs": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / peak, 3)}
+    out["naive_over_direct_latency"] = round(out["naive_dequant_transpose_requant"]["us"] / out["A2_transpose"]["us"], 2)
+    return out
+
+
+# =============================================================================================
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+
+    rank, local_rank, world = D.env()
+    if world != args.gpus:
+        log(f"[bench] WORLD_SIZE={world} but --gpus {args.gpus}; launch N>1 under torchrun")
+        if args.gpus > 1 and world == 1:
+            sys.exit(2)
+    group = D.expert_group(rank)
+    cfg = {"workload": "DeepSeek-V3 MoE layer hot path, one EP8 expert-group shard per GPU (32 of 256 experts), "
+                       "16384 tokens top-8, hidden 7168, expert FFN 2x2048: A1 x2, A3 plan+move, A5, A4, A2 x2",
+           "tokens": T_GLOBAL, "hidden": HIDDEN, "ffn": FFN, "experts": N_EXPERTS, "top_k": TOP_K,
+           "local_experts": N_EXPERTS // D.NUM_GROUPS, "align": ALIGN, "routing": "DSv3 group-limited top-8, "
+           "skewed expert bias N(0,1) + Gumbel, seed 2511023020", "parallelism": f"ep-group shard x{world} (weak)"}
+
+    if args.impl == "reference":
+        run_reference(args, rank, world, group, cfg)
+        return
+
+    D.init("nccl")
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    hw = HostWorkload(group)
+    ds = DeviceStep(hw, device)
+    op_bytes = hw.op_bytes()
+    step_bytes = sum(op_bytes.values())
+    peaks = RL.measured_peaks(ROOT)
+    peak = peaks["hbm_gbs"]
+
+    for _ in range(args.warmup):
+        ds.timed_step()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    D.barrier(device)
+    torch.cuda.synchronize(device)
+    per_step = []
+    for _ in range(args.steps):
+        per_step.append(ds.timed_step())
+    torch.cuda.synchronize(device)
+    D.barrier(device)
+    clk = clocks.stop()
+
+    step_ms = [sum(p) for p in per_step]
+    total_ms = sum(step_ms)
+    max_total_ms = D.max_over_ranks(total_ms, device)
+    all_bytes = D.sum_over_ranks(step_bytes * args.steps, device)
+    value = all_bytes / (max_total_ms / 1e3) / 1e9
+    op_ms = {op: statistics.mean(p[i] for p in per_step) for i, op in enumerate(OPS)}
+    ops = {op: {"us": round(op_ms[op] * 1e3, 2), "bytes": op_bytes[op],
+                "gbs": round(op_bytes[op] / op_ms[op] / 1e6, 1),
+                "frac": round(op_bytes[op] / op_ms[op] / 1e6 / peak, 3),
+                "share": round(op_ms[op] / statistics.mean(step_ms), 3)} for op in OPS}
+    dom = max(OPS, key=lambda o: op_ms[o])
+    traffic = ncu_traffic(dom)
+    cfg.update({"expert_group": group, "recv_tokens": hw.T_recv, "padded_rows": hw.R, "valid_rows": hw.valid_rows,
+                "l2": "flushed before every step (256 MiB write outside the timed events)",
+                "timing": "CUDA events on the launching stream; all kernels of a step enqueued behind a spin "
+                          "kernel so they run back to back"})
+
+    e2e = None
+    if not args.no_e2e:
+        r = run_e2e(ds, min(args.steps, 5))
+        e_ms = D.max_over_ranks(r["ms_per_step"], device)
+        e2e = {"value": round(D.sum_over_ranks(step_bytes, device) / (e_ms / 1e3) / 1e9, 2), "unit": "GB/s",
+               "ms_per_step": round(e_ms, 3), "h2d_bytes_per_step": r["h2d_bytes_per_step"],
+               "d2h_bytes_per_step": r["d2h_bytes_per_step"],
+               "note": "H2D of all step inputs from pinned host memory + the step + checksum kernels + D2H of "
+                       "the output checksums, per step, CUDA events"}
+
+    parity = None if args.no_verify else verify(ds)
+    sums = D.gather_checksums(ds.checksums(), device)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nbytes, secs, desc = oracle_sample(hw, 1.0, None)
+        cpu = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": desc, "seconds": round(secs, 2)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(max_total_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "e4m3",
+            "dtypes": {"codes": "e4m3 (u8)", "scales": "ue8m0 (u8)", "bf16_io": "bf16", "math": "fp32 (fp64 refine)"},
+            "data": "synthetic (seeded; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
+            "frac_of_hbm_peak": round(value / world / peak, 3),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ops[dom]["gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": ops[dom]["frac"], "traffic": traffic, "peak_source": peaks["source"],
+                         "algorithmic_bytes_per_launch": op_bytes[dom]},
+            "ops": ops, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": KERNELS_PER_STEP * args.steps,
+            "clocks": clk, "parity": parity,
+            "checksums": {f"rank{r}": f"{(sum(c) & ((1 << 64) - 1)):016x}" for r, c in enumerate(sums)},
+        }
+        if world == 1:
+            line["cfg2"] = cfg2_measure(device, peak)
+        print(json.dumps(line), flush=True)
+    D.barrier(device)
+    if D.dist.is_initialized():
+        D.dist.destroy_process_group()
+
+
+def ncu_traffic(kernel_op: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    v = d.get(kernel_op)
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+
+
+def run_reference(args, rank, world, group, cfg):
+    """The reference arm: the CPU oracle as it stands, on host cores, each step a bounded sample."""
+    if rank != 0:
+        return
+    hw = HostWorkload(group)
+    frac = 1.0 / 8
+    for _ in range(args.warmup):
+        oracle_sample(hw, frac, None)
+    nb, ts, desc = 0.0, 0.0, ""
+    for _ in range(args.steps):
+        b, t, desc = oracle_sample(hw, frac, None)
+        nb, ts = nb + b, ts + t
+    v = nb / ts / 1e9
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ts / args.steps * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "impl": "reference",
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
