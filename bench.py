@@ -12,7 +12,7 @@ rank of a DeepSeek-V3 MoE layer (16384 tokens, top-8 of 256 experts, hidden 7168
     A1  quantize the rank's 2048-token BF16 output gradient dY (backward entry cast)
     A2  scaling-aware transpose of X_perm [R, 7168] and of A [R, 2048], segments = experts (Alg. 1)
 
-Inputs are synthetic (synth/, seeded) and resident in HBM; the L2 is flushed (256 MiB write)
+Inputs are synthetic (synth/, seeded) and resident in HBM; the L2 is flushed (256 MiB write + 256 MiB read)
 before every step, outside the timed events.  All kernels of a step are enqueued while the
 stream is held by a short spin kernel, so the events measure back-to-back GPU execution.
 value = algorithmic bytes of all ranks' steps / max-over-ranks time (GB/s); weak scaling (every
@@ -145,6 +145,7 @@ class DeviceStep:
         self.h = hw.h.to(device)
         self.y = hw.y.to(device)
         self.l2_flush = torch.empty(256 << 20, dtype=u8, device=device)
+        self.l2_clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(len(OPS) + 1)]
 
     def launch_ops(self, record: bool) -> None:
@@ -176,9 +177,16 @@ class DeviceStep:
         if record:
             ev[8].record()
 
+    def flush_l2(self) -> None:
+        """Write a 256 MiB buffer (evicts everything), then read another 256 MiB buffer so the L2 is
+        left holding CLEAN unrelated lines: the timed kernels neither hit in L2 nor pay the
+        write-back of the flush buffer's dirty lines."""
+        self.l2_flush.zero_()
+        self.l2_clean.sum()
+
     def timed_step(self) -> list[float]:
         """L2 flush, hold the stream, enqueue the step with events, release; returns per-op ms."""
-        self.l2_flush.zero_()
+        self.flush_l2()
         torch.cuda._sleep(2_000_000)   # ~1 ms spin: the whole step is enqueued before it runs
         self.launch_ops(record=True)
         self.events[-1].synchronize()
@@ -218,7 +226,7 @@ def run_e2e(ds: DeviceStep, steps: int) -> dict:
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     for it in range(steps + 1):
-        ds.l2_flush.zero_()
+        ds.flush_l2()
         torch.cuda.synchronize(ds.dev)
         s.record()
         for k, t in pinned.items():
@@ -383,17 +391,19 @@ def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
     sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
     ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, 1), dtype=torch.uint8, device=device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ops = {"A1_quantize": (lambda: F.fp8flow_quantize_rowwise(x, q, s), RL.quantize_bytes(rows, cols)),
            "A2_transpose": (lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT), RL.transpose_bytes([rows], cols)),
            "naive_dequant_transpose_requant": (lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws),
                                                RL.transpose_bytes([rows], cols))}
-    out = {"shape": [rows, cols], "l2": "flushed before each launch"}
+    out = {"shape": [rows, cols], "l2": "flushed before each launch (256 MiB write + 256 MiB read)"}
     for name, (fn, nbytes) in ops.items():
         fn()
         ts = []
         for _ in range(reps):
             flush.zero_()
+            clean.sum()
             torch.cuda._sleep(1_000_000)
             ev[0].record()
             fn()
@@ -471,7 +481,8 @@ def main():
     dom = max(OPS, key=lambda o: op_ms[o])
     traffic = ncu_traffic(dom)
     cfg.update({"expert_group": group, "recv_tokens": hw.T_recv, "padded_rows": hw.R, "valid_rows": hw.valid_rows,
-                "l2": "flushed before every step (256 MiB write outside the timed events)",
+                "l2": "flushed before every step outside the timed events: 256 MiB write, then a 256 MiB "
+                      "read so the L2 holds clean unrelated lines",
                 "timing": "CUDA events on the launching stream; all kernels of a step enqueued behind a spin "
                           "kernel so they run back to back"})
 

@@ -2,12 +2,21 @@
 // architecture check, status codes, and dispatch to the sm_100a kernels.  No compute happens on
 // the host and there is no fallback path.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/fp8flow.h"
 #include "kernels.h"
 
 using namespace fp8flow;
+
+int fp8flow::sched_for(const char* op, int tuned_default) {
+  char name[64] = "FP8FLOW_SCHED_";
+  strncat(name, op, sizeof(name) - strlen(name) - 1);
+  const char* v = getenv(name);
+  if (v && v[0] >= '0' && v[0] <= '2' && v[1] == 0) return v[0] - '0';
+  return tuned_default;
+}
 
 namespace {
 

@@ -63,6 +63,23 @@ __device__ __forceinline__ float scale_from_byte(uint32_t byte) {
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+// Warp-level work-item schedules (all items are independent):
+//   kSchedOnePerWarp  : one item per warp, grid = ceil(items / warps per CTA); the hardware CTA
+//                       scheduler balances (short-lived CTAs, no tail beyond one item)
+//   kSchedBlocked     : one wave of CTAs, warp g takes the contiguous range [g*n/W, (g+1)*n/W)
+//   kSchedInterleaved : one wave of CTAs, warp g takes items g, g+W, g+2W, ...
+enum Sched : int { kSchedOnePerWarp = 0, kSchedBlocked = 1, kSchedInterleaved = 2 };
+struct ItemIter {
+  int64_t cur, end, step;
+};
+__device__ __forceinline__ ItemIter warp_item_iter(int64_t n_items, int sched) {
+  const int64_t wpb = blockDim.x >> 5;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * wpb;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * wpb + (threadIdx.x >> 5);
+  if (sched == kSchedBlocked) return {g * n_items / W, (g + 1) * n_items / W, 1};
+  return {g, n_items, W};
+}
+
 // half-warp (16 lanes) max reduction; every lane of the half receives the result
 __device__ __forceinline__ uint32_t halfwarp_max_u32(uint32_t v) {
   v = max(v, __shfl_xor_sync(0xffffffffu, v, 8));
@@ -73,35 +90,45 @@ __device__ __forceinline__ uint32_t halfwarp_max_u32(uint32_t v) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Exponent shift of 4 packed codes by the same k >= 0 (derivation after Eq. 11):
-// result = E4M3_RNE(decode(c) * 2^-k).  Fast path: every nonzero code stays normal (E > k), so
-// the result is the exponent-field edit c - (k << 3) per byte.  Otherwise: exact f16 route --
-// e4m3 -> f16 (exact), multiply by 2^-min(k,24) in f16 (exact unless the product is < 2^-24,
-// in which case the E4M3 result is +-0 either way), then one RNE cvt back to E4M3.
+// Exponent shift of 4 packed codes of one row by the same k >= 0 (derivation after Eq. 11,
+// P:186-198): result = E4M3_RNE(decode(c) * 2^-k) -- the exponent edit E' = E - k whenever the
+// result stays normal, RNE into the subnormal grid otherwise (R7).
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t f16_pow2_neg(uint32_t k) {
-  // f16 bit pattern of 2^-k for k in [0, 24]
-  return k <= 14u ? ((15u - k) << 10) : (1u << (24u - k));
+// Branch-free.  The 7 magnitude bits of an E4M3 code placed at bits 7..13 of an f16 are the f16
+// whose value is decode(code) * 2^-8 -- for normal AND subnormal codes (E4M3's subnormal grid
+// 2^-9 maps onto f16 multiples of 2^-17, which f16 represents exactly).  So the up-conversion is
+// a mask + shift (bytes 0,2 and bytes 1,3 form two f16x2), the rescale by 2^(8-k) is one HMUL2
+// per pair (exact whenever the E4M3 result can be nonzero), and the single RNE rounding is the
+// hardware cvt.rn.satfinite f16x2 -> e4m3x2 on magnitudes; the sign bits are re-attached
+// unchanged (so an underflow to zero keeps its sign, R10).
+__device__ __forceinline__ uint32_t f16x2_pow2(int e) {
+  // f16x2 with both halves = 2^e, e in [-24, 8] (normal for e >= -14, subnormal below)
+  const uint32_t h = e >= -14 ? static_cast<uint32_t>(e + 15) << 10 : (1u << (e + 24));
+  return h | (h << 16);
 }
-static __device__ __noinline__ uint32_t shift4_slow(uint32_t w, uint32_t k) {
-  uint32_t kk = k > 24u ? 24u : k;
-  uint32_t m = f16_pow2_neg(kk);
-  __half2 mul = __halves2half2(__ushort_as_half(static_cast<unsigned short>(m)),
-                               __ushort_as_half(static_cast<unsigned short>(m)));
-  uint32_t lo = cvt_f16x2_from_e4m3x2(w & 0xFFFFu);
-  uint32_t hi = cvt_f16x2_from_e4m3x2(w >> 16);
-  __half2 l2 = __hmul2(*reinterpret_cast<__half2*>(&lo), mul);
-  __half2 h2 = __hmul2(*reinterpret_cast<__half2*>(&hi), mul);
-  uint32_t rl = cvt_e4m3x2_from_f16x2(*reinterpret_cast<uint32_t*>(&l2));
-  uint32_t rh = cvt_e4m3x2_from_f16x2(*reinterpret_cast<uint32_t*>(&h2));
-  return (rl & 0xFFFFu) | (rh << 16);
+// multiplier for shift4: 2^(8-k) as f16x2, k >= 0 (k > 32 behaves like k = 32: all results +-0)
+__device__ __forceinline__ uint32_t shift_multiplier(uint32_t k) {
+  const int e = 8 - static_cast<int>(k > 32u ? 32u : k);
+  return f16x2_pow2(e < -24 ? -24 : e);
 }
-__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t k) {
-  uint32_t e4 = (w >> 3) & 0x0F0F0F0Fu;
-  uint32_t gt = __vcmpgtu4(e4, k * 0x01010101u);           // 0xFF where E > k (k <= 255)
-  uint32_t nz = __vcmpne4(w & 0x7F7F7F7Fu, 0u);             // 0xFF where the code is not +-0
-  if ((nz & ~gt) == 0u) return w - (((k & 31u) << 3) * 0x01010101u & gt);
-  return shift4_slow(w, k);
+// two f16x2 (bytes 0,2 and 1,3) -> 4 E4M3 codes in byte order 0,1,2,3
+__device__ __forceinline__ uint32_t cvt_e4m3x4_from_f16x2_pairs(uint32_t p02, uint32_t p13) {
+  uint32_t r;
+  asm("{\n\t.reg .b16 lo, hi;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f16x2 lo, %1;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f16x2 hi, %2;\n\t"
+      "mov.b32 %0, {lo, hi};\n\t}"
+      : "=r"(r)
+      : "r"(p02), "r"(p13));
+  return __byte_perm(r, 0u, 0x3120);  // [c0, c2, c1, c3] -> [c0, c1, c2, c3]
+}
+__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t m2) {
+  const uint32_t lo02 = (w & 0x007F007Fu) << 7;            // bytes 0, 2 -> f16 halves (value * 2^-8)
+  const uint32_t hi13 = (w >> 1) & 0x3F803F80u;            // bytes 1, 3
+  __half2 p02 = __hmul2(*reinterpret_cast<const __half2*>(&lo02), *reinterpret_cast<const __half2*>(&m2));
+  __half2 p13 = __hmul2(*reinterpret_cast<const __half2*>(&hi13), *reinterpret_cast<const __half2*>(&m2));
+  return cvt_e4m3x4_from_f16x2_pairs(*reinterpret_cast<uint32_t*>(&p02), *reinterpret_cast<uint32_t*>(&p13)) |
+         (w & 0x80808080u);
 }
 
 // ------------------------------------------------------------------------------------------

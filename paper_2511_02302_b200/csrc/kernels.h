@@ -13,6 +13,30 @@ struct DeviceInfo {
   int cc_major, cc_minor;
 };
 
+// resident CTAs per SM of a kernel (query once per call site: `static const int occ = ...`)
+template <typename Kernel>
+inline int occupancy_of(Kernel kernel, int threads, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  return occ;
+}
+// one full wave of CTAs (SMs x occupancy), capped by the work available
+inline int64_t one_wave_grid(int occ, int num_sms, int64_t max_ctas) {
+  int64_t g = static_cast<int64_t>(num_sms) * occ;
+  if (g > max_ctas) g = max_ctas;
+  return g < 1 ? 1 : g;
+}
+
+// Work-item schedule of an op (see Sched in common.cuh): the tuned default, overridable for
+// tuning experiments with FP8FLOW_SCHED_<OP> (0 one-item-per-warp, 1 blocked, 2 interleaved).
+int sched_for(const char* op, int tuned_default);
+// grid for a warp-item kernel under a schedule
+inline int64_t sched_grid(int sched, int64_t n_items, int warps_per_cta, int occ, int num_sms) {
+  const int64_t need = (n_items + warps_per_cta - 1) / warps_per_cta;
+  if (sched == 0) return need < 1 ? 1 : need;
+  return one_wave_grid(occ, num_sms, need);
+}
+
 cudaError_t launch_quantize_rowwise(const void* x, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s,
                                     int64_t ld_s, cudaStream_t stream, int num_sms);
 

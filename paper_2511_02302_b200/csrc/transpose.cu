@@ -27,7 +27,8 @@
 
 namespace fp8flow {
 
-constexpr int kTStages = 4;
+constexpr int kTStages = 3;
+constexpr int kTBlocksPerSm = 3;
 constexpr int kTThreads = 256;
 constexpr int kMaxSegs = 1024;
 constexpr int kTileBytes = kTile * kTile;
@@ -132,6 +133,18 @@ __device__ __forceinline__ void load_segments(TransposeSmem& sm, const int32_t* 
   __syncthreads();
 }
 
+// warp-cooperative: the segment owning row block rb = #{e in [1, num_segs) : blk_prefix[e] <= rb}
+// (blk_prefix is non-decreasing, blk_prefix[0] = 0; empty segments are skipped automatically)
+__device__ __forceinline__ int find_segment_warp(const int32_t* blk_prefix, int num_segs, int rb) {
+  const int lane = threadIdx.x & 31;
+  int cnt = 0;
+  for (int base = 1; base < num_segs; base += 32) {
+    const int e = base + lane;
+    cnt += __popc(__ballot_sync(0xffffffffu, e < num_segs && blk_prefix[e] <= rb));
+  }
+  return cnt;
+}
+
 // largest e in [0, num_segs) with blk_prefix[e] <= rb  (the segment that owns row block rb)
 __device__ __forceinline__ int find_segment(const int32_t* blk_prefix, int num_segs, int rb) {
   int lo = 0, hi = num_segs;  // invariant: blk_prefix[lo] <= rb < blk_prefix[hi]
@@ -143,7 +156,7 @@ __device__ __forceinline__ int find_segment(const int32_t* blk_prefix, int num_s
   return lo;
 }
 
-__global__ void __launch_bounds__(kTThreads, 2)
+__global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
     scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q, const uint8_t* __restrict__ s,
                                    int64_t ld_s, int64_t rows, int64_t cols, const int32_t* __restrict__ seg_offsets,
                                    int32_t num_segs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
@@ -185,48 +198,48 @@ __global__ void __launch_bounds__(kTThreads, 2)
   const int g = tid >> 3;  // row quad 0..31
   const int c = tid & 7;   // 16-byte column chunk 0..7
 
+  // tile i of this CTA is t = first + i * stride; (rb, jb) advance incrementally (no division)
+  const int stride_rb = static_cast<int>(stride / n_jb), stride_jb = static_cast<int>(stride % n_jb);
+  int rb = static_cast<int>(first / n_jb), jb = static_cast<int>(first % n_jb);
   for (int64_t i = 0; i < n_local; ++i) {
-    const int64_t t = first + i * stride;
-    const int rb = static_cast<int>(t / n_jb);
-    const int jb = static_cast<int>(t - static_cast<int64_t>(rb) * n_jb);
-    const int e = find_segment(sm.blk_prefix, nsegs, rb);
+    if (i > 0) {
+      jb += stride_jb;
+      rb += stride_rb;
+      if (jb >= n_jb) {
+        jb -= n_jb;
+        ++rb;
+      }
+    }
+    const int e = find_segment_warp(sm.blk_prefix, nsegs, rb);
     const int o = sm.seg_off[e];
     const int m = sm.seg_off[e + 1] - o;
     const int ib = rb - sm.blk_prefix[e];
     const int r0 = o + ib * kTile;
     const int rows_valid = min(kTile, m - ib * kTile);  // multiple of 16
 
-    // ---- block scale max (Algorithm 1: S_max = max_i S_i^row) -------------------------------
-    uint32_t sw = 0;
-    if (4 * g < rows_valid) sw = *reinterpret_cast<const uint32_t*>(s + jb * ld_s + r0 + 4 * g);
-    uint32_t mx = max(max(sw & 0xFFu, (sw >> 8) & 0xFFu), max((sw >> 16) & 0xFFu, sw >> 24));
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    if (lane == 0) sm.red[warp] = mx;
-    __syncthreads();  // S1
-    uint32_t tmax = sm.red[0];
-#pragma unroll
-    for (int w = 1; w < kTThreads / 32; ++w) tmax = max(tmax, sm.red[w]);
+    // ---- block scale max (Algorithm 1: S_max = max_i S_i^row), per warp, no CTA barrier:
+    // lane l loads the 4 scale bytes of rows 4l..4l+3 (one 128-byte run per warp)
+    uint32_t sw_l = 0;
+    if (4 * lane < rows_valid) sw_l = __ldg(reinterpret_cast<const uint32_t*>(s + jb * ld_s + r0 + 4 * lane));
+    const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
+    const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
+    const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);  // this thread's rows 4g..4g+3
 
     // ---- wait for the tile, shift rows, transpose 4x4 byte blocks ------------------------------
     const int st = static_cast<int>(i % kTStages);
     mbar_wait(&sm.full_bar[st], static_cast<uint32_t>((i / kTStages) & 1));
-    uint4 rv[4];
+    uint32_t R[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      rv[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
-      const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
-      if (k != 0u) {
-        rv[r].x = shift4(rv[r].x, k);
-        rv[r].y = shift4(rv[r].y, k);
-        rv[r].z = shift4(rv[r].z, k);
-        rv[r].w = shift4(rv[r].w, k);
-      }
+      const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
+      const uint32_t m2 = shift_multiplier(tmax - ((sw >> (8 * r)) & 0xFFu));  // k = T_max - T_row
+      R[r][0] = shift4(v.x, m2);
+      R[r][1] = shift4(v.y, m2);
+      R[r][2] = shift4(v.z, m2);
+      R[r][3] = shift4(v.w, m2);
     }
-    const uint32_t R[4][4] = {{rv[0].x, rv[0].y, rv[0].z, rv[0].w},
-                              {rv[1].x, rv[1].y, rv[1].z, rv[1].w},
-                              {rv[2].x, rv[2].y, rv[2].z, rv[2].w},
-                              {rv[3].x, rv[3].y, rv[3].z, rv[3].w}};
     const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
+    if (i > 0) __syncthreads();  // previous tile's read-out of sm.out is complete
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(kTThreads, 2)
       sm.out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
       sm.out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
     }
-    __syncthreads();  // S2: tile consumed, out buffer complete
+    __syncthreads();  // tile consumed (stage free), out buffer complete
 
     if (tid == 0 && i + kTStages < n_local) issue(i + kTStages);
 
