@@ -1,0 +1,92 @@
+"""The N>1 host path on CPU: expert-group sharding and the post-timing collectives of
+paper_2511_02302_b200/dist.py, run with world_size 2 over gloo (the GPU box uses NCCL)."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    from paper_2511_02302_b200 import dist as D
+
+    assert D.env() == (rank, rank, world)
+    assert D.init("gloo")
+    g = D.expert_group(rank)
+    t_max = D.max_over_ranks(10.0 + rank)
+    b_sum = D.sum_over_ranks(100.0 * (rank + 1))
+    big = (1 << 64) - 1 - rank                    # uint64 values above 2^63 survive the int64 carrier
+    sums = D.gather_checksums([rank, big])
+    D.barrier()
+    q.put((rank, g, t_max, b_sum, sums))
+    D.dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharding_and_collectives():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [o[1] for o in out] == [0, 1]                      # distinct expert groups
+    assert all(o[2] == 11.0 for o in out)                     # max over ranks
+    assert all(o[3] == 300.0 for o in out)                    # sum over ranks
+    expect = [[0, (1 << 64) - 1], [1, (1 << 64) - 2]]
+    assert all(o[4] == expect for o in out)
+
+
+def test_single_process_defaults(monkeypatch):
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE"):
+        monkeypatch.delenv(k, raising=False)
+    from paper_2511_02302_b200 import dist as D
+
+    assert D.env() == (0, 0, 1)
+    assert D.init("gloo") is False
+    assert D.max_over_ranks(3.5) == 3.5 and D.sum_over_ranks(2.0) == 2.0
+    assert D.gather_checksums([5]) == [[5]]
+    assert [D.expert_group(r) for r in range(10)] == [0, 1, 2, 3, 4, 5, 6, 7, 0, 1]
+
+
+def test_roofline_byte_formulas():
+    from paper_2511_02302_b200 import roofline as RL
+
+    assert RL.quantize_bytes(4096, 7168) == 4096 * 7168 * 3 + 4096 * 56          # 3.008 B/elem
+    assert RL.transpose_bytes([4096], 7168) == 4096 * 7168 * 2 + 4096 * 56 + 32 * 7168
+    assert RL.transpose_bytes([16, 0, 144], 128) == 160 * 128 * 2 + 160 + (1 + 0 + 2) * 128
+    assert RL.swiglu_quant_bytes(10, 2048) == 10 * (4 * 2048 + 2048 + 16)           # 5.008 B/output
+    assert RL.unpermute_bytes(5, 3, 8, 128, True) == 5 * 256 + 3 * 256 + 3 * 8 * 8
+    assert RL.permute_move_bytes(3, 16, 128) == 3 * 129 + 16 * 129 + 16 * 4
+    p = RL.measured_peaks("/nonexistent")
+    assert p["hbm_gbs"] == 6650.0 and "fallback" in p["source"]
+
+
+@pytest.mark.parametrize("group", [0, 3])
+def test_expert_shard_is_what_dispatch_would_deliver(group):
+    import numpy as np
+
+    import synth
+
+    idx, probs = synth.routing(2000, 7)
+    sh = synth.expert_shard(idx, probs, group, 8)
+    e0 = group * 32
+    local = (idx.numpy() >= e0) & (idx.numpy() < e0 + 32)
+    assert np.array_equal(sh.recv_tokens, np.nonzero(local.any(1))[0])
+    assert np.array_equal(sh.topk_idx, idx.numpy()[sh.recv_tokens])
+    # every token's experts are distinct (precondition of the plan) and routing is group-limited
+    assert all(len(set(r)) == 8 for r in idx.numpy()[:200])
+    assert all(len({e // 32 for e in r}) <= 4 for r in idx.numpy()[:200])
