@@ -18,6 +18,7 @@
 // Move: warp item = 4 consecutive output rows (balanced contiguous item ranges per warp, one wave
 // of CTAs); the 4 rows stream with 128-bit loads and stores (16 in flight per lane), their scale
 // bytes are gathered per 1x128 tile (all gathers issued before the stores).
+#include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -191,63 +192,110 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
 // ---------------------------------------------------------------------------------------------
 // A3 move
 // ---------------------------------------------------------------------------------------------
-constexpr int kMoveRows = 4;    // output rows per warp item
-constexpr int kMoveBatch = 16;  // 16-byte loads in flight per lane
+// Move on the bulk-copy engine: one CTA per SM; warp 0, lane 0 streams whole rows global ->
+// shared -> global with 1D bulk copies (cp.async.bulk, mbarrier-completed loads, bulk-group stores)
+// through a ring of row slots, keeping kMoveLead rows in flight per SM with no register staging.
+// PAD rows are stored from a zeroed row.  Warps 1-7 gather the rows' scale bytes meanwhile.
+// Rows are dealt to CTAs in chunks of kMoveChunk, interleaved.
+constexpr int kMoveChunk = 4;
+constexpr int kMoveStoreSlack = 8;  // slots whose bulk stores may still be reading shared memory
+constexpr int kMaxMoveSlots = 32;
+constexpr size_t kMoveSmemBudget = 220 * 1024;
 
-__global__ void __launch_bounds__(256) permute_pad_kernel(const uint8_t* __restrict__ q_tok,
-                                                          const uint8_t* __restrict__ s_tok, int64_t ld_s_tok,
-                                                          int64_t H, const int32_t* __restrict__ src_of_row,
-                                                          const int32_t* __restrict__ expert_offsets, int E_loc,
-                                                          int64_t max_rows, uint8_t* __restrict__ q_out,
-                                                          uint8_t* __restrict__ s_out, int sched) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ int64_t move_row(int64_t n, int64_t cta, int64_t G) {
+  return (cta + (n / kMoveChunk) * G) * kMoveChunk + (n % kMoveChunk);
+}
+
+__global__ void __launch_bounds__(256, 1) permute_pad_kernel(const uint8_t* __restrict__ q_tok,
+                                                             const uint8_t* __restrict__ s_tok, int64_t ld_s_tok,
+                                                             int64_t H, const int32_t* __restrict__ src_of_row,
+                                                             const int32_t* __restrict__ expert_offsets, int E_loc,
+                                                             int64_t max_rows, uint8_t* __restrict__ q_out,
+                                                             uint8_t* __restrict__ s_out, int nslots) {
+  extern __shared__ __align__(128) uint8_t smem_move[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_move);
+  uint8_t* zero = smem_move + 8 * kMaxMoveSlots;  // 256 B in: 128-byte aligned
+  uint8_t* slots = zero + H;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t R = expert_offsets[E_loc];
-  const int n_vec = static_cast<int>(H / 16);  // 16-byte chunks per row
-  const int n_tiles = static_cast<int>(H / kTile);
-  for (ItemIter it = warp_item_iter((R + kMoveRows - 1) / kMoveRows, sched); it.cur < it.end; it.cur += it.step) {
-    const int64_t item = it.cur;
-    const int64_t r0 = item * kMoveRows;
-    int32_t src[kMoveRows];
-#pragma unroll
-    for (int rr = 0; rr < kMoveRows; ++rr) src[rr] = (r0 + rr < R) ? __ldg(src_of_row + r0 + rr) : -2;
-    // --- codes: the 4 rows flattened into 4 * n_vec 16-byte chunks, 16 loads in flight per lane
-    const int total = kMoveRows * n_vec;
-    for (int v0 = 0; v0 < total; v0 += 32 * kMoveBatch) {
-      uint4 buf[kMoveBatch];
-#pragma unroll
-      for (int u = 0; u < kMoveBatch; ++u) {
-        const int v = v0 + u * 32 + lane;
-        const int rr = v / n_vec, cv = v - rr * n_vec;
-        int32_t sr = -2;
-#pragma unroll
-        for (int q = 0; q < kMoveRows; ++q)
-          if (q == rr) sr = src[q];
-        buf[u] = make_uint4(0, 0, 0, 0);
-        if (v < total && sr >= 0) buf[u] = ld_nc_v4(q_tok + static_cast<int64_t>(sr) * H + 16 * cv);
+  const int64_t G = gridDim.x, cta = blockIdx.x;
+  const int64_t n_chunks = (R + kMoveChunk - 1) / kMoveChunk;
+  const int64_t my_chunks = cta < n_chunks ? (n_chunks - cta + G - 1) / G : 0;
+  int64_t n_rows = my_chunks * kMoveChunk;  // rows of this CTA (the last chunk of all may be partial)
+  if (my_chunks > 0 && move_row(n_rows - 1, cta, G) >= R) n_rows -= move_row(n_rows - 1, cta, G) - R + 1;
+
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) mbar_init(&full[i], 1);
+    mbar_init_fence();
+  }
+  for (int64_t i = tid * 16; i < H; i += 256 * 16) *reinterpret_cast<uint4*>(zero + i) = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();  // zero row (generic writes) is read by bulk stores (async proxy)
+  __syncthreads();
+
+  if (warp == 0) {
+    // the whole warp walks the rows (lane l holds the source of row batch+l); lane 0 issues.
+    // Ring positions and global row indices advance incrementally (no division in the loop).
+    const int lead = nslots - kMoveStoreSlack;  // rows whose loads are in flight ahead of the stores
+    const int nr = static_cast<int>(n_rows);
+    uint32_t phase_bits = 0;
+    int32_t src_prev = -1, src_cur = -1;
+    int slot_ld = 0, slot_st = 0, k_st = 0;  // k_st: position of the store row inside its chunk
+    int64_t row_st = cta * kMoveChunk;       // global row of the store stage
+    const int64_t chunk_jump = (G - 1) * kMoveChunk + 1;
+    for (int n = 0; n < nr + lead; ++n) {
+      if ((n & 31) == 0) {  // next batch of 32 row sources, one per lane
+        src_prev = src_cur;
+        const int ln = n + lane;
+        src_cur = ln < nr ? __ldg(src_of_row + move_row(ln, cta, G)) : -1;
       }
-#pragma unroll
-      for (int u = 0; u < kMoveBatch; ++u) {
-        const int v = v0 + u * 32 + lane;
-        const int rr = v / n_vec, cv = v - rr * n_vec;
-        if (v < total && r0 + rr < R) st_v4(q_out + (r0 + rr) * H + 16 * cv, buf[u]);
+      const int m = n - lead;  // store stage
+      if (m >= 0) {
+        const int ml = m - (n & ~31);  // < 0: the row is in the previous batch
+        const int32_t sm_src = __shfl_sync(0xffffffffu, ml >= 0 ? src_cur : src_prev, ml & 31);
+        if (lane == 0) {
+          const uint8_t* from = zero;
+          if (sm_src >= 0) {
+            mbar_wait(&full[slot_st], (phase_bits >> slot_st) & 1u);
+            phase_bits ^= 1u << slot_st;
+            from = slots + static_cast<int64_t>(slot_st) * H;
+          }
+          bulk_store_1d(q_out + row_st * H, from, static_cast<uint32_t>(H));
+          bulk_commit();
+        }
+        if (++slot_st == nslots) slot_st = 0;
+        if (++k_st == kMoveChunk) {
+          k_st = 0;
+          row_st += chunk_jump;
+        } else {
+          ++row_st;
+        }
+      }
+      if (n < nr) {  // load stage
+        const int32_t sn = __shfl_sync(0xffffffffu, src_cur, n & 31);
+        if (lane == 0) {
+          if (n >= nslots) bulk_wait_read<kMoveStoreSlack>();  // row n - nslots's store has read the slot
+          if (sn >= 0) {
+            mbar_expect_tx(&full[slot_ld], static_cast<uint32_t>(H));
+            bulk_load_1d(slots + static_cast<int64_t>(slot_ld) * H, q_tok + static_cast<int64_t>(sn) * H,
+                         static_cast<uint32_t>(H), &full[slot_ld]);
+          }
+        }
+        if (++slot_ld == nslots) slot_ld = 0;
       }
     }
-    // --- scales: (row, tile) pairs of the item spread over the lanes; gathers issued first
-    constexpr int kMaxPairsPerLane = kMoveRows * 128 / 32;  // hidden <= 16384
-    uint8_t b[kMaxPairsPerLane];
-#pragma unroll
-    for (int i = 0; i < kMaxPairsPerLane; ++i) {
-      const int p = lane + 32 * i, rr = p & (kMoveRows - 1), tl = p / kMoveRows;
-      int32_t sr = -2;
-#pragma unroll
-      for (int q = 0; q < kMoveRows; ++q)
-        if (q == rr) sr = src[q];
-      b[i] = (tl < n_tiles && sr >= 0) ? __ldg(s_tok + static_cast<int64_t>(tl) * ld_s_tok + sr) : static_cast<uint8_t>(0);
-    }
-#pragma unroll
-    for (int i = 0; i < kMaxPairsPerLane; ++i) {
-      const int p = lane + 32 * i, rr = p & (kMoveRows - 1), tl = p / kMoveRows;
-      if (tl < n_tiles && r0 + rr < R) s_out[static_cast<int64_t>(tl) * max_rows + r0 + rr] = b[i];
+    if (lane == 0) bulk_wait_all();
+  } else {
+    // scale bytes: (local row, tile) pairs over warps 1..7; PAD rows -> 0x00
+    const int n_tiles = static_cast<int>(H / kTile);
+    const int pairs = static_cast<int>(n_rows) * n_tiles;
+    const int nr = static_cast<int>(n_rows);
+    for (int p = tid - 32; p < pairs; p += 224) {
+      const int tl = p / nr;
+      const int n = p - tl * nr;
+      const int64_t r = move_row(n, cta, G);
+      const int32_t src = __ldg(src_of_row + r);
+      s_out[static_cast<int64_t>(tl) * max_rows + r] =
+          src >= 0 ? __ldg(s_tok + static_cast<int64_t>(tl) * ld_s_tok + src) : static_cast<uint8_t>(0);
     }
   }
 }
@@ -255,123 +303,162 @@ __global__ void __launch_bounds__(256) permute_pad_kernel(const uint8_t* __restr
 cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
                                const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_local_experts,
                                int64_t max_rows, uint8_t* q_out, uint8_t* s_out, cudaStream_t stream, int num_sms) {
-  static const int occ = occupancy_of(permute_pad_kernel, 256, 0);
-  const int sched = sched_for("A3", kSchedOnePerWarp);
-  // the actual row count lives on the device: size the grid for max_rows (idle warps exit)
-  const int64_t grid = sched_grid(sched, (max_rows + kMoveRows - 1) / kMoveRows, 8, occ, num_sms);
-  permute_pad_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
-      q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out, sched);
+  int nslots = static_cast<int>((kMoveSmemBudget - 8 * kMaxMoveSlots - hidden) / hidden);
+  if (nslots > kMaxMoveSlots) nslots = kMaxMoveSlots;
+  if (nslots < kMoveStoreSlack + 2) return cudaErrorInvalidValue;  // hidden too large for the ring
+  const size_t smem = 8 * kMaxMoveSlots + static_cast<size_t>(hidden) * (1 + nslots);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(permute_pad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(8 * kMaxMoveSlots + kMoveSmemBudget));
+    attr = true;
+  }
+  int64_t grid = (max_rows + kMoveChunk - 1) / kMoveChunk;
+  if (grid > num_sms) grid = num_sms;
+  if (grid < 1) grid = 1;
+  permute_pad_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
+      q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out, nslots);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------------
-// A4 unpermute + unpad: warp item = (token, 1024-column chunk), balanced contiguous item ranges
-// per warp over one wave of CTAs.  The token's local rows are compacted in k order across lanes
-// (ballot + __fns, once per token); each lane owns 8 BF16 (16 B) per 256-column step and issues
-// all loads of a row group before the fused multiply-adds, so several 128-bit loads per lane are
-// in flight (4 steps x <= 2 rows on the common path, 2 steps x 4 rows otherwise).
-// fp32 acc = fmaf(p_k, x_k, acc) in k order from +0 (p = 1 when probs is NULL: fmaf(1, x, acc) ==
-// acc + x exactly), then BF16 RNE.
+// A4 unpermute + unpad on the bulk-copy engine.  One CTA per SM; tokens dealt round-robin.
+//   warp 0 (producer): per token, compacts its local rows in k order (ballot + __fns) and streams
+//     each row (2H bytes) global -> shared with a 1D bulk copy into a ring of row slots
+//     (mbarrier `full[slot]` counts the bytes; `empty[slot]` is released by the consumers).
+//   warps 1-7 (consumers, 224 threads): per token, in the same order, wait for each row, accumulate
+//     acc = fmaf(p_k, x_k, acc) in fp32 in k order from +0 over their 16-byte chunks, round to BF16
+//     (RNE) and store 128-bit.  Tokens without a local expert produce +0.
+// Up to nslots rows (e.g. 15 x 14 KB) are in flight per SM without register staging.
 // ---------------------------------------------------------------------------------------------
-template <int NROWS, int U>
-__device__ __forceinline__ void unpermute_chunk(const __nv_bfloat16* __restrict__ x, int64_t H, int64_t h0, int nk,
-                                                int32_t comp_row, float comp_p, float (&acc)[U][8]) {
-  // local rows [0, nk) in k order, held one per lane (comp_row / comp_p of lane i = i-th term);
-  // groups of NROWS rows: all loads of a group are issued before its FMAs
-#pragma unroll 1
-  for (int g = 0; g < nk; g += NROWS) {
-    uint4 v[NROWS][U];
-    float p[NROWS];
-#pragma unroll
-    for (int j = 0; j < NROWS; ++j) {
-      const int32_t r = __shfl_sync(0xffffffffu, comp_row, (g + j) & 31);
-      p[j] = __shfl_sync(0xffffffffu, comp_p, (g + j) & 31);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t h = h0 + u * 256;
-        v[j][u] = (g + j < nk && h < H) ? ld_nc_v4(x + static_cast<int64_t>(r) * H + h) : make_uint4(0, 0, 0, 0);
-      }
+constexpr int kUnpermConsumerWarps = 7;
+constexpr int kMaxUnpermSlots = 16;
+constexpr int kUnpermChunksPerThread = 4;  // 224 threads x 4 x 8 BF16 = 7168 columns per pass
+constexpr size_t kUnpermSmemBudget = 220 * 1024;
+
+__global__ void __launch_bounds__(256, 1) unpermute_unpad_kernel(const __nv_bfloat16* __restrict__ x, int64_t H,
+                                                                 const int32_t* __restrict__ row_map,
+                                                                 const float* __restrict__ probs, int64_t T, int K,
+                                                                 __nv_bfloat16* __restrict__ y, int nslots) {
+  extern __shared__ __align__(128) uint8_t smem_unperm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_unperm);
+  uint64_t* empty = full + kMaxUnpermSlots;
+  uint8_t* slots = smem_unperm + 16 * kMaxUnpermSlots;  // 256 B in
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = gridDim.x;
+  const int64_t row_bytes = 2 * H;
+
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kUnpermConsumerWarps);
     }
-#pragma unroll
-    for (int j = 0; j < NROWS; ++j) {
-      if (g + j < nk) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t w[4] = {v[j][u].x, v[j][u].y, v[j][u].z, v[j][u].w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[u][2 * i] = __fmaf_rn(p[j], bf16lo_to_f32(w[i]), acc[u][2 * i]);
-            acc[u][2 * i + 1] = __fmaf_rn(p[j], bf16hi_to_f32(w[i]), acc[u][2 * i + 1]);
-          }
+    mbar_init_fence();
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // ---------------- producer
+    int slot = 0;
+    uint32_t parity = 0;   // parity of the current ring lap
+    bool wrapped = false;  // the ring has been filled once: slots must be released before reuse
+    // routing rows are read two tokens ahead so their latency never stalls the copy issue
+    int64_t t = blockIdx.x;
+    int32_t row_a = (t < T && lane < K) ? row_map[t * K + lane] : -1;
+    int32_t row_b = (t + G < T && lane < K) ? row_map[(t + G) * K + lane] : -1;
+    for (; t < T; t += G) {
+      const int32_t my_row = row_a;
+      row_a = row_b;
+      row_b = (t + 2 * G < T && lane < K) ? row_map[(t + 2 * G) * K + lane] : -1;
+      const uint32_t valid = __ballot_sync(0xffffffffu, my_row >= 0);
+      const int nk = __popc(valid);
+      const int32_t comp_row = __shfl_sync(0xffffffffu, my_row, static_cast<int>(__fns(valid, 0, lane + 1)) & 31);
+      for (int i = 0; i < nk; ++i) {
+        const int32_t r = __shfl_sync(0xffffffffu, comp_row, i);
+        if (lane == 0) {
+          if (wrapped) mbar_wait(&empty[slot], parity ^ 1u);  // released after the previous lap
+          mbar_expect_tx(&full[slot], static_cast<uint32_t>(row_bytes));
+          bulk_load_1d(slots + slot * row_bytes, x + static_cast<int64_t>(r) * H, static_cast<uint32_t>(row_bytes),
+                       &full[slot]);
+        }
+        if (++slot == nslots) {
+          slot = 0;
+          parity ^= 1u;
+          wrapped = true;
         }
       }
     }
-  }
-}
-
-template <int U>
-__device__ __forceinline__ void unpermute_store(__nv_bfloat16* __restrict__ yrow, int64_t H, int64_t h0,
-                                                const float (&acc)[U][8]) {
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t h = h0 + u * 256;
-    if (h < H) {
-      uint32_t o[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        __nv_bfloat162 b = __floats2bfloat162_rn(acc[u][2 * i], acc[u][2 * i + 1]);
-        o[i] = *reinterpret_cast<uint32_t*>(&b);
-      }
-      st_v4(yrow + h, make_uint4(o[0], o[1], o[2], o[3]));
-    }
-  }
-}
-
-constexpr int kUnpermChunk = 1024;  // BF16 columns per warp item (32 lanes x 8 x 4)
-
-__global__ void __launch_bounds__(256, 2) unpermute_unpad_kernel(const __nv_bfloat16* __restrict__ x, int64_t H,
-                                                              const int32_t* __restrict__ row_map,
-                                                              const float* __restrict__ probs, int64_t T, int K,
-                                                              __nv_bfloat16* __restrict__ y, int sched) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n_chunks = (H + kUnpermChunk - 1) / kUnpermChunk;
-  int64_t cur_t = -1;
-  int nk = 0;
-  int32_t comp_row = -1;
-  float comp_p = 0.0f;
-  for (ItemIter it = warp_item_iter(T * n_chunks, sched); it.cur < it.end; it.cur += it.step) {
-    const int64_t item = it.cur;  // item = (token, 1024-column chunk)
-    const int64_t t = item / n_chunks;
-    const int64_t h0 = (item - t * n_chunks) * kUnpermChunk + lane * 8;
-    if (t != cur_t) {  // consecutive items share the token: compact its local terms once
-      cur_t = t;
-      const int32_t my_row = lane < K ? row_map[t * K + lane] : -1;
-      const float my_p = lane < K ? (probs != nullptr ? probs[t * K + lane] : 1.0f) : 0.0f;
+  } else {  // ---------------- consumers
+    const int ct = tid - 32;
+    const int64_t n_chunks = H / 8;
+    int slot0 = 0;           // ring slot of the token's first row
+    uint32_t parity0 = 0;    // its lap parity
+    int64_t t = blockIdx.x;
+    // software-pipelined routing reads: the next token's row_map / probs are loaded one token ahead
+    int32_t nxt_row = (t < T && lane < K) ? row_map[t * K + lane] : -1;
+    float nxt_p = (t < T && lane < K) ? (probs != nullptr ? probs[t * K + lane] : 1.0f) : 0.0f;
+    for (; t < T; t += G) {
+      const int32_t my_row = nxt_row;
+      const float my_p = nxt_p;
+      const int64_t tn = t + G;
+      nxt_row = (tn < T && lane < K) ? row_map[tn * K + lane] : -1;
+      nxt_p = (tn < T && lane < K) ? (probs != nullptr ? probs[tn * K + lane] : 1.0f) : 0.0f;
       const uint32_t valid = __ballot_sync(0xffffffffu, my_row >= 0);
-      nk = __popc(valid);
-      const int src = static_cast<int>(__fns(valid, 0, lane + 1)) & 31;  // lane i <- i-th term (k order)
-      comp_row = __shfl_sync(0xffffffffu, my_row, src);
-      comp_p = __shfl_sync(0xffffffffu, my_p, src);
-    }
-    __nv_bfloat16* yrow = y + t * H;
-    if (nk <= 2) {
-      float acc[4][8];
+      const int nk = __popc(valid);
+      const float comp_p = __shfl_sync(0xffffffffu, my_p, static_cast<int>(__fns(valid, 0, lane + 1)) & 31);
+      for (int64_t c0 = 0; c0 < n_chunks; c0 += 224 * kUnpermChunksPerThread) {
+        float acc[kUnpermChunksPerThread][8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+        for (int q = 0; q < kUnpermChunksPerThread; ++q)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[u][i] = 0.0f;
-      unpermute_chunk<2, 4>(x, H, h0, nk, comp_row, comp_p, acc);
-      unpermute_store<4>(yrow, H, h0, acc);
-    } else {
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        float acc[2][8];
+          for (int j = 0; j < 8; ++j) acc[q][j] = 0.0f;
+        int slot = slot0;
+        uint32_t parity = parity0;
+        for (int i = 0; i < nk; ++i) {
+          const float pk = __shfl_sync(0xffffffffu, comp_p, i);
+          mbar_wait(&full[slot], parity);
+          const uint8_t* base = slots + slot * row_bytes;
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+          for (int q = 0; q < kUnpermChunksPerThread; ++q) {
+            const int64_t c = c0 + ct + 224 * q;
+            if (c < n_chunks) {
+              const uint4 v = *reinterpret_cast<const uint4*>(base + c * 16);
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[u][i] = 0.0f;
-        unpermute_chunk<4, 2>(x, H, h0 + hh * 512, nk, comp_row, comp_p, acc);
-        unpermute_store<2>(yrow, H, h0 + hh * 512, acc);
+              for (int j = 0; j < 4; ++j) {
+                acc[q][2 * j] = __fmaf_rn(pk, bf16lo_to_f32(w[j]), acc[q][2 * j]);
+                acc[q][2 * j + 1] = __fmaf_rn(pk, bf16hi_to_f32(w[j]), acc[q][2 * j + 1]);
+              }
+            }
+          }
+          // the last pass over the columns releases the slot
+          if (c0 + 224 * kUnpermChunksPerThread >= n_chunks) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+          }
+          if (++slot == nslots) {
+            slot = 0;
+            parity ^= 1u;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kUnpermChunksPerThread; ++q) {
+          const int64_t c = c0 + ct + 224 * q;
+          if (c < n_chunks) {
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              __nv_bfloat162 bb = __floats2bfloat162_rn(acc[q][2 * j], acc[q][2 * j + 1]);
+              o[j] = *reinterpret_cast<uint32_t*>(&bb);
+            }
+            st_v4(y + t * H + c * 8, make_uint4(o[0], o[1], o[2], o[3]));
+          }
+        }
+      }
+      for (int i = 0; i < nk; ++i) {  // advance the token's first slot past its rows
+        if (++slot0 == nslots) {
+          slot0 = 0;
+          parity0 ^= 1u;
+        }
       }
     }
   }
@@ -379,13 +466,24 @@ __global__ void __launch_bounds__(256, 2) unpermute_unpad_kernel(const __nv_bflo
 
 cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t* row_map, const float* probs,
                                    int64_t num_tokens, int32_t top_k, void* y, cudaStream_t stream, int num_sms) {
-  static const int occ = occupancy_of(unpermute_unpad_kernel, 256, 0);
-  const int64_t items = num_tokens * ((hidden + kUnpermChunk - 1) / kUnpermChunk);
-  const int sched = sched_for("A4", kSchedInterleaved);
-  const int64_t grid = sched_grid(sched, items, 8, occ, num_sms);
-  unpermute_unpad_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(
+  const int64_t row_bytes = 2 * hidden;
+  int nslots = static_cast<int>(kUnpermSmemBudget / row_bytes);
+  if (nslots > kMaxUnpermSlots) nslots = kMaxUnpermSlots;
+  // a token's rows must all fit the ring when the columns take more than one consumer pass
+  const bool multi_pass = hidden / 8 > 224 * kUnpermChunksPerThread;
+  if (nslots < 2 || (multi_pass && nslots < top_k)) return cudaErrorInvalidValue;
+  const size_t smem = 16 * kMaxUnpermSlots + static_cast<size_t>(row_bytes) * nslots;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(unpermute_unpad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(16 * kMaxUnpermSlots + kUnpermSmemBudget));
+    attr = true;
+  }
+  int64_t grid = num_tokens < num_sms ? num_tokens : num_sms;
+  if (grid < 1) grid = 1;
+  unpermute_unpad_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
       static_cast<const __nv_bfloat16*>(x), hidden, row_map, probs, num_tokens, top_k,
-      static_cast<__nv_bfloat16*>(y), sched);
+      static_cast<__nv_bfloat16*>(y), nslots);
   return cudaGetLastError();
 }
 

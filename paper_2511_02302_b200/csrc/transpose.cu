@@ -22,6 +22,7 @@
 //     redux.sync max per warp, 8-entry smem combine.
 #include <cuda.h>
 
+#include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -35,6 +36,7 @@ constexpr int kTileBytes = kTile * kTile;
 
 struct TransposeSmem {
   uint8_t in[kTStages][kTileBytes];
+  uint32_t sc[kTStages][kTile / 4];  // the 128 row-scale bytes of each staged tile
   uint32_t out[kTile * kTile / 4];
   uint64_t full_bar[kTStages];
   uint32_t red[kTThreads / 32];
@@ -42,41 +44,6 @@ struct TransposeSmem {
   int32_t blk_prefix[kMaxSegs + 1];
   int32_t total_rb;
 };
-
-// ---------------------------------------------------------------------------------------------
-// PTX wrappers: mbarrier + TMA
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                            int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // block-wide exclusive scan of one value per thread (blockDim.x == kTThreads); returns the
 // exclusive prefix and writes the block total to *total (visible after the trailing sync).
@@ -163,7 +130,7 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   TransposeSmem& sm = *reinterpret_cast<TransposeSmem*>(smem_raw);
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31;
   const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
 
   if (tid == 0) {
@@ -175,33 +142,40 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
   load_segments(sm, seg_offsets, nsegs, rows);
 
   const int n_jb = static_cast<int>(cols / kTile);
-  const int64_t total_tiles = static_cast<int64_t>(sm.total_rb) * n_jb;
-  const int64_t first = blockIdx.x;
-  const int64_t stride = gridDim.x;
-  const int64_t n_local = first < total_tiles ? (total_tiles - first + stride - 1) / stride : 0;
+  const int total_tiles = sm.total_rb * n_jb;  // < 2^31 (rows < 2^31, checked by the ABI)
+  const int first = blockIdx.x;
+  const int stride = gridDim.x;
+  const int n_local = first < total_tiles ? (total_tiles - first + stride - 1) / stride : 0;
 
-  auto issue = [&](int64_t i) {
-    const int64_t t = first + i * stride;
-    const int rb = static_cast<int>(t / n_jb);
-    const int jb = static_cast<int>(t - static_cast<int64_t>(rb) * n_jb);
+  // producer: tile i of this CTA is t = first + i * stride; the 16 KB code tile (TMA 2D) and its
+  // 128-byte run of row scales (1D bulk copy, rows_valid bytes) land on the same mbarrier
+  auto issue = [&](int i) {
+    const int t = first + i * stride;
+    const int rb = t / n_jb;
+    const int jb = t - rb * n_jb;
     const int e = find_segment(sm.blk_prefix, nsegs, rb);
-    const int r0 = sm.seg_off[e] + (rb - sm.blk_prefix[e]) * kTile;
-    const int st = static_cast<int>(i % kTStages);
-    mbar_expect_tx(&sm.full_bar[st], kTileBytes);
+    const int ib = rb - sm.blk_prefix[e];
+    const int r0 = sm.seg_off[e] + ib * kTile;
+    const int rows_valid = min(kTile, sm.seg_off[e + 1] - r0);
+    const int st = i % kTStages;
+    mbar_expect_tx(&sm.full_bar[st], kTileBytes + rows_valid);
     tma_load_2d(sm.in[st], &tmap_q, &sm.full_bar[st], jb * kTile, r0);
+    bulk_load_1d(sm.sc[st], s + static_cast<int64_t>(jb) * ld_s + r0, rows_valid, &sm.full_bar[st]);
   };
 
   if (tid == 0) {
-    for (int64_t i = 0; i < n_local && i < kTStages; ++i) issue(i);
+    for (int i = 0; i < n_local && i < kTStages; ++i) issue(i);
   }
 
   const int g = tid >> 3;  // row quad 0..31
   const int c = tid & 7;   // 16-byte column chunk 0..7
 
-  // tile i of this CTA is t = first + i * stride; (rb, jb) advance incrementally (no division)
-  const int stride_rb = static_cast<int>(stride / n_jb), stride_jb = static_cast<int>(stride % n_jb);
-  int rb = static_cast<int>(first / n_jb), jb = static_cast<int>(first % n_jb);
-  for (int64_t i = 0; i < n_local; ++i) {
+  // (rb, jb) of tile i advance incrementally (no division in the loop)
+  const int stride_rb = stride / n_jb, stride_jb = stride % n_jb;
+  int rb = first / n_jb, jb = first % n_jb;
+  int st = 0;
+  uint32_t phase = 0;
+  for (int i = 0; i < n_local; ++i) {
     if (i > 0) {
       jb += stride_jb;
       rb += stride_rb;
@@ -214,20 +188,17 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
     const int o = sm.seg_off[e];
     const int m = sm.seg_off[e + 1] - o;
     const int ib = rb - sm.blk_prefix[e];
-    const int r0 = o + ib * kTile;
     const int rows_valid = min(kTile, m - ib * kTile);  // multiple of 16
 
+    mbar_wait(&sm.full_bar[st], phase);
     // ---- block scale max (Algorithm 1: S_max = max_i S_i^row), per warp, no CTA barrier:
-    // lane l loads the 4 scale bytes of rows 4l..4l+3 (one 128-byte run per warp)
-    uint32_t sw_l = 0;
-    if (4 * lane < rows_valid) sw_l = __ldg(reinterpret_cast<const uint32_t*>(s + jb * ld_s + r0 + 4 * lane));
+    // lane l reads the staged scale bytes of rows 4l..4l+3; rows beyond the segment count as 0
+    const uint32_t sw_l = (4 * lane < rows_valid) ? sm.sc[st][lane] : 0u;
     const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
     const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
     const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);  // this thread's rows 4g..4g+3
 
-    // ---- wait for the tile, shift rows, transpose 4x4 byte blocks ------------------------------
-    const int st = static_cast<int>(i % kTStages);
-    mbar_wait(&sm.full_bar[st], static_cast<uint32_t>((i / kTStages) & 1));
+    // ---- shift rows, transpose 4x4 byte blocks ----------------------------------------------
     uint32_t R[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -237,6 +208,10 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
       R[r][1] = shift4(v.y, m2);
       R[r][2] = shift4(v.z, m2);
       R[r][3] = shift4(v.w, m2);
+    }
+    if (++st == kTStages) {
+      st = 0;
+      phase ^= 1u;
     }
     const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
     if (i > 0) __syncthreads();  // previous tile's read-out of sm.out is complete
