@@ -18,6 +18,16 @@ int fp8flow::sched_for(const char* op, int tuned_default) {
   return tuned_default;
 }
 
+int fp8flow::tune_int(const char* name, int tuned_default) {
+  char env[64] = "FP8FLOW_";
+  strncat(env, name, sizeof(env) - strlen(env) - 1);
+  const char* v = getenv(env);
+  if (!v || !*v) return tuned_default;
+  char* end = nullptr;
+  const long x = strtol(v, &end, 10);
+  return (*end == 0 && x > 0 && x < (1 << 20)) ? static_cast<int>(x) : tuned_default;
+}
+
 namespace {
 
 thread_local int g_last_cuda_error = 0;

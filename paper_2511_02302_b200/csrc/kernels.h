@@ -30,6 +30,8 @@ inline int64_t one_wave_grid(int occ, int num_sms, int64_t max_ctas) {
 // Work-item schedule of an op (see Sched in common.cuh): the tuned default, overridable for
 // tuning experiments with FP8FLOW_SCHED_<OP> (0 one-item-per-warp, 1 blocked, 2 interleaved).
 int sched_for(const char* op, int tuned_default);
+// Integer tuning knob FP8FLOW_<name> (tuning experiments only), else the tuned default.
+int tune_int(const char* name, int tuned_default);
 // grid for a warp-item kernel under a schedule
 inline int64_t sched_grid(int sched, int64_t n_items, int warps_per_cta, int occ, int num_sms) {
   const int64_t need = (n_items + warps_per_cta - 1) / warps_per_cta;

@@ -198,7 +198,7 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
 // PAD rows are stored from a zeroed row.  Warps 1-7 gather the rows' scale bytes meanwhile.
 // Rows are dealt to CTAs in chunks of kMoveChunk, interleaved.
 constexpr int kMoveChunk = 4;
-constexpr int kMoveStoreSlack = 8;  // slots whose bulk stores may still be reading shared memory
+constexpr int kMoveStoreSlack = 4;  // slots whose bulk stores may still be reading shared memory
 constexpr int kMaxMoveSlots = 32;
 constexpr size_t kMoveSmemBudget = 220 * 1024;
 
@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(256, 1) permute_pad_kernel(const uint8_t* __re
 cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
                                const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_local_experts,
                                int64_t max_rows, uint8_t* q_out, uint8_t* s_out, cudaStream_t stream, int num_sms) {
-  int nslots = static_cast<int>((kMoveSmemBudget - 8 * kMaxMoveSlots - hidden) / hidden);
+  const int ctas = tune_int("CTAS_PER_SM_A3", 2);  // co-resident CTAs per SM (smem budget split)
+  const size_t budget = kMoveSmemBudget / ctas;
+  int nslots = static_cast<int>((budget - 8 * kMaxMoveSlots - hidden) / hidden);
   if (nslots > kMaxMoveSlots) nslots = kMaxMoveSlots;
   if (nslots < kMoveStoreSlack + 2) return cudaErrorInvalidValue;  // hidden too large for the ring
   const size_t smem = 8 * kMaxMoveSlots + static_cast<size_t>(hidden) * (1 + nslots);
@@ -314,7 +316,7 @@ cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64
     attr = true;
   }
   int64_t grid = (max_rows + kMoveChunk - 1) / kMoveChunk;
-  if (grid > num_sms) grid = num_sms;
+  if (grid > static_cast<int64_t>(num_sms) * ctas) grid = static_cast<int64_t>(num_sms) * ctas;
   if (grid < 1) grid = 1;
   permute_pad_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
       q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out, nslots);
@@ -467,7 +469,8 @@ __global__ void __launch_bounds__(256, 1) unpermute_unpad_kernel(const __nv_bflo
 cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t* row_map, const float* probs,
                                    int64_t num_tokens, int32_t top_k, void* y, cudaStream_t stream, int num_sms) {
   const int64_t row_bytes = 2 * hidden;
-  int nslots = static_cast<int>(kUnpermSmemBudget / row_bytes);
+  const int ctas = tune_int("CTAS_PER_SM_A4", 2);  // co-resident CTAs per SM (smem budget split)
+  int nslots = static_cast<int>(kUnpermSmemBudget / ctas / row_bytes);
   if (nslots > kMaxUnpermSlots) nslots = kMaxUnpermSlots;
   // a token's rows must all fit the ring when the columns take more than one consumer pass
   const bool multi_pass = hidden / 8 > 224 * kUnpermChunksPerThread;
@@ -479,7 +482,8 @@ cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t*
                          static_cast<int>(16 * kMaxUnpermSlots + kUnpermSmemBudget));
     attr = true;
   }
-  int64_t grid = num_tokens < num_sms ? num_tokens : num_sms;
+  const int64_t max_grid = static_cast<int64_t>(num_sms) * ctas;
+  int64_t grid = num_tokens < max_grid ? num_tokens : max_grid;
   if (grid < 1) grid = 1;
   unpermute_unpad_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
       static_cast<const __nv_bfloat16*>(x), hidden, row_map, probs, num_tokens, top_k,
