@@ -488,8 +488,8 @@ def main():
         run_reference(args, rank, world, group, cfg)
         return
 
-    D.init("nccl")
-    device = torch.device("cuda", local_rank)
+    D.init(D.backend())
+    device = D.local_device(local_rank)
     torch.cuda.set_device(device)
     hw = HostWorkload(group)
     ds = DeviceStep(hw, device)
@@ -501,7 +501,7 @@ def main():
     for _ in range(args.warmup):
         ds.timed_step_concurrent()
         ds.timed_step()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(device.index)
     clocks.start()
     D.barrier(device)
     torch.cuda.synchronize(device)

@@ -28,17 +28,19 @@
 
 namespace fp8flow {
 
-constexpr int kTStages = 3;
-constexpr int kTBlocksPerSm = 3;
+// kernel variants <STAGES, OUTBUF>: TMA stages of the input ring, and 1 or 2 staging buffers for
+// the transposed tile (2 removes one CTA barrier per tile at the cost of 16 KB of shared memory)
 constexpr int kTThreads = 256;
 constexpr int kMaxSegs = 1024;
 constexpr int kTileBytes = kTile * kTile;
 
+template <int STAGES, int OUTBUF>
 struct TransposeSmem {
-  uint8_t in[kTStages][kTileBytes];
-  uint32_t sc[kTStages][kTile / 4];  // the 128 row-scale bytes of each staged tile
-  uint32_t out[kTile * kTile / 4];
-  uint64_t full_bar[kTStages];
+  uint8_t in[STAGES][kTileBytes];
+  uint32_t sc[STAGES][kTile / 4];  // the 128 row-scale bytes of each staged tile
+  uint32_t out[OUTBUF][kTile * kTile / 4];
+  uint64_t full_bar[STAGES];
+  uint32_t mult[33];               // f16x2 multiplier 2^(8-k) for k = 0..32
   uint32_t red[kTThreads / 32];
   int32_t seg_off[kMaxSegs + 1];
   int32_t blk_prefix[kMaxSegs + 1];
@@ -70,7 +72,8 @@ __device__ __forceinline__ int block_exclusive_scan(int v, uint32_t* warp_tmp, i
 }
 
 // Loads the segment offsets and builds blk_prefix[e] = sum_{e'<e} ceil(m_e'/128) in smem.
-__device__ __forceinline__ void load_segments(TransposeSmem& sm, const int32_t* seg_offsets, int32_t num_segs,
+template <typename Smem>
+__device__ __forceinline__ void load_segments(Smem& sm, const int32_t* seg_offsets, int32_t num_segs,
                                               int64_t rows) {
   const int tid = threadIdx.x;
   if (seg_offsets == nullptr) {
@@ -123,12 +126,15 @@ __device__ __forceinline__ int find_segment(const int32_t* blk_prefix, int num_s
   return lo;
 }
 
-__global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
+template <int STAGES, int OUTBUF, int MINB>
+__global__ void __launch_bounds__(kTThreads, MINB)
     scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q, const uint8_t* __restrict__ s,
                                    int64_t ld_s, int64_t rows, int64_t cols, const int32_t* __restrict__ seg_offsets,
                                    int32_t num_segs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  TransposeSmem& sm = *reinterpret_cast<TransposeSmem*>(smem_raw);
+  using Smem = TransposeSmem<STAGES, OUTBUF>;
+  constexpr int kTStages = STAGES;
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
@@ -139,7 +145,8 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)) : "memory");
   }
-  load_segments(sm, seg_offsets, nsegs, rows);
+  if (tid <= 32) sm.mult[tid] = shift_multiplier(static_cast<uint32_t>(tid));
+  load_segments(sm, seg_offsets, nsegs, rows);  // (ends with a CTA barrier)
 
   const int n_jb = static_cast<int>(cols / kTile);
   const int total_tiles = sm.total_rb * n_jb;  // < 2^31 (rows < 2^31, checked by the ABI)
@@ -203,7 +210,8 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
-      const uint32_t m2 = shift_multiplier(tmax - ((sw >> (8 * r)) & 0xFFu));  // k = T_max - T_row
+      const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
+      const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
       R[r][0] = shift4(v.x, m2);
       R[r][1] = shift4(v.y, m2);
       R[r][2] = shift4(v.z, m2);
@@ -214,7 +222,8 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
       phase ^= 1u;
     }
     const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
-    if (i > 0) __syncthreads();  // previous tile's read-out of sm.out is complete
+    uint32_t* out = sm.out[OUTBUF == 2 ? (i & 1) : 0];
+    if (OUTBUF == 1 && i > 0) __syncthreads();  // previous tile's read-out of the buffer is complete
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
@@ -222,10 +231,10 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
       const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
       const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
       const int j0 = 16 * c + 4 * w;
-      sm.out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
-      sm.out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
-      sm.out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
-      sm.out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
+      out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
+      out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
+      out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
+      out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
     }
     __syncthreads();  // tile consumed (stage free), out buffer complete
 
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(kTThreads, kTBlocksPerSm)
       const int j = (tid >> 3) + 32 * it;
       if (16 * c < rows_valid) {
         const int phys = c ^ ((j >> 4) & 7);
-        const uint4 v = *reinterpret_cast<const uint4*>(&sm.out[j * 32 + 4 * phys]);
+        const uint4 v = *reinterpret_cast<const uint4*>(&out[j * 32 + 4 * phys]);
         st_v4(qTe + (static_cast<int64_t>(jb) * kTile + j) * m + ib * kTile + 16 * c, v);
       }
     }
@@ -268,17 +277,19 @@ static PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
-static int transpose_blocks_per_sm() {
+template <int S, int O, int B>
+static void launch_transpose_variant(const CUtensorMap& map, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                                     const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
+                                     cudaStream_t stream, int num_sms, int64_t ub_tiles) {
   static int occ = 0;
   if (occ == 0) {
-    cudaFuncSetAttribute(scaling_aware_transpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(TransposeSmem)));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scaling_aware_transpose_kernel, kTThreads,
-                                                      sizeof(TransposeSmem)) != cudaSuccess ||
-        occ < 1)
-      occ = 1;
+    cudaFuncSetAttribute(scaling_aware_transpose_kernel<S, O, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(TransposeSmem<S, O>)));
+    occ = occupancy_of(scaling_aware_transpose_kernel<S, O, B>, kTThreads, sizeof(TransposeSmem<S, O>));
   }
-  return occ;
+  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
+  scaling_aware_transpose_kernel<S, O, B><<<static_cast<unsigned>(grid), kTThreads, sizeof(TransposeSmem<S, O>),
+                                             stream>>>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
 }
 
 cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows,
@@ -296,11 +307,19 @@ cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, i
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  int64_t grid = static_cast<int64_t>(num_sms) * transpose_blocks_per_sm();
-  if (grid > ub_tiles) grid = ub_tiles;
-  if (grid < 1) grid = 1;
-  scaling_aware_transpose_kernel<<<static_cast<unsigned>(grid), kTThreads, sizeof(TransposeSmem), stream>>>(
-      map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
+  switch (tune_int("A2_VARIANT", 0)) {
+    case 1:  // 2 stages, double staging buffer: 3 CTAs/SM, one barrier per tile
+      launch_transpose_variant<2, 2, 3>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
+      break;
+    case 2:  // 2 stages, single staging buffer: 4 CTAs/SM
+      launch_transpose_variant<2, 1, 4>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
+      break;
+    case 3:  // 4 stages, double staging buffer: 2 CTAs/SM
+      launch_transpose_variant<4, 2, 2>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
+      break;
+    default:  // 3 stages, single staging buffer: 3 CTAs/SM
+      launch_transpose_variant<3, 1, 3>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
+  }
   return cudaGetLastError();
 }
 

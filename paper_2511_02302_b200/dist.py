@@ -38,17 +38,34 @@ def expert_group(rank: int, num_groups: int = NUM_GROUPS) -> int:
     return rank % num_groups
 
 
+def backend() -> str:
+    """Collective backend: NCCL on the GPU box; FP8FLOW_DIST_BACKEND=gloo runs several ranks on one
+    GPU (a test of the multi-rank orchestration when only one device is available)."""
+    return os.environ.get("FP8FLOW_DIST_BACKEND", "nccl")
+
+
+def local_device(local_rank: int) -> torch.device:
+    n = torch.cuda.device_count()
+    return torch.device("cuda", local_rank % n if n else 0)
+
+
 def barrier(device: torch.device | None = None) -> None:
     if dist.is_initialized():
-        if device is not None and device.type == "cuda":
+        if device is not None and device.type == "cuda" and dist.get_backend() == "nccl":
             dist.barrier(device_ids=[device.index])
         else:
             dist.barrier()
 
 
+def _coll_device(device):
+    """gloo collectives run on host tensors; NCCL on the rank's GPU."""
+    return torch.device("cpu") if dist.get_backend() == "gloo" else device
+
+
 def _reduce(x: float, op, device) -> float:
     if not dist.is_initialized():
         return float(x)
+    device = _coll_device(device)
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=op)
     return float(t.item())
@@ -64,6 +81,8 @@ def sum_over_ranks(x: float, device=torch.device("cpu")) -> float:
 
 def gather_checksums(values: list[int], device=torch.device("cpu")) -> list[list[int]]:
     """All-gather a list of uint64 checksums (carried as int64 bit patterns) from every rank."""
+    if dist.is_initialized():
+        device = _coll_device(device)
     t = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v for v in values], dtype=torch.int64, device=device)
     if not dist.is_initialized():
         return [[v & ((1 << 64) - 1) for v in t.tolist()]]
