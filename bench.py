@@ -469,6 +469,7 @@ def main():
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="config 5: transpose vs naive bandwidth sweep (one JSON line)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
 
@@ -491,6 +492,15 @@ def main():
     D.init(D.backend())
     device = D.local_device(local_rank)
     torch.cuda.set_device(device)
+    if args.sweep:
+        peaks = RL.measured_peaks(ROOT)
+        rows = run_sweep(device, peaks["hbm_gbs"], world)
+        if rank == 0:
+            print(json.dumps({"sweep": "config 5: scaling-aware transpose vs naive dequant->transpose->requant",
+                              "n_gpus": world, "scaling": "weak (same shape per GPU)", "peak_gbs": peaks["hbm_gbs"],
+                              "peak_source": peaks["source"], "l2": "flushed before each launch", "rows": rows}))
+        D.barrier(device)
+        return
     hw = HostWorkload(group)
     ds = DeviceStep(hw, device)
     op_bytes = hw.op_bytes()
@@ -572,6 +582,59 @@ def main():
     D.barrier(device)
     if D.dist.is_initialized():
         D.dist.destroy_process_group()
+
+
+SWEEP_SHAPES = [(128, 128), (256, 256), (512, 512), (1024, 1024), (2048, 2048), (4096, 4096), (4096, 7168),
+                (8192, 7168), (16384, 7168), (32768, 7168), (65536, 7168)]
+
+
+def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
+    """Config 5: scaling-aware transpose vs the naive dequant -> transpose -> requant comparator,
+    128^2 .. 65536x7168, the same shape on every GPU (weak scaling).  Latency per launch (L2
+    flushed before each), GB/s on A2's algorithmic bytes, naive/direct latency ratio."""
+    from paper_2511_02302_b200 import fp8flow as F
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    out = []
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            clean.sum()
+            torch.cuda._sleep(200_000)
+            ev[0].record()
+            fn()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        return statistics.median(ts)
+
+    for rows, cols in SWEEP_SHAPES:
+        x = synth.activations_bf16_device(rows, cols, synth.BASE_SEED + rows + cols, device)
+        q = torch.empty(rows, cols, dtype=torch.uint8, device=device)
+        s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=device)
+        F.fp8flow_quantize_rowwise(x, q, s)
+        del x
+        qT = torch.empty(rows * cols, dtype=torch.uint8, device=device)
+        sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
+        ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, 1), dtype=torch.uint8, device=device)
+        t_d = timed(lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT))
+        t_n = timed(lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws))
+        t_d = D.max_over_ranks(t_d, device)
+        t_n = D.max_over_ranks(t_n, device)
+        nb = RL.transpose_bytes([rows], cols)
+        out.append({"shape": [rows, cols], "direct_us": round(t_d * 1e3, 2), "naive_us": round(t_n * 1e3, 2),
+                    "naive_over_direct": round(t_n / t_d, 2),
+                    "direct_gbs_per_gpu": round(nb / t_d / 1e6, 1), "direct_frac": round(nb / t_d / 1e6 / peak, 3),
+                    "naive_effective_gbs_per_gpu": round(nb / t_n / 1e6, 1),
+                    "naive_actual_gbs_per_gpu": round(RL.naive_transpose_actual_bytes([rows], cols) / t_n / 1e6, 1),
+                    "direct_gbs_all_gpus": round(world * nb / t_d / 1e6, 1)})
+        del q, s, qT, sT, ws
+    return out
 
 
 def ncu_traffic(kernel_op: str):

@@ -59,6 +59,21 @@ def activations_bf16(rows: int, cols: int, seed: int, outlier_frac: float = 0.01
     return (z * gain * ch).to(torch.bfloat16)
 
 
+def activations_bf16_device(rows: int, cols: int, seed: int, device, outlier_frac: float = 0.01,
+                            outlier_gain: float = 20.0, gain_sigma: float = 1.0) -> torch.Tensor:
+    """Same recipe as activations_bf16, drawn on the device (Philox) for the large bandwidth sweep."""
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) & 0xFFFFFFFFFFFFFFFF)
+    z = torch.randn(rows, cols, generator=g, device=device, dtype=torch.float32)
+    gain = torch.exp(torch.randn(rows, 1, generator=g, device=device, dtype=torch.float32) * gain_sigma)
+    n_out = int(round(outlier_frac * cols))
+    ch = torch.ones(1, cols, dtype=torch.float32, device=device)
+    if n_out > 0:
+        idx = torch.randperm(cols, generator=g, device=device)[:n_out]
+        ch[0, idx] = outlier_gain
+    return (z.mul_(gain).mul_(ch)).to(torch.bfloat16)
+
+
 def normal_bf16(rows: int, cols: int, seed: int, sigma: float = 1.0) -> torch.Tensor:
     g = _gen(seed)
     return (torch.randn(rows, cols, generator=g, dtype=torch.float32) * sigma).to(torch.bfloat16)
