@@ -25,7 +25,7 @@ int fp8flow::tune_int(const char* name, int tuned_default) {
   if (!v || !*v) return tuned_default;
   char* end = nullptr;
   const long x = strtol(v, &end, 10);
-  return (*end == 0 && x > 0 && x < (1 << 20)) ? static_cast<int>(x) : tuned_default;
+  return (*end == 0 && x >= 0 && x < (1 << 20)) ? static_cast<int>(x) : tuned_default;
 }
 
 namespace {

@@ -18,6 +18,8 @@
 // Move: warp item = 4 consecutive output rows (balanced contiguous item ranges per warp, one wave
 // of CTAs); the 4 rows stream with 128-bit loads and stores (16 in flight per lane), their scale
 // bytes are gathered per 1x128 tile (all gathers issued before the stores).
+#include <cooperative_groups.h>
+
 #include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
@@ -166,6 +168,133 @@ __global__ void __launch_bounds__(kChunk) plan_place_kernel(const int32_t* __res
   }
 }
 
+// Single-launch plan (cooperative launch, all chunk CTAs co-resident): each CTA builds its chunk's
+// (expert x token) bit matrix once, derives its per-expert counts from it by popcount and publishes
+// them, then one grid-wide barrier, then the same placement as plan_place without re-reading the
+// routing rows.  Used whenever the chunks fit on the GPU at once; otherwise the 2-kernel path.
+__global__ void __launch_bounds__(kChunk) plan_fused_kernel(const int32_t* __restrict__ topk_idx, int64_t T, int K,
+                                                            int e0, int E_loc, int align, int64_t n_chunks,
+                                                            int32_t* __restrict__ chunk_counts,
+                                                            int32_t* __restrict__ expert_offsets,
+                                                            int32_t* __restrict__ row_map,
+                                                            int32_t* __restrict__ src_of_row, int64_t max_rows,
+                                                            int32_t* __restrict__ status) {
+  extern __shared__ uint32_t smem_plan[];
+  uint32_t* bits = smem_plan;                                            // [E_loc][kWords]
+  int32_t* pre = reinterpret_cast<int32_t*>(bits + E_loc * kWords);      // [E_loc][kWords]
+  int32_t* off = pre + E_loc * kWords;                                   // [E_loc + 1]
+  int32_t* base = off + E_loc + 1;                                       // [E_loc]
+  __shared__ int32_t warp_tot[kChunk / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t chunk = blockIdx.x;
+  const int64_t t = chunk * kChunk + tid;
+
+  for (int i = tid; i < E_loc * kWords; i += kChunk) bits[i] = 0;
+  __syncthreads();
+  int32_t le[16];  // this token's local expert ids (-1: not local), k order; K <= 16
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    le[k] = -1;
+    if (k < K && t < T) {
+      const int e = topk_idx[t * K + k] - e0;
+      if (e >= 0 && e < E_loc) le[k] = e;
+    }
+    if (le[k] >= 0) atomicOr(&bits[le[k] * kWords + (tid >> 5)], 1u << lane);
+  }
+  __syncthreads();
+  // prefix popcounts along each expert row; the row total is this chunk's count for the expert
+  for (int r0 = warp * 2; r0 < E_loc; r0 += (kChunk / 32) * 2) {
+    const int row = r0 + (lane >> 4), wi = lane & 15;
+    const bool ok = row < E_loc;
+    const int c = ok ? __popc(bits[row * kWords + wi]) : 0;
+    int inc = c;
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, d, 16);
+      if (wi >= d) inc += n;
+    }
+    if (ok) {
+      pre[row * kWords + wi] = inc - c;
+      if (wi == 15) chunk_counts[chunk * E_loc + row] = inc;
+    }
+  }
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+
+  // per-expert totals and this chunk's base (2 experts per thread: E_loc <= 1024)
+  int cnt[2] = {0, 0}, pad[2] = {0, 0};
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int e = 2 * tid + j;
+    if (e < E_loc) {
+      int total = 0, mine = 0;
+#pragma unroll 8
+      for (int64_t c = 0; c < n_chunks; ++c) {
+        const int v = __ldcg(chunk_counts + c * E_loc + e);
+        mine += (c < chunk) ? v : 0;
+        total += v;
+      }
+      base[e] = mine;
+      cnt[j] = total;
+      pad[j] = (total + align - 1) / align * align;
+    }
+  }
+  const int tsum = pad[0] + pad[1];
+  int incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += n;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  int wbase = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kChunk / 32; ++w) {
+    wbase += (w < warp) ? warp_tot[w] : 0;
+    all += warp_tot[w];
+  }
+  int run = wbase + incl - tsum;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int e = 2 * tid + j;
+    if (e < E_loc) {
+      off[e] = run;
+      if (chunk == 0) {
+        expert_offsets[e] = run;
+        for (int r = run + cnt[j]; r < run + pad[j]; ++r)
+          if (r < max_rows) src_of_row[r] = -1;  // PAD rows (R16: after the real rows)
+      }
+      run += pad[j];
+    }
+  }
+  if (tid == 0) {
+    off[E_loc] = all;
+    if (chunk == 0) {
+      expert_offsets[E_loc] = all;
+      *status = all > max_rows ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (t < T) {
+    const uint32_t below = (1u << lane) - 1u;
+    const int w = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < K) {
+        int32_t row = -1;
+        if (le[k] >= 0) {
+          const int e = le[k];
+          row = off[e] + base[e] + pre[e * kWords + w] + __popc(bits[e * kWords + w] & below);
+          if (row < max_rows) src_of_row[row] = static_cast<int32_t>(t);
+          else row = -1;
+        }
+        row_map[t * K + k] = row;
+      }
+    }
+  }
+}
+
 cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int32_t top_k, int32_t expert_begin,
                                 int32_t num_local_experts, int32_t align, int32_t* row_map, int32_t* src_of_row,
                                 int64_t max_rows, int32_t* expert_offsets, void* ws, cudaStream_t stream) {
@@ -173,6 +302,31 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
   const int64_t grid = chunks > 0 ? chunks : 1;  // one CTA even without tokens: writes offsets
   int32_t* status = static_cast<int32_t*>(ws);
   int32_t* chunk_counts = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + 256);
+  const size_t smem = static_cast<size_t>(num_local_experts) * kWords * 8 + 4 * (2 * num_local_experts + 1);
+  // single cooperative launch when every chunk CTA can be resident at once
+  static int coop_occ = -1;
+  if (coop_occ < 0) {
+    int dev = 0, coop = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(plan_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+    int occ = 0;
+    if (coop && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plan_fused_kernel, kChunk, 64 * 1024) ==
+                    cudaSuccess)
+      coop_occ = occ * sms;  // conservative: occupancy at 64 KB of shared memory
+    else
+      coop_occ = 0;
+  }
+  if (top_k <= 16 && smem <= 64 * 1024 && grid <= coop_occ && tune_int("PLAN_FUSED", 1) == 1) {
+    int64_t n_chunks = grid;
+    int K = top_k, e0 = expert_begin, E = num_local_experts, al = align;
+    int64_t T = num_tokens, mr = max_rows;
+    void* args[] = {const_cast<int32_t**>(&topk_idx), &T, &K, &e0, &E, &al, &n_chunks, &chunk_counts,
+                    &expert_offsets, &row_map, &src_of_row, &mr, &status};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_fused_kernel), dim3(static_cast<unsigned>(grid)),
+                                       dim3(kChunk), args, smem, stream);
+  }
   if (chunks == 0) {
     cudaError_t e = cudaMemsetAsync(chunk_counts, 0, 4 * static_cast<size_t>(num_local_experts), stream);
     if (e != cudaSuccess) return e;
@@ -180,7 +334,6 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
     plan_count_kernel<<<static_cast<unsigned>(chunks), kChunk, 4 * num_local_experts, stream>>>(
         topk_idx, num_tokens, top_k, expert_begin, num_local_experts, chunk_counts);
   }
-  const size_t smem = static_cast<size_t>(num_local_experts) * kWords * 8 + 4 * (2 * num_local_experts + 1);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(plan_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   plan_place_kernel<<<static_cast<unsigned>(grid), kChunk, smem, stream>>>(
@@ -303,7 +456,7 @@ __global__ void __launch_bounds__(256, 1) permute_pad_kernel(const uint8_t* __re
 cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
                                const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_local_experts,
                                int64_t max_rows, uint8_t* q_out, uint8_t* s_out, cudaStream_t stream, int num_sms) {
-  const int ctas = tune_int("CTAS_PER_SM_A3", 2);  // co-resident CTAs per SM (smem budget split)
+  const int ctas = tune_int("CTAS_PER_SM_A3", 2) > 0 ? tune_int("CTAS_PER_SM_A3", 2) : 1;  // co-resident CTAs per SM (smem budget split)
   const size_t budget = kMoveSmemBudget / ctas;
   int nslots = static_cast<int>((budget - 8 * kMaxMoveSlots - hidden) / hidden);
   if (nslots > kMaxMoveSlots) nslots = kMaxMoveSlots;
@@ -469,7 +622,7 @@ __global__ void __launch_bounds__(256, 1) unpermute_unpad_kernel(const __nv_bflo
 cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t* row_map, const float* probs,
                                    int64_t num_tokens, int32_t top_k, void* y, cudaStream_t stream, int num_sms) {
   const int64_t row_bytes = 2 * hidden;
-  const int ctas = tune_int("CTAS_PER_SM_A4", 2);  // co-resident CTAs per SM (smem budget split)
+  const int ctas = tune_int("CTAS_PER_SM_A4", 2) > 0 ? tune_int("CTAS_PER_SM_A4", 2) : 1;  // co-resident CTAs per SM (smem budget split)
   int nslots = static_cast<int>(kUnpermSmemBudget / ctas / row_bytes);
   if (nslots > kMaxUnpermSlots) nslots = kMaxUnpermSlots;
   // a token's rows must all fit the ring when the columns take more than one consumer pass

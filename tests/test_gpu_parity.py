@@ -190,10 +190,12 @@ def run_plan(F, topk_idx, e0, E_loc, align=16, max_rows=None):
     return host(row_map), host(src), host(off), int(host(ws[:4].view(torch.int32))[0])
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])  # single cooperative launch / 2-kernel fallback
 @pytest.mark.parametrize("T,E,K,group,ngroups,align", [
     (16384, 256, 8, 0, 8, 16), (16384, 256, 8, 5, 8, 16), (3000, 64, 6, 0, 1, 16), (777, 32, 4, 1, 4, 128),
     (5, 8, 2, 0, 2, 16)])
-def test_permute_plan_parity(F, orc, T, E, K, group, ngroups, align):
+def test_permute_plan_parity(F, orc, T, E, K, group, ngroups, align, fused, monkeypatch):
+    monkeypatch.setenv("FP8FLOW_PLAN_FUSED", fused)
     idx, _ = synth.routing(T, 400 + T, num_experts=E, top_k=K, num_groups=min(8, E // 4), topk_groups=2)
     per = E // ngroups
     e0 = group * per
@@ -202,6 +204,13 @@ def test_permute_plan_parity(F, orc, T, E, K, group, ngroups, align):
     assert status == 0
     assert np.array_equal(off, off_ref) and np.array_equal(rm, rm_ref)
     assert np.array_equal(src[: off[-1]], src_ref[: off[-1]])
+
+
+def test_permute_plan_zero_tokens(F):
+    idx = np.zeros((0, 8), np.int32)
+    rm, src, off, status = run_plan(F, np.zeros((1, 8), np.int32)[:0], 0, 4, 16, max_rows=16)
+    assert off.tolist() == [0, 0, 0, 0, 0] and status == 0
+    del idx
 
 
 def test_permute_plan_no_tokens_for_some_experts(F, orc):
