@@ -587,6 +587,9 @@ __global__ void __launch_bounds__(256, 1) unpermute_unpad_kernel(const __nv_bflo
           }
           // the last pass over the columns releases the slot
           if (c0 + 224 * kUnpermChunksPerThread >= n_chunks) {
+            // the warp's generic-proxy reads of the slot are ordered before the producer's next
+            // async-proxy (bulk copy) write into it
+            fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
           }

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
       va[i] = *reinterpret_cast<const uint4*>(&sm.a[st][off]);
       vb[i] = *reinterpret_cast<const uint4*>(&sm.b[st][off]);
     }
+    fence_proxy_async_smem();  // reads (generic proxy) before the next TMA write (async proxy)
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // stage data is in registers: release it
     if (++st == kSwStages) {
