@@ -63,6 +63,8 @@ def lib():
                 "orc_swiglu_f32": (None, [P, I64, I64, P]),
                 "orc_swiglu_quant": (None, [P, I64, I64, P, P, I64]),
                 "orc_checksum64": (ctypes.c_uint64, [P, I64]),
+                "orc_swiglu_bwd_f32": (None, [P, P, I64, I64, P]),
+                "orc_swiglu_bwd_quant": (None, [P, P, I64, I64, P, P, I64]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -300,6 +302,36 @@ def swiglu_quant(h_bits, ld_s: int | None = None, threads: int | None = None):
 
     def work(lo, hi):
         L.orc_swiglu_quant(_p(h_bits, lo * F2 * 2), hi - lo, F, _p(q, lo * F), _p(s, lo), ld_s)
+
+    _run_split(rows, threads, work)
+    return q, s
+
+
+def swiglu_bwd_f32(h_bits, dA_bits):
+    """NEXT-1: fp32 [rows, 2F] = [dA*b*silu'(a) | dA*silu(a)] (fp64 evaluation, one rounding)."""
+    h_bits = np.ascontiguousarray(h_bits, dtype=np.uint16)
+    dA_bits = np.ascontiguousarray(dA_bits, dtype=np.uint16)
+    rows, F2 = h_bits.shape
+    assert dA_bits.shape == (rows, F2 // 2)
+    dh = np.zeros((rows, F2), np.float32)
+    lib().orc_swiglu_bwd_f32(_p(h_bits), _p(dA_bits), rows, F2 // 2, _p(dh))
+    return dh
+
+
+def swiglu_bwd_quant(h_bits, dA_bits, ld_s: int | None = None, threads: int | None = None):
+    """NEXT-1: h BF16 [rows, 2F], dA BF16 [rows, F] -> (q [rows, 2F], s [2F/128, ld_s])."""
+    h_bits = np.ascontiguousarray(h_bits, dtype=np.uint16)
+    dA_bits = np.ascontiguousarray(dA_bits, dtype=np.uint16)
+    rows, F2 = h_bits.shape
+    F = F2 // 2
+    ld_s = rows if ld_s is None else ld_s
+    q = np.zeros((rows, F2), np.uint8)
+    s = np.zeros((F2 // 128, ld_s), np.uint8)
+    L = lib()
+
+    def work(lo, hi):
+        L.orc_swiglu_bwd_quant(_p(h_bits, lo * F2 * 2), _p(dA_bits, lo * F * 2), hi - lo, F, _p(q, lo * F2),
+                               _p(s, lo), ld_s)
 
     _run_split(rows, threads, work)
     return q, s

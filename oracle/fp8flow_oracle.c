@@ -28,6 +28,9 @@
  *   orc_swiglu_f32             pinned against torch float64 silu (library routine)
  *   orc_swiglu_quant           partly pinned (H=0, special cases); beyond that the fp64
  *                               definition + tolerance governs -- "parity partly unpinned"
+ *   orc_swiglu_bwd_f32         pinned against torch float64 autograd of silu(a)*b (library) and
+ *                               central finite differences of the fp64 forward
+ *   orc_swiglu_bwd_quant       as orc_swiglu_quant: the fp64 definition + tolerance beyond pins
  *   orc_checksum64             closed form (DESIGN.md §4 C11)
  */
 #include <math.h>
@@ -399,6 +402,45 @@ void orc_swiglu_quant(const uint16_t* h, int64_t rows, int64_t F, uint8_t* q, ui
         orc_swiglu_f32(h + i * 2 * F, 1, F, yf);
         for (int64_t j = 0; j < F; j++) yd[j] = (double)yf[j];
         quantize_row_f64(yd, F, q + i * F, s, ld_s, i);
+    }
+    free(yf);
+    free(yd);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT-1 SwiGLU backward (the activation's gradient at the BF16 boundary; R31):
+ *     y = silu(a) * b, silu(a) = a * sig(a), sig(a) = 1 / (1 + e^-a)
+ *     da = dA * b * silu'(a),  silu'(a) = sig(a) * (1 + a * (1 - sig(a)))
+ *     db = dA * silu(a)
+ *     dH = [da | db]  (the gate half first, the same column order as h)
+ *     evaluated in double, each rounded once to fp32.
+ * ------------------------------------------------------------------------------------------ */
+void orc_swiglu_bwd_f32(const uint16_t* h, const uint16_t* dA, int64_t rows, int64_t F, float* dh)
+{
+    for (int64_t i = 0; i < rows; i++)
+        for (int64_t j = 0; j < F; j++) {
+            double a = bf16_to_double(h[i * 2 * F + j]);
+            double b = bf16_to_double(h[i * 2 * F + F + j]);
+            double g = bf16_to_double(dA[i * F + j]);
+            double sig = 1.0 / (1.0 + exp(-a));
+            double silu = a * sig;
+            double dsilu = sig * (1.0 + a * (1.0 - sig));
+            dh[i * 2 * F + j] = (float)(g * b * dsilu);
+            dh[i * 2 * F + F + j] = (float)(g * silu);
+        }
+}
+
+/* NEXT-1 fused SwiGLU backward + quantize: C4 applied to each row of the fp32 dH (1x128 tiles along
+ * 2F, fp32 amax).  q [rows][2F], s [2F/128][ld_s]. */
+void orc_swiglu_bwd_quant(const uint16_t* h, const uint16_t* dA, int64_t rows, int64_t F, uint8_t* q, uint8_t* s,
+                          int64_t ld_s)
+{
+    float* yf = (float*)malloc(sizeof(float) * (size_t)(2 * F));
+    double* yd = (double*)malloc(sizeof(double) * (size_t)(2 * F));
+    for (int64_t i = 0; i < rows; i++) {
+        orc_swiglu_bwd_f32(h + i * 2 * F, dA + i * F, 1, F, yf);
+        for (int64_t j = 0; j < 2 * F; j++) yd[j] = (double)yf[j];
+        quantize_row_f64(yd, 2 * F, q + i * 2 * F, s, ld_s, i);
     }
     free(yf);
     free(yd);

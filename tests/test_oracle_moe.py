@@ -172,3 +172,59 @@ def test_swiglu_quant_special_cases(orc):
     q, s = orc.swiglu_quant(synth.bf16_bits(h))
     q2, s2 = orc.quantize_rows_f64(orc.swiglu_f32(synth.bf16_bits(h)).astype(np.float64))
     assert np.array_equal(q, q2) and np.array_equal(s, s2)
+
+
+# ------------------------------------------------------------------------------ NEXT-1 SwiGLU backward
+def test_swiglu_bwd_matches_torch_float64_autograd(orc):
+    """Library pin: torch float64 autograd of silu(a) * b with upstream gradient dA."""
+    rows, F = 128, 256
+    h = synth.normal_bf16(rows, 2 * F, 20, sigma=1.5)
+    dA = synth.normal_bf16(rows, F, 21, sigma=0.7)
+    dh = orc.swiglu_bwd_f32(synth.bf16_bits(h), synth.bf16_bits(dA))
+    hd = h.to(torch.float64).requires_grad_(True)
+    y = torch.nn.functional.silu(hd[:, :F]) * hd[:, F:]
+    y.backward(dA.to(torch.float64))
+    ref = hd.grad.to(torch.float32).numpy()
+    diff = dh != ref
+    assert diff.mean() < 1e-4                       # fp32 rounding-boundary cases only
+    if diff.any():
+        assert np.all(np.abs(dh[diff].view(np.int32) - ref[diff].view(np.int32)) == 1)
+
+
+def test_swiglu_bwd_central_differences(orc):
+    """the analytic gradient agrees with central differences of the fp64 forward."""
+    rng = np.random.default_rng(22)
+    a = rng.normal(0, 2, 400)
+    b = rng.normal(0, 1, 400)
+    # BF16-representable inputs so the oracle sees exactly these values
+    a = torch.tensor(a).to(torch.bfloat16).to(torch.float64).numpy()
+    b = torch.tensor(b).to(torch.bfloat16).to(torch.float64).numpy()
+    h = np.concatenate([a, b])[None, :].astype(np.float64)
+    hb = synth.bf16_bits(torch.from_numpy(h).to(torch.bfloat16))
+    one = synth.bf16_bits(torch.ones(1, 400, dtype=torch.bfloat16))
+    dh = orc.swiglu_bwd_f32(hb, one).astype(np.float64)[0]
+    f = lambda aa, bb: aa / (1 + np.exp(-aa)) * bb  # noqa: E731
+    eps = 1e-4
+    fd_a = (f(a + eps, b) - f(a - eps, b)) / (2 * eps)
+    fd_b = (f(a, b + eps) - f(a, b - eps)) / (2 * eps)
+    scale = np.maximum(1.0, np.abs(fd_a))
+    assert np.all(np.abs(dh[:400] - fd_a) <= 1e-6 * scale + 2e-7 * np.abs(b) * 4)
+    assert np.all(np.abs(dh[400:] - fd_b) <= 1e-6 * np.maximum(1.0, np.abs(fd_b)))
+
+
+def test_swiglu_bwd_special_cases_and_quant(orc):
+    # S:327: a = 0, b = 1, dY = 1 -> da = silu'(0) = 0.5, db = silu(0) = 0
+    F = 128
+    h = torch.zeros(1, 2 * F)
+    h[0, F:] = 1.0
+    dh = orc.swiglu_bwd_f32(synth.bf16_bits(h.to(torch.bfloat16)), synth.bf16_bits(torch.ones(1, F).to(torch.bfloat16)))
+    assert np.all(dh[0, :F] == 0.5) and np.all(dh[0, F:] == 0.0)
+    # dA = 0 -> dH = 0 -> zero codes and the neutral scale (R11)
+    hb = synth.bf16_bits(synth.normal_bf16(4, 2 * F, 23))
+    q, s = orc.swiglu_bwd_quant(hb, np.zeros((4, F), np.uint16))
+    assert np.all((q & 0x7F) == 0) and np.all(s == 0)
+    # fused = quantize(dH) on the fp32 values
+    dA = synth.bf16_bits(synth.normal_bf16(4, F, 24))
+    q, s = orc.swiglu_bwd_quant(hb, dA)
+    q2, s2 = orc.quantize_rows_f64(orc.swiglu_bwd_f32(hb, dA).astype(np.float64))
+    assert np.array_equal(q, q2) and np.array_equal(s, s2)
