@@ -423,6 +423,33 @@ class ClockSampler:
 # =============================================================================================
 # config-2 sub-measurement (4096 x 7168, one expert): A1, A2 and the naive comparator
 # =============================================================================================
+def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20) -> dict:
+    """NEXT rows measured on the same workload (not part of the headline step): NEXT-1 fused
+    SwiGLU backward + quant of dA [R, 2048] with the saved fc1 output h [R, 4096]."""
+    F = ds.F
+    hw = ds.hw
+    dA = synth.normal_bf16(hw.R, FFN, synth.BASE_SEED + 5, sigma=0.5).to(ds.dev)
+    q = torch.empty(hw.R, 2 * FFN, dtype=torch.uint8, device=ds.dev)
+    s = torch.empty(2 * FFN // 128, hw.R, dtype=torch.uint8, device=ds.dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    fn = lambda: F.fp8flow_swiglu_bwd_quant(ds.h, dA, q, s, rows_dev=ds.off[hw.E_loc:])  # noqa: E731
+    fn()
+    ts = []
+    for _ in range(reps):
+        ds.flush_l2()
+        torch.cuda._sleep(1_000_000)
+        ev[0].record()
+        fn()
+        ev[1].record()
+        ev[1].synchronize()
+        ts.append(ev[0].elapsed_time(ev[1]))
+    ms = statistics.median(ts)
+    nb = RL.swiglu_bwd_quant_bytes(hw.R, FFN)
+    return {"NEXT1_swiglu_bwd_quant": {"us": round(ms * 1e3, 2), "bytes": nb, "gbs": round(nb / ms / 1e6, 1),
+                                       "frac": round(nb / ms / 1e6 / peak, 3),
+                                       "shape": {"h": [hw.R, 2 * FFN], "dA": [hw.R, FFN]}}}
+
+
 def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
     from paper_2511_02302_b200 import fp8flow as F
 
@@ -578,6 +605,7 @@ def main():
         }
         if world == 1:
             line["cfg2"] = cfg2_measure(device, peak)
+            line["next_ops"] = next_ops_measure(ds, peak)
         print(json.dumps(line), flush=True)
     D.barrier(device)
     if D.dist.is_initialized():

@@ -184,6 +184,22 @@ FP8FLOW_API int fp8flow_unpermute_unpad(const void* x_bf16, int64_t hidden, cons
 FP8FLOW_API int fp8flow_swiglu_quant(const void* h_bf16, int64_t rows_max, const int32_t* rows_dev, int64_t ffn, uint8_t* q,
                          uint8_t* s, int64_t ld_s, void* stream);
 
+/* ==========================================================================================
+ * NEXT-1  Fused SwiGLU backward + quantization: the activation's gradient at the BF16 boundary of
+ *     the backward pass (R31), from the saved fc1 output h = [a | b] and the upstream
+ *     gradient dA (fc2 dgrad output):
+ *        da = dA * b * silu'(a),  silu'(a) = sig(a) (1 + a (1 - sig(a))),   db = dA * silu(a)
+ *     dH = [da | db] quantized row-wise (A1's 1x128 tiles along 2*ffn) for the fc1 dgrad/wgrad
+ *     GEMMs.  Reference: fp64 evaluation rounded once to fp32; acceptance as A5.
+ *   h_bf16  [rows_max][2*ffn] BF16, dA_bf16 [rows_max][ffn] BF16 (16-byte aligned)
+ *   rows_dev device int32 actual row count or NULL (rows_max)
+ *   q       [rows_max][2*ffn] E4M3 codes; s [2*ffn/128][ld_s] MN-major, ld_s >= rows_max, % 16 == 0
+ *   ffn % 128 == 0.
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_swiglu_bwd_quant(const void* h_bf16, const void* dA_bf16, int64_t rows_max,
+                                         const int32_t* rows_dev, int64_t ffn, uint8_t* q, uint8_t* s,
+                                         int64_t ld_s, void* stream);
+
 /* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
  * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */
 FP8FLOW_API int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream);

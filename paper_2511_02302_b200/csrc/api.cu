@@ -214,6 +214,19 @@ int fp8flow_swiglu_quant(const void* h_bf16, int64_t rows_max, const int32_t* ro
       launch_swiglu_quant(h_bf16, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<cudaStream_t>(stream), sms));
 }
 
+int fp8flow_swiglu_bwd_quant(const void* h_bf16, const void* dA_bf16, int64_t rows_max, const int32_t* rows_dev,
+                             int64_t ffn, uint8_t* q, uint8_t* s, int64_t ld_s, void* stream) {
+  if (rows_max < 0 || ffn <= 0 || ffn % 128 != 0) return FP8FLOW_ERR_SHAPE;
+  if (ld_s < rows_max || ld_s % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (rows_max == 0) return FP8FLOW_OK;
+  if (!h_bf16 || !dA_bf16 || !q || !s) return FP8FLOW_ERR_NULL;
+  if (!aligned16(h_bf16) || !aligned16(dA_bf16) || !aligned16(q)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_swiglu_bwd_quant(h_bf16, dA_bf16, rows_max, rows_dev, ffn, q, s, ld_s,
+                                          static_cast<cudaStream_t>(stream), sms));
+}
+
 int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream) {
   if (nbytes < 0) return FP8FLOW_ERR_SHAPE;
   if (!out_dev || (nbytes > 0 && !buf)) return FP8FLOW_ERR_NULL;

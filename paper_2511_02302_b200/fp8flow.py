@@ -42,6 +42,7 @@ SIGNATURES = {
     "fp8flow_unpermute_unpad": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _I32, _P, _P]),
     "fp8flow_swiglu_quant": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _P]),
     "fp8flow_checksum64": (ctypes.c_int, [_P, _I64, _P, _P]),
+    "fp8flow_swiglu_bwd_quant": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P]),
 }
 
 
@@ -179,6 +180,16 @@ def fp8flow_swiglu_quant(h: torch.Tensor, q: torch.Tensor, s: torch.Tensor, rows
     rows_max, F2 = h.shape
     _check(lib().fp8flow_swiglu_quant(_ptr(h), rows_max, _ptr(rows_dev), F2 // 2, _ptr(_u8(q)), _ptr(_u8(s)),
                                       s.shape[1], _stream(stream)), "fp8flow_swiglu_quant")
+
+
+def fp8flow_swiglu_bwd_quant(h: torch.Tensor, dA: torch.Tensor, q: torch.Tensor, s: torch.Tensor,
+                             rows_dev: torch.Tensor | None = None, stream=None) -> None:
+    """NEXT-1: h bf16 [rows, 2F], dA bf16 [rows, F] -> q uint8 [rows, 2F], s uint8 [2F/128, ld_s]."""
+    assert h.dtype == torch.bfloat16 and dA.dtype == torch.bfloat16
+    rows_max, F2 = h.shape
+    assert dA.shape == (rows_max, F2 // 2)
+    _check(lib().fp8flow_swiglu_bwd_quant(_ptr(h), _ptr(dA), rows_max, _ptr(rows_dev), F2 // 2, _ptr(_u8(q)),
+                                          _ptr(_u8(s)), s.shape[1], _stream(stream)), "fp8flow_swiglu_bwd_quant")
 
 
 def fp8flow_checksum64(buf: torch.Tensor, out: torch.Tensor, stream=None) -> None:

@@ -54,6 +54,12 @@ def swiglu_quant_bytes(rows: int, ffn: int) -> int:
     return rows * (4 * ffn + ffn + ffn // 128)
 
 
+def swiglu_bwd_quant_bytes(rows: int, ffn: int) -> int:
+    """NEXT-1: BF16 h [rows, 2F] and dA [rows, F] read, E4M3 dH [rows, 2F] written, one scale byte
+    per 1x128 output tile (4.008 B per output element)."""
+    return rows * (4 * ffn + 2 * ffn + 2 * ffn + 2 * ffn // 128)
+
+
 def measured_peaks(root: str) -> dict:
     """HBM copy bandwidth to use as the roofline denominator: the driver-measured figure when
     MEASURED_PEAKS.json exists, else the profiling guide's fallback (6650 GB/s)."""

@@ -341,3 +341,54 @@ def test_checksum_matches_oracle(F, orc):
         torch.cuda.synchronize()
         got = int(np.array(out.cpu().numpy()).view(np.uint64)[0])
         assert got == orc.checksum64(b)
+
+
+# =========================================================================================== NEXT-1
+def run_swiglu_bwd(F, h_bits, dA_bits, rows_dev=None):
+    rows, F2 = h_bits.shape
+    ld_s = (rows + 15) // 16 * 16
+    q = torch.empty(rows, F2, dtype=torch.uint8, device="cuda")
+    s = torch.full((F2 // 128, ld_s), 0xAB, dtype=torch.uint8, device="cuda")
+    F.fp8flow_swiglu_bwd_quant(bf16_dev(h_bits), bf16_dev(dA_bits), q, s,
+                               rows_dev=None if rows_dev is None else dev(rows_dev))
+    torch.cuda.synchronize()
+    return host(q), host(s)
+
+
+@pytest.mark.parametrize("rows,ffn,sigma", [(64, 128, 1.5), (100, 2048, 1.5), (2048, 2048, 3.0),
+                                            (15872, 2048, 1.5)])
+def test_swiglu_bwd_quant_parity(F, orc, rows, ffn, sigma):
+    hb = synth.bf16_bits(synth.normal_bf16(rows, 2 * ffn, 800 + rows, sigma=sigma))
+    db = synth.bf16_bits(synth.normal_bf16(rows, ffn, 801 + rows, sigma=0.5))
+    q, s = run_swiglu_bwd(F, hb, db)
+    q_ref, s_ref = orc.swiglu_bwd_quant(hb, db, ld_s=s.shape[1])
+    check_swiglu(q, s, q_ref, s_ref, rows)
+
+
+def test_swiglu_bwd_quant_adversarial(F, orc):
+    """a at the root of silu' (~ -1.2785), whole tiles near it, tile maxima at 448*2^T, |a| > 64,
+    tiny gradients, zero rows, and rows_dev."""
+    rows, ffn = 64, 256
+    rng = np.random.default_rng(31)
+    a = rng.normal(0, 1.5, (rows, ffn)).astype(np.float32)
+    b = rng.normal(0, 1.0, (rows, ffn)).astype(np.float32)
+    g = rng.normal(0, 1.0, (rows, ffn)).astype(np.float32)
+    a[0:8, :] = -1.2785 + rng.normal(0, 1e-3, (8, ffn))            # whole tiles at the root of silu'
+    a[8:16, ::3] = -1.2785
+    for i in range(16, 40):                                          # db tile maxima near 448*2^T
+        T = int(rng.integers(-4, 4))
+        a[i, 5] = 30.0
+        g[i, 5] = 448.0 * 2.0 ** T / 30.0 * (1 + (i - 28) * 2.0 ** -9)
+    a[40, :] = -80.0
+    a[41, :] = 70.0
+    g[42, :] = 1e-30
+    a[43, :], b[43, :], g[43, :] = 0.0, 0.0, 0.0
+    h = np.concatenate([a, b], axis=1)
+    hb = synth.bf16_bits(torch.from_numpy(h).to(torch.bfloat16))
+    dbits = synth.bf16_bits(torch.from_numpy(g).to(torch.bfloat16))
+    q, s = run_swiglu_bwd(F, hb, dbits)
+    q_ref, s_ref = orc.swiglu_bwd_quant(hb, dbits, ld_s=s.shape[1])
+    check_swiglu(q, s, q_ref, s_ref, rows)
+    q2, s2 = run_swiglu_bwd(F, hb, dbits, rows_dev=np.array([48], np.int32))
+    check_swiglu(q2, s2, q_ref, s_ref, 48)
+    assert np.all(s2[:, 48:] == 0xAB)
