@@ -355,7 +355,7 @@ def run_swiglu_bwd(F, h_bits, dA_bits, rows_dev=None):
     return host(q), host(s)
 
 
-@pytest.mark.parametrize("rows,ffn,sigma", [(64, 128, 1.5), (100, 2048, 1.5), (2048, 2048, 3.0),
+@pytest.mark.parametrize("rows,ffn,sigma", [(64, 128, 1.5), (77, 384, 2.0), (100, 2048, 1.5), (2048, 2048, 3.0),
                                             (15872, 2048, 1.5)])
 def test_swiglu_bwd_quant_parity(F, orc, rows, ffn, sigma):
     hb = synth.bf16_bits(synth.normal_bf16(rows, 2 * ffn, 800 + rows, sigma=sigma))
