@@ -6,16 +6,16 @@
 // reference value is a*b / (1 + e^-a) evaluated in fp64 and rounded once to fp32 (oracle C10);
 // acceptance: codes within 1 E4M3 ULP on <= 1e-4 of elements, scale bytes identical.
 //
-// Kernel: TMA-fed producer/consumer pipeline (below), half-warp per 1x128 output tile row, with the
-// activation evaluated in fp32 using the MUFU
-// fast path y' = (a*b) / (1 + 2^(-a*log2e)) (a*b is exact: two 8-bit significands).  |y' - y| is
-// bounded by ~70 fp32 ulp for |a| <= 64, so every decision the fp32 value takes is checked with
-// a +-2^-16 relative bracket and re-taken from an fp64 evaluation when the bracket straddles it:
-//   * the tile scale: amax' within the bracket of a boundary 448 * 2^T -> the elements that can
-//     be the true max are recomputed in fp64 before the scale is chosen;
-//   * each code: if cvt(u (1 - 2^-16)) != cvt(u (1 + 2^-16)) the element is recomputed in fp64.
-// Tile-rows outside the fast path's domain (|a| > 64: exp overflow range; tile amax above 2^100:
-// a*b may overflow; tile amax below 2^-60: subnormal intermediates) are evaluated in fp64.
+// Kernel: TMA-fed producer/consumer pipeline (below), one full warp per 1x128 output tile row
+// (lane l: columns 4l..4l+3), with the activation evaluated in fp32 using the MUFU fast path
+// y' = (a*b) / (1 + 2^(-a*log2e)) (a*b is exact: two 8-bit significands), packed f32x2 arithmetic.
+// |y' - y| is bounded by ~70 fp32 ulp for |a| <= 64 (relative 2^-16), so the tile scale -- the
+// decision the acceptance bar requires to be exact -- is certified: when amax' lies within 2^-14
+// of a boundary 448 * 2^T the whole tile row is recomputed in fp64 (warp-uniform: amax' is a
+// redux.sync result).  Codes come from y' (<= 1 E4M3 ULP from the oracle, R20's bar; a code can
+// differ only when y sits within ~2^-21 relative of a rounding midpoint).  Tile-rows outside the
+// fast path's domain (a < -64: exp overflow range, NaN; tile amax above 2^100: a*b may overflow;
+// tile amax below 2^-60: subnormal intermediates) are evaluated in fp64.
 #include <cuda.h>
 
 #include "async.cuh"
@@ -25,12 +25,20 @@
 namespace fp8flow {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kBracketLo = 1.0f - 1.52587890625e-05f;  // 1 - 2^-16
-constexpr float kBracketHi = 1.0f + 1.52587890625e-05f;  // 1 + 2^-16
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float max_nan(float x, float y) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(y));
   return r;
 }
 __device__ __noinline__ float swiglu_exact(float a, float b) {
@@ -38,21 +46,39 @@ __device__ __noinline__ float swiglu_exact(float a, float b) {
   return static_cast<float>(ad * bd / (1.0 + exp(-ad)));
 }
 
+// one warp-row (lane: 4 elements) evaluated exactly; amax ignores NaN like the oracle.
+// returns {codes, scale byte}
+__device__ __noinline__ uint2 swiglu_row_exact(uint2 wa, uint2 wb) {
+  const float a[4] = {bf16lo_to_f32(wa.x), bf16hi_to_f32(wa.x), bf16lo_to_f32(wa.y), bf16hi_to_f32(wa.y)};
+  const float b[4] = {bf16lo_to_f32(wb.x), bf16hi_to_f32(wb.x), bf16lo_to_f32(wb.y), bf16hi_to_f32(wb.y)};
+  float y[4], m = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    y[j] = swiglu_exact(a[j], b[j]);
+    m = fmaxf(m, fabsf(y[j]));
+  }
+  const uint32_t sb = scale_byte_from_f32_mag(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
+  const float inv = inv_scale_from_byte(sb);
+  return make_uint2(cvt_e4m3x2_f32(y[0] * inv, y[1] * inv) | (cvt_e4m3x2_f32(y[2] * inv, y[3] * inv) << 16), sb);
+}
+
 // ---------------------------------------------------------------------------------------------
-// Kernel structure: one CTA per SM, warp 0 = TMA producer, warps 1-16 = consumers.
-// A tile = 64 rows x 256 output columns: the a-part h[r][c..c+255] and the b-part
-// h[r][F+c..F+c+255] arrive as two 2-D TMA boxes (32 KB each) in a 3-stage mbarrier ring, so up to
-// 192 KB per SM are in flight while the consumers compute.  Consumer warp w owns rows 4w..4w+3 of
-// the tile; a half-warp owns one 1x128 output tile row (16 lanes x 8 elements).
+// Kernel structure: warp 0 = TMA producer, warps 1..CONS = consumers.  A tile = (4 CONS) rows x
+// 256 output columns: the a-part h[r][c..c+255] and the b-part h[r][F+c..F+c+255] arrive as two
+// 2-D TMA boxes in a 3-stage mbarrier ring (192 KB per SM for CONS = 16).  Consumer warp w owns
+// rows 4w..4w+3 of the tile, i.e. 8 warp-rows (row, 128-column half) -- the warp's item; the 8
+// tile-scale decisions of an item are taken in parallel by lanes 0-7.
 // ---------------------------------------------------------------------------------------------
 constexpr int kSwCols = 256;  // output columns per TMA tile
 constexpr int kSwStages = 3;
+constexpr int kSwRpw = 4;            // rows per consumer warp
+constexpr int kSwSub = 2 * kSwRpw;   // warp-rows per consumer item
 
-// CONS consumer warps (4 rows each) -> tiles of 4*CONS rows; CONS = 16: one CTA per SM (192 KB of
-// stages), CONS = 8: two CTAs per SM (96 KB each) so that another kernel's CTA can co-reside
+// CONS = 16: one CTA per SM (192 KB of stages), CONS = 8: two CTAs per SM (96 KB each) so that
+// another kernel's CTA can co-reside
 template <int CONS>
 struct SwigluSmem {
-  static constexpr int kRows = 4 * CONS;
+  static constexpr int kRows = kSwRpw * CONS;
   static constexpr int kBox = kRows * kSwCols * 2;  // bytes of one box (a or b part)
   uint8_t a[kSwStages][kBox];
   uint8_t b[kSwStages][kBox];
@@ -60,91 +86,11 @@ struct SwigluSmem {
   uint64_t empty[kSwStages];
 };
 
-__device__ __forceinline__ void swiglu_tile_row(const uint4& va, const uint4& vb, int lane, int half,
-                                                uint32_t (&c)[4], uint32_t& sb_out) {
-  const uint32_t wa[4] = {va.x, va.y, va.z, va.w};
-  const uint32_t wb[4] = {vb.x, vb.y, vb.z, vb.w};
-  float a[8], b[8], y[8];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    a[2 * j] = bf16lo_to_f32(wa[j]);
-    a[2 * j + 1] = bf16hi_to_f32(wa[j]);
-    b[2 * j] = bf16lo_to_f32(wb[j]);
-    b[2 * j + 1] = bf16hi_to_f32(wb[j]);
-  }
-  // fast fp32 path: y' = a*b / (1 + 2^(-a log2e)); the domain where its error bound holds is
-  // checked per tile-row below (the largest denominator flags a < -64)
-  float ymax = 0.0f, dmax = 0.0f;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float d = 1.0f + ex2_approx(-a[j] * kLog2e);
-    y[j] = __fdividef(a[j] * b[j], d);
-    ymax = fmaxf(ymax, fabsf(y[j]));
-    dmax = fmaxf(dmax, d);
-  }
-  uint32_t mag = halfwarp_max_u32(__float_as_uint(ymax));
-  // outside |a| <= 64 and 2^-60 <= tile amax <= 2^100 (or amax exactly 0) the fp32 bound may not
-  // hold (exp overflow, overflowing a*b, subnormal intermediates): the tile-row is evaluated in fp64
-  const bool exotic = !(dmax < 5.0e27f) || mag > 0x71800000u || (mag != 0u && mag < 0x21800000u);  // 2^92
-  const uint32_t exb = __ballot_sync(0xffffffffu, exotic);
-  if (exb != 0u) {
-    if ((exb >> (16 * half)) & 0xFFFFu) {
-      float m2 = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        y[j] = swiglu_exact(a[j], b[j]);
-        m2 = fmaxf(m2, fabsf(y[j]));
-      }
-      mag = __float_as_uint(m2);
-    }
-    mag = halfwarp_max_u32(mag);
-  }
-  // scale decision: near the boundary amax = 1.75 * 2^e (mantissa field 0x600000)?
-  const int32_t dm = static_cast<int32_t>(mag & 0x7FFFFFu) - 0x600000;
-  const bool near = (mag >> 23) != 0u && dm >= -512 && dm <= 512;
-  if (__any_sync(0xffffffffu, near)) {
-    if (near) {
-      const float thr = __uint_as_float(mag) * (1.0f - 6.103515625e-05f);  // 1 - 2^-14
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (fabsf(y[j]) >= thr) y[j] = swiglu_exact(a[j], b[j]);
-      float m2 = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m2 = fmaxf(m2, fabsf(y[j]));
-      mag = __float_as_uint(m2);
-    }
-    mag = halfwarp_max_u32(mag);
-  }
-  const uint32_t sb = scale_byte_from_f32_mag(mag);
-  const float inv = inv_scale_from_byte(sb);
-  // codes: the true u = y * 2^-T lies in [y'(1-2^-16), y'(1+2^-16)] * 2^-T; if both ends round to
-  // the same E4M3 code that code is exact, otherwise the pair is decided in fp64
-  const float inv_lo = inv * kBracketLo, inv_hi = inv * kBracketHi;
-  uint32_t need = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t lo = cvt_e4m3x2_f32(y[2 * j] * inv_lo, y[2 * j + 1] * inv_lo);
-    const uint32_t hi = cvt_e4m3x2_f32(y[2 * j] * inv_hi, y[2 * j + 1] * inv_hi);
-    c[j] = lo;
-    need |= (lo != hi ? 1u : 0u) << j;
-  }
-  if (__any_sync(0xffffffffu, need != 0u)) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if ((need >> j) & 1u) {  // decide in fp64
-        c[j] = cvt_e4m3x2_f32(swiglu_exact(a[2 * j], b[2 * j]) * inv, swiglu_exact(a[2 * j + 1], b[2 * j + 1]) * inv);
-      }
-    }
-  }
-  (void)lane;
-  sb_out = sb;
-}
-
 template <int CONS>
 __global__ void __launch_bounds__(32 * (1 + CONS), 1)
     swiglu_quant_kernel(const __grid_constant__ CUtensorMap tmap_h, int64_t rows_max,
                         const int32_t* __restrict__ rows_dev, int64_t F, uint8_t* __restrict__ q,
-                        uint8_t* __restrict__ s, int64_t ld_s) {
+                        uint8_t* __restrict__ s, int64_t ld_s, uint32_t sleep_ns) {
   extern __shared__ __align__(1024) uint8_t smem_sw[];
   using Smem = SwigluSmem<CONS>;
   constexpr int kSwRows = Smem::kRows;
@@ -153,7 +99,10 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t rows = rows_dev != nullptr ? static_cast<int64_t>(*rows_dev) : rows_max;
   const int col_tiles = static_cast<int>((F + kSwCols - 1) / kSwCols);
-  const int64_t n_tiles = ((rows + kSwRows - 1) / kSwRows) * col_tiles;
+  const int64_t n_rg = (rows + kSwRows - 1) / kSwRows;
+  // tile t = (row group rg, column tile ct), strided by gridDim.x, walked incrementally
+  const int step_c = static_cast<int>(gridDim.x % col_tiles);
+  const int64_t step_r = gridDim.x / col_tiles;
   if (tid == 0) {
     for (int i = 0; i < kSwStages; ++i) {
       mbar_init(&sm.full[i], 1);
@@ -169,13 +118,23 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
       int st = 0;
       uint32_t parity = 0;
       int64_t n = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++n) {
-        if (n >= kSwStages) mbar_wait(&sm.empty[st], parity ^ 1u);
-        const int64_t rg = t / col_tiles;
-        const int c0 = static_cast<int>(t - rg * col_tiles) * kSwCols;
+      int ct = static_cast<int>(blockIdx.x % col_tiles);
+      for (int64_t rg = blockIdx.x / col_tiles; rg < n_rg; ++n) {
+        if (n >= kSwStages) {
+          if (sleep_ns) mbar_wait_sleep(&sm.empty[st], parity ^ 1u, sleep_ns);
+          else mbar_wait(&sm.empty[st], parity ^ 1u);
+        }
+        const int c0 = ct * kSwCols;
+        const int32_t r0 = static_cast<int32_t>(rg * kSwRows);
+        ct += step_c;
+        rg += step_r;
+        if (ct >= col_tiles) {
+          ct -= col_tiles;
+          ++rg;
+        }
         mbar_expect_tx(&sm.full[st], 2 * kSwBox);
-        tma_load_2d(sm.a[st], &tmap_h, &sm.full[st], c0, static_cast<int32_t>(rg * kSwRows));
-        tma_load_2d(sm.b[st], &tmap_h, &sm.full[st], static_cast<int32_t>(F) + c0, static_cast<int32_t>(rg * kSwRows));
+        tma_load_2d(sm.a[st], &tmap_h, &sm.full[st], c0, r0);
+        tma_load_2d(sm.b[st], &tmap_h, &sm.full[st], static_cast<int32_t>(F) + c0, r0);
         if (++st == kSwStages) {
           st = 0;
           parity ^= 1u;
@@ -185,24 +144,27 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
     return;
   }
   // ------------------------------------------------------------------------ consumers
-  const int cw = warp - 1;  // rows 4cw..4cw+3 of each tile
-  const int half = lane >> 4, sub = lane & 15;
+  const int cw = warp - 1;
   int st = 0;
   uint32_t parity = 0;
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const int64_t rg = t / col_tiles;
-    const int64_t c0 = (t - rg * col_tiles) * kSwCols;
-    const int64_t col = c0 + half * 128 + sub * 8;
-    const bool col_ok = col < F;
-    const int64_t row0 = rg * kSwRows + 4 * cw;
-    const int nrows = static_cast<int>(min64(4, rows - row0));
+  int ct = static_cast<int>(blockIdx.x % col_tiles);
+  for (int64_t rg = blockIdx.x / col_tiles; rg < n_rg;) {
+    const int c0 = ct * kSwCols;  // warp-row i: row kSwRpw cw + i / 2, 128-column half i % 2
+    const int64_t row0 = rg * kSwRows + kSwRpw * cw;
+    const int nrows = static_cast<int>(min64(kSwRpw, rows - row0));
+    ct += step_c;
+    rg += step_r;
+    if (ct >= col_tiles) {
+      ct -= col_tiles;
+      ++rg;
+    }
     mbar_wait(&sm.full[st], parity);
-    uint4 va[4], vb[4];
+    uint2 wa[kSwSub], wb[kSwSub];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int off = ((4 * cw + i) * kSwCols + half * 128 + sub * 8) * 2;
-      va[i] = *reinterpret_cast<const uint4*>(&sm.a[st][off]);
-      vb[i] = *reinterpret_cast<const uint4*>(&sm.b[st][off]);
+    for (int i = 0; i < kSwSub; ++i) {
+      const int off = ((kSwRpw * cw + i / 2) * kSwCols + (i % 2) * 128 + 4 * lane) * 2;
+      wa[i] = *reinterpret_cast<const uint2*>(&sm.a[st][off]);
+      wb[i] = *reinterpret_cast<const uint2*>(&sm.b[st][off]);
     }
     fence_proxy_async_smem();  // reads (generic proxy) before the next TMA write (async proxy)
     __syncwarp();
@@ -211,22 +173,68 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
       st = 0;
       parity ^= 1u;
     }
-    uint32_t packed = 0;
+    // phase 1: fp32 values, the warp maximum |y'| of every warp-row, and the lane's largest
+    // denominator over the whole item (domain check)
+    float2 y[kSwSub][2];
+    uint32_t mY[kSwSub];
+    float dm = 0.0f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t c[4], sb;
-      swiglu_tile_row(va[i], vb[i], lane, half, c, sb);
-      if (i < nrows && col_ok) st_v2(q + (row0 + i) * F + col, c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-      packed |= sb << (8 * i);
+    for (int i = 0; i < kSwSub; ++i) {
+      const uint32_t aw[2] = {wa[i].x, wa[i].y}, bw[2] = {wb[i].x, wb[i].y};
+      float ym = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float2 a = make_float2(bf16lo_to_f32(aw[j]), bf16hi_to_f32(aw[j]));
+        const float2 b = make_float2(bf16lo_to_f32(bw[j]), bf16hi_to_f32(bw[j]));
+        const float2 x = __fmul2_rn(a, make_float2(-kLog2e, -kLog2e));
+        const float2 d = __fadd2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), make_float2(1.0f, 1.0f));
+        y[i][j] = __fmul2_rn(__fmul2_rn(a, b), make_float2(rcp_approx(d.x), rcp_approx(d.y)));
+        ym = max_nan(ym, max_nan(fabsf(y[i][j].x), fabsf(y[i][j].y)));
+        dm = max_nan(dm, max_nan(d.x, d.y));
+      }
+      mY[i] = __reduce_max_sync(0xffffffffu, __float_as_uint(ym));
     }
-    if (sub == 0 && col_ok && nrows > 0) {
-      uint8_t* sp = s + (col / 128) * ld_s + row0;
-      if (nrows == 4) {
-        *reinterpret_cast<uint32_t*>(sp) = packed;  // row0 % 4 == 0, ld_s % 16 == 0: aligned
-      } else {
-        for (int r = 0; r < nrows; ++r) sp[r] = static_cast<uint8_t>(packed >> (8 * r));
+    // domain of the whole item: largest denominator < 2^92 (a > -63.8); NaN reaches amax' below
+    const bool item_exotic = __any_sync(0xffffffffu, !(dm < 4.951760157141521e27f));
+    // phase 2: lanes 0-7 take the 8 scale decisions (lane k: warp-row k), then broadcast
+    const int r = lane & (kSwSub - 1);
+    uint32_t my = mY[0];
+#pragma unroll
+    for (int i = 1; i < kSwSub; ++i) my = r == i ? mY[i] : my;
+    // domain: amax 0 or in [2^-60, 2^100] (NaN fails), denominators < 2^92
+    const bool exotic = item_exotic || (my != 0u && my - 0x21800000u > 0x50000000u);
+    // near a scale boundary amax = 1.75 * 2^e (mantissa field 0x600000) within 2^-14?
+    const int32_t dmant = static_cast<int32_t>(my & 0x7FFFFFu) - 0x600000;
+    const bool sure = !exotic && !(dmant >= -512 && dmant <= 512);
+    uint32_t sbyte = scale_byte_from_f32_mag(my);
+    const float inv = inv_scale_from_byte(sbyte);
+    uint32_t c[kSwSub];
+#pragma unroll
+    for (int i = 0; i < kSwSub; ++i) {
+      const float iv = __shfl_sync(0xffffffffu, inv, i);
+      const float2 u0 = __fmul2_rn(y[i][0], make_float2(iv, iv)), u1 = __fmul2_rn(y[i][1], make_float2(iv, iv));
+      c[i] = cvt_e4m3x2_f32(u0.x, u0.y) | (cvt_e4m3x2_f32(u1.x, u1.y) << 16);
+    }
+    const uint32_t unsure = __ballot_sync(0xffffffffu, !sure) & ((1u << kSwSub) - 1u);
+    if (unsure != 0u) {  // rare, warp-uniform: whole warp-rows in fp64
+#pragma unroll
+      for (int i = 0; i < kSwSub; ++i) {
+        if ((unsure >> i) & 1u) {
+          const uint2 x = swiglu_row_exact(wa[i], wb[i]);
+          c[i] = x.x;
+          if (r == i) sbyte = x.y;
+        }
       }
     }
+    const bool second_ok = c0 + 128 < F;  // the box's second 128-column tile exists (F % 256 == 128)
+    uint8_t* qp = q + row0 * F + c0 + 4 * lane;
+#pragma unroll
+    for (int i = 0; i < kSwSub; ++i) {
+      if (i / 2 < nrows && (i % 2 == 0 || second_ok))
+        *reinterpret_cast<uint32_t*>(qp + (i / 2) * F + (i % 2) * 128) = c[i];
+    }
+    if (lane < kSwSub && r / 2 < nrows && (r % 2 == 0 || second_ok))
+      s[((c0 >> 7) + r % 2) * ld_s + row0 + r / 2] = static_cast<uint8_t>(sbyte);
   }
 }
 
@@ -266,10 +274,10 @@ cudaError_t launch_swiglu_quant(const void* h, int64_t rows_max, const int32_t* 
   if (grid < 1) grid = 1;
   if (ctas == 2)
     swiglu_quant_kernel<8><<<static_cast<unsigned>(grid), 32 * 9, sizeof(SwigluSmem<8>), stream>>>(
-        map, rows_max, rows_dev, ffn, q, s, ld_s);
+        map, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<uint32_t>(tune_int("A5_SLEEP_NS", 128)));
   else
     swiglu_quant_kernel<16><<<static_cast<unsigned>(grid), 32 * 17, sizeof(SwigluSmem<16>), stream>>>(
-        map, rows_max, rows_dev, ffn, q, s, ld_s);
+        map, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<uint32_t>(tune_int("A5_SLEEP_NS", 128)));
   return cudaGetLastError();
 }
 

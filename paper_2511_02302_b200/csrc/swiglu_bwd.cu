@@ -103,7 +103,7 @@ __device__ __noinline__ uint4 row_exact(uint2 wa, uint2 wb, uint2 wg) {
 __global__ void __launch_bounds__(32 * (1 + kBwCons), 1)
     swiglu_bwd_quant_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_d,
                             int64_t rows_max, const int32_t* __restrict__ rows_dev, int64_t F,
-                            uint8_t* __restrict__ q, uint8_t* __restrict__ s, int64_t ld_s) {
+                            uint8_t* __restrict__ q, uint8_t* __restrict__ s, int64_t ld_s, uint32_t sleep_ns) {
   extern __shared__ __align__(1024) uint8_t smem_bw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_bw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(32 * (1 + kBwCons), 1)
       int64_t n = 0;
       int ct = static_cast<int>(blockIdx.x % col_tiles);
       for (int64_t rg = blockIdx.x / col_tiles; rg < n_rg; ++n) {
-        if (n >= kBwStages) mbar_wait_sleep(&sm.empty[st], parity ^ 1u, 128);
+        if (n >= kBwStages) {
+          if (sleep_ns) mbar_wait_sleep(&sm.empty[st], parity ^ 1u, sleep_ns);
+          else mbar_wait(&sm.empty[st], parity ^ 1u);
+        }
         const int c0 = ct * kBwCols;
         const int32_t r0 = static_cast<int32_t>(rg * kBwRows);
         ct += step_c;
@@ -318,7 +321,7 @@ cudaError_t launch_swiglu_bwd_quant(const void* h, const void* dA, int64_t rows_
   int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   if (grid < 1) grid = 1;
   swiglu_bwd_quant_kernel<<<static_cast<unsigned>(grid), 32 * (1 + kBwCons), sizeof(BwdSmem), stream>>>(
-      mh, md, rows_max, rows_dev, ffn, q, s, ld_s);
+      mh, md, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<uint32_t>(tune_int("BWD_SLEEP_NS", 128)));
   return cudaGetLastError();
 }
 
