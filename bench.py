@@ -425,29 +425,46 @@ class ClockSampler:
 # =============================================================================================
 def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20) -> dict:
     """NEXT rows measured on the same workload (not part of the headline step): NEXT-1 fused
-    SwiGLU backward + quant of dA [R, 2048] with the saved fc1 output h [R, 4096]."""
+    SwiGLU backward + quant of dA [R, 2048] with the saved fc1 output h [R, 4096], and the
+    dual-output SwiGLU + quant emitting A row-wise and column-wise (per expert) in one pass, against
+    the two launches (A5 then A2) it replaces."""
     F = ds.F
     hw = ds.hw
     dA = synth.normal_bf16(hw.R, FFN, synth.BASE_SEED + 5, sigma=0.5).to(ds.dev)
     q = torch.empty(hw.R, 2 * FFN, dtype=torch.uint8, device=ds.dev)
     s = torch.empty(2 * FFN // 128, hw.R, dtype=torch.uint8, device=ds.dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    fn = lambda: F.fp8flow_swiglu_bwd_quant(ds.h, dA, q, s, rows_dev=ds.off[hw.E_loc:])  # noqa: E731
-    fn()
-    ts = []
-    for _ in range(reps):
-        ds.flush_l2()
-        torch.cuda._sleep(1_000_000)
-        ev[0].record()
+    rows_dev = ds.off[hw.E_loc:]
+
+    def med(fn):
         fn()
-        ev[1].record()
-        ev[1].synchronize()
-        ts.append(ev[0].elapsed_time(ev[1]))
-    ms = statistics.median(ts)
-    nb = RL.swiglu_bwd_quant_bytes(hw.R, FFN)
-    return {"NEXT1_swiglu_bwd_quant": {"us": round(ms * 1e3, 2), "bytes": nb, "gbs": round(nb / ms / 1e6, 1),
-                                       "frac": round(nb / ms / 1e6 / peak, 3),
-                                       "shape": {"h": [hw.R, 2 * FFN], "dA": [hw.R, FFN]}}}
+        ts = []
+        for _ in range(reps):
+            ds.flush_l2()
+            torch.cuda._sleep(1_000_000)
+            ev[0].record()
+            fn()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        return statistics.median(ts)
+
+    def line(ms, nb, **kw):
+        return {"us": round(ms * 1e3, 2), "bytes": nb, "gbs": round(nb / ms / 1e6, 1),
+                "frac": round(nb / ms / 1e6 / peak, 3), **kw}
+
+    out = {}
+    ms = med(lambda: F.fp8flow_swiglu_bwd_quant(ds.h, dA, q, s, rows_dev=rows_dev))
+    out["NEXT1_swiglu_bwd_quant"] = line(ms, RL.swiglu_bwd_quant_bytes(hw.R, FFN),
+                                         shape={"h": [hw.R, 2 * FFN], "dA": [hw.R, FFN]})
+    segs = [int(v) for v in hw.padded]
+    nb = RL.swiglu_quant_dual_bytes(segs, FFN)
+    ms_two = med(lambda: (F.fp8flow_swiglu_quant(ds.h, ds.q_a, ds.s_a, rows_dev=rows_dev),
+                          F.fp8flow_scaling_aware_transpose(ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off)))
+    ms = med(lambda: F.fp8flow_swiglu_quant_dual(ds.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off))
+    out["NEXT1_swiglu_quant_dual"] = line(ms, nb, segments=len(segs),
+                                          vs_A5_then_A2_us=round(ms_two * 1e3, 2))
+    return out
 
 
 def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
@@ -466,7 +483,11 @@ def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
     ops = {"A1_quantize": (lambda: F.fp8flow_quantize_rowwise(x, q, s), RL.quantize_bytes(rows, cols)),
            "A2_transpose": (lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT), RL.transpose_bytes([rows], cols)),
            "naive_dequant_transpose_requant": (lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws),
-                                               RL.transpose_bytes([rows], cols))}
+                                               RL.transpose_bytes([rows], cols)),
+           "A1_then_A2_two_launches": (lambda: (F.fp8flow_quantize_rowwise(x, q, s),
+                                                F.fp8flow_scaling_aware_transpose(q, s, qT, sT)),
+                                       RL.quantize_dual_bytes([rows], cols)),
+           "NEXT1_quantize_dual": (lambda: F.fp8flow_quantize_dual(x, q, s, qT, sT), RL.quantize_dual_bytes([rows], cols))}
     out = {"shape": [rows, cols], "l2": "flushed before each launch (256 MiB write + 256 MiB read)"}
     for name, (fn, nbytes) in ops.items():
         fn()

@@ -200,6 +200,30 @@ FP8FLOW_API int fp8flow_swiglu_bwd_quant(const void* h_bf16, const void* dA_bf16
                                          const int32_t* rows_dev, int64_t ffn, uint8_t* q, uint8_t* s,
                                          int64_t ld_s, void* stream);
 
+/* ==========================================================================================
+ * NEXT-1  Dual-output fusions (R32): one read of the BF16 input
+ *     produces both the row-wise FP8 tensor (Fprop/Dgrad operand) and its column-wise
+ *     scaling-aware transpose (Wgrad operand) per segment.  The result is by definition the
+ *     composition: (q, s) = A1(x) [resp. A5(h)], (qT, sT) = A2(q, s, seg_offsets) -- bit-identical
+ *     to calling the two entry points in sequence, with one fewer pass over q.
+ *
+ *   fp8flow_quantize_dual: x_bf16 [rows][cols] (A1's input); rows % 16 == 0, cols % 128 == 0.
+ *   fp8flow_swiglu_quant_dual: h_bf16 [rows_max][2*ffn] (A5's input); the output columns are ffn.
+ *     rows_dev: actual row count (device int32) or NULL, used only when seg_offsets is NULL.
+ *   seg_offsets  device int32 [num_segs + 1] (segment lengths multiples of 16), or NULL = one
+ *                segment [0, rows); 1 <= num_segs <= 1024.  For the SwiGLU variant the last
+ *                offset is the actual row count.
+ *   q, s, ld_s   row-wise output as A1 / A5 (s MN-major [cols/128][ld_s], ld_s >= rows, % 16 == 0)
+ *   qT, sT       column-wise output as A2 (same capacities and per-segment placement).
+ *   All pointers 16-byte aligned.
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_quantize_dual(const void* x_bf16, int64_t rows, int64_t cols, const int32_t* seg_offsets,
+                                      int32_t num_segs, uint8_t* q, uint8_t* s, int64_t ld_s, uint8_t* qT,
+                                      uint8_t* sT, void* stream);
+FP8FLOW_API int fp8flow_swiglu_quant_dual(const void* h_bf16, int64_t rows_max, const int32_t* rows_dev,
+                                          int64_t ffn, const int32_t* seg_offsets, int32_t num_segs, uint8_t* q,
+                                          uint8_t* s, int64_t ld_s, uint8_t* qT, uint8_t* sT, void* stream);
+
 /* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
  * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */
 FP8FLOW_API int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream);

@@ -227,6 +227,34 @@ int fp8flow_swiglu_bwd_quant(const void* h_bf16, const void* dA_bf16, int64_t ro
                                           static_cast<cudaStream_t>(stream), sms));
 }
 
+int fp8flow_quantize_dual(const void* x_bf16, int64_t rows, int64_t cols, const int32_t* seg_offsets,
+                          int32_t num_segs, uint8_t* q, uint8_t* s, int64_t ld_s, uint8_t* qT, uint8_t* sT,
+                          void* stream) {
+  if (rows == 0 && !seg_offsets) return FP8FLOW_OK;
+  int st = check_transpose_args(q, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
+  if (st != FP8FLOW_OK) return st;
+  if (!x_bf16) return FP8FLOW_ERR_NULL;
+  if (!aligned16(x_bf16)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_quantize_dual(x_bf16, rows, cols, seg_offsets, num_segs, q, s, ld_s, qT, sT,
+                                       static_cast<cudaStream_t>(stream), sms));
+}
+
+int fp8flow_swiglu_quant_dual(const void* h_bf16, int64_t rows_max, const int32_t* rows_dev, int64_t ffn,
+                              const int32_t* seg_offsets, int32_t num_segs, uint8_t* q, uint8_t* s, int64_t ld_s,
+                              uint8_t* qT, uint8_t* sT, void* stream) {
+  if (rows_max == 0) return FP8FLOW_OK;
+  int st = check_transpose_args(q, s, ld_s, rows_max, ffn, seg_offsets, num_segs, qT, sT);
+  if (st != FP8FLOW_OK) return st;
+  if (!h_bf16) return FP8FLOW_ERR_NULL;
+  if (!aligned16(h_bf16)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_swiglu_quant_dual(h_bf16, rows_max, rows_dev, ffn, seg_offsets, num_segs, q, s, ld_s, qT,
+                                           sT, static_cast<cudaStream_t>(stream), sms));
+}
+
 int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream) {
   if (nbytes < 0) return FP8FLOW_ERR_SHAPE;
   if (!out_dev || (nbytes > 0 && !buf)) return FP8FLOW_ERR_NULL;

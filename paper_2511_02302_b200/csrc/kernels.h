@@ -64,6 +64,12 @@ cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t*
 cudaError_t launch_swiglu_quant(const void* h, int64_t rows_max, const int32_t* rows_dev, int64_t ffn, uint8_t* q,
                                 uint8_t* s, int64_t ld_s, cudaStream_t stream, int num_sms);
 
+cudaError_t launch_quantize_dual(const void* x, int64_t rows, int64_t cols, const int32_t* seg_offsets,
+                                 int32_t num_segs, uint8_t* q, uint8_t* s, int64_t ld_s, uint8_t* qT, uint8_t* sT,
+                                 cudaStream_t stream, int num_sms);
+cudaError_t launch_swiglu_quant_dual(const void* h, int64_t rows_max, const int32_t* rows_dev, int64_t ffn,
+                                     const int32_t* seg_offsets, int32_t num_segs, uint8_t* q, uint8_t* s,
+                                     int64_t ld_s, uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms);
 cudaError_t launch_swiglu_bwd_quant(const void* h, const void* dA, int64_t rows_max, const int32_t* rows_dev,
                                     int64_t ffn, uint8_t* q, uint8_t* s, int64_t ld_s, cudaStream_t stream,
                                     int num_sms);

@@ -21,46 +21,9 @@
 #include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
+#include "swiglu_math.cuh"
 
 namespace fp8flow {
-
-constexpr float kLog2e = 1.4426950408889634f;
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float max_nan(float x, float y) {
-  float r;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(x), "f"(y));
-  return r;
-}
-__device__ __noinline__ float swiglu_exact(float a, float b) {
-  const double ad = static_cast<double>(a), bd = static_cast<double>(b);
-  return static_cast<float>(ad * bd / (1.0 + exp(-ad)));
-}
-
-// one warp-row (lane: 4 elements) evaluated exactly; amax ignores NaN like the oracle.
-// returns {codes, scale byte}
-__device__ __noinline__ uint2 swiglu_row_exact(uint2 wa, uint2 wb) {
-  const float a[4] = {bf16lo_to_f32(wa.x), bf16hi_to_f32(wa.x), bf16lo_to_f32(wa.y), bf16hi_to_f32(wa.y)};
-  const float b[4] = {bf16lo_to_f32(wb.x), bf16hi_to_f32(wb.x), bf16lo_to_f32(wb.y), bf16hi_to_f32(wb.y)};
-  float y[4], m = 0.0f;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    y[j] = swiglu_exact(a[j], b[j]);
-    m = fmaxf(m, fabsf(y[j]));
-  }
-  const uint32_t sb = scale_byte_from_f32_mag(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
-  const float inv = inv_scale_from_byte(sb);
-  return make_uint2(cvt_e4m3x2_f32(y[0] * inv, y[1] * inv) | (cvt_e4m3x2_f32(y[2] * inv, y[3] * inv) << 16), sb);
-}
 
 // ---------------------------------------------------------------------------------------------
 // Kernel structure: warp 0 = TMA producer, warps 1..CONS = consumers.  A tile = (4 CONS) rows x
@@ -173,59 +136,9 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
       st = 0;
       parity ^= 1u;
     }
-    // phase 1: fp32 values, the warp maximum |y'| of every warp-row, and the lane's largest
-    // denominator over the whole item (domain check)
-    float2 y[kSwSub][2];
-    uint32_t mY[kSwSub];
-    float dm = 0.0f;
-#pragma unroll
-    for (int i = 0; i < kSwSub; ++i) {
-      const uint32_t aw[2] = {wa[i].x, wa[i].y}, bw[2] = {wb[i].x, wb[i].y};
-      float ym = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float2 a = make_float2(bf16lo_to_f32(aw[j]), bf16hi_to_f32(aw[j]));
-        const float2 b = make_float2(bf16lo_to_f32(bw[j]), bf16hi_to_f32(bw[j]));
-        const float2 x = __fmul2_rn(a, make_float2(-kLog2e, -kLog2e));
-        const float2 d = __fadd2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), make_float2(1.0f, 1.0f));
-        y[i][j] = __fmul2_rn(__fmul2_rn(a, b), make_float2(rcp_approx(d.x), rcp_approx(d.y)));
-        ym = max_nan(ym, max_nan(fabsf(y[i][j].x), fabsf(y[i][j].y)));
-        dm = max_nan(dm, max_nan(d.x, d.y));
-      }
-      mY[i] = __reduce_max_sync(0xffffffffu, __float_as_uint(ym));
-    }
-    // domain of the whole item: largest denominator < 2^92 (a > -63.8); NaN reaches amax' below
-    const bool item_exotic = __any_sync(0xffffffffu, !(dm < 4.951760157141521e27f));
-    // phase 2: lanes 0-7 take the 8 scale decisions (lane k: warp-row k), then broadcast
-    const int r = lane & (kSwSub - 1);
-    uint32_t my = mY[0];
-#pragma unroll
-    for (int i = 1; i < kSwSub; ++i) my = r == i ? mY[i] : my;
-    // domain: amax 0 or in [2^-60, 2^100] (NaN fails), denominators < 2^92
-    const bool exotic = item_exotic || (my != 0u && my - 0x21800000u > 0x50000000u);
-    // near a scale boundary amax = 1.75 * 2^e (mantissa field 0x600000) within 2^-14?
-    const int32_t dmant = static_cast<int32_t>(my & 0x7FFFFFu) - 0x600000;
-    const bool sure = !exotic && !(dmant >= -512 && dmant <= 512);
-    uint32_t sbyte = scale_byte_from_f32_mag(my);
-    const float inv = inv_scale_from_byte(sbyte);
     uint32_t c[kSwSub];
-#pragma unroll
-    for (int i = 0; i < kSwSub; ++i) {
-      const float iv = __shfl_sync(0xffffffffu, inv, i);
-      const float2 u0 = __fmul2_rn(y[i][0], make_float2(iv, iv)), u1 = __fmul2_rn(y[i][1], make_float2(iv, iv));
-      c[i] = cvt_e4m3x2_f32(u0.x, u0.y) | (cvt_e4m3x2_f32(u1.x, u1.y) << 16);
-    }
-    const uint32_t unsure = __ballot_sync(0xffffffffu, !sure) & ((1u << kSwSub) - 1u);
-    if (unsure != 0u) {  // rare, warp-uniform: whole warp-rows in fp64
-#pragma unroll
-      for (int i = 0; i < kSwSub; ++i) {
-        if ((unsure >> i) & 1u) {
-          const uint2 x = swiglu_row_exact(wa[i], wb[i]);
-          c[i] = x.x;
-          if (r == i) sbyte = x.y;
-        }
-      }
-    }
+    const uint32_t sbyte = swiglu_quant_rows<kSwSub>(wa, wb, c);
+    const int r = lane & (kSwSub - 1);
     const bool second_ok = c0 + 128 < F;  // the box's second 128-column tile exists (F % 256 == 128)
     uint8_t* qp = q + row0 * F + c0 + 4 * lane;
 #pragma unroll

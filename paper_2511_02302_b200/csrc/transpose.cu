@@ -25,6 +25,7 @@
 #include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
+#include "segments.cuh"
 
 namespace fp8flow {
 
@@ -47,85 +48,6 @@ struct TransposeSmem {
   int32_t total_rb;
 };
 
-// block-wide exclusive scan of one value per thread (blockDim.x == kTThreads); returns the
-// exclusive prefix and writes the block total to *total (visible after the trailing sync).
-__device__ __forceinline__ int block_exclusive_scan(int v, uint32_t* warp_tmp, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    int n = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += n;
-  }
-  if (lane == 31) warp_tmp[warp] = static_cast<uint32_t>(incl);
-  __syncthreads();
-  int base = 0, all = 0;
-#pragma unroll
-  for (int w = 0; w < kTThreads / 32; ++w) {
-    int t = static_cast<int>(warp_tmp[w]);
-    base += (w < warp) ? t : 0;
-    all += t;
-  }
-  if (threadIdx.x == 0) *total = all;
-  __syncthreads();
-  return base + incl - v;
-}
-
-// Loads the segment offsets and builds blk_prefix[e] = sum_{e'<e} ceil(m_e'/128) in smem.
-template <typename Smem>
-__device__ __forceinline__ void load_segments(Smem& sm, const int32_t* seg_offsets, int32_t num_segs,
-                                              int64_t rows) {
-  const int tid = threadIdx.x;
-  if (seg_offsets == nullptr) {
-    if (tid == 0) {
-      sm.seg_off[0] = 0;
-      sm.seg_off[1] = static_cast<int32_t>(rows);
-    }
-  } else {
-    for (int i = tid; i <= num_segs; i += kTThreads) sm.seg_off[i] = seg_offsets[i];
-  }
-  __syncthreads();
-  // 4 consecutive segments per thread (num_segs <= 1024)
-  int nb[4], tsum = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int e = tid * 4 + i;
-    nb[i] = e < num_segs ? (sm.seg_off[e + 1] - sm.seg_off[e] + kTile - 1) / kTile : 0;
-    tsum += nb[i];
-  }
-  int run = block_exclusive_scan(tsum, sm.red, &sm.total_rb);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int e = tid * 4 + i;
-    if (e <= num_segs) sm.blk_prefix[e] = run;
-    run += nb[i];
-  }
-  __syncthreads();
-}
-
-// warp-cooperative: the segment owning row block rb = #{e in [1, num_segs) : blk_prefix[e] <= rb}
-// (blk_prefix is non-decreasing, blk_prefix[0] = 0; empty segments are skipped automatically)
-__device__ __forceinline__ int find_segment_warp(const int32_t* blk_prefix, int num_segs, int rb) {
-  const int lane = threadIdx.x & 31;
-  int cnt = 0;
-  for (int base = 1; base < num_segs; base += 32) {
-    const int e = base + lane;
-    cnt += __popc(__ballot_sync(0xffffffffu, e < num_segs && blk_prefix[e] <= rb));
-  }
-  return cnt;
-}
-
-// largest e in [0, num_segs) with blk_prefix[e] <= rb  (the segment that owns row block rb)
-__device__ __forceinline__ int find_segment(const int32_t* blk_prefix, int num_segs, int rb) {
-  int lo = 0, hi = num_segs;  // invariant: blk_prefix[lo] <= rb < blk_prefix[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (blk_prefix[mid] <= rb) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
-
 template <int STAGES, int OUTBUF, int MINB>
 __global__ void __launch_bounds__(kTThreads, MINB)
     scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q, const uint8_t* __restrict__ s,
@@ -146,7 +68,7 @@ __global__ void __launch_bounds__(kTThreads, MINB)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)) : "memory");
   }
   if (tid <= 32) sm.mult[tid] = shift_multiplier(static_cast<uint32_t>(tid));
-  load_segments(sm, seg_offsets, nsegs, rows);  // (ends with a CTA barrier)
+  load_segments<kTThreads>(sm, seg_offsets, nsegs, rows);  // (ends with a CTA barrier)
 
   const int n_jb = static_cast<int>(cols / kTile);
   const int total_tiles = sm.total_rb * n_jb;  // < 2^31 (rows < 2^31, checked by the ABI)
@@ -350,7 +272,7 @@ __global__ void seg_prefix_kernel(const int32_t* __restrict__ seg_offsets, int32
     nb[i] = e < nsegs ? (so[e + 1] - so[e] + kTile - 1) / kTile : 0;
     tsum += nb[i];
   }
-  int run = block_exclusive_scan(tsum, red, &total);
+  int run = block_exclusive_scan<kTThreads>(tsum, red, &total);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int e = tid * 4 + i;

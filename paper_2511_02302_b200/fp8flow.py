@@ -43,6 +43,8 @@ SIGNATURES = {
     "fp8flow_swiglu_quant": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _P]),
     "fp8flow_checksum64": (ctypes.c_int, [_P, _I64, _P, _P]),
     "fp8flow_swiglu_bwd_quant": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P]),
+    "fp8flow_quantize_dual": (ctypes.c_int, [_P, _I64, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
+    "fp8flow_swiglu_quant_dual": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
 }
 
 
@@ -190,6 +192,29 @@ def fp8flow_swiglu_bwd_quant(h: torch.Tensor, dA: torch.Tensor, q: torch.Tensor,
     assert dA.shape == (rows_max, F2 // 2)
     _check(lib().fp8flow_swiglu_bwd_quant(_ptr(h), _ptr(dA), rows_max, _ptr(rows_dev), F2 // 2, _ptr(_u8(q)),
                                           _ptr(_u8(s)), s.shape[1], _stream(stream)), "fp8flow_swiglu_bwd_quant")
+
+
+def fp8flow_quantize_dual(x: torch.Tensor, q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor, sT: torch.Tensor,
+                          seg_offsets: torch.Tensor | None = None, stream=None) -> None:
+    """NEXT-1 dual output: x bf16 [rows, cols] -> q, s (as A1) and qT, sT (as A2 of q, s)."""
+    assert x.dtype == torch.bfloat16 and x.dim() == 2
+    rows, cols = x.shape
+    nseg = 0 if seg_offsets is None else seg_offsets.numel() - 1
+    _check(lib().fp8flow_quantize_dual(_ptr(x), rows, cols, _ptr(seg_offsets), nseg, _ptr(_u8(q)), _ptr(_u8(s)),
+                                       s.shape[1], _ptr(_u8(qT)), _ptr(_u8(sT)), _stream(stream)),
+           "fp8flow_quantize_dual")
+
+
+def fp8flow_swiglu_quant_dual(h: torch.Tensor, q: torch.Tensor, s: torch.Tensor, qT: torch.Tensor, sT: torch.Tensor,
+                              seg_offsets: torch.Tensor | None = None, rows_dev: torch.Tensor | None = None,
+                              stream=None) -> None:
+    """NEXT-1 dual output: h bf16 [rows, 2F] -> q, s (as A5) and qT, sT (as A2 of q, s)."""
+    assert h.dtype == torch.bfloat16 and h.dim() == 2
+    rows_max, F2 = h.shape
+    nseg = 0 if seg_offsets is None else seg_offsets.numel() - 1
+    _check(lib().fp8flow_swiglu_quant_dual(_ptr(h), rows_max, _ptr(rows_dev), F2 // 2, _ptr(seg_offsets), nseg,
+                                           _ptr(_u8(q)), _ptr(_u8(s)), s.shape[1], _ptr(_u8(qT)), _ptr(_u8(sT)),
+                                           _stream(stream)), "fp8flow_swiglu_quant_dual")
 
 
 def fp8flow_checksum64(buf: torch.Tensor, out: torch.Tensor, stream=None) -> None:

@@ -60,6 +60,21 @@ def swiglu_bwd_quant_bytes(rows: int, ffn: int) -> int:
     return rows * (4 * ffn + 2 * ffn + 2 * ffn + 2 * ffn // 128)
 
 
+def quantize_dual_bytes(seg_lengths, cols: int) -> int:
+    """NEXT-1 dual A1: BF16 read once, row-wise codes + scales and column-wise codes + block scales
+    written once."""
+    m = sum(seg_lengths)
+    blocks = sum((x + 127) // 128 for x in seg_lengths)
+    return m * cols * (2 + 1 + 1) + m * (cols // 128) + blocks * cols
+
+
+def swiglu_quant_dual_bytes(seg_lengths, ffn: int) -> int:
+    """NEXT-1 dual A5: BF16 h [m, 2F] read once, row-wise and column-wise codes + scales written."""
+    m = sum(seg_lengths)
+    blocks = sum((x + 127) // 128 for x in seg_lengths)
+    return m * (4 * ffn + ffn + ffn) + m * (ffn // 128) + blocks * ffn
+
+
 def measured_peaks(root: str) -> dict:
     """HBM copy bandwidth to use as the roofline denominator: the driver-measured figure when
     MEASURED_PEAKS.json exists, else the profiling guide's fallback (6650 GB/s)."""

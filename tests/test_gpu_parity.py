@@ -392,3 +392,93 @@ def test_swiglu_bwd_quant_adversarial(F, orc):
     q2, s2 = run_swiglu_bwd(F, hb, dbits, rows_dev=np.array([48], np.int32))
     check_swiglu(q2, s2, q_ref, s_ref, 48)
     assert np.all(s2[:, 48:] == 0xAB)
+
+
+# ============================================================================ NEXT-1 dual output
+def run_dual(F, inp, seg, swiglu=False, rows_dev=None):
+    """Returns (q, s, qT, sT) of the dual-output kernel, outputs pre-filled with sentinels."""
+    rows, in_cols = inp.shape
+    cols = in_cols // 2 if swiglu else in_cols
+    nseg = 1 if seg is None else len(seg) - 1
+    ld_s = (rows + 15) // 16 * 16
+    nbytes, ntiles = F.transpose_out_shapes(rows, cols, nseg)
+    q = torch.full((rows, cols), 0xAB, dtype=torch.uint8, device="cuda")
+    s = torch.full((cols // 128, ld_s), 0xAB, dtype=torch.uint8, device="cuda")
+    qT = torch.full((max(nbytes, 16),), 0xCD, dtype=torch.uint8, device="cuda")
+    sT = torch.full((ntiles, cols), 0xCD, dtype=torch.uint8, device="cuda")
+    seg_t = None if seg is None else dev(np.asarray(seg, np.int32))
+    if swiglu:
+        F.fp8flow_swiglu_quant_dual(inp, q, s, qT, sT, seg_offsets=seg_t,
+                                    rows_dev=None if rows_dev is None else dev(np.asarray([rows_dev], np.int32)))
+    else:
+        F.fp8flow_quantize_dual(inp, q, s, qT, sT, seg_offsets=seg_t)
+    torch.cuda.synchronize()
+    return host(q), host(s), host(qT), host(sT)
+
+
+DUAL_SEGS = [None, [0, 16, 16, 160, 288, 304, 560, 576]]
+
+
+@pytest.mark.parametrize("seg", DUAL_SEGS)
+@pytest.mark.parametrize("cols", [128, 384, 7168])
+def test_quantize_dual_parity(F, orc, seg, cols):
+    """q, s bit-exact vs the oracle's A1; qT, sT bit-exact vs the oracle's A2 of that (R32)."""
+    rows = 576 if seg is not None else 320
+    x = synth.activations_bf16(rows, cols, 900 + cols)
+    q, s, qT, sT = run_dual(F, x.cuda(), seg)
+    q_ref, s_ref = orc.quantize_rowwise_bf16(synth.bf16_bits(x), ld_s=s.shape[1])
+    assert np.array_equal(q, q_ref)
+    assert np.array_equal(s[:, :rows], s_ref[:, :rows])
+    qT_ref, sT_ref = orc.scaling_aware_transpose(q_ref, s_ref[:, :rows], seg)
+    assert np.array_equal(qT[: qT_ref.size], qT_ref)
+    assert np.array_equal(sT[: sT_ref.shape[0]], sT_ref)
+
+
+def test_quantize_dual_equals_composition(F, orc):
+    """Bit-identical to A1 followed by A2 on the device at the bench's X shape class."""
+    seg = np.concatenate([[0], np.cumsum([512, 16, 0, 1040, 2528])]).astype(np.int32)
+    rows, cols = int(seg[-1]), 7168
+    x = synth.activations_bf16(rows, cols, 77).cuda()
+    q, s, qT, sT = run_dual(F, x, seg)
+    q1, s1 = run_quantize(F, x, ld_s=s.shape[1])
+    qT1, sT1 = run_transpose(F, q1, s1[:, :rows], seg)
+    assert np.array_equal(q, q1) and np.array_equal(s[:, :rows], s1[:, :rows])
+    assert np.array_equal(qT, qT1) and np.array_equal(sT, sT1)
+
+
+@pytest.mark.parametrize("seg,ffn", [(None, 256), ([0, 16, 16, 160, 288, 304, 560, 576], 384),
+                                     ([0, 528, 1040, 1056, 2048], 2048)])
+def test_swiglu_quant_dual_parity(F, orc, seg, ffn):
+    """q, s at the A5 bar vs the oracle; qT, sT bit-exact vs the oracle's A2 of the kernel's own
+    q, s (the composition semantics, R32)."""
+    rows = 320 if seg is None else seg[-1]
+    hb = synth.bf16_bits(synth.normal_bf16(rows, 2 * ffn, 950 + ffn, sigma=1.5))
+    q, s, qT, sT = run_dual(F, bf16_dev(hb), seg, swiglu=True)
+    q_ref, s_ref = orc.swiglu_quant(hb, ld_s=s.shape[1])
+    check_swiglu(q, s, q_ref, s_ref, rows)
+    qT_ref, sT_ref = orc.scaling_aware_transpose(q, s[:, :rows], seg)
+    assert np.array_equal(qT[: qT_ref.size], qT_ref)
+    assert np.array_equal(sT[: sT_ref.shape[0]], sT_ref)
+
+
+def test_swiglu_quant_dual_equals_composition(F, orc):
+    """Bit-identical to A5 then A2 on the device, with the rows given by the last offset (PAD rows
+    of h beyond it are never read into the outputs) and the wild inputs of A5's edge test."""
+    seg = np.concatenate([[0], np.cumsum([528, 0, 16, 1024, 144])]).astype(np.int32)
+    rows_max, ffn = int(seg[-1]) + 64, 2048
+    rng = np.random.default_rng(12)
+    a = rng.normal(0, 1.5, (rows_max, ffn)).astype(np.float32)
+    b = rng.normal(0, 1.5, (rows_max, ffn)).astype(np.float32)
+    a[5, :7] = [-70.0, -100.0, 90.0, -88.5, 0.0, -0.0, 1e-30]
+    b[9, :] = 0.0
+    h = torch.from_numpy(np.concatenate([a, b], 1)).to(torch.bfloat16).cuda()
+    rows = int(seg[-1])
+    q, s, qT, sT = run_dual(F, h, seg, swiglu=True)
+    q1 = torch.full((rows_max, ffn), 0xAB, dtype=torch.uint8, device="cuda")
+    s1 = torch.full((ffn // 128, s.shape[1]), 0xAB, dtype=torch.uint8, device="cuda")
+    F.fp8flow_swiglu_quant(h, q1, s1, rows_dev=dev(np.asarray([rows], np.int32)))
+    torch.cuda.synchronize()
+    q1, s1 = host(q1), host(s1)
+    assert np.array_equal(q[:rows], q1[:rows]) and np.array_equal(s[:, :rows], s1[:, :rows])
+    qT1, sT1 = run_transpose(F, q1[:rows], s1[:, :rows], seg)
+    assert np.array_equal(qT[: qT1.size], qT1) and np.array_equal(sT[: sT1.shape[0]], sT1)
