@@ -224,6 +224,27 @@ FP8FLOW_API int fp8flow_swiglu_quant_dual(const void* h_bf16, int64_t rows_max, 
                                           int64_t ffn, const int32_t* seg_offsets, int32_t num_segs, uint8_t* q,
                                           uint8_t* s, int64_t ld_s, uint8_t* qT, uint8_t* sT, void* stream);
 
+/* ==========================================================================================
+ * NEXT-2  Block-scaled FP8 GEMM, the consumer of the casting-free path (
+ *     P:43): the row-wise (A1/A3/A5) or column-wise (A2) FP8 outputs with their
+ *     1x128 UE8M0 scales feed the 5th-generation tensor cores directly (tcgen05.mma
+ *     kind::mxf8f6f4.block_scale; a 1x128 power-of-two scale is replicated to the four 1x32 MX
+ *     blocks, losslessly).  DESIGN.md R33.
+ *        D[m][n] = sum_k dec(A[m][k]) 2^(sa[k/128][m] - 127) * dec(B_g[n][k]) 2^(sb_g[k/128][n] - 127)
+ *     accumulated in fp32 by the tensor core; D stored as fp32 or BF16 (RNE).
+ *   A       [M][K] E4M3, K-major (row-major with K contiguous); sa [K/128][ld_sa] MN-major
+ *   B       [num_groups][N][K] E4M3, K-major; sb [num_groups][K/128][ld_sb] MN-major
+ *   seg_offsets device int32 [num_groups + 1] splitting the rows of A into groups (experts;
+ *           segment lengths multiples of 16), or NULL = one group of M rows; 1 <= num_groups <= 512
+ *   D       [M][N] fp32 (d_f32 != 0) or BF16; rows outside every group are not written
+ *   M % 16 == 0, N % 256 == 0, K % 128 == 0, ld_sa >= M, ld_sb >= N, both % 16 == 0;
+ *   all pointers 16-byte aligned, A and B 1024-byte aligned recommended.
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B,
+                                         const uint8_t* sb, int64_t ld_sb, int64_t M, int64_t N, int64_t K,
+                                         const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
+                                         void* stream);
+
 /* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
  * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */
 FP8FLOW_API int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream);

@@ -65,6 +65,7 @@ def lib():
                 "orc_checksum64": (ctypes.c_uint64, [P, I64]),
                 "orc_swiglu_bwd_f32": (None, [P, P, I64, I64, P]),
                 "orc_swiglu_bwd_quant": (None, [P, P, I64, I64, P, P, I64]),
+                "orc_gemm_blockscaled": (None, [P, P, I64, P, P, I64, I64, I64, I64, P, I32, I64, I64, P]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -340,3 +341,26 @@ def swiglu_bwd_quant(h_bits, dA_bits, ld_s: int | None = None, threads: int | No
 def checksum64(buf: np.ndarray) -> int:
     b = np.ascontiguousarray(buf).view(np.uint8).reshape(-1)
     return int(lib().orc_checksum64(_p(b), b.size))
+
+
+def gemm_blockscaled(A, sa, B, sb, seg_offsets=None, threads: int | None = None):
+    """NEXT-2 (R33): D[m][n] = sum_k dequant(A)[m][k] * dequant(B_g)[n][k] in fp64.
+    A u8 [M, K], sa u8 [K/128, ld_sa]; B u8 [G, N, K] (or [N, K]), sb u8 [G, K/128, ld_sb] (or 2-D).
+    Rows outside every group are NaN."""
+    A = np.ascontiguousarray(A, dtype=np.uint8)
+    sa = np.ascontiguousarray(sa, dtype=np.uint8)
+    B = np.ascontiguousarray(B, dtype=np.uint8)
+    sb = np.ascontiguousarray(sb, dtype=np.uint8)
+    M, K = A.shape
+    N = B.shape[-2]
+    D = np.full((M, N), np.nan, np.float64)
+    seg = None if seg_offsets is None else np.ascontiguousarray(seg_offsets, dtype=np.int32)
+    groups = 1 if seg is None else len(seg) - 1
+    L = lib()
+
+    def work(lo, hi):
+        L.orc_gemm_blockscaled(_p(A), _p(sa), sa.shape[-1], _p(B), _p(sb), sb.shape[-1], M, N, K, _p(seg), groups,
+                               lo, hi, _p(D))
+
+    _run_split(M, threads, work)
+    return D

@@ -32,6 +32,8 @@
  *                               central finite differences of the fp64 forward
  *   orc_swiglu_bwd_quant       as orc_swiglu_quant: the fp64 definition + tolerance beyond pins
  *   orc_checksum64             closed form (DESIGN.md §4 C11)
+ *   orc_gemm_blockscaled       pinned (torch float64 matmul of torch-decoded operands, one-hot
+ *                               rows = scaled B columns, linearity in the scale exponents)
  */
 #include <math.h>
 #include <stdint.h>
@@ -452,4 +454,35 @@ uint64_t orc_checksum64(const uint8_t* buf, int64_t nbytes)
     uint64_t acc = 0;
     for (int64_t i = 0; i < nbytes; i++) acc += (uint64_t)buf[i] * ((uint64_t)i * 0x9E3779B97F4A7C15ull + 1ull);
     return acc;
+}
+
+
+/* NEXT-2 (R33): the GEMM that consumes the FP8 operands, by its plain
+ * definition -- dequantize both operands exactly (Eq. 4) and sum the products in fp64:
+ *     D[m][n] = sum_k decode(A[m][k]) 2^(sa[k/128][m]-127) * decode(B_g[n][k]) 2^(sb_g[k/128][n]-127)
+ * A [M][K], B [groups][N][K] (K contiguous), sa [K/128][ld_sa], sb [groups][K/128][ld_sb];
+ * group g covers rows [seg[g], seg[g+1]) (seg = NULL: one group of M rows).  Rows outside every
+ * group are left untouched.  D [M][N] fp64. */
+void orc_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B, const uint8_t* sb,
+                          int64_t ld_sb, int64_t M, int64_t N, int64_t K, const int32_t* seg, int32_t groups,
+                          int64_t m_lo, int64_t m_hi, double* D)
+{
+    for (int32_t g = 0; g < (seg ? groups : 1); g++) {
+        int64_t r_begin = seg ? seg[g] : 0, r_end = seg ? seg[g + 1] : M;
+        if (r_begin < m_lo) r_begin = m_lo;
+        if (r_end > m_hi) r_end = m_hi;
+        const uint8_t* Bg = B + (int64_t)g * N * K;
+        const uint8_t* sbg = sb + (int64_t)g * (K / 128) * ld_sb;
+        for (int64_t m = r_begin; m < r_end; m++) {
+            for (int64_t n = 0; n < N; n++) {
+                double acc = 0.0;
+                for (int64_t k = 0; k < K; k++) {
+                    double a = orc_decode_e4m3(A[m * K + k]) * ldexp(1.0, (int)sa[(k / 128) * ld_sa + m] - 127);
+                    double b = orc_decode_e4m3(Bg[n * K + k]) * ldexp(1.0, (int)sbg[(k / 128) * ld_sb + n] - 127);
+                    acc += a * b;
+                }
+                D[m * N + n] = acc;
+            }
+        }
+    }
 }

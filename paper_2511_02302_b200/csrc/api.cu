@@ -255,6 +255,22 @@ int fp8flow_swiglu_quant_dual(const void* h_bf16, int64_t rows_max, const int32_
                                            sT, static_cast<cudaStream_t>(stream), sms));
 }
 
+int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B, const uint8_t* sb,
+                             int64_t ld_sb, int64_t M, int64_t N, int64_t K, const int32_t* seg_offsets,
+                             int32_t num_groups, void* D, int32_t d_f32, void* stream) {
+  if (M < 0 || N <= 0 || K <= 0 || M % 16 != 0 || N % 256 != 0 || K % 128 != 0) return FP8FLOW_ERR_SHAPE;
+  if (M > INT32_MAX - 128 || N > (1 << 24)) return FP8FLOW_ERR_SHAPE;
+  if (ld_sa < M || ld_sa % 16 != 0 || ld_sb < N || ld_sb % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (seg_offsets && (num_groups < 1 || num_groups > 512)) return FP8FLOW_ERR_ARG;
+  if (M == 0 && !seg_offsets) return FP8FLOW_OK;
+  if (!A || !sa || !B || !sb || !D) return FP8FLOW_ERR_NULL;
+  if (!aligned16(A) || !aligned16(sa) || !aligned16(B) || !aligned16(sb) || !aligned16(D)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_gemm_blockscaled(A, sa, ld_sa, B, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32,
+                                          static_cast<cudaStream_t>(stream), sms));
+}
+
 int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream) {
   if (nbytes < 0) return FP8FLOW_ERR_SHAPE;
   if (!out_dev || (nbytes > 0 && !buf)) return FP8FLOW_ERR_NULL;

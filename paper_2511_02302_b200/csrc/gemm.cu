@@ -1,0 +1,317 @@
+// gemm.cu -- NEXT-2: the consumer of the casting-free FP8 path: an sm_100a
+// block-scaled FP8 GEMM on the 5th-generation tensor cores, fed directly by the row-wise (A1, A3,
+// A5) and column-wise (A2) outputs with their 1x128 UE8M0 scales -- no dequantization, no cast.
+//
+//     D[m][n] = sum_k  dec(A[m][k]) 2^(TA[k/128][m])  *  dec(B[n][k]) 2^(TB[k/128][n])
+//
+// A [M][K] and B [N][K] are K-major E4M3 (Fprop: A = X_perm, B = W_e; Wgrad: A, B = the transposed
+// operands of A2), scales MN-major like every other op of the library.  Groups (experts) split M:
+// rows [o_g, o_g+1) use B_g = B + g*N*K and its scales (one GEMM per local expert).
+//
+// Why this maps onto tcgen05 without any rescaling: a 1x128 power-of-two scale is a UE8M0 byte, and
+// kind::mxf8f6f4.block_scale consumes one UE8M0 byte per 32-element K block -- replicating the
+// byte x4 is lossless.  Accumulation is the tensor core's fp32.
+//
+// Kernel (one 128 x 256 output tile per CTA, K in steps of 128):
+//   * warp 0: TMEM allocation (512 columns: accumulator 256 + scale factors) and the TMA producer --
+//     per K step the A tile (128 x 128 B) and B tile (256 x 128 B) with 128-byte swizzle, plus the
+//     raw scale runs (128 + 256 bytes, 1D bulk copies) into a 4-stage mbarrier ring;
+//   * warp 1: expands the scale runs into the tensor-memory scale-factor layout (each byte x4, the
+//     32-row x 16-byte chunks that tcgen05.cp.32x128b.warpx4 broadcasts to the four lane quadrants),
+//     then one elected lane issues tcgen05.cp (SFA, SFB) and 4 x tcgen05.mma (M128 N256 K32) and
+//     commits the stage back to the producer;
+//   * warps 2-5: epilogue -- tcgen05.ld 32x32b of their lane quadrant, fp32 -> BF16 (RNE) or fp32,
+//     masked to the group's rows.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "async.cuh"
+#include "common.cuh"
+#include "kernels.h"
+#include "segments.cuh"
+
+namespace fp8flow {
+
+namespace {
+
+constexpr int kGM = 128, kGN = 256, kGK = 128;  // CTA tile
+constexpr int kGStages = 4;
+constexpr int kGThreads = 192;                  // 6 warps
+constexpr int kGMaxGroups = 512;  // load_segments covers 4 x 192 segments
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kSfCol = 256;                // scale-factor columns start after the accumulator
+
+struct __align__(1024) GemmStage {
+  uint8_t a[kGM * kGK];     // 16 KB, 128B-swizzled by TMA
+  uint8_t b[kGN * kGK];     // 32 KB
+  uint8_t sa[kGM];          // raw scale bytes of the 128 A rows
+  uint8_t sb[kGN];          // raw scale bytes of the 256 B rows
+  uint8_t sfa[512];         // tcgen05.cp source: 32 rows x 16 B
+  uint8_t sfb[2][512];
+};
+
+struct GemmSmem {
+  GemmStage st[kGStages];
+  uint64_t full[kGStages];
+  uint64_t empty[kGStages];
+  uint64_t tmem_full;
+  uint32_t tmem_base;
+  uint32_t red[kGThreads / 32];
+  int32_t seg_off[kGMaxGroups + 1];
+  int32_t blk_prefix[kGMaxGroups + 1];
+  int32_t total_rb;
+};
+
+// ---- tcgen05 wrappers ------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_cp_32x128b_warpx4(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+__device__ __forceinline__ void tc_mma_mxf8(uint32_t d_taddr, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t sfa_taddr, uint32_t sfb_taddr) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_taddr),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_taddr), "r"(sfb_taddr));
+}
+__device__ __forceinline__ void tc_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// shared-memory matrix descriptors (sm_100 "version 1" format)
+__device__ __forceinline__ uint64_t desc_kmajor_sw128(const void* p) {
+  // K-major, 128-byte swizzle: 8-row core-matrix groups 1024 B apart (SBO), LBO unused (1)
+  const uint64_t addr = smem_u32(p);
+  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ uint64_t desc_sf_chunk(const void* p) {
+  // 32 rows x 16 B, no swizzle: core matrices (8 rows x 16 B) 128 B apart (SBO)
+  const uint64_t addr = smem_u32(p);
+  return ((addr & 0x3FFFFull) >> 4) | ((128ull >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor: kind::mxf8f6f4.block_scale, E4M3 x E4M3, fp32 accumulate, K-major A and
+// B, M = 128, N = 256, UE8M0 scales, scale-factor byte `sf_id` of each 32-bit TMEM word
+__host__ __device__ constexpr uint32_t idesc_mxf8(uint32_t sf_id) {
+  return (sf_id << 4) | (static_cast<uint32_t>(kGN >> 3) << 17) | (1u << 23) | (static_cast<uint32_t>(kGM >> 4) << 24) |
+         (sf_id << 29);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(kGThreads, 1)
+    gemm_blockscaled_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                            const uint8_t* __restrict__ sa, int64_t ld_sa, const uint8_t* __restrict__ sb,
+                            int64_t ld_sb, int64_t M, int64_t N, int64_t K, const int32_t* __restrict__ seg_offsets,
+                            int32_t num_groups, void* __restrict__ D, int32_t d_f32) {
+  extern __shared__ __align__(1024) uint8_t smem_gemm[];
+  // 128-byte-swizzled TMA destinations need 1024-byte alignment: align the base explicitly
+  GemmSmem& sm = *reinterpret_cast<GemmSmem*>((reinterpret_cast<uintptr_t>(smem_gemm) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ngroups = seg_offsets == nullptr ? 1 : num_groups;
+
+  if (warp == 0) {
+    tmem_alloc(&sm.tmem_base, kTmemCols);
+  }
+  if (tid == 32) {
+    for (int i = 0; i < kGStages; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    mbar_init(&sm.tmem_full, 1);
+    mbar_init_fence();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+  }
+  tc_fence_before();
+  load_segments<kGThreads>(sm, seg_offsets, ngroups, M);  // ends with a CTA barrier
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  // this CTA's tile: (row block rb over all groups, column tile nt)
+  const int n_nt = static_cast<int>(N / kGN);
+  const int rb = static_cast<int>(blockIdx.x) / n_nt, nt = static_cast<int>(blockIdx.x) - rb * n_nt;
+  const bool has_tile = rb < sm.total_rb;
+  const int g = has_tile ? find_segment(sm.blk_prefix, ngroups, rb) : 0;
+  const int r0 = sm.seg_off[g] + (rb - sm.blk_prefix[g]) * kGM;
+  const int rows_valid = has_tile ? min(kGM, sm.seg_off[g + 1] - r0) : 0;
+  const int n0 = nt * kGN;
+  const int nk = static_cast<int>(K / kGK);
+
+  if (warp == 0) {  // --------------------------------------------------------- TMA producer
+    if (lane == 0 && has_tile) {
+      const uint32_t sa_bytes = static_cast<uint32_t>(min64(kGM, ld_sa - r0));
+      const uint8_t* sbg = sb + static_cast<int64_t>(g) * (K / kGK) * ld_sb;
+      int st = 0;
+      uint32_t parity = 0;
+      for (int kb = 0; kb < nk; ++kb) {
+        if (kb >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
+        GemmStage& S = sm.st[st];
+        mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK + sa_bytes + kGN);
+        tma_load_2d(S.a, &tmap_a, &sm.full[st], kb * kGK, r0);
+        tma_load_2d(S.b, &tmap_b, &sm.full[st], kb * kGK, static_cast<int32_t>(g * N + n0));
+        bulk_load_1d(S.sa, sa + static_cast<int64_t>(kb) * ld_sa + r0, sa_bytes, &sm.full[st]);
+        bulk_load_1d(S.sb, sbg + static_cast<int64_t>(kb) * ld_sb + n0, kGN, &sm.full[st]);
+        if (++st == kGStages) {
+          st = 0;
+          parity ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {  // ----------------------------------------- scale expansion + MMA issue
+    if (has_tile) {
+      int st = 0;
+      uint32_t parity = 0;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&sm.full[st], parity);
+        GemmStage& S = sm.st[st];
+        // SF chunk layout: byte (r % 32) * 16 + (r / 32) * 4 + j holds row r's scale for K block j
+        // of this 128-wide K step; a 1x128 scale is the same for all four 32-wide blocks
+        {
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) w[i] = S.sa[lane + 32 * i] * 0x01010101u;
+          *reinterpret_cast<uint4*>(&S.sfa[lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[i] = S.sb[128 * c + lane + 32 * i] * 0x01010101u;
+            *reinterpret_cast<uint4*>(&S.sfb[c][lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.cp (async proxy)
+        __syncwarp();
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sfa_t = tmem + kSfCol + 16u * (kb & 1);
+          const uint32_t sfb_t = sfa_t + 4u;
+          tc_cp_32x128b_warpx4(sfa_t, desc_sf_chunk(S.sfa));
+          tc_cp_32x128b_warpx4(sfb_t, desc_sf_chunk(S.sfb[0]));
+          tc_cp_32x128b_warpx4(sfb_t + 4u, desc_sf_chunk(S.sfb[1]));
+          const uint64_t adesc = desc_kmajor_sw128(S.a), bdesc = desc_kmajor_sw128(S.b);
+#pragma unroll
+          for (int k = 0; k < kGK / 32; ++k) {
+            // advance the start address by 32 bytes (one K=32 slice) inside the swizzle atom
+            tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(k)),
+                        (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
+          }
+          tc_commit(&sm.empty[st]);  // the stage (and its SF chunks) is free when these MMAs complete
+        }
+        __syncwarp();
+        if (++st == kGStages) {
+          st = 0;
+          parity ^= 1u;
+        }
+      }
+      if (lane == 0) tc_commit(&sm.tmem_full);
+      __syncwarp();
+    }
+  } else {  // ------------------------------------------------------------------- epilogue
+    if (has_tile) {
+      const int q = warp & 3;  // TMEM lane quadrant this warp may access
+      mbar_wait(&sm.tmem_full, 0);
+      tc_fence_after();
+      const int row = 32 * q + lane;
+      const bool ok = row < rows_valid;
+      const int64_t grow = static_cast<int64_t>(r0) + row;
+#pragma unroll 1
+      for (int c = 0; c < kGN; c += 32) {
+        uint32_t v[32];
+        tc_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(c), v);
+        if (ok) {
+          if (d_f32) {
+            float* dp = static_cast<float*>(D) + grow * N + n0 + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+          } else {
+            __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(D) + grow * N + n0 + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8)
+              st_v4(dp + j, make_uint4(pack_bf16x2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
+                                       pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])),
+                                       pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5])),
+                                       pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]))));
+          }
+        }
+      }
+      tc_fence_before();
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+typedef CUresult (*PFN_encodeTiled_g)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B,
+                                    const uint8_t* sb, int64_t ld_sb, int64_t M, int64_t N, int64_t K,
+                                    const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
+                                    cudaStream_t stream, int num_sms) {
+  (void)num_sms;
+  static PFN_encodeTiled_g encode = nullptr;
+  if (!encode) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) != cudaSuccess ||
+        qres != cudaDriverEntryPointSuccess)
+      return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_encodeTiled_g>(p);
+    cudaFuncSetAttribute(gemm_blockscaled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(GemmSmem) + 1024));
+  }
+  const int groups = seg_offsets == nullptr ? 1 : num_groups;
+  CUtensorMap ma, mb;
+  const cuuint32_t estride[2] = {1, 1};
+  const cuuint64_t gdim_a[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+  const cuuint64_t gstr_a[1] = {static_cast<cuuint64_t>(K)};
+  const cuuint32_t box_a[2] = {kGK, kGM};
+  const cuuint64_t gdim_b[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N) * groups};
+  const cuuint64_t gstr_b[1] = {static_cast<cuuint64_t>(K)};
+  const cuuint32_t box_b[2] = {kGK, kGN};
+  if (encode(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(A), gdim_a, gstr_a, box_a, estride,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+      encode(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(B), gdim_b, gstr_b, box_b, estride,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  // grid: upper bound of row blocks over all groups x column tiles; CTAs past the real count exit
+  const int64_t rb_ub = M / kGM + groups;
+  const int64_t grid = rb_ub * (N / kGN);
+  gemm_blockscaled_kernel<<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
+      ma, mb, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
+  return cudaGetLastError();
+}
+
+}  // namespace fp8flow

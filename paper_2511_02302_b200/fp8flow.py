@@ -45,6 +45,7 @@ SIGNATURES = {
     "fp8flow_swiglu_bwd_quant": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P]),
     "fp8flow_quantize_dual": (ctypes.c_int, [_P, _I64, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
     "fp8flow_swiglu_quant_dual": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
+    "fp8flow_gemm_blockscaled": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _P, _I32, _P]),
 }
 
 
@@ -215,6 +216,22 @@ def fp8flow_swiglu_quant_dual(h: torch.Tensor, q: torch.Tensor, s: torch.Tensor,
     _check(lib().fp8flow_swiglu_quant_dual(_ptr(h), rows_max, _ptr(rows_dev), F2 // 2, _ptr(seg_offsets), nseg,
                                            _ptr(_u8(q)), _ptr(_u8(s)), s.shape[1], _ptr(_u8(qT)), _ptr(_u8(sT)),
                                            _stream(stream)), "fp8flow_swiglu_quant_dual")
+
+
+def fp8flow_gemm_blockscaled(A: torch.Tensor, sa: torch.Tensor, B: torch.Tensor, sb: torch.Tensor, D: torch.Tensor,
+                             seg_offsets: torch.Tensor | None = None, stream=None) -> None:
+    """NEXT-2: A uint8 [M, K] + sa [K/128, ld_sa]; B uint8 [G, N, K] (or [N, K]) + sb [G, K/128, ld_sb]
+    (or [K/128, ld_sb]); D float32 or bfloat16 [M, N]."""
+    M, K = A.shape
+    N = B.shape[-2]
+    G = 1 if B.dim() == 2 else B.shape[0]
+    assert D.shape == (M, N) and D.dtype in (torch.float32, torch.bfloat16)
+    ngroups = 0 if seg_offsets is None else seg_offsets.numel() - 1
+    assert seg_offsets is None or ngroups == G
+    _check(lib().fp8flow_gemm_blockscaled(_ptr(_u8(A)), _ptr(_u8(sa)), sa.shape[-1], _ptr(_u8(B)), _ptr(_u8(sb)),
+                                          sb.shape[-1], M, N, K, _ptr(seg_offsets), ngroups, _ptr(D),
+                                          1 if D.dtype == torch.float32 else 0, _stream(stream)),
+           "fp8flow_gemm_blockscaled")
 
 
 def fp8flow_checksum64(buf: torch.Tensor, out: torch.Tensor, stream=None) -> None:

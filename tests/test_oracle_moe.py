@@ -228,3 +228,65 @@ def test_swiglu_bwd_special_cases_and_quant(orc):
     q, s = orc.swiglu_bwd_quant(hb, dA)
     q2, s2 = orc.quantize_rows_f64(orc.swiglu_bwd_f32(hb, dA).astype(np.float64))
     assert np.array_equal(q, q2) and np.array_equal(s, s2)
+
+
+# ============================================================================ NEXT-2 GEMM oracle
+def _torch_dequant(q, s):
+    """Independent decode: torch's float8_e4m3fn reinterpretation (a library routine) times 2^T."""
+    vals = torch.from_numpy(np.ascontiguousarray(q)).view(torch.float8_e4m3fn).to(torch.float64)
+    K = q.shape[1]
+    T = torch.from_numpy(s[: K // 128, : q.shape[0]].astype(np.int64) - 127).T          # [rows, K/128]
+    return vals * torch.pow(2.0, T.repeat_interleave(128, dim=1).to(torch.float64))
+
+
+def _rand_operand(rng, rows, K, ld):
+    q = rng.integers(0, 256, (rows, K), dtype=np.uint8)
+    q[(q & 0x7F) == 0x7F] = 0x3C                                                         # no NaN codes
+    s = rng.integers(110, 140, (K // 128, ld), dtype=np.uint8)
+    return q, s
+
+
+def test_gemm_oracle_vs_torch_matmul(orc):
+    """Pin: torch float64 matmul of torch-decoded, scaled operands, with groups over M."""
+    rng = np.random.default_rng(41)
+    M, N, K, G = 96, 48, 384, 3
+    A, sa = _rand_operand(rng, M, K, 112)
+    Bs = [_rand_operand(rng, N, K, 64) for _ in range(G)]
+    B = np.stack([b[0] for b in Bs])
+    sb = np.stack([b[1] for b in Bs])
+    seg = np.array([0, 16, 16, 80], np.int32)                                            # empty group, rows 80.. none
+    D = orc.gemm_blockscaled(A, sa, B, sb, seg)
+    Ad = _torch_dequant(A, sa)
+    for g in range(G):
+        lo, hi = seg[g], seg[g + 1]
+        ref = (Ad[lo:hi] @ _torch_dequant(B[g], sb[g]).T).numpy()
+        np.testing.assert_allclose(D[lo:hi], ref, rtol=1e-12, atol=0)
+    assert np.all(np.isnan(D[80:]))                                                      # outside every group
+
+
+def test_gemm_oracle_one_hot_rows(orc):
+    """Pin (closed form): a row of A holding the single code 0x38 (= 1.0) at column k with scale
+    byte t selects 2^(t-127) * dequant(B)[:, k]."""
+    rng = np.random.default_rng(42)
+    M, N, K = 16, 32, 256
+    A = np.zeros((M, K), np.uint8)
+    sa = np.full((K // 128, M), 127, np.uint8)
+    ks = rng.integers(0, K, M)
+    for m in range(M):
+        A[m, ks[m]] = 0x38
+        sa[ks[m] // 128, m] = 120 + m
+    B, sb = _rand_operand(rng, N, K, N)
+    D = orc.gemm_blockscaled(A, sa, B, sb)
+    Bd = orc.dequantize_rows(B, sb)
+    for m in range(M):
+        np.testing.assert_array_equal(D[m], 2.0 ** (120 + m - 127) * Bd[:, ks[m]])
+
+
+def test_gemm_oracle_scale_linearity(orc):
+    """Pin: adding d to every scale byte of A multiplies D by 2^d exactly (pow2 scales)."""
+    rng = np.random.default_rng(43)
+    A, sa = _rand_operand(rng, 32, 256, 32)
+    B, sb = _rand_operand(rng, 16, 256, 16)
+    D0 = orc.gemm_blockscaled(A, sa, B, sb)
+    D1 = orc.gemm_blockscaled(A, sa + 3, B, sb)
+    np.testing.assert_array_equal(D1, D0 * 8.0)
