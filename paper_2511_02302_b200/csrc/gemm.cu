@@ -12,16 +12,20 @@
 // kind::mxf8f6f4.block_scale consumes one UE8M0 byte per 32-element K block -- replicating the
 // byte x4 is lossless.  Accumulation is the tensor core's fp32.
 //
-// Kernel (one 128 x 256 output tile per CTA, K in steps of 128):
-//   * warp 0: TMEM allocation (512 columns: accumulator 256 + scale factors) and the TMA producer --
-//     per K step the A tile (128 x 128 B) and B tile (256 x 128 B) with 128-byte swizzle, plus the
-//     raw scale runs (128 + 256 bytes, 1D bulk copies) into a 4-stage mbarrier ring;
-//   * warp 1: expands the scale runs into the tensor-memory scale-factor layout (each byte x4, the
-//     32-row x 16-byte chunks that tcgen05.cp.32x128b.warpx4 broadcasts to the four lane quadrants),
-//     then one elected lane issues tcgen05.cp (SFA, SFB) and 4 x tcgen05.mma (M128 N256 K32) and
-//     commits the stage back to the producer;
-//   * warps 2-5: epilogue -- tcgen05.ld 32x32b of their lane quadrant, fp32 -> BF16 (RNE) or fp32,
-//     masked to the group's rows.
+// Kernel: persistent, one CTA per SM walking 128 x 256 output tiles (row blocks of all groups x
+// column tiles), K in steps of 128 through a 4-stage mbarrier ring.  Warp roles:
+//   * warp 0: TMEM allocation (512 columns: the 256-column fp32 accumulator + scale factors) and
+//     the TMA producer -- per K step the A tile (128 x 128 B) and B tile (256 x 128 B) with
+//     128-byte swizzle, plus the raw scale runs (128 + 256 bytes, 1D bulk copies);
+//   * warp 1: MMA issuer -- one elected lane issues tcgen05.cp (SFA, SFB into a double-buffered
+//     set of scale-factor columns) and 4 x tcgen05.mma (M128 N256 K32) per K step, commits each
+//     stage back to the producer and each finished tile to the epilogue;
+//   * warp 2: expands each stage's scale runs into the tensor-memory scale-factor layout (a 1x128
+//     byte replicated x4; 32-row x 16-byte chunks that tcgen05.cp.32x128b.warpx4 broadcasts to
+//     the four lane quadrants), off the MMA issuer's critical path;
+//   * warps 3-10: epilogue -- two warps per TMEM lane quadrant (128 columns each) load the whole
+//     accumulator with tcgen05.ld, hand the tensor memory back at once (so the next tile's MMAs
+//     overlap these stores), convert fp32 -> BF16 (RNE) or keep fp32, and store the group's rows.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -36,8 +40,8 @@ namespace {
 
 constexpr int kGM = 128, kGN = 256, kGK = 128;  // CTA tile
 constexpr int kGStages = 4;
-constexpr int kGThreads = 192;                  // 6 warps
-constexpr int kGMaxGroups = 512;  // load_segments covers 4 x 192 segments
+constexpr int kGThreads = 352;                  // 11 warps
+constexpr int kGMaxGroups = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kSfCol = 256;                // scale-factor columns start after the accumulator
 
@@ -54,7 +58,9 @@ struct GemmSmem {
   GemmStage st[kGStages];
   uint64_t full[kGStages];
   uint64_t empty[kGStages];
-  uint64_t tmem_full;
+  uint64_t sfready[kGStages];  // the stage's scale-factor chunks are expanded
+  uint64_t tmem_full;          // accumulator complete (tcgen05.commit)
+  uint64_t tmem_empty;         // accumulator read out by the 8 epilogue warps
   uint32_t tmem_base;
   uint32_t red[kGThreads / 32];
   int32_t seg_off[kGMaxGroups + 1];
@@ -123,6 +129,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// tile t -> (group, first row, valid rows, first column)
+struct GemmTile {
+  int g, r0, rows, n0;
+};
+__device__ __forceinline__ GemmTile gemm_tile(const GemmSmem& sm, int ngroups, int n_nt, int t) {
+  const int rb = t / n_nt, nt = t - rb * n_nt;
+  const int g = find_segment(sm.blk_prefix, ngroups, rb);
+  const int r0 = sm.seg_off[g] + (rb - sm.blk_prefix[g]) * kGM;
+  return {g, r0, min(kGM, sm.seg_off[g + 1] - r0), nt * kGN};
+}
+
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_blockscaled_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const uint8_t* __restrict__ sa, int64_t ld_sa, const uint8_t* __restrict__ sb,
@@ -134,15 +151,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ngroups = seg_offsets == nullptr ? 1 : num_groups;
 
-  if (warp == 0) {
-    tmem_alloc(&sm.tmem_base, kTmemCols);
-  }
+  if (warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   if (tid == 32) {
     for (int i = 0; i < kGStages; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], 1);
+      mbar_init(&sm.sfready[i], 1);
     }
     mbar_init(&sm.tmem_full, 1);
+    mbar_init(&sm.tmem_empty, 8);
     mbar_init_fence();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
@@ -151,74 +168,54 @@ __global__ void __launch_bounds__(kGThreads, 1)
   load_segments<kGThreads>(sm, seg_offsets, ngroups, M);  // ends with a CTA barrier
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-
-  // this CTA's tile: (row block rb over all groups, column tile nt)
   const int n_nt = static_cast<int>(N / kGN);
-  const int rb = static_cast<int>(blockIdx.x) / n_nt, nt = static_cast<int>(blockIdx.x) - rb * n_nt;
-  const bool has_tile = rb < sm.total_rb;
-  const int g = has_tile ? find_segment(sm.blk_prefix, ngroups, rb) : 0;
-  const int r0 = sm.seg_off[g] + (rb - sm.blk_prefix[g]) * kGM;
-  const int rows_valid = has_tile ? min(kGM, sm.seg_off[g + 1] - r0) : 0;
-  const int n0 = nt * kGN;
+  const int total_tiles = sm.total_rb * n_nt;
   const int nk = static_cast<int>(K / kGK);
 
   if (warp == 0) {  // --------------------------------------------------------- TMA producer
-    if (lane == 0 && has_tile) {
-      const uint32_t sa_bytes = static_cast<uint32_t>(min64(kGM, ld_sa - r0));
-      const uint8_t* sbg = sb + static_cast<int64_t>(g) * (K / kGK) * ld_sb;
-      int st = 0;
+    if (lane == 0) {
+      int st = 0, n = 0;
       uint32_t parity = 0;
-      for (int kb = 0; kb < nk; ++kb) {
-        if (kb >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
-        GemmStage& S = sm.st[st];
-        mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK + sa_bytes + kGN);
-        tma_load_2d(S.a, &tmap_a, &sm.full[st], kb * kGK, r0);
-        tma_load_2d(S.b, &tmap_b, &sm.full[st], kb * kGK, static_cast<int32_t>(g * N + n0));
-        bulk_load_1d(S.sa, sa + static_cast<int64_t>(kb) * ld_sa + r0, sa_bytes, &sm.full[st]);
-        bulk_load_1d(S.sb, sbg + static_cast<int64_t>(kb) * ld_sb + n0, kGN, &sm.full[st]);
-        if (++st == kGStages) {
-          st = 0;
-          parity ^= 1u;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const GemmTile T = gemm_tile(sm, ngroups, n_nt, t);
+        const uint32_t sa_bytes = static_cast<uint32_t>(min64(kGM, ld_sa - T.r0));
+        const uint8_t* sbg = sb + static_cast<int64_t>(T.g) * (K / kGK) * ld_sb;
+        for (int kb = 0; kb < nk; ++kb, ++n) {
+          if (n >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
+          GemmStage& S = sm.st[st];
+          mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK + sa_bytes + kGN);
+          tma_load_2d(S.a, &tmap_a, &sm.full[st], kb * kGK, T.r0);
+          tma_load_2d(S.b, &tmap_b, &sm.full[st], kb * kGK, static_cast<int32_t>(T.g * N + T.n0));
+          bulk_load_1d(S.sa, sa + static_cast<int64_t>(kb) * ld_sa + T.r0, sa_bytes, &sm.full[st]);
+          bulk_load_1d(S.sb, sbg + static_cast<int64_t>(kb) * ld_sb + T.n0, kGN, &sm.full[st]);
+          if (++st == kGStages) {
+            st = 0;
+            parity ^= 1u;
+          }
         }
       }
     }
-  } else if (warp == 1) {  // ----------------------------------------- scale expansion + MMA issue
-    if (has_tile) {
-      int st = 0;
-      uint32_t parity = 0;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&sm.full[st], parity);
-        GemmStage& S = sm.st[st];
-        // SF chunk layout: byte (r % 32) * 16 + (r / 32) * 4 + j holds row r's scale for K block j
-        // of this 128-wide K step; a 1x128 scale is the same for all four 32-wide blocks
-        {
-          uint32_t w[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) w[i] = S.sa[lane + 32 * i] * 0x01010101u;
-          *reinterpret_cast<uint4*>(&S.sfa[lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) w[i] = S.sb[128 * c + lane + 32 * i] * 0x01010101u;
-            *reinterpret_cast<uint4*>(&S.sfb[c][lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
-        fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.cp (async proxy)
-        __syncwarp();
+  } else if (warp == 1) {  // ------------------------------------------------------ MMA issue
+    int st = 0, step = 0;
+    uint32_t parity = 0;
+    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+      if (i > 0) mbar_wait(&sm.tmem_empty, (i - 1) & 1);  // the previous tile has been read out
+      tc_fence_after();
+      for (int kb = 0; kb < nk; ++kb, ++step) {
+        mbar_wait(&sm.sfready[st], parity);  // implies the stage's TMA data has landed
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sfa_t = tmem + kSfCol + 16u * (kb & 1);
+          GemmStage& S = sm.st[st];
+          const uint32_t sfa_t = tmem + kSfCol + 16u * (step & 1);
           const uint32_t sfb_t = sfa_t + 4u;
           tc_cp_32x128b_warpx4(sfa_t, desc_sf_chunk(S.sfa));
           tc_cp_32x128b_warpx4(sfb_t, desc_sf_chunk(S.sfb[0]));
           tc_cp_32x128b_warpx4(sfb_t + 4u, desc_sf_chunk(S.sfb[1]));
           const uint64_t adesc = desc_kmajor_sw128(S.a), bdesc = desc_kmajor_sw128(S.b);
 #pragma unroll
-          for (int k = 0; k < kGK / 32; ++k) {
-            // advance the start address by 32 bytes (one K=32 slice) inside the swizzle atom
+          for (int k = 0; k < kGK / 32; ++k)  // +32 bytes (one K=32 slice) inside the swizzle atom
             tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(k)),
                         (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
-          }
           tc_commit(&sm.empty[st]);  // the stage (and its SF chunks) is free when these MMAs complete
         }
         __syncwarp();
@@ -230,35 +227,70 @@ __global__ void __launch_bounds__(kGThreads, 1)
       if (lane == 0) tc_commit(&sm.tmem_full);
       __syncwarp();
     }
-  } else {  // ------------------------------------------------------------------- epilogue
-    if (has_tile) {
-      const int q = warp & 3;  // TMEM lane quadrant this warp may access
-      mbar_wait(&sm.tmem_full, 0);
-      tc_fence_after();
-      const int row = 32 * q + lane;
-      const bool ok = row < rows_valid;
-      const int64_t grow = static_cast<int64_t>(r0) + row;
-#pragma unroll 1
-      for (int c = 0; c < kGN; c += 32) {
-        uint32_t v[32];
-        tc_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(c), v);
-        if (ok) {
-          if (d_f32) {
-            float* dp = static_cast<float*>(D) + grow * N + n0 + c;
+  } else if (warp == 2) {  // --------------------------------------------- scale expansion
+    int st = 0;
+    uint32_t parity = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&sm.full[st], parity);
+        GemmStage& S = sm.st[st];
+        // chunk byte (r % 32) * 16 + (r / 32) * 4 + j = row r's scale for the 32-wide K block j;
+        // a 1x128 scale is the same for all four
+        uint32_t w[4];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        for (int i = 0; i < 4; ++i) w[i] = S.sa[lane + 32 * i] * 0x01010101u;
+        *reinterpret_cast<uint4*>(&S.sfa[lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) w[i] = S.sb[128 * c + lane + 32 * i] * 0x01010101u;
+          *reinterpret_cast<uint4*>(&S.sfb[c][lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.cp (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.sfready[st]);
+        if (++st == kGStages) {
+          st = 0;
+          parity ^= 1u;
+        }
+      }
+    }
+  } else {  // ------------------------------------------------------------------- epilogue
+    const int q = warp & 3;           // TMEM lane quadrant this warp may access
+    const int half = (warp - 3) >> 2;  // columns [128 half, 128 half + 128)
+    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+      const GemmTile T = gemm_tile(sm, ngroups, n_nt, t);
+      mbar_wait(&sm.tmem_full, i & 1);
+      tc_fence_after();
+      uint32_t v[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tc_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half + 32 * c),
+                         v[c]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tmem_empty);  // the MMAs of the next tile may start
+      const int row = 32 * q + lane;
+      if (row < T.rows) {
+        const int64_t grow = static_cast<int64_t>(T.r0) + row;
+        const int col0 = T.n0 + 128 * half;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (d_f32) {
+            float* dp = static_cast<float*>(D) + grow * N + col0 + 32 * c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[c][j], v[c][j + 1], v[c][j + 2], v[c][j + 3]));
           } else {
-            __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(D) + grow * N + n0 + c;
+            __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(D) + grow * N + col0 + 32 * c;
 #pragma unroll
             for (int j = 0; j < 32; j += 8)
-              st_v4(dp + j, make_uint4(pack_bf16x2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])),
-                                       pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])),
-                                       pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5])),
-                                       pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]))));
+              st_v4(dp + j, make_uint4(pack_bf16x2(__uint_as_float(v[c][j]), __uint_as_float(v[c][j + 1])),
+                                       pack_bf16x2(__uint_as_float(v[c][j + 2]), __uint_as_float(v[c][j + 3])),
+                                       pack_bf16x2(__uint_as_float(v[c][j + 4]), __uint_as_float(v[c][j + 5])),
+                                       pack_bf16x2(__uint_as_float(v[c][j + 6]), __uint_as_float(v[c][j + 7]))));
           }
         }
       }
-      tc_fence_before();
     }
   }
   __syncthreads();
@@ -278,7 +310,6 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
                                     const uint8_t* sb, int64_t ld_sb, int64_t M, int64_t N, int64_t K,
                                     const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
                                     cudaStream_t stream, int num_sms) {
-  (void)num_sms;
   static PFN_encodeTiled_g encode = nullptr;
   if (!encode) {
     void* p = nullptr;
@@ -306,9 +337,9 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  // grid: upper bound of row blocks over all groups x column tiles; CTAs past the real count exit
-  const int64_t rb_ub = M / kGM + groups;
-  const int64_t grid = rb_ub * (N / kGN);
+  // persistent: at most one CTA per SM, tiles walked with a static stride
+  const int64_t tiles_ub = (M / kGM + groups) * (N / kGN);
+  const int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   gemm_blockscaled_kernel<<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
       ma, mb, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
   return cudaGetLastError();
