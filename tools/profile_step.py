@@ -1,0 +1,56 @@
+"""Profiling driver (not product): warms up bench.py's step, then runs ONE serial pass of the
+step's 9 launches plus the NEXT-row kernels (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM
+on a 2048-row slice) between cudaProfilerStart/Stop, so that
+    ncu --set full --profile-from-start off ... python tools/profile_step.py
+captures exactly one launch of each kernel, in this order."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import synth  # noqa: E402
+
+ORDER = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
+         "A2_transpose_xperm", "A2_transpose_a", "NEXT1_swiglu_bwd_quant", "NEXT1_swiglu_quant_dual",
+         "NEXT2_gemm_fc1_fprop"]
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    hw = bench.HostWorkload(0)
+    ds = bench.DeviceStep(hw, dev)
+    F = ds.F
+    dA = synth.normal_bf16(hw.R, bench.FFN, synth.BASE_SEED + 5, sigma=0.5).to(dev)
+    qb = torch.empty(hw.R, 2 * bench.FFN, dtype=torch.uint8, device=dev)
+    sbw = torch.empty(2 * bench.FFN // 128, hw.R, dtype=torch.uint8, device=dev)
+    E = hw.E_loc
+    W = torch.randint(0, 0x7E, (E, 2 * bench.FFN, bench.HIDDEN), dtype=torch.uint8, device=dev)
+    sW = torch.full((E, bench.HIDDEN // 128, 2 * bench.FFN), 115, dtype=torch.uint8, device=dev)
+    Dg = torch.empty(hw.R, 2 * bench.FFN, dtype=torch.bfloat16, device=dev)
+    rows_dev = ds.off[E:]
+
+    def extra():
+        F.fp8flow_swiglu_bwd_quant(ds.h, dA, qb, sbw, rows_dev=rows_dev)
+        F.fp8flow_swiglu_quant_dual(ds.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off)
+        F.fp8flow_gemm_blockscaled(ds.x_perm, ds.s_perm, W, sW, Dg, seg_offsets=ds.off)
+
+    for _ in range(3):
+        ds.launch_ops(record=False)
+        extra()
+    torch.cuda.synchronize()
+    ds.flush_l2()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    ds.launch_ops(record=False)
+    extra()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print("profiled:", ", ".join(ORDER))
+
+
+if __name__ == "__main__":
+    main()
