@@ -245,6 +245,20 @@ FP8FLOW_API int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, in
                                          const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
                                          void* stream);
 
+/* NEXT-2 Wgrad: groups split K (each expert's tokens): D_e = AT_e * BT_e^T, i.e.
+ *        D_e[m][n] = sum_{k < m_e} dec(AT_e[m][k]) 2^(saT[P_e + k/128][m] - 127) * dec(BT_e[n][k]) 2^(sbT[P_e + k/128][n] - 127)
+ *     with both operands exactly as A2 (fp8flow_scaling_aware_transpose) leaves them for the same
+ *     segments: AT_e = [Ma][m_e] at byte offset Ma*o_e, saT rows P_e .. P_e + ceil(m_e/128) - 1
+ *     (P_e = sum_{e'<e} ceil(m_e'/128)), likewise BT/sbT with Nb.  Example: dW1_e = dH_e^T X_e with
+ *     AT = A2(dH), BT = A2(X_perm).  Segment lengths multiples of 16 (a partial last K block is
+ *     zero-padded); a group with no rows gets D_e = 0.
+ *   D  [num_groups][Ma][Nb] fp32 (d_f32 != 0) or BF16.  Ma % 128 == 0, Nb % 256 == 0,
+ *   1 <= num_groups <= 512, seg_offsets device int32 [num_groups + 1] (required).
+ * ========================================================================================== */
+FP8FLOW_API int fp8flow_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT,
+                                   const uint8_t* sbT, int64_t Nb, const int32_t* seg_offsets, int32_t num_groups,
+                                   void* D, int32_t d_f32, void* stream);
+
 /* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
  * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */
 FP8FLOW_API int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream);

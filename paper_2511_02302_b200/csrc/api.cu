@@ -271,6 +271,19 @@ int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa,
                                           static_cast<cudaStream_t>(stream), sms));
 }
 
+int fp8flow_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT, const uint8_t* sbT,
+                       int64_t Nb, const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
+                       void* stream) {
+  if (Ma <= 0 || Nb <= 0 || Ma % 128 != 0 || Nb % 256 != 0 || Ma > (1 << 24) || Nb > (1 << 24)) return FP8FLOW_ERR_SHAPE;
+  if (num_groups < 1 || num_groups > 512) return FP8FLOW_ERR_ARG;
+  if (!AT || !saT || !BT || !sbT || !D || !seg_offsets) return FP8FLOW_ERR_NULL;
+  if (!aligned16(AT) || !aligned16(saT) || !aligned16(BT) || !aligned16(sbT) || !aligned16(D)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_gemm_wgrad(AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32,
+                                    static_cast<cudaStream_t>(stream), sms));
+}
+
 int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream) {
   if (nbytes < 0) return FP8FLOW_ERR_SHAPE;
   if (!out_dev || (nbytes > 0 && !buf)) return FP8FLOW_ERR_NULL;

@@ -300,6 +300,244 @@ __global__ void __launch_bounds__(kGThreads, 1)
   }
 }
 
+// =============================================================================================
+// Wgrad: groups split K (the tokens of each expert), e.g. dW1_e = dH_e^T X_e.  Both operands are
+// A2's column-wise outputs: per segment e a [rows][m_e] K-major matrix at byte offset rows * o_e,
+// scales sT rows P_e .. P_e + ceil(m_e/128) - 1 (A2's layout).  The row stride m_e changes per
+// group (and m_e is only a multiple of 16), so the operand tiles are loaded with cp.async 16-byte
+// chunks written straight into the 128-byte-swizzled K-major layout (chunk c of row r lands at
+// r * 128 + ((c ^ (r % 8)) * 16), the pattern TMA's SWIZZLE_128B produces), zero-filled past the
+// segment's last token; a group with no tokens gets D_e = 0.
+// Warps: 0-1 cp.async producers (warp 0 also owns TMEM), 2 MMA issuer, 3 scale expansion,
+// 4-11 epilogue (as in the Fprop kernel).
+// =============================================================================================
+constexpr int kWThreads = 384;
+constexpr int kWProd = 64;  // producer threads
+
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct WgradSmem {
+  GemmStage st[kGStages];
+  uint64_t full[kGStages];     // kWProd producer arrivals (after their copies landed + proxy fence)
+  uint64_t empty[kGStages];
+  uint64_t sfready[kGStages];
+  uint64_t tmem_full;
+  uint64_t tmem_empty;
+  uint32_t tmem_base;
+  uint32_t red[kWThreads / 32];
+  int32_t seg_off[kGMaxGroups + 1];
+  int32_t blk_prefix[kGMaxGroups + 1];
+  int32_t total_rb;
+};
+
+__global__ void __launch_bounds__(kWThreads, 1)
+    gemm_wgrad_kernel(const uint8_t* __restrict__ AT, const uint8_t* __restrict__ saT, int64_t Ma,
+                      const uint8_t* __restrict__ BT, const uint8_t* __restrict__ sbT, int64_t Nb,
+                      const int32_t* __restrict__ seg_offsets, int32_t num_groups, void* __restrict__ D,
+                      int32_t d_f32) {
+  extern __shared__ __align__(1024) uint8_t smem_wg[];
+  WgradSmem& sm = *reinterpret_cast<WgradSmem*>((reinterpret_cast<uintptr_t>(smem_wg) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
+  if (tid == 32) {
+    for (int i = 0; i < kGStages; ++i) {
+      mbar_init(&sm.full[i], kWProd);
+      mbar_init(&sm.empty[i], 1);
+      mbar_init(&sm.sfready[i], 1);
+    }
+    mbar_init(&sm.tmem_full, 1);
+    mbar_init(&sm.tmem_empty, 8);
+    mbar_init_fence();
+  }
+  tc_fence_before();
+  load_segments<kWThreads>(sm, seg_offsets, num_groups, 0);  // blk_prefix[e] = P_e (scale-tile rows)
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const int n_mt = static_cast<int>(Ma / kGM), n_nt = static_cast<int>(Nb / kGN);
+  const int per_group = n_mt * n_nt;
+  const int total_tiles = num_groups * per_group;
+  auto tile_of = [&](int t, int& e, int& m0, int& n0) {
+    e = t / per_group;
+    const int r = t - e * per_group;
+    m0 = (r / n_nt) * kGM;
+    n0 = (r % n_nt) * kGN;
+  };
+
+  if (warp < 2) {  // ------------------------------------------------------- cp.async producers
+    int st = 0, n = 0, prev = -1;
+    uint32_t parity = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int e, m0, n0;
+      tile_of(t, e, m0, n0);
+      const int o = sm.seg_off[e], me = sm.seg_off[e + 1] - o;
+      const int nk = (me + kGK - 1) / kGK;
+      const uint8_t* a_base = AT + Ma * o + static_cast<int64_t>(m0) * me;
+      const uint8_t* b_base = BT + Nb * o + static_cast<int64_t>(n0) * me;
+      for (int kb = 0; kb < nk; ++kb, ++n) {
+        if (n >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
+        GemmStage& S = sm.st[st];
+        const int kv = me - kb * kGK;  // valid K bytes in this step (>= 16)
+#pragma unroll 4
+        for (int q = tid; q < kGM * 8; q += kWProd) {
+          const int r = q >> 3, c = q & 7;
+          const uint32_t ok = 16 * c < kv ? 16u : 0u;
+          cp_async_16(&S.a[r * 128 + ((c ^ (r & 7)) * 16)], a_base + static_cast<int64_t>(r) * me + kb * kGK + (ok ? 16 * c : 0),
+                      ok);
+        }
+#pragma unroll 4
+        for (int q = tid; q < kGN * 8; q += kWProd) {
+          const int r = q >> 3, c = q & 7;
+          const uint32_t ok = 16 * c < kv ? 16u : 0u;
+          cp_async_16(&S.b[r * 128 + ((c ^ (r & 7)) * 16)], b_base + static_cast<int64_t>(r) * me + kb * kGK + (ok ? 16 * c : 0),
+                      ok);
+        }
+        const int64_t srow = sm.blk_prefix[e] + kb;  // this K block's row of sT
+        if (tid < kGM / 16) cp_async_16(&S.sa[16 * tid], saT + srow * Ma + m0 + 16 * tid, 16);
+        else if (tid < kGM / 16 + kGN / 16) {
+          const int j = tid - kGM / 16;
+          cp_async_16(&S.sb[16 * j], sbT + srow * Nb + n0 + 16 * j, 16);
+        }
+        cp_async_commit();
+        if (prev >= 0) {  // the previous stage's copies have landed: publish it
+          cp_async_wait<1>();
+          fence_proxy_async_smem();
+          mbar_arrive(&sm.full[prev]);
+        }
+        prev = st;
+        if (++st == kGStages) {
+          st = 0;
+          parity ^= 1u;
+        }
+      }
+    }
+    if (prev >= 0) {
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      mbar_arrive(&sm.full[prev]);
+    }
+  } else if (warp == 2) {  // ------------------------------------------------------ MMA issue
+    int st = 0, step = 0;
+    uint32_t parity = 0;
+    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+      int e, m0, n0;
+      tile_of(t, e, m0, n0);
+      const int me = sm.seg_off[e + 1] - sm.seg_off[e];
+      const int nk = (me + kGK - 1) / kGK;
+      if (i > 0) mbar_wait(&sm.tmem_empty, (i - 1) & 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nk; ++kb, ++step) {
+        mbar_wait(&sm.sfready[st], parity);
+        tc_fence_after();
+        if (lane == 0) {
+          GemmStage& S = sm.st[st];
+          const uint32_t sfa_t = tmem + kSfCol + 16u * (step & 1);
+          const uint32_t sfb_t = sfa_t + 4u;
+          tc_cp_32x128b_warpx4(sfa_t, desc_sf_chunk(S.sfa));
+          tc_cp_32x128b_warpx4(sfb_t, desc_sf_chunk(S.sfb[0]));
+          tc_cp_32x128b_warpx4(sfb_t + 4u, desc_sf_chunk(S.sfb[1]));
+          const uint64_t adesc = desc_kmajor_sw128(S.a), bdesc = desc_kmajor_sw128(S.b);
+          const int kv = me - kb * kGK;
+          const int slices = kv >= kGK ? kGK / 32 : (kv + 31) / 32;  // zero-filled past the segment
+          for (int k = 0; k < slices; ++k)
+            tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(k)),
+                        (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
+          tc_commit(&sm.empty[st]);
+        }
+        __syncwarp();
+        if (++st == kGStages) {
+          st = 0;
+          parity ^= 1u;
+        }
+      }
+      if (lane == 0) tc_commit(&sm.tmem_full);
+      __syncwarp();
+    }
+  } else if (warp == 3) {  // --------------------------------------------- scale expansion
+    int st = 0;
+    uint32_t parity = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int e, m0, n0;
+      tile_of(t, e, m0, n0);
+      const int nk = (sm.seg_off[e + 1] - sm.seg_off[e] + kGK - 1) / kGK;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&sm.full[st], parity);
+        GemmStage& S = sm.st[st];
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = S.sa[lane + 32 * i] * 0x01010101u;
+        *reinterpret_cast<uint4*>(&S.sfa[lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) w[i] = S.sb[128 * c + lane + 32 * i] * 0x01010101u;
+          *reinterpret_cast<uint4*>(&S.sfb[c][lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.sfready[st]);
+        if (++st == kGStages) {
+          st = 0;
+          parity ^= 1u;
+        }
+      }
+    }
+  } else {  // ------------------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+      int e, m0, n0;
+      tile_of(t, e, m0, n0);
+      const bool empty_group = sm.seg_off[e + 1] == sm.seg_off[e];
+      mbar_wait(&sm.tmem_full, i & 1);
+      tc_fence_after();
+      uint32_t v[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tc_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half + 32 * c),
+                         v[c]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tmem_empty);
+      if (empty_group) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[c][j] = 0u;  // no tokens: dW_e = 0
+      }
+      const int64_t grow = static_cast<int64_t>(e) * Ma + m0 + 32 * q + lane;
+      const int col0 = n0 + 128 * half;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (d_f32) {
+          float* dp = static_cast<float*>(D) + grow * Nb + col0 + 32 * c;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[c][j], v[c][j + 1], v[c][j + 2], v[c][j + 3]));
+        } else {
+          __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(D) + grow * Nb + col0 + 32 * c;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8)
+            st_v4(dp + j, make_uint4(pack_bf16x2(__uint_as_float(v[c][j]), __uint_as_float(v[c][j + 1])),
+                                     pack_bf16x2(__uint_as_float(v[c][j + 2]), __uint_as_float(v[c][j + 3])),
+                                     pack_bf16x2(__uint_as_float(v[c][j + 4]), __uint_as_float(v[c][j + 5])),
+                                     pack_bf16x2(__uint_as_float(v[c][j + 6]), __uint_as_float(v[c][j + 7]))));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
 typedef CUresult (*PFN_encodeTiled_g)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -342,6 +580,27 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
   const int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   gemm_blockscaled_kernel<<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
       ma, mb, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
+  return cudaGetLastError();
+}
+
+}  // namespace fp8flow
+
+namespace fp8flow {
+
+cudaError_t launch_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT, const uint8_t* sbT,
+                              int64_t Nb, const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
+                              cudaStream_t stream, int num_sms) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(WgradSmem) + 1024));
+    attr = true;
+  }
+  const int64_t tiles = static_cast<int64_t>(num_groups) * (Ma / kGM) * (Nb / kGN);
+  const int64_t grid = tiles < num_sms ? tiles : num_sms;
+  if (grid < 1) return cudaSuccess;
+  gemm_wgrad_kernel<<<static_cast<unsigned>(grid), kWThreads, sizeof(WgradSmem) + 1024, stream>>>(
+      AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32);
   return cudaGetLastError();
 }
 

@@ -138,3 +138,51 @@ def test_gemm_consumes_hot_path_outputs(F, orc):
     D2 = run_gemm(F, A2, sA2, B2[:256], sB2[:, :256])
     check(D2, orc.gemm_blockscaled(A2, sA2, B2[:256], sB2[:, :256]), abs_ref(orc, A2, sA2, B2[:256], sB2[:, :256]),
           slice(0, N), what="wgrad")
+
+
+def test_gemm_dgrad_on_transposed_weights(F, orc):
+    """Dgrad with the same kernel: dX = dY W contracts over N, so the B operand is W^T in K-major
+    form -- exactly A2's column-wise output of the row-wise FP8 weights (no re-quantization)."""
+    T, N, H = 256, 384, 256
+    dy = synth.normal_bf16(T, N, 81)
+    w = synth.normal_bf16(N, H, 82, sigma=0.05)
+    qd, sd = orc.quantize_rowwise_bf16(synth.bf16_bits(dy))          # A: [T][N], K = N
+    qw, sw = orc.quantize_rowwise_bf16(synth.bf16_bits(w))           # W: [N][H] row-wise along H
+    wT, swT = orc.scaling_aware_transpose(qw, sw)                    # W^T: [H][N], scales [N/128][H]
+    B = wT.reshape(H, N)
+    D = run_gemm(F, qd, sd, B, np.ascontiguousarray(swT))
+    check(D, orc.gemm_blockscaled(qd, sd, B, swT), abs_ref(orc, qd, sd, B, swT), slice(0, T), what="dgrad")
+    exact = (dy.double() @ w.double()).numpy()
+    assert np.max(np.abs(D - exact)) <= 0.1 * np.max(np.abs(exact))
+
+
+@pytest.mark.parametrize("m", [[128, 256], [16, 0, 144, 528, 48]])
+def test_gemm_wgrad_grouped_k(F, orc, m):
+    """Wgrad with groups over K (each expert's tokens, multiples of 16, an empty expert, partial K
+    blocks): dW_e = dH_e^T X_e straight from A2's column-wise outputs of dH and X_perm."""
+    seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
+    R, Ma, Nb = int(seg[-1]), 128, 256
+    dh = synth.normal_bf16(R, Ma, 91)
+    x = synth.activations_bf16(R, Nb, 92)
+    qd, sd = orc.quantize_rowwise_bf16(synth.bf16_bits(dh))
+    qx, sx = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
+    dT, sdT = orc.scaling_aware_transpose(qd, sd, seg)
+    xT, sxT = orc.scaling_aware_transpose(qx, sx, seg)
+    G = len(m)
+    D = torch.full((G, Ma, Nb), float("nan"), dtype=torch.float32, device="cuda")
+    F.fp8flow_gemm_wgrad(torch.from_numpy(dT).cuda(), torch.from_numpy(np.ascontiguousarray(sdT)).cuda(),
+                         torch.from_numpy(xT).cuda(), torch.from_numpy(np.ascontiguousarray(sxT)).cuda(), D,
+                         torch.from_numpy(seg).cuda())
+    torch.cuda.synchronize()
+    D = D.cpu().numpy()
+    P = np.concatenate([[0], np.cumsum((np.asarray(m) + 127) // 128)])
+    for e in range(G):
+        o, me = int(seg[e]), int(m[e])
+        if me == 0:
+            assert np.all(D[e] == 0.0)
+            continue
+        A = dT[Ma * o: Ma * (o + me)].reshape(Ma, me)
+        B = xT[Nb * o: Nb * (o + me)].reshape(Nb, me)
+        sA, sB = sdT[P[e]:P[e + 1]], sxT[P[e]:P[e + 1]]
+        check(D[e], orc.gemm_blockscaled(A, sA, B, sB), orc.gemm_blockscaled(A & 0x7F, sA, B & 0x7F, sB),
+              slice(0, Ma), what=f"wgrad e{e} m_e={me}")
