@@ -58,6 +58,7 @@ struct GemmSmem {
   GemmStage st[kGStages];
   uint64_t full[kGStages];
   uint64_t empty[kGStages];
+  alignas(1024) uint8_t stg[8][2048];  // BF16 epilogue staging: one 32 x 32 box per epilogue warp
   uint64_t sfready[kGStages];  // the stage's scale-factor chunks are expanded
   uint64_t tmem_full;          // accumulator complete (tcgen05.commit)
   uint64_t tmem_empty;         // accumulator read out by the 8 epilogue warps
@@ -129,6 +130,37 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// BF16 epilogue of one warp: its 32 accumulator rows (lane = row) x 128 columns (v[c][j] = column
+// 32c + j) leave through shared memory as four 32x32 TMA box stores -- full 64-byte row segments
+// instead of 32 scattered 16-byte stores per instruction.  NBUF staging buffers of 2 KB (32 rows x
+// 64 B); a buffer is rewritten only after the TMA engine has read it.
+template <int NBUF>
+__device__ __forceinline__ void epilogue_bf16_tma(const CUtensorMap* tmap_d, uint8_t* stage, const uint32_t (&v)[4][32],
+                                                  int col0, int row0, int lane, int& pending) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint8_t* buf = stage + (c % NBUF) * 2048;
+    if (pending >= NBUF) {
+      if (lane == 0) bulk_wait_read<NBUF - 1>();
+      __syncwarp();
+    }
+    uint4* dst = reinterpret_cast<uint4*>(buf + lane * 64);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      dst[j] = make_uint4(pack_bf16x2(__uint_as_float(v[c][8 * j]), __uint_as_float(v[c][8 * j + 1])),
+                          pack_bf16x2(__uint_as_float(v[c][8 * j + 2]), __uint_as_float(v[c][8 * j + 3])),
+                          pack_bf16x2(__uint_as_float(v[c][8 * j + 4]), __uint_as_float(v[c][8 * j + 5])),
+                          pack_bf16x2(__uint_as_float(v[c][8 * j + 6]), __uint_as_float(v[c][8 * j + 7])));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmap_d, buf, col0 + 32 * c, row0);
+      bulk_commit();
+    }
+    pending = pending < NBUF ? pending + 1 : NBUF;
+  }
+}
+
 // tile t -> (group, first row, valid rows, first column)
 struct GemmTile {
   int g, r0, rows, n0;
@@ -142,7 +174,7 @@ __device__ __forceinline__ GemmTile gemm_tile(const GemmSmem& sm, int ngroups, i
 
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_blockscaled_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                            const uint8_t* __restrict__ sa, int64_t ld_sa, const uint8_t* __restrict__ sb,
+                            const __grid_constant__ CUtensorMap tmap_d, const uint8_t* __restrict__ sa, int64_t ld_sa, const uint8_t* __restrict__ sb,
                             int64_t ld_sb, int64_t M, int64_t N, int64_t K, const int32_t* __restrict__ seg_offsets,
                             int32_t num_groups, void* __restrict__ D, int32_t d_f32) {
   extern __shared__ __align__(1024) uint8_t smem_gemm[];
@@ -258,6 +290,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   } else {  // ------------------------------------------------------------------- epilogue
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int half = (warp - 3) >> 2;  // columns [128 half, 128 half + 128)
+    int pending = 0;
     for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
       const GemmTile T = gemm_tile(sm, ngroups, n_nt, t);
       mbar_wait(&sm.tmem_full, i & 1);
@@ -271,7 +304,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tmem_empty);  // the MMAs of the next tile may start
       const int row = 32 * q + lane;
-      if (row < T.rows) {
+      if (!d_f32 && 32 * q + 32 <= T.rows) {  // all 32 rows of this warp belong to the group
+        epilogue_bf16_tma<1>(&tmap_d, sm.stg[warp - 3], v, T.n0 + 128 * half, T.r0 + 32 * q, lane, pending);
+      } else if (row < T.rows) {
         const int64_t grow = static_cast<int64_t>(T.r0) + row;
         const int col0 = T.n0 + 128 * half;
 #pragma unroll
@@ -293,6 +328,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
   }
+  if (warp >= 3 && lane == 0) bulk_wait_all();  // TMA stores of the epilogue
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -313,6 +349,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
 // =============================================================================================
 constexpr int kWThreads = 384;
 constexpr int kWProd = 64;  // producer threads
+constexpr int kWStages = 3;  // (smem for two BF16 staging boxes per epilogue warp)
 
 __device__ __forceinline__ void cp_async_16(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
@@ -323,10 +360,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 struct WgradSmem {
-  GemmStage st[kGStages];
-  uint64_t full[kGStages];     // kWProd producer arrivals (after their copies landed + proxy fence)
-  uint64_t empty[kGStages];
-  uint64_t sfready[kGStages];
+  GemmStage st[kWStages];
+  alignas(1024) uint8_t stg[8][2 * 2048];  // BF16 epilogue staging: two 32 x 32 boxes per epilogue warp
+  uint64_t full[kWStages];     // kWProd producer arrivals (after their copies landed + proxy fence)
+  uint64_t empty[kWStages];
+  uint64_t sfready[kWStages];
   uint64_t tmem_full;
   uint64_t tmem_empty;
   uint32_t tmem_base;
@@ -337,7 +375,7 @@ struct WgradSmem {
 };
 
 __global__ void __launch_bounds__(kWThreads, 1)
-    gemm_wgrad_kernel(const uint8_t* __restrict__ AT, const uint8_t* __restrict__ saT, int64_t Ma,
+    gemm_wgrad_kernel(const __grid_constant__ CUtensorMap tmap_d, const uint8_t* __restrict__ AT, const uint8_t* __restrict__ saT, int64_t Ma,
                       const uint8_t* __restrict__ BT, const uint8_t* __restrict__ sbT, int64_t Nb,
                       const int32_t* __restrict__ seg_offsets, int32_t num_groups, void* __restrict__ D,
                       int32_t d_f32) {
@@ -347,7 +385,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
 
   if (warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   if (tid == 32) {
-    for (int i = 0; i < kGStages; ++i) {
+    for (int i = 0; i < kWStages; ++i) {
       mbar_init(&sm.full[i], kWProd);
       mbar_init(&sm.empty[i], 1);
       mbar_init(&sm.sfready[i], 1);
@@ -381,7 +419,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
       const uint8_t* a_base = AT + Ma * o + static_cast<int64_t>(m0) * me;
       const uint8_t* b_base = BT + Nb * o + static_cast<int64_t>(n0) * me;
       for (int kb = 0; kb < nk; ++kb, ++n) {
-        if (n >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
+        if (n >= kWStages) mbar_wait(&sm.empty[st], parity ^ 1u);
         GemmStage& S = sm.st[st];
         const int kv = me - kb * kGK;  // valid K bytes in this step (>= 16)
 #pragma unroll 4
@@ -411,7 +449,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
           mbar_arrive(&sm.full[prev]);
         }
         prev = st;
-        if (++st == kGStages) {
+        if (++st == kWStages) {
           st = 0;
           parity ^= 1u;
         }
@@ -451,7 +489,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
           tc_commit(&sm.empty[st]);
         }
         __syncwarp();
-        if (++st == kGStages) {
+        if (++st == kWStages) {
           st = 0;
           parity ^= 1u;
         }
@@ -482,7 +520,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.sfready[st]);
-        if (++st == kGStages) {
+        if (++st == kWStages) {
           st = 0;
           parity ^= 1u;
         }
@@ -491,6 +529,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
   } else {  // ------------------------------------------------------------------- epilogue
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;
+    int pending = 0;
     for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
       int e, m0, n0;
       tile_of(t, e, m0, n0);
@@ -513,6 +552,10 @@ __global__ void __launch_bounds__(kWThreads, 1)
       }
       const int64_t grow = static_cast<int64_t>(e) * Ma + m0 + 32 * q + lane;
       const int col0 = n0 + 128 * half;
+      if (!d_f32) {
+        epilogue_bf16_tma<2>(&tmap_d, sm.stg[warp - 4], v, col0, static_cast<int>(grow - lane), lane, pending);
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (d_f32) {
@@ -531,6 +574,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
       }
     }
   }
+  if (warp >= 4 && lane == 0) bulk_wait_all();  // TMA stores of the epilogue
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -543,6 +587,18 @@ typedef CUresult (*PFN_encodeTiled_g)(CUtensorMap*, CUtensorMapDataType, cuuint3
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 }  // namespace
+
+static PFN_encodeTiled_g encode_g() {
+  static PFN_encodeTiled_g fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_g>(p);
+  }
+  return fn;
+}
 
 cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B,
                                     const uint8_t* sb, int64_t ld_sb, int64_t M, int64_t N, int64_t K,
@@ -560,7 +616,17 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
                          static_cast<int>(sizeof(GemmSmem) + 1024));
   }
   const int groups = seg_offsets == nullptr ? 1 : num_groups;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, md;
+  {  // BF16 output boxes of 32 rows x 32 columns (unused for fp32 output)
+    const cuuint64_t gdim_d[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M > 0 ? M : 1)};
+    const cuuint64_t gstr_d[1] = {static_cast<cuuint64_t>(N) * 2};
+    const cuuint32_t box_d[2] = {32, 32};
+    const cuuint32_t es[2] = {1, 1};
+    if (encode(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, gdim_d, gstr_d, box_d, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   const cuuint32_t estride[2] = {1, 1};
   const cuuint64_t gdim_a[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
   const cuuint64_t gstr_a[1] = {static_cast<cuuint64_t>(K)};
@@ -579,7 +645,7 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
   const int64_t tiles_ub = (M / kGM + groups) * (N / kGN);
   const int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   gemm_blockscaled_kernel<<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
-      ma, mb, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
+      ma, mb, md, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
   return cudaGetLastError();
 }
 
@@ -596,11 +662,22 @@ cudaError_t launch_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma,
                          static_cast<int>(sizeof(WgradSmem) + 1024));
     attr = true;
   }
+  PFN_encodeTiled_g encode = encode_g();
+  if (!encode) return cudaErrorNotSupported;
+  CUtensorMap md;
+  const cuuint64_t gdim_d[2] = {static_cast<cuuint64_t>(Nb), static_cast<cuuint64_t>(num_groups) * Ma};
+  const cuuint64_t gstr_d[1] = {static_cast<cuuint64_t>(Nb) * 2};
+  const cuuint32_t box_d[2] = {32, 32};
+  const cuuint32_t es[2] = {1, 1};
+  if (encode(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, gdim_d, gstr_d, box_d, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   const int64_t tiles = static_cast<int64_t>(num_groups) * (Ma / kGM) * (Nb / kGN);
   const int64_t grid = tiles < num_sms ? tiles : num_sms;
   if (grid < 1) return cudaSuccess;
   gemm_wgrad_kernel<<<static_cast<unsigned>(grid), kWThreads, sizeof(WgradSmem) + 1024, stream>>>(
-      AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32);
+      md, AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32);
   return cudaGetLastError();
 }
 
