@@ -529,6 +529,42 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
                      "peak_tflops": round(fp8_peak, 1), "shape": {"M": hw.R, "N": N, "K": K, "groups": E},
                      "parity_rows": "first row of every expert vs oracle fp64; max (|err| - 2^-8|ref|)/(|A||B|^T)",
                      "parity_worst": worst, "parity_ok": worst <= 2.0 ** -14}
+        del W, sW, Dout
+
+    # Wgrad of fc1, all FP8: dH from NEXT-1 (SwiGLU backward + quant) -> A2 per expert -> grouped-K
+    # GEMM with A2(X_perm) from the step: dW1_e = dH_e^T X_e, BF16 [32][4096][7168]
+    dA = synth.normal_bf16(hw.R, FFN, synth.BASE_SEED + 5, sigma=0.5).to(dev)
+    qh = torch.empty(hw.R, 2 * FFN, dtype=torch.uint8, device=dev)
+    sh = torch.empty(2 * FFN // 128, hw.R, dtype=torch.uint8, device=dev)
+    F.fp8flow_swiglu_bwd_quant(ds.h, dA, qh, sh, rows_dev=ds.off[E:])
+    hT = torch.empty(hw.R * 2 * FFN, dtype=torch.uint8, device=dev)
+    shT = torch.empty(hw.R // 128 + E, 2 * FFN, dtype=torch.uint8, device=dev)
+    F.fp8flow_scaling_aware_transpose(qh, sh, hT, shT, seg_offsets=ds.off)
+    dW = torch.empty(E, 2 * FFN, HIDDEN, dtype=torch.bfloat16, device=dev)
+    ms = timed(lambda: F.fp8flow_gemm_wgrad(hT, shT, ds.xT, ds.sxT, dW, ds.off))
+    flops = 2.0 * hw.R * 2 * FFN * HIDDEN
+    tf = flops / ms / 1e9
+    from oracle import gemm_blockscaled as orc_gemm  # test infrastructure: the verify leg only
+    offs = ds.off.cpu().numpy()
+    P = np.concatenate([[0], np.cumsum((np.diff(offs) + 127) // 128)])
+    e = int(np.argmax(np.diff(offs)))  # the largest expert: rows 0 and 2F-1 of dW_e
+    o, me = int(offs[e]), int(offs[e + 1] - offs[e])
+    Fh = 2 * FFN
+    Ae = hT[Fh * o: Fh * (o + me)].view(Fh, me).cpu().numpy()
+    Be = ds.xT[HIDDEN * o: HIDDEN * (o + me)].view(HIDDEN, me).cpu().numpy()
+    sA, sB = shT[P[e]:P[e + 1]].cpu().numpy(), ds.sxT[P[e]:P[e + 1]].cpu().numpy()
+    worst = 0.0
+    for r in (0, Fh - 1):
+        ref = orc_gemm(Ae[r:r + 1], sA[:, r:r + 16], Be, sB)[0]
+        mag = orc_gemm(Ae[r:r + 1] & 0x7F, sA[:, r:r + 16], Be & 0x7F, sB)[0]
+        err = np.abs(dW[e, r].float().cpu().numpy() - ref) - 2.0 ** -8 * np.abs(ref)
+        worst = max(worst, float(np.max(err / (mag + 1e-30))))
+    out["NEXT2_gemm_fc1_wgrad"] = {"us": round(ms * 1e3, 1), "tflops": round(tf, 1), "frac": round(tf / fp8_peak, 3),
+                                   "peak_tflops": round(fp8_peak, 1),
+                                   "shape": {"Ma": Fh, "Nb": HIDDEN, "K_total": hw.R, "groups": E},
+                                   "operands": "A2(NEXT-1 dH) and A2(X_perm) from the step, groups over K",
+                                   "parity_rows": f"expert {e} (m_e={me}), rows 0 and {Fh - 1} vs oracle fp64",
+                                   "parity_worst": worst, "parity_ok": worst <= 2.0 ** -14}
     return out
 
 
