@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(kDThreads, 1)
       mbar_init(&sm.empty[i], kDRowWarps / 2);  // the row warps of one half tile
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.cfull[b], kDRowWarps);
-      mbar_init(&sm.cempty[b], kDTrWarps);
+      mbar_init(&sm.cfull[b], kDRowWarps * 32);  // every lane of every row warp
+      mbar_init(&sm.cempty[b], kDTrWarps * 32);  // every transpose thread
     }
     mbar_init_fence();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
       }
       if (lane == 0) sm.wmax[b][warp] = wm;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.cfull[b]);  // release: the warp's code rows are visible
+      mbar_arrive(&sm.cfull[b]);  // release (per lane): this lane's code-tile writes are visible
     }
     return;
   }
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
       R[r][3] = shift4(v.w, m2);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.cempty[b]);  // code tile b, its scales and maxima are consumed
+    mbar_arrive(&sm.cempty[b]);  // (per thread) its reads of code tile b, scales and maxima are done
     const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);
     uint32_t* out = sm.out[b];
 #pragma unroll

@@ -188,10 +188,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
     for (int i = 0; i < kGStages; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], 1);
-      mbar_init(&sm.sfready[i], 1);
+      mbar_init(&sm.sfready[i], 32);  // every lane of the scale-expansion warp
     }
     mbar_init(&sm.tmem_full, 1);
-    mbar_init(&sm.tmem_empty, 8);
+    mbar_init(&sm.tmem_empty, 8 * 32);  // every epilogue thread
     mbar_init_fence();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.cp (async proxy)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.sfready[st]);
+        mbar_arrive(&sm.sfready[st]);
         if (++st == kGStages) {
           st = 0;
           parity ^= 1u;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                          v[c]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tmem_empty);  // the MMAs of the next tile may start
+      mbar_arrive(&sm.tmem_empty);  // the MMAs of the next tile may start
       const int row = 32 * q + lane;
       if (!d_f32 && 32 * q + 32 <= T.rows) {  // all 32 rows of this warp belong to the group
         epilogue_bf16_tma<1>(&tmap_d, sm.stg[warp - 3], v, T.n0 + 128 * half, T.r0 + 32 * q, lane, pending);
@@ -388,10 +388,10 @@ __global__ void __launch_bounds__(kWThreads, 1)
     for (int i = 0; i < kWStages; ++i) {
       mbar_init(&sm.full[i], kWProd);
       mbar_init(&sm.empty[i], 1);
-      mbar_init(&sm.sfready[i], 1);
+      mbar_init(&sm.sfready[i], 32);  // every lane of the scale-expansion warp
     }
     mbar_init(&sm.tmem_full, 1);
-    mbar_init(&sm.tmem_empty, 8);
+    mbar_init(&sm.tmem_empty, 8 * 32);  // every epilogue thread
     mbar_init_fence();
   }
   tc_fence_before();
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.sfready[st]);
+        mbar_arrive(&sm.sfready[st]);
         if (++st == kWStages) {
           st = 0;
           parity ^= 1u;
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
                          v[c]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tmem_empty);
+      mbar_arrive(&sm.tmem_empty);
       if (empty_group) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
