@@ -18,10 +18,11 @@
 //     swiglu_math.cuh, identical to the A5 kernel's).  Codes go to global memory (row-wise output)
 //     and to a double-buffered 16 KB row-major code tile in shared memory, scale bytes to global
 //     and shared memory; the tile's buffer is handed over on an mbarrier (cfull);
-//   * warps 16-23, transpose warps (A2's core): thread (g, c) shifts a 4-row x 16-byte chunk of the
-//     code tile by k = T_max - T_row, transposes 4x4 byte blocks with PRMT into a swizzled,
-//     double-buffered 16 KB staging buffer, returns the code tile (cempty), and after one named
-//     barrier of its 256 threads the block leaves as coalesced 128-bit stores.
+//   * warps 16-23, transpose warps (A2's arithmetic): warp w owns 16 complete output rows of the
+//     block (block columns 16w..16w+15); lane a reads block rows 4a..4a+3 of that column chunk
+//     (the code tile's chunks are XOR-swizzled by row/4 so these reads are conflict-free), shifts
+//     them by k = T_max - T_row, transposes 4x4 byte blocks in registers and stores one 32-bit
+//     word per output row -- a full 128-byte line per warp store; no staging buffer, no barrier.
 #include <cuda.h>
 
 #include "async.cuh"
@@ -48,8 +49,8 @@ template <int OP, int STAGES>
 struct DualSmem {
   static constexpr int kParts = OP == 0 ? 1 : 2;
   uint8_t in[STAGES][kParts][kDBox];  // ring of half-tile stages
-  uint32_t ctile[2][kDT * kDT / 4];   // row-major codes of the block (double buffer)
-  uint32_t out[2][kDT * kDT / 4];     // transposed codes, 16-byte-chunk XOR swizzle (A2's)
+  uint32_t ctile[2][kDT * kDT / 4];   // codes of the block, row-major with 16-byte chunks XOR-swizzled
+                                      // by (row / 4) % 8 (double buffer)
   uint32_t sc[2][kDT / 4];            // row scale bytes of the block
   uint32_t wmax[2][kDRowWarps];       // per row warp: max scale byte of its valid rows
   uint64_t full[STAGES];
@@ -63,7 +64,6 @@ struct DualSmem {
   int32_t total_rb;
 };
 
-__device__ __forceinline__ void transpose_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // A1 on N rows (lane: 4 columns of each): exact integer amax over |bf16| bit patterns, scale byte
 // from the amax bits, codes = RNE(x * 2^-T) (the product is exact).  c[i]: the lane's 4 codes of
@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
       if (i >= 2) mbar_wait(&sm.cempty[b], ((i >> 1) - 1) & 1);  // tile i-2's transpose is done with b
       if (active) {
 #pragma unroll
-        for (int r = 0; r < kDRpw; ++r) sm.ctile[b][(wr0 + r) * (kDT / 4) + lane] = cw[r];
+        for (int r = 0; r < kDRpw; ++r) {  // word `lane` of row wr0+r: chunk lane/4 lands at (lane/4) ^ ((row/4) % 8)
+          const int row = wr0 + r;
+          sm.ctile[b][row * (kDT / 4) + ((((lane >> 2) ^ (row >> 2)) & 7) << 2) + (lane & 3)] = cw[r];
+        }
         if (lane < kDRpw) reinterpret_cast<uint8_t*>(sm.sc[b])[wr0 + lane] = static_cast<uint8_t>(sbyte);
       }
       if (lane == 0) sm.wmax[b][warp] = wm;
@@ -242,9 +245,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
   }
 
   // ----------------------------------------------------------------------- transpose warps
-  const int lt = tid - kDRowWarps * 32;  // 0..255
-  const int g = lt >> 3;                 // row quad 0..31
-  const int c = lt & 7;                  // 16-byte column chunk 0..7
+  // warp w owns output rows 16w .. 16w+15 of the block (= block columns, chunk w of every code
+  // row); lane a holds block rows 4a..4a+3 (conflict-free: the chunk swizzle depends on row / 4),
+  // so every output row leaves as one 128-byte line per warp store -- no staging buffer, no barrier
+  const int w = warp - kDRowWarps;  // 0..7
   for (int t = first, i = 0; t < total_tiles; t += stride, ++i) {
     if (i > 0) {
       jb += stride_jb;
@@ -263,12 +267,13 @@ __global__ void __launch_bounds__(kDThreads, 1)
     mbar_wait(&sm.cfull[b], (i >> 1) & 1);
     uint32_t tmax = 0;
 #pragma unroll
-    for (int w = 0; w < kDRowWarps; ++w) tmax = max(tmax, sm.wmax[b][w]);
-    const uint32_t sw = sm.sc[b][g];  // scale bytes of rows 4g..4g+3
+    for (int x = 0; x < kDRowWarps; ++x) tmax = max(tmax, sm.wmax[b][x]);
+    const uint32_t sw = sm.sc[b][lane];  // scale bytes of rows 4a..4a+3
+    const int pchunk = ((w ^ lane) & 7) << 2;  // physical word offset of chunk w in rows 4a..4a+3
     uint32_t R[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const uint4 v = *reinterpret_cast<const uint4*>(&sm.ctile[b][(4 * g + r) * (kDT / 4) + 4 * c]);
+      const uint4 v = *reinterpret_cast<const uint4*>(&sm.ctile[b][(4 * lane + r) * (kDT / 4) + pchunk]);
       const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // rows outside the segment: never stored
       const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
       R[r][0] = shift4(v.x, m2);
@@ -276,37 +281,26 @@ __global__ void __launch_bounds__(kDThreads, 1)
       R[r][2] = shift4(v.z, m2);
       R[r][3] = shift4(v.w, m2);
     }
-    __syncwarp();
     mbar_arrive(&sm.cempty[b]);  // (per thread) its reads of code tile b, scales and maxima are done
-    const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);
-    uint32_t* out = sm.out[b];
+    if (4 * lane < rows_valid) {
+      uint8_t* out = qT + cols * static_cast<int64_t>(o) + (static_cast<int64_t>(jb) * kDT + 16 * w) * m + ib * kDT +
+                     4 * lane;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
-      const uint32_t t1 = __byte_perm(R[0][w], R[1][w], 0x7362);
-      const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
-      const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
-      const int j0 = 16 * c + 4 * w;
-      out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
-      out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
-      out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
-      out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
-    }
-    transpose_sync();  // staging buffer b complete (buffer b is rewritten two tiles later, after
-                       // the next tile's transpose_sync, by which time this read-out is done)
-    uint8_t* qTe = qT + cols * static_cast<int64_t>(o);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int j = g + 32 * it;
-      if (16 * c < rows_valid) {
-        const int phys = c ^ ((j >> 4) & 7);
-        const uint4 v = *reinterpret_cast<const uint4*>(&out[j * 32 + 4 * phys]);
-        st_v4(qTe + (static_cast<int64_t>(jb) * kDT + j) * m + ib * kDT + 16 * c, v);
+      for (int qd = 0; qd < 4; ++qd) {
+        const uint32_t t0 = __byte_perm(R[0][qd], R[1][qd], 0x5140);
+        const uint32_t t1 = __byte_perm(R[0][qd], R[1][qd], 0x7362);
+        const uint32_t t2 = __byte_perm(R[2][qd], R[3][qd], 0x5140);
+        const uint32_t t3 = __byte_perm(R[2][qd], R[3][qd], 0x7362);
+        uint8_t* o4 = out + static_cast<int64_t>(4 * qd) * m;
+        *reinterpret_cast<uint32_t*>(o4) = __byte_perm(t0, t2, 0x5410);
+        *reinterpret_cast<uint32_t*>(o4 + m) = __byte_perm(t0, t2, 0x7632);
+        *reinterpret_cast<uint32_t*>(o4 + 2 * m) = __byte_perm(t1, t3, 0x5410);
+        *reinterpret_cast<uint32_t*>(o4 + 3 * m) = __byte_perm(t1, t3, 0x7632);
       }
     }
-    if (lt < 8) {
+    if (w == 0 && lane < 8) {
       const uint32_t b4 = tmax * 0x01010101u;
-      st_v4(sT + static_cast<int64_t>(rb) * cols + jb * kDT + 16 * lt, make_uint4(b4, b4, b4, b4));
+      st_v4(sT + static_cast<int64_t>(rb) * cols + jb * kDT + 16 * lane, make_uint4(b4, b4, b4, b4));
     }
   }
 }
@@ -362,13 +356,13 @@ cudaError_t launch_dual(const void* in, int64_t in_cols, int64_t rows_max, const
 cudaError_t launch_quantize_dual(const void* x, int64_t rows, int64_t cols, const int32_t* seg_offsets,
                                  int32_t num_segs, uint8_t* q, uint8_t* s, int64_t ld_s, uint8_t* qT, uint8_t* sT,
                                  cudaStream_t stream, int num_sms) {
-  return launch_dual<0, 8>(x, cols, rows, nullptr, cols, seg_offsets, num_segs, q, s, ld_s, qT, sT, stream, num_sms);
+  return launch_dual<0, 10>(x, cols, rows, nullptr, cols, seg_offsets, num_segs, q, s, ld_s, qT, sT, stream, num_sms);
 }
 
 cudaError_t launch_swiglu_quant_dual(const void* h, int64_t rows_max, const int32_t* rows_dev, int64_t ffn,
                                      const int32_t* seg_offsets, int32_t num_segs, uint8_t* q, uint8_t* s,
                                      int64_t ld_s, uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
-  return launch_dual<1, 4>(h, 2 * ffn, rows_max, rows_dev, ffn, seg_offsets, num_segs, q, s, ld_s, qT, sT, stream,
+  return launch_dual<1, 5>(h, 2 * ffn, rows_max, rows_dev, ffn, seg_offsets, num_segs, q, s, ld_s, qT, sT, stream,
                            num_sms);
 }
 
