@@ -84,6 +84,29 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(cta_mask)
+               : "memory");
+}
+// TMA 2D load multicast to the CTAs of `cta_mask` (same shared-memory offsets and mbarrier in each)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1,
+                                               uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void tc_cp_32x128b_warpx4(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc));
 }
@@ -172,6 +195,23 @@ __device__ __forceinline__ GemmTile gemm_tile(const GemmSmem& sm, int ngroups, i
   return {g, r0, min(kGM, sm.seg_off[g + 1] - r0), nt * kGN};
 }
 
+// the i-th tile of this CTA (-1 when done).  CL = 1: t = blockIdx.x + i * gridDim.x.  CL = 2: the
+// two CTAs of a cluster take the two column tiles (2p', 2p'+1) of the same row block, so they share
+// the A tile (each loads one half and multicasts it to both).
+template <int CL>
+__device__ __forceinline__ int cta_tile(int i, int total_rb, int n_nt) {
+  if (CL == 1) {
+    const int t = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+    return t < total_rb * n_nt ? t : -1;
+  }
+  const int pairs_per_rb = n_nt / 2;
+  const int p = static_cast<int>(blockIdx.x) / 2 + i * static_cast<int>(gridDim.x / 2);
+  if (p >= total_rb * pairs_per_rb) return -1;
+  const int rb = p / pairs_per_rb;
+  return rb * n_nt + 2 * (p - rb * pairs_per_rb) + static_cast<int>(blockIdx.x & 1);
+}
+
+template <int CL>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_blockscaled_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const __grid_constant__ CUtensorMap tmap_d, const uint8_t* __restrict__ sa, int64_t ld_sa, const uint8_t* __restrict__ sb,
@@ -187,7 +227,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (tid == 32) {
     for (int i = 0; i < kGStages; ++i) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 1);
+      mbar_init(&sm.empty[i], CL);  // the MMA commits of every CTA that reads the stage's A tile
       mbar_init(&sm.sfready[i], 32);  // every lane of the scale-expansion warp
     }
     mbar_init(&sm.tmem_full, 1);
@@ -198,17 +238,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
   }
   tc_fence_before();
   load_segments<kGThreads>(sm, seg_offsets, ngroups, M);  // ends with a CTA barrier
+  if (CL > 1) cluster_sync_all();  // the peer's barriers exist before any multicast targets them
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const int n_nt = static_cast<int>(N / kGN);
-  const int total_tiles = sm.total_rb * n_nt;
   const int nk = static_cast<int>(K / kGK);
 
   if (warp == 0) {  // --------------------------------------------------------- TMA producer
     if (lane == 0) {
       int st = 0, n = 0;
       uint32_t parity = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const int half = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+      for (int i = 0, t; (t = cta_tile<CL>(i, sm.total_rb, n_nt)) >= 0; ++i) {
         const GemmTile T = gemm_tile(sm, ngroups, n_nt, t);
         const uint32_t sa_bytes = static_cast<uint32_t>(min64(kGM, ld_sa - T.r0));
         const uint8_t* sbg = sb + static_cast<int64_t>(T.g) * (K / kGK) * ld_sb;
@@ -216,7 +257,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
           if (n >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
           GemmStage& S = sm.st[st];
           mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK + sa_bytes + kGN);
-          tma_load_2d(S.a, &tmap_a, &sm.full[st], kb * kGK, T.r0);
+          if (CL == 1)
+            tma_load_2d(S.a, &tmap_a, &sm.full[st], kb * kGK, T.r0);
+          else  // this CTA's half of the shared A tile, into both CTAs of the pair
+            tma_load_2d_mc(S.a + half * (kGM / 2) * kGK, &tmap_a, &sm.full[st], kb * kGK, T.r0 + half * (kGM / 2),
+                           0x3);
           tma_load_2d(S.b, &tmap_b, &sm.full[st], kb * kGK, static_cast<int32_t>(T.g * N + T.n0));
           bulk_load_1d(S.sa, sa + static_cast<int64_t>(kb) * ld_sa + T.r0, sa_bytes, &sm.full[st]);
           bulk_load_1d(S.sb, sbg + static_cast<int64_t>(kb) * ld_sb + T.n0, kGN, &sm.full[st]);
@@ -230,7 +275,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   } else if (warp == 1) {  // ------------------------------------------------------ MMA issue
     int st = 0, step = 0;
     uint32_t parity = 0;
-    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+    for (int i = 0; cta_tile<CL>(i, sm.total_rb, n_nt) >= 0; ++i) {
       if (i > 0) mbar_wait(&sm.tmem_empty, (i - 1) & 1);  // the previous tile has been read out
       tc_fence_after();
       for (int kb = 0; kb < nk; ++kb, ++step) {
@@ -248,7 +293,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
           for (int k = 0; k < kGK / 32; ++k)  // +32 bytes (one K=32 slice) inside the swizzle atom
             tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(k)),
                         (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
-          tc_commit(&sm.empty[st]);  // the stage (and its SF chunks) is free when these MMAs complete
+          // the stage (and its SF chunks) is free when these MMAs complete -- in every CTA of the
+          // pair, since the peer multicasts its half of A into this stage too
+          if (CL == 1) tc_commit(&sm.empty[st]);
+          else tc_commit_mc(&sm.empty[st], 0x3);
         }
         __syncwarp();
         if (++st == kGStages) {
@@ -262,7 +310,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   } else if (warp == 2) {  // --------------------------------------------- scale expansion
     int st = 0;
     uint32_t parity = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int i = 0; cta_tile<CL>(i, sm.total_rb, n_nt) >= 0; ++i) {
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&sm.full[st], parity);
         GemmStage& S = sm.st[st];
@@ -291,7 +339,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int half = (warp - 3) >> 2;  // columns [128 half, 128 half + 128)
     int pending = 0;
-    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+    for (int i = 0, t; (t = cta_tile<CL>(i, sm.total_rb, n_nt)) >= 0; ++i) {
       const GemmTile T = gemm_tile(sm, ngroups, n_nt, t);
       mbar_wait(&sm.tmem_full, i & 1);
       tc_fence_after();
@@ -330,6 +378,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   }
   if (warp >= 3 && lane == 0) bulk_wait_all();  // TMA stores of the epilogue
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no multicast or remote commit may target an exited CTA
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -612,9 +661,13 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
         qres != cudaDriverEntryPointSuccess)
       return cudaErrorNotSupported;
     encode = reinterpret_cast<PFN_encodeTiled_g>(p);
-    cudaFuncSetAttribute(gemm_blockscaled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_blockscaled_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(GemmSmem) + 1024));
+    cudaFuncSetAttribute(gemm_blockscaled_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(GemmSmem) + 1024));
   }
+  // CTA pairs (clusters of 2) share the A tile of a row block when N has an even number of tiles
+  const int cl = (N / kGN) % 2 == 0 && tune_int("GEMM_CLUSTER", 2) == 2 ? 2 : 1;
   const int groups = seg_offsets == nullptr ? 1 : num_groups;
   CUtensorMap ma, mb, md;
   {  // BF16 output boxes of 32 rows x 32 columns (unused for fp32 output)
@@ -630,7 +683,7 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
   const cuuint32_t estride[2] = {1, 1};
   const cuuint64_t gdim_a[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
   const cuuint64_t gstr_a[1] = {static_cast<cuuint64_t>(K)};
-  const cuuint32_t box_a[2] = {kGK, kGM};
+  const cuuint32_t box_a[2] = {kGK, static_cast<cuuint32_t>(kGM / cl)};  // a pair loads half each
   const cuuint64_t gdim_b[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N) * groups};
   const cuuint64_t gstr_b[1] = {static_cast<cuuint64_t>(K)};
   const cuuint32_t box_b[2] = {kGK, kGN};
@@ -641,12 +694,30 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  // persistent: at most one CTA per SM, tiles walked with a static stride
+  // persistent: at most one CTA per SM, tiles walked with a static stride (pairs of tiles for cl = 2)
   const int64_t tiles_ub = (M / kGM + groups) * (N / kGN);
-  const int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
-  gemm_blockscaled_kernel<<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
-      ma, mb, md, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
-  return cudaGetLastError();
+  int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
+  if (cl == 1) {
+    gemm_blockscaled_kernel<1><<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
+        ma, mb, md, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
+    return cudaGetLastError();
+  }
+  grid = grid / 2 * 2;
+  if (grid < 2) grid = 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kGThreads);
+  cfg.dynamicSmemBytes = sizeof(GemmSmem) + 1024;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_blockscaled_kernel<2>, ma, mb, md, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets,
+                            num_groups, D, d_f32);
 }
 
 }  // namespace fp8flow
