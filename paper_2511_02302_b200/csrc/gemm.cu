@@ -16,13 +16,18 @@
 // column tiles), K in steps of 128 through a 4-stage mbarrier ring.  Warp roles:
 //   * warp 0: TMEM allocation (512 columns: the 256-column fp32 accumulator + scale factors) and
 //     the TMA producer -- per K step the A tile (128 x 128 B) and B tile (256 x 128 B) with
-//     128-byte swizzle, plus the raw scale runs (128 + 256 bytes, 1D bulk copies);
-//   * warp 1: MMA issuer -- one elected lane issues tcgen05.cp (SFA, SFB into a double-buffered
-//     set of scale-factor columns) and 4 x tcgen05.mma (M128 N256 K32) per K step, commits each
-//     stage back to the producer and each finished tile to the epilogue;
-//   * warp 2: expands each stage's scale runs into the tensor-memory scale-factor layout (a 1x128
-//     byte replicated x4; 32-row x 16-byte chunks that tcgen05.cp.32x128b.warpx4 broadcasts to
-//     the four lane quadrants), off the MMA issuer's critical path;
+//     128-byte swizzle; every four K steps the scale runs of those steps (TMA boxes of the
+//     MN-major scale tensors: 4 x 128 and 4 x 256 bytes) into a 2-slot scale ring.  CTA pairs
+//     (clusters of 2) working on the two column tiles of one row block load half of the shared A
+//     tile each and multicast it to both;
+//   * warp 1: MMA issuer -- one elected lane issues, once per four K steps, tcgen05.cp of the
+//     scale-factor chunks (SFA, SFB) into a double-buffered set of TMEM columns, and per K step
+//     4 x tcgen05.mma (M128 N256 K32) with sf_id = the step's position in its group; commits each
+//     stage (multicast to the pair), each scale slot, and each finished tile;
+//   * warp 2: expands each scale slot into the tensor-memory scale-factor layout: byte j of the
+//     word of row r is row r's 1x128 scale of K step kb0 + j (32-row x 16-byte chunks that
+//     tcgen05.cp.32x128b.warpx4 broadcasts to the four lane quadrants) -- one copy set per four
+//     steps instead of one per step (12 % of the tensor pipe's time at one set per step);
 //   * warps 3-10: epilogue -- two warps per TMEM lane quadrant (128 columns each) load the whole
 //     accumulator with tcgen05.ld, hand the tensor memory back at once (so the next tile's MMAs
 //     overlap these stores), convert fp32 -> BF16 (RNE) or keep fp32, and store the group's rows.
@@ -54,12 +59,30 @@ struct __align__(1024) GemmStage {
   uint8_t sfb[2][512];
 };
 
+// Fprop: operand stages carry only A and B; the scales travel on their own ring, four K steps per
+// slot: byte j of a scale-factor word is the scale of K step kb0 + j, so one set of tcgen05.cp
+// serves four K steps (sf_id = j selects it for all four 32-wide MMAs of step kb0 + j).
+struct __align__(1024) FpStage {
+  uint8_t a[kGM * kGK];  // 16 KB, 128B-swizzled by TMA
+  uint8_t b[kGN * kGK];  // 32 KB
+};
+constexpr int kSfGroup = 4;  // K steps per scale slot
+struct __align__(128) FpSf {
+  uint8_t sa[kSfGroup][kGM];  // raw scale runs of 4 K steps (TMA box of the MN-major scale tensor)
+  uint8_t sb[kSfGroup][kGN];
+  uint8_t sfa[512];           // tcgen05.cp sources: 32 rows x 16 B
+  uint8_t sfb[2][512];
+};
+
 struct GemmSmem {
-  GemmStage st[kGStages];
+  FpStage st[kGStages];
+  alignas(1024) uint8_t stg[8][2048];  // BF16 epilogue staging: one 32 x 32 box per epilogue warp
+  FpSf sf[2];
   uint64_t full[kGStages];
   uint64_t empty[kGStages];
-  alignas(1024) uint8_t stg[8][2048];  // BF16 epilogue staging: one 32 x 32 box per epilogue warp
-  uint64_t sfready[kGStages];  // the stage's scale-factor chunks are expanded
+  uint64_t sffull[2];          // a slot's raw scales landed (TMA)
+  uint64_t sfready[2];         // its scale-factor chunks are expanded
+  uint64_t sfempty[2];         // the MMAs that read it completed (tcgen05.commit)
   uint64_t tmem_full;          // accumulator complete (tcgen05.commit)
   uint64_t tmem_empty;         // accumulator read out by the 8 epilogue warps
   uint32_t tmem_base;
@@ -214,8 +237,9 @@ __device__ __forceinline__ int cta_tile(int i, int total_rb, int n_nt) {
 template <int CL>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_blockscaled_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                            const __grid_constant__ CUtensorMap tmap_d, const uint8_t* __restrict__ sa, int64_t ld_sa, const uint8_t* __restrict__ sb,
-                            int64_t ld_sb, int64_t M, int64_t N, int64_t K, const int32_t* __restrict__ seg_offsets,
+                            const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_sa,
+                            const __grid_constant__ CUtensorMap tmap_sb, int64_t M, int64_t N, int64_t K,
+                            const int32_t* __restrict__ seg_offsets,
                             int32_t num_groups, void* __restrict__ D, int32_t d_f32) {
   extern __shared__ __align__(1024) uint8_t smem_gemm[];
   // 128-byte-swizzled TMA destinations need 1024-byte alignment: align the base explicitly
@@ -228,7 +252,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
     for (int i = 0; i < kGStages; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], CL);  // the MMA commits of every CTA that reads the stage's A tile
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.sffull[i], 1);
       mbar_init(&sm.sfready[i], 32);  // every lane of the scale-expansion warp
+      mbar_init(&sm.sfempty[i], 1);
     }
     mbar_init(&sm.tmem_full, 1);
     mbar_init(&sm.tmem_empty, 8 * 32);  // every epilogue thread
@@ -246,25 +274,33 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
   if (warp == 0) {  // --------------------------------------------------------- TMA producer
     if (lane == 0) {
-      int st = 0, n = 0;
-      uint32_t parity = 0;
+      int st = 0, n = 0, ss = 0, ns = 0;
+      uint32_t parity = 0, sparity = 0;
       const int half = CL > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+      const int kt = static_cast<int>(K / kGK);  // scale rows per group of B
       for (int i = 0, t; (t = cta_tile<CL>(i, sm.total_rb, n_nt)) >= 0; ++i) {
         const GemmTile T = gemm_tile(sm, ngroups, n_nt, t);
-        const uint32_t sa_bytes = static_cast<uint32_t>(min64(kGM, ld_sa - T.r0));
-        const uint8_t* sbg = sb + static_cast<int64_t>(T.g) * (K / kGK) * ld_sb;
         for (int kb = 0; kb < nk; ++kb, ++n) {
+          if (kb % kSfGroup == 0) {  // scales of K steps kb .. kb+3 (rows past the end: zero / unused)
+            if (ns >= 2) mbar_wait(&sm.sfempty[ss], sparity ^ 1u);
+            mbar_expect_tx(&sm.sffull[ss], kSfGroup * (kGM + kGN));
+            tma_load_2d(sm.sf[ss].sa, &tmap_sa, &sm.sffull[ss], T.r0, kb);
+            tma_load_2d(sm.sf[ss].sb, &tmap_sb, &sm.sffull[ss], T.n0, T.g * kt + kb);
+            ++ns;
+            if (++ss == 2) {
+              ss = 0;
+              sparity ^= 1u;
+            }
+          }
           if (n >= kGStages) mbar_wait(&sm.empty[st], parity ^ 1u);
-          GemmStage& S = sm.st[st];
-          mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK + sa_bytes + kGN);
+          FpStage& S = sm.st[st];
+          mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK);
           if (CL == 1)
             tma_load_2d(S.a, &tmap_a, &sm.full[st], kb * kGK, T.r0);
           else  // this CTA's half of the shared A tile, into both CTAs of the pair
             tma_load_2d_mc(S.a + half * (kGM / 2) * kGK, &tmap_a, &sm.full[st], kb * kGK, T.r0 + half * (kGM / 2),
                            0x3);
           tma_load_2d(S.b, &tmap_b, &sm.full[st], kb * kGK, static_cast<int32_t>(T.g * N + T.n0));
-          bulk_load_1d(S.sa, sa + static_cast<int64_t>(kb) * ld_sa + T.r0, sa_bytes, &sm.full[st]);
-          bulk_load_1d(S.sb, sbg + static_cast<int64_t>(kb) * ld_sb + T.n0, kGN, &sm.full[st]);
           if (++st == kGStages) {
             st = 0;
             parity ^= 1u;
@@ -273,65 +309,88 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
   } else if (warp == 1) {  // ------------------------------------------------------ MMA issue
-    int st = 0, step = 0;
-    uint32_t parity = 0;
+    int st = 0, ss = 0, ng = 0;
+    uint32_t parity = 0, sparity = 0;
     for (int i = 0; cta_tile<CL>(i, sm.total_rb, n_nt) >= 0; ++i) {
       if (i > 0) mbar_wait(&sm.tmem_empty, (i - 1) & 1);  // the previous tile has been read out
       tc_fence_after();
-      for (int kb = 0; kb < nk; ++kb, ++step) {
-        mbar_wait(&sm.sfready[st], parity);  // implies the stage's TMA data has landed
+      uint32_t sfa_t = 0, sfb_t = 0;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int j = kb % kSfGroup;
+        if (j == 0) {  // one set of scale-factor copies per four K steps
+          mbar_wait(&sm.sfready[ss], sparity);
+          tc_fence_after();
+          sfa_t = tmem + kSfCol + 16u * (ng & 1);
+          sfb_t = sfa_t + 4u;
+          if (lane == 0) {
+            tc_cp_32x128b_warpx4(sfa_t, desc_sf_chunk(sm.sf[ss].sfa));
+            tc_cp_32x128b_warpx4(sfb_t, desc_sf_chunk(sm.sf[ss].sfb[0]));
+            tc_cp_32x128b_warpx4(sfb_t + 4u, desc_sf_chunk(sm.sf[ss].sfb[1]));
+          }
+        }
+        mbar_wait(&sm.full[st], parity);
         tc_fence_after();
         if (lane == 0) {
-          GemmStage& S = sm.st[st];
-          const uint32_t sfa_t = tmem + kSfCol + 16u * (step & 1);
-          const uint32_t sfb_t = sfa_t + 4u;
-          tc_cp_32x128b_warpx4(sfa_t, desc_sf_chunk(S.sfa));
-          tc_cp_32x128b_warpx4(sfb_t, desc_sf_chunk(S.sfb[0]));
-          tc_cp_32x128b_warpx4(sfb_t + 4u, desc_sf_chunk(S.sfb[1]));
+          FpStage& S = sm.st[st];
           const uint64_t adesc = desc_kmajor_sw128(S.a), bdesc = desc_kmajor_sw128(S.b);
 #pragma unroll
           for (int k = 0; k < kGK / 32; ++k)  // +32 bytes (one K=32 slice) inside the swizzle atom
-            tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(k)),
+            tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(j)),
                         (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
-          // the stage (and its SF chunks) is free when these MMAs complete -- in every CTA of the
-          // pair, since the peer multicasts its half of A into this stage too
+          // the stage is free when these MMAs complete -- in every CTA of the pair, since the
+          // peer multicasts its half of A into this stage too
           if (CL == 1) tc_commit(&sm.empty[st]);
           else tc_commit_mc(&sm.empty[st], 0x3);
+          if (j == kSfGroup - 1 || kb == nk - 1) tc_commit(&sm.sfempty[ss]);  // the scale slot too
         }
         __syncwarp();
         if (++st == kGStages) {
           st = 0;
           parity ^= 1u;
+        }
+        if (j == kSfGroup - 1 || kb == nk - 1) {
+          ++ng;
+          if (++ss == 2) {
+            ss = 0;
+            sparity ^= 1u;
+          }
         }
       }
       if (lane == 0) tc_commit(&sm.tmem_full);
       __syncwarp();
     }
   } else if (warp == 2) {  // --------------------------------------------- scale expansion
-    int st = 0;
-    uint32_t parity = 0;
+    int ss = 0;
+    uint32_t sparity = 0;
     for (int i = 0; cta_tile<CL>(i, sm.total_rb, n_nt) >= 0; ++i) {
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&sm.full[st], parity);
-        GemmStage& S = sm.st[st];
-        // chunk byte (r % 32) * 16 + (r / 32) * 4 + j = row r's scale for the 32-wide K block j;
-        // a 1x128 scale is the same for all four
+      for (int kb = 0; kb < nk; kb += kSfGroup) {
+        mbar_wait(&sm.sffull[ss], sparity);
+        FpSf& S = sm.sf[ss];
+        // chunk byte (r % 32) * 16 + (r / 32) * 4 + j = row r's scale for K step kb + j (one
+        // 1x128 scale covers the four 32-wide MX blocks of its step: the MMAs of step kb + j all
+        // read byte j)
         uint32_t w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = S.sa[lane + 32 * i] * 0x01010101u;
+        for (int i2 = 0; i2 < 4; ++i2) {
+          const int r = lane + 32 * i2;
+          w[i2] = S.sa[0][r] | (S.sa[1][r] << 8) | (S.sa[2][r] << 16) | (static_cast<uint32_t>(S.sa[3][r]) << 24);
+        }
         *reinterpret_cast<uint4*>(&S.sfa[lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) w[i] = S.sb[128 * c + lane + 32 * i] * 0x01010101u;
+          for (int i2 = 0; i2 < 4; ++i2) {
+            const int r = 128 * c + lane + 32 * i2;
+            w[i2] = S.sb[0][r] | (S.sb[1][r] << 8) | (S.sb[2][r] << 16) | (static_cast<uint32_t>(S.sb[3][r]) << 24);
+          }
           *reinterpret_cast<uint4*>(&S.sfb[c][lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.cp (async proxy)
         __syncwarp();
-        mbar_arrive(&sm.sfready[st]);
-        if (++st == kGStages) {
-          st = 0;
-          parity ^= 1u;
+        mbar_arrive(&sm.sfready[ss]);
+        if (++ss == 2) {
+          ss = 0;
+          sparity ^= 1u;
         }
       }
     }
@@ -694,12 +753,30 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
+  // MN-major scale tensors as 2D maps: sa [K/128][ld_sa], sb [groups * K/128][ld_sb]; boxes of four
+  // K steps x 128 (A rows) / 256 (B rows) bytes
+  CUtensorMap msa, msb;
+  {
+    const cuuint64_t gdim_sa[2] = {static_cast<cuuint64_t>(ld_sa), static_cast<cuuint64_t>(K / kGK)};
+    const cuuint64_t gstr_sa[1] = {static_cast<cuuint64_t>(ld_sa)};
+    const cuuint32_t box_sa[2] = {kGM, kSfGroup};
+    const cuuint64_t gdim_sb[2] = {static_cast<cuuint64_t>(ld_sb), static_cast<cuuint64_t>(K / kGK) * groups};
+    const cuuint64_t gstr_sb[1] = {static_cast<cuuint64_t>(ld_sb)};
+    const cuuint32_t box_sb[2] = {kGN, kSfGroup};
+    if (encode(&msa, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(sa), gdim_sa, gstr_sa, box_sa, estride,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        encode(&msb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(sb), gdim_sb, gstr_sb, box_sb, estride,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   // persistent: at most one CTA per SM, tiles walked with a static stride (pairs of tiles for cl = 2)
   const int64_t tiles_ub = (M / kGM + groups) * (N / kGN);
   int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   if (cl == 1) {
     gemm_blockscaled_kernel<1><<<static_cast<unsigned>(grid), kGThreads, sizeof(GemmSmem) + 1024, stream>>>(
-        ma, mb, md, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets, num_groups, D, d_f32);
+        ma, mb, md, msa, msb, M, N, K, seg_offsets, num_groups, D, d_f32);
     return cudaGetLastError();
   }
   grid = grid / 2 * 2;
@@ -716,8 +793,8 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_blockscaled_kernel<2>, ma, mb, md, sa, ld_sa, sb, ld_sb, M, N, K, seg_offsets,
-                            num_groups, D, d_f32);
+  return cudaLaunchKernelEx(&cfg, gemm_blockscaled_kernel<2>, ma, mb, md, msa, msb, M, N, K, seg_offsets, num_groups,
+                            D, d_f32);
 }
 
 }  // namespace fp8flow
