@@ -152,6 +152,22 @@ __device__ __forceinline__ void tc_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[3
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// four 32-column loads in flight, one wait (the epilogue holds the accumulator for less time)
+__device__ __forceinline__ void tc_ld_128cols(uint32_t taddr, uint32_t (&v)[4][32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[c][0]), "=r"(v[c][1]), "=r"(v[c][2]), "=r"(v[c][3]), "=r"(v[c][4]), "=r"(v[c][5]), "=r"(v[c][6]),
+          "=r"(v[c][7]), "=r"(v[c][8]), "=r"(v[c][9]), "=r"(v[c][10]), "=r"(v[c][11]), "=r"(v[c][12]),
+          "=r"(v[c][13]), "=r"(v[c][14]), "=r"(v[c][15]), "=r"(v[c][16]), "=r"(v[c][17]), "=r"(v[c][18]),
+          "=r"(v[c][19]), "=r"(v[c][20]), "=r"(v[c][21]), "=r"(v[c][22]), "=r"(v[c][23]), "=r"(v[c][24]),
+          "=r"(v[c][25]), "=r"(v[c][26]), "=r"(v[c][27]), "=r"(v[c][28]), "=r"(v[c][29]), "=r"(v[c][30]),
+          "=r"(v[c][31])
+        : "r"(taddr + static_cast<uint32_t>(32 * c)));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 
 // shared-memory matrix descriptors (sm_100 "version 1" format)
 __device__ __forceinline__ uint64_t desc_kmajor_sw128(const void* p) {
@@ -403,10 +419,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       mbar_wait(&sm.tmem_full, i & 1);
       tc_fence_after();
       uint32_t v[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tc_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half + 32 * c),
-                         v[c]);
+      tc_ld_128cols(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half), v);
       tc_fence_before();
       __syncwarp();
       mbar_arrive(&sm.tmem_empty);  // the MMAs of the next tile may start
@@ -645,10 +658,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
       mbar_wait(&sm.tmem_full, i & 1);
       tc_fence_after();
       uint32_t v[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tc_ld_32x32b_x32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half + 32 * c),
-                         v[c]);
+      tc_ld_128cols(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half), v);
       tc_fence_before();
       __syncwarp();
       mbar_arrive(&sm.tmem_empty);

@@ -84,6 +84,37 @@ def test_validation_before_any_cuda_call(L):
                                      ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16), 10, None) == 5
 
 
+def test_validation_of_next_row_entry_points(L):
+    """NEXT-1 / NEXT-2 entry points reject bad arguments synchronously, with the documented codes."""
+    P = ctypes.c_void_p
+    a16 = P(16)
+    # SwiGLU backward: ffn % 128, ld_s < rows, NULL, alignment
+    assert L.fp8flow_swiglu_bwd_quant(None, None, 4, None, 100, None, None, 16, None) == 2
+    assert L.fp8flow_swiglu_bwd_quant(None, None, 32, None, 128, None, None, 16, None) == 2
+    assert L.fp8flow_swiglu_bwd_quant(None, None, 4, None, 128, None, None, 16, None) == 1
+    assert L.fp8flow_swiglu_bwd_quant(P(8), a16, 4, None, 128, a16, a16, 16, None) == 3
+    # dual outputs: transpose-style shape rules (rows % 16, cols % 128), NULL input, segment count
+    assert L.fp8flow_quantize_dual(a16, 24, 128, None, 0, a16, a16, 32, a16, a16, None) == 2
+    assert L.fp8flow_quantize_dual(None, 32, 128, None, 0, a16, a16, 32, a16, a16, None) == 1
+    assert L.fp8flow_quantize_dual(a16, 32, 128, a16, 2000, a16, a16, 32, a16, a16, None) == 4
+    assert L.fp8flow_swiglu_quant_dual(a16, 32, None, 100, None, 0, a16, a16, 32, a16, a16, None) == 2
+    assert L.fp8flow_swiglu_quant_dual(P(8), 32, None, 128, None, 0, a16, a16, 32, a16, a16, None) == 3
+    # GEMM: M % 16, N % 256, K % 128, ld_sa < M, groups out of range, NULL, alignment
+    assert L.fp8flow_gemm_blockscaled(a16, a16, 32, a16, a16, 256, 24, 256, 128, None, 0, a16, 1, None) == 2
+    assert L.fp8flow_gemm_blockscaled(a16, a16, 32, a16, a16, 256, 32, 128, 128, None, 0, a16, 1, None) == 2
+    assert L.fp8flow_gemm_blockscaled(a16, a16, 32, a16, a16, 256, 32, 256, 100, None, 0, a16, 1, None) == 2
+    assert L.fp8flow_gemm_blockscaled(a16, a16, 16, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 2
+    assert L.fp8flow_gemm_blockscaled(a16, a16, 32, a16, a16, 256, 32, 256, 128, a16, 600, a16, 1, None) == 4
+    assert L.fp8flow_gemm_blockscaled(None, a16, 32, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 1
+    assert L.fp8flow_gemm_blockscaled(P(8), a16, 32, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 3
+    assert L.fp8flow_gemm_blockscaled(None, None, 0, None, None, 256, 0, 256, 128, None, 0, None, 1, None) == 0
+    # Wgrad: Ma % 128, Nb % 256, groups required, NULL
+    assert L.fp8flow_gemm_wgrad(a16, a16, 100, a16, a16, 256, a16, 4, a16, 1, None) == 2
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 200, a16, 4, a16, 1, None) == 2
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, a16, 0, a16, 1, None) == 4
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, None, 4, a16, 1, None) == 1
+
+
 def test_no_device_means_error_not_fallback(L):
     import torch
 
