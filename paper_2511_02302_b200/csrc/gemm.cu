@@ -141,17 +141,6 @@ __device__ __forceinline__ void tc_mma_mxf8(uint32_t d_taddr, uint64_t adesc, ui
       "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_taddr),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_taddr), "r"(sfb_taddr));
 }
-__device__ __forceinline__ void tc_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 // four 32-column loads in flight, one wait (the epilogue holds the accumulator for less time)
 __device__ __forceinline__ void tc_ld_128cols(uint32_t taddr, uint32_t (&v)[4][32]) {
 #pragma unroll
@@ -476,9 +465,6 @@ __device__ __forceinline__ void cp_async_16(void* dst, const void* src, uint32_t
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 struct WgradSmem {
   GemmStage st[kWStages];
@@ -530,7 +516,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
   };
 
   if (warp < 2) {  // ------------------------------------------------------- cp.async producers
-    int st = 0, n = 0, prev = -1;
+    int st = 0, n = 0;
     uint32_t parity = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       int e, m0, n0;
@@ -563,23 +549,16 @@ __global__ void __launch_bounds__(kWThreads, 1)
           const int j = tid - kGM / 16;
           cp_async_16(&S.sb[16 * j], sbT + srow * Nb + n0 + 16 * j, 16);
         }
-        cp_async_commit();
-        if (prev >= 0) {  // the previous stage's copies have landed: publish it
-          cp_async_wait<1>();
-          fence_proxy_async_smem();
-          mbar_arrive(&sm.full[prev]);
-        }
-        prev = st;
+        // this thread's copies arrive on the stage's barrier when they land (noinc: the 64
+        // producer arrivals are the barrier's expected count) -- no blocking wait, the producer
+        // runs ahead as far as the ring allows
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[st]))
+                     : "memory");
         if (++st == kWStages) {
           st = 0;
           parity ^= 1u;
         }
       }
-    }
-    if (prev >= 0) {
-      cp_async_wait<0>();
-      fence_proxy_async_smem();
-      mbar_arrive(&sm.full[prev]);
     }
   } else if (warp == 2) {  // ------------------------------------------------------ MMA issue
     int st = 0, step = 0;
@@ -594,6 +573,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
       for (int kb = 0; kb < nk; ++kb, ++step) {
         mbar_wait(&sm.sfready[st], parity);
         tc_fence_after();
+        fence_proxy_async_smem();  // the operands were written by cp.async (generic proxy)
         if (lane == 0) {
           GemmStage& S = sm.st[st];
           const uint32_t sfa_t = tmem + kSfCol + 16u * (step & 1);
