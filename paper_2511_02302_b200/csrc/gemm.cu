@@ -468,7 +468,7 @@ __device__ __forceinline__ void cp_async_16(void* dst, const void* src, uint32_t
 
 struct WgradSmem {
   GemmStage st[kWStages];
-  alignas(1024) uint8_t stg[8][2 * 2048];  // BF16 epilogue staging: two 32 x 32 boxes per epilogue warp
+  alignas(1024) uint8_t stg[8][4 * 2048];  // BF16 epilogue staging: four 32 x 32 boxes per epilogue warp
   uint64_t full[kWStages];     // kWProd producer arrivals (after their copies landed + proxy fence)
   uint64_t empty[kWStages];
   uint64_t sfready[kWStages];
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
       const int64_t grow = static_cast<int64_t>(e) * Ma + m0 + 32 * q + lane;
       const int col0 = n0 + 128 * half;
       if (!d_f32) {
-        epilogue_bf16_tma<2>(&tmap_d, sm.stg[warp - 4], v, col0, static_cast<int>(grow - lane), lane, pending);
+        epilogue_bf16_tma<4>(&tmap_d, sm.stg[warp - 4], v, col0, static_cast<int>(grow - lane), lane, pending);
         continue;
       }
 #pragma unroll
