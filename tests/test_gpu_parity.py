@@ -482,3 +482,62 @@ def test_swiglu_quant_dual_equals_composition(F, orc):
     assert np.array_equal(q[:rows], q1[:rows]) and np.array_equal(s[:, :rows], s1[:, :rows])
     qT1, sT1 = run_transpose(F, q1[:rows], s1[:, :rows], seg)
     assert np.array_equal(qT[: qT1.size], qT1) and np.array_equal(sT[: sT1.shape[0]], sT1)
+
+
+# ======================================================================= CUDA-graph capturability
+def test_all_ops_capture_into_a_cuda_graph(F, orc):
+    """The header's promise: every call is asynchronous, never synchronises and keeps
+    data-dependent sizes on the device, so a whole step captures into a CUDA graph; replays give
+    the eager results bit for bit (and the oracle's)."""
+    T, H, FF, K, E_loc = 96, 256, 256, 4, 8
+    x = synth.activations_bf16(T, H, 11).cuda()
+    g = torch.Generator().manual_seed(12)
+    idx = torch.stack([torch.randperm(16, generator=g)[:K] for _ in range(T)]).to(torch.int32).cuda()
+    probs = torch.rand(T, K, generator=g).cuda()
+    max_rows = F.permute_max_rows(T, K, E_loc)
+    h = synth.normal_bf16(max_rows, 2 * FF, 13, sigma=1.5).cuda()
+    y_in = synth.normal_bf16(max_rows, H, 14).cuda()
+    ws = torch.empty(F.fp8flow_permute_workspace_bytes(T, K, E_loc), dtype=torch.uint8, device="cuda")
+    bufs = {
+        "q": torch.empty(T, H, dtype=torch.uint8, device="cuda"), "s": torch.empty(H // 128, 96, dtype=torch.uint8, device="cuda"),
+        "row_map": torch.empty(T, K, dtype=torch.int32, device="cuda"),
+        "src": torch.empty(max_rows, dtype=torch.int32, device="cuda"),
+        "off": torch.empty(E_loc + 1, dtype=torch.int32, device="cuda"),
+        "q_out": torch.empty(max_rows, H, dtype=torch.uint8, device="cuda"),
+        "s_out": torch.empty(H // 128, max_rows, dtype=torch.uint8, device="cuda"),
+        "qa": torch.empty(max_rows, FF, dtype=torch.uint8, device="cuda"),
+        "sa": torch.empty(FF // 128, max_rows, dtype=torch.uint8, device="cuda"),
+        "y": torch.empty(T, H, dtype=torch.bfloat16, device="cuda"),
+        "qT": torch.empty(max_rows * H, dtype=torch.uint8, device="cuda"),
+        "sT": torch.empty(max_rows // 128 + E_loc, H, dtype=torch.uint8, device="cuda"),
+    }
+
+    def step():
+        b = bufs
+        F.fp8flow_quantize_rowwise(x, b["q"], b["s"])
+        F.fp8flow_permute_plan(idx, 0, E_loc, 16, b["row_map"], b["src"], b["off"], ws)
+        F.fp8flow_permute_pad(b["q"], b["s"], b["src"], b["off"], b["q_out"], b["s_out"])
+        F.fp8flow_swiglu_quant(h, b["qa"], b["sa"], rows_dev=b["off"][E_loc:])
+        F.fp8flow_unpermute_unpad(y_in, b["row_map"], probs, b["y"])
+        F.fp8flow_scaling_aware_transpose(b["q_out"], b["s_out"], b["qT"], b["sT"], seg_offsets=b["off"])
+
+    step()
+    torch.cuda.synchronize()
+    eager = {k: v.clone() for k, v in bufs.items()}
+    for v in bufs.values():
+        v.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    R = int(eager["off"][-1])
+    for k in ("q", "s", "row_map", "off", "y"):
+        assert torch.equal(bufs[k], eager[k]), k
+    assert torch.equal(bufs["src"][:R], eager["src"][:R])
+    assert torch.equal(bufs["q_out"][:R], eager["q_out"][:R]) and torch.equal(bufs["s_out"][:, :R], eager["s_out"][:, :R])
+    assert torch.equal(bufs["qa"][:R], eager["qa"][:R]) and torch.equal(bufs["sa"][:, :R], eager["sa"][:, :R])
+    assert torch.equal(bufs["qT"][: R * H], eager["qT"][: R * H])
+    q_ref, s_ref = orc.quantize_rowwise_bf16(synth.bf16_bits(x.cpu()), ld_s=96)
+    assert np.array_equal(host(bufs["q"]), q_ref)
