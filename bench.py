@@ -403,6 +403,17 @@ def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # =============================================================================================
 # clocks
 # =============================================================================================
@@ -632,6 +643,30 @@ def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
         ms = statistics.median(ts)
         out[name] = {"us": round(ms * 1e3, 2), "gbs": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / peak, 3)}
     out["naive_over_direct_latency"] = round(out["naive_dequant_transpose_requant"]["us"] / out["A2_transpose"]["us"], 2)
+    # hot-L2 numbers (labelled as such): the working set (58.7 MB in + 29.4 MB out)
+    # fits the 126 MB L2, so back-to-back launches without a flush, 20 per CUDA graph replay
+    # (launch overhead separated), per launch
+    hot = {}
+    for name in ("A1_quantize", "A2_transpose"):
+        fn, nbytes = ops[name]
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            ev[0].record()
+            g.replay()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]) / 20)
+        ms = statistics.median(ts)
+        hot[name] = {"us": round(ms * 1e3, 2), "gbs": round(nbytes / ms / 1e6, 1)}
+    out["hot_l2_graph"] = hot
     return out
 
 
@@ -737,8 +772,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nbytes, secs, desc = oracle_sample(hw, 1.0, None)
+        nb1, secs1, desc1 = oracle_sample(hw, 1.0 / 16, 1)  # the same oracle on one core, 1/16 of the sample
         cpu = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": desc, "seconds": round(secs, 2)}
+               "sample": desc, "seconds": round(secs, 2), "cpu_model": cpu_model(),
+               "single_thread": {"value": round(nb1 / secs1 / 1e9, 4), "unit": "GB/s", "sample": desc1,
+                                 "seconds": round(secs1, 2)}}
 
     if rank == 0:
         line = {
