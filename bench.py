@@ -845,7 +845,27 @@ def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
         t_d = D.max_over_ranks(t_d, device)
         t_n = D.max_over_ranks(t_n, device)
         nb = RL.transpose_bytes([rows], cols)
-        out.append({"shape": [rows, cols], "direct_us": round(t_d * 1e3, 2), "naive_us": round(t_n * 1e3, 2),
+        extra = {}
+        if nb < (1 << 20):  # under 1 MB, time inside a CUDA graph to separate launch overhead
+            fns = {"direct": lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT),
+                   "naive": lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws)}
+            for name, fn in fns.items():
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for _ in range(50):
+                        fn()
+                g.replay()
+                torch.cuda.synchronize()
+                ts = []
+                for _ in range(reps):
+                    ev[0].record()
+                    g.replay()
+                    ev[1].record()
+                    ev[1].synchronize()
+                    ts.append(ev[0].elapsed_time(ev[1]) / 50)
+                extra[f"{name}_us_graph_hot_l2"] = round(statistics.median(ts) * 1e3, 2)
+        out.append({"shape": [rows, cols], "direct_us": round(t_d * 1e3, 2), "naive_us": round(t_n * 1e3, 2), **extra,
                     "naive_over_direct": round(t_n / t_d, 2),
                     "direct_gbs_per_gpu": round(nb / t_d / 1e6, 1), "direct_frac": round(nb / t_d / 1e6 / peak, 3),
                     "naive_effective_gbs_per_gpu": round(nb / t_n / 1e6, 1),
