@@ -786,6 +786,9 @@ def main():
             "dtypes": {"codes": "e4m3 (u8)", "scales": "ue8m0 (u8)", "bf16_io": "bf16", "math": "fp32 (fp64 refine)"},
             "data": "synthetic (seeded; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
             "frac_of_hbm_peak": round(value / world / peak, 3),
+            "per_gpu_gbs": round(value / world, 1),
+            "step_us_quantiles": {q: round(float(np.percentile(step_ms, p)) * 1e3, 1)
+                                  for q, p in (("p10", 10), ("p50", 50), ("p90", 90))},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ops[dom]["gbs"], "peak": peak, "unit": "GB/s",
                          "frac": ops[dom]["frac"], "traffic": traffic, "peak_source": peaks["source"],
                          "algorithmic_bytes_per_launch": op_bytes[dom]},
