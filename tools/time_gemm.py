@@ -71,3 +71,24 @@ m[-1] += 15872 - m.sum()
 seg = [0] + list(np.cumsum(m).astype(int))
 case("grouped fc1 fprop 32 experts N=4096", 15872, 4096, 7168, 32, seg)
 case("grouped fc2 fprop 32 experts N=7168", 15872, 7168, 2048, 32, seg)
+
+
+def wgrad_case(name, Ma, Nb, m):
+    seg = torch.tensor([0] + list(np.cumsum(m).astype(int)), dtype=torch.int32, device=dev)
+    R = int(sum(m))
+    G = len(m)
+    P = int(sum((x + 127) // 128 for x in m))
+    AT = torch.randint(0, 120, (R * Ma,), dtype=torch.uint8, device=dev)
+    BT = torch.randint(0, 120, (R * Nb,), dtype=torch.uint8, device=dev)
+    saT = torch.full((P, Ma), 120, dtype=torch.uint8, device=dev)
+    sbT = torch.full((P, Nb), 120, dtype=torch.uint8, device=dev)
+    D = torch.empty(G, Ma, Nb, dtype=torch.bfloat16, device=dev)
+    ms = med(lambda: F.fp8flow_gemm_wgrad(AT, saT, BT, sbT, D, seg), reps=5)
+    flops = 2.0 * R * Ma * Nb
+    tf = flops / ms / 1e9
+    out_gbs = D.numel() * 2 / ms / 1e6
+    print(f"{name:34s} {ms * 1e3:9.1f} us  {tf:7.1f} TFLOP/s  frac {tf / fp8_peak:.3f}  (BF16 dW written at "
+          f"{out_gbs:.0f} GB/s)", flush=True)
+
+
+wgrad_case("grouped fc1 wgrad 32 experts", 4096, 7168, list(m))
