@@ -66,6 +66,7 @@ def lib():
                 "orc_swiglu_bwd_f32": (None, [P, P, I64, I64, P]),
                 "orc_swiglu_bwd_quant": (None, [P, P, I64, I64, P, P, I64]),
                 "orc_gemm_blockscaled": (None, [P, P, I64, P, P, I64, I64, I64, I64, P, I32, I64, I64, P]),
+                "orc_combine": (None, [P, P, I64, P, I32, P, I64, I64, I32, P]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -364,3 +365,51 @@ def gemm_blockscaled(A, sa, B, sb, seg_offsets=None, threads: int | None = None)
 
     _run_split(M, threads, work)
     return D
+
+
+# --------------------------------------------------------------------------------------------
+# NEXT-3: expert-parallel dispatch + permute and combine across ranks
+# --------------------------------------------------------------------------------------------
+def dispatch_permute_pad(q_list, s_list, topk_list, rank: int, num_experts: int, align: int = 16,
+                         max_rows: int | None = None, threads: int | None = None):
+    """What rank `rank` of n = len(q_list) holds after the FP8 dispatch (the row-wise codes
+    and their scales travel) and the fused permute + pad (C8) of the tokens it received: by
+    definition the C8 plan and move over every rank's tokens gathered in rank order (global token
+    id = r * tokens_per_rank + t) restricted to the rank's experts [rank*E/n, (rank+1)*E/n).
+    q_list[r] [Tpr, H] uint8, s_list[r] [H/128, ld] uint8 (first Tpr columns used), topk_list[r]
+    [Tpr, K] int32.  Returns (q_out, s_out, row_map [n*Tpr, K], src_of_row, offsets)."""
+    n = len(q_list)
+    e_per = num_experts // n
+    q_all = np.concatenate([np.ascontiguousarray(q) for q in q_list], axis=0)
+    tpr = q_list[0].shape[0]
+    s_all = np.concatenate([np.ascontiguousarray(s)[:, :tpr] for s in s_list], axis=1)
+    topk_all = np.concatenate([np.ascontiguousarray(t, dtype=np.int32) for t in topk_list], axis=0)
+    row_map, src, off = permute_plan(topk_all, rank * e_per, e_per, align=align, max_rows=max_rows)
+    q_out, s_out = permute_pad(q_all, s_all, src, off, max_rows=len(src), threads=threads)
+    return q_out, s_out, row_map, src, off
+
+
+def combine(x_list, row_map_list, topk_idx, experts_per_rank: int, probs=None, token_begin: int = 0,
+            threads: int | None = None):
+    """NEXT-3 combine (orc_combine): the owner's tokens [token_begin, token_begin + T) summed over
+    their top_k expert outputs x_list[d] (BF16 bits [rows_d, H]) located by row_map_list[d]
+    ([T_global, K], rank d's plan).  Returns y BF16 bits [T, H]."""
+    xs = [np.ascontiguousarray(x, dtype=np.uint16) for x in x_list]
+    rms = [np.ascontiguousarray(r, dtype=np.int32) for r in row_map_list]
+    topk_idx = np.ascontiguousarray(topk_idx, dtype=np.int32)
+    T, K = topk_idx.shape
+    H = xs[0].shape[1]
+    if probs is not None:
+        probs = np.ascontiguousarray(probs, dtype=np.float32)
+    xp = (ctypes.c_void_p * len(xs))(*[x.ctypes.data for x in xs])
+    rp = (ctypes.c_void_p * len(rms))(*[r.ctypes.data for r in rms])
+    y = np.zeros((T, H), np.uint16)
+    L = lib()
+
+    def work(lo, hi):
+        L.orc_combine(ctypes.cast(xp, ctypes.c_void_p), ctypes.cast(rp, ctypes.c_void_p), H, _p(topk_idx, 4 * lo * K),
+                      experts_per_rank, _p(probs, 4 * lo * K) if probs is not None else None, token_begin + lo,
+                      hi - lo, K, _p(y, 2 * lo * H))
+
+    _run_split(T, threads, work)
+    return y

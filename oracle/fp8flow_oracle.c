@@ -34,6 +34,11 @@
  *   orc_checksum64             closed form (DESIGN.md §4 C11)
  *   orc_gemm_blockscaled       pinned (torch float64 matmul of torch-decoded operands, one-hot
  *                               rows = scaled B columns, linearity in the scale exponents)
+ *   orc_combine                pinned (n = 1 reduces to C9; one-hot gates = the expert row;
+ *                               combine(dispatch(Q)) = K * dequant(Q) exactly for any rank count)
+ * NEXT-3's dispatch is the composition gather-in-rank-order -> C8 plan -> C8 move (oracle/__init__.py
+ * dispatch_permute_pad), pinned by the routing-pair partition over ranks and byte equality of every
+ * row with its source token.
  */
 #include <math.h>
 #include <stdint.h>
@@ -483,6 +488,37 @@ void orc_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, co
                 }
                 D[m * N + n] = acc;
             }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT-3 (R34) combine: the owner of a token gathers its top_k expert
+ * outputs from the ranks that computed them and sums them as C9 does ("unpermutation, and
+ * combination"; BF16 at this boundary).  Rank d owns experts [d*E_per, (d+1)*E_per) and
+ * holds x_d [rows_d][H] BF16 with its plan's row_map_d [T_global][K] (the C8 plan over every
+ * rank's tokens, global token id = rank * tokens_per_rank + t).  For the owner's tokens
+ * t = 0..T-1 (global id token_begin + t):
+ *     y[t][h] = BF16_RNE( sum over k = 0..K-1 of p[t][k] * x_d[row_map_d[gt][k]][h] ),
+ *     d = topk_idx[t][k] / E_per, gt = token_begin + t,
+ * fp32 accumulation with one fused multiply-add per term in k order from +0.0 (p = 1, plain add,
+ * when probs is NULL), exactly C9's arithmetic.  x[d] / row_map[d] are arrays of n pointers.
+ * ------------------------------------------------------------------------------------------ */
+void orc_combine(const uint16_t* const* x, const int32_t* const* row_map, int64_t H, const int32_t* topk_idx,
+                 int32_t E_per, const float* probs, int64_t token_begin, int64_t T, int32_t K, uint16_t* y)
+{
+    for (int64_t t = 0; t < T; t++) {
+        int64_t gt = token_begin + t;
+        for (int64_t h = 0; h < H; h++) {
+            float acc = 0.0f;
+            for (int32_t k = 0; k < K; k++) {
+                int32_t d = topk_idx[t * K + k] / E_per;
+                int32_t r = row_map[d][gt * K + k];
+                float xv = (float)bf16_to_double(x[d][(int64_t)r * H + h]);
+                if (probs) acc = fmaf(probs[t * K + k], xv, acc);
+                else acc = acc + xv;
+            }
+            y[t * H + h] = orc_round_bf16((double)acc);
         }
     }
 }
