@@ -503,8 +503,120 @@ def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20) -> dict:
     out["NEXT1_swiglu_quant_dual"] = line(ms, nb, segments=len(segs),
                                           vs_A5_then_A2_us=round(ms_two * 1e3, 2))
     out.update(gemm_measure(ds, reps))
+    out.update(ep_measure(ds.dev, peak, reps))
     return out
 
+
+def ep_measure(device, peak: float, reps: int = 20) -> dict:
+    """NEXT-3 on one GPU: the 8 expert-parallel ranks of the DeepSeek-V3 layer (2048 tokens each,
+    16384 in all, top-8 of 256 experts, 32 per rank) held as virtual ranks on this device, so the
+    peer reads are HBM reads here (NVLink reads on the 8-GPU box).  Times rank 0's receive side
+    (dispatch + fused permute/pad kernel alone, and with the routing gather + plan) and its BF16
+    combine over the 8 ranks' expert outputs; outputs are checked against A3 / A4 on the
+    concatenation (both oracle-parity-tested)."""
+    from paper_2511_02302_b200 import ep
+    from paper_2511_02302_b200 import fp8flow as F
+
+    n, tpr = D.NUM_GROUPS, T_GLOBAL // D.NUM_GROUPS
+    E = 256
+    idx, probs = synth.routing(T_GLOBAL, synth.BASE_SEED)
+    x = synth.activations_bf16_device(T_GLOBAL, HIDDEN, synth.BASE_SEED + 1, device)
+    ranks = []
+    for r in range(n):
+        q = torch.empty(tpr, HIDDEN, dtype=torch.uint8, device=device)
+        s_ = torch.empty(HIDDEN // 128, tpr, dtype=torch.uint8, device=device)
+        F.fp8flow_quantize_rowwise(x[r * tpr:(r + 1) * tpr], q, s_)
+        ranks.append({"q": q, "s": s_, "topk": idx[r * tpr:(r + 1) * tpr].contiguous().to(device),
+                      "probs": probs[r * tpr:(r + 1) * tpr].contiguous().to(device)})
+    del x
+    i32 = torch.int32
+    plans = []
+    for g in range(n):
+        _, per = ep.expert_range(g, n, E)
+        mr = F.permute_max_rows(T_GLOBAL, TOP_K, per)
+        plans.append(dict(topk_all=torch.empty(T_GLOBAL, TOP_K, dtype=i32, device=device),
+                          row_map=torch.empty(T_GLOBAL, TOP_K, dtype=i32, device=device),
+                          src=torch.empty(mr, dtype=i32, device=device),
+                          off=torch.empty(per + 1, dtype=i32, device=device),
+                          ws=torch.empty(F.fp8flow_permute_workspace_bytes(T_GLOBAL, TOP_K, per),
+                                         dtype=torch.uint8, device=device),
+                          q_out=torch.empty(mr, HIDDEN, dtype=torch.uint8, device=device),
+                          s_out=torch.empty(HIDDEN // 128, mr, dtype=torch.uint8, device=device)))
+    peers = ep.LocalPeers(ranks)
+
+    def receive(g, kernel_only=False):
+        p = plans[g]
+        if kernel_only:
+            F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), tpr, tpr, HIDDEN, p["row_map"],
+                                           p["src"], p["off"], p["q_out"], p["s_out"])
+        else:
+            ep.dispatch_permute(peers, g, tpr, HIDDEN, TOP_K, E, tpr, p["topk_all"], p["row_map"], p["src"],
+                                p["off"], p["ws"], p["q_out"], p["s_out"])
+
+    for g in range(n):
+        receive(g)
+    torch.cuda.synchronize(device)
+    # expert outputs (BF16, as from fc2) on every rank; combine inputs
+    for g in range(n):
+        R = int(plans[g]["off"][-1].item())
+        ranks[g]["x"] = synth.normal_bf16_device(plans[g]["q_out"].shape[0], HIDDEN, synth.BASE_SEED + 40 + g, device)
+        ranks[g]["x"][R:] = 0
+        ranks[g]["row_map"] = plans[g]["row_map"]
+    peers = ep.LocalPeers(ranks)
+    y = torch.empty(tpr, HIDDEN, dtype=torch.bfloat16, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def med(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            torch.cuda._sleep(1_000_000)
+            ev[0].record()
+            fn()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        return statistics.median(ts)
+
+    p0 = plans[0]
+    src0 = p0["src"].cpu().numpy()
+    R0 = int(p0["off"][-1].item())
+    uniq = int(np.count_nonzero((p0["row_map"].cpu().numpy() >= 0).any(axis=1)))
+    nb_d = RL.dispatch_permute_bytes(uniq, R0, T_GLOBAL, TOP_K, HIDDEN)
+    ms_k = med(lambda: receive(0, kernel_only=True))
+    ms_all = med(lambda: receive(0))
+    nb_c = RL.combine_bytes(tpr, TOP_K, HIDDEN, True)
+    ms_c = med(lambda: ep.combine(peers, 0, tpr, HIDDEN, E, ranks[0]["topk"], ranks[0]["probs"], y))
+    # checks: dispatch == A3 on the concatenation; combine == A4 on the concatenation
+    q_cat = torch.cat([r["q"] for r in ranks])
+    s_cat = torch.cat([r["s"] for r in ranks], dim=1).contiguous()
+    ref_q, ref_s = torch.empty_like(p0["q_out"]), torch.empty_like(p0["s_out"])
+    F.fp8flow_permute_pad(q_cat, s_cat, p0["src"], p0["off"], ref_q, ref_s)
+    ok_d = bool(torch.equal(ref_q[:R0], p0["q_out"][:R0]) and torch.equal(ref_s[:, :R0], p0["s_out"][:, :R0]))
+    base = [0]
+    for g in range(n):
+        base.append(base[-1] + ranks[g]["x"].shape[0])
+    x_cat = torch.cat([r["x"] for r in ranks])
+    rm_glob = torch.full((tpr, TOP_K), -1, dtype=i32, device=device)
+    for g in range(n):
+        rm = plans[g]["row_map"][:tpr]
+        rm_glob = torch.where(rm >= 0, rm + base[g], rm_glob)
+    y_ref = torch.empty_like(y)
+    F.fp8flow_unpermute_unpad(x_cat, rm_glob.contiguous(), ranks[0]["probs"], y_ref)
+    torch.cuda.synchronize(device)
+    ok_c = bool(torch.equal(y.view(torch.int16), y_ref.view(torch.int16)))
+    del src0
+
+    def line(ms, nb, **kw):
+        return {"us": round(ms * 1e3, 2), "bytes": nb, "gbs": round(nb / ms / 1e6, 1),
+                "frac": round(nb / ms / 1e6 / peak, 3), **kw}
+
+    note = "8 virtual EP ranks on one GPU: peer reads are local HBM here, NVLink on the 8-GPU box"
+    return {"NEXT3_dispatch_permute_pad": line(ms_k, nb_d, rank=0, recv_tokens=uniq, rows=R0, parity=ok_d,
+                                               with_gather_and_plan_us=round(ms_all * 1e3, 2), note=note),
+            "NEXT3_combine_unpermute": line(ms_c, nb_c, rank=0, tokens=tpr, parity=ok_c, note=note)}
 
 def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
     """NEXT-2: the block-scaled FP8 grouped GEMMs that consume the step's outputs directly -- fc1

@@ -259,6 +259,81 @@ FP8FLOW_API int fp8flow_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_
                                    const uint8_t* sbT, int64_t Nb, const int32_t* seg_offsets, int32_t num_groups,
                                    void* D, int32_t d_f32, void* stream);
 
+/* ==========================================================================================
+ * NEXT-3  Expert-parallel FP8 dispatch / BF16 combine over peer memory (
+ *     DESIGN.md R34).  The MoE layer's stages are routing -> dispatch -> permutation -> experts ->
+ *     unpermutation -> combination; dispatch ships the row-wise FP8 format, codes
+ *     and scales together, and the combine is BF16.  Rank r of n owns tokens
+ *     [r*T_per_rank, (r+1)*T_per_rank) (global token id) and experts [r*E_per, (r+1)*E_per).
+ *
+ *   Peer tables: `peer_*` arguments are HOST arrays of n device pointers, entry r = rank r's
+ *   buffer as mapped in the calling process (CUDA IPC via fp8flow_ipc_* on a multi-GPU node, or
+ *   plain device pointers when several ranks share one device).  They are copied by value into
+ *   the launch (CUDA-graph capturable); 1 <= n <= FP8FLOW_MAX_RANKS.  Every rank's buffers must
+ *   be complete before a peer reads them: call fp8flow_peer_barrier on the same stream first.
+ *   Buffers read by peers must not be overwritten until the peers are done (next barrier).
+ * ========================================================================================== */
+#define FP8FLOW_MAX_RANKS 64
+#define FP8FLOW_IPC_HANDLE_BYTES 64
+
+/* CUDA IPC plumbing (host calls, synchronous).  fp8flow_ipc_get_handle exports the allocation that
+ * contains dev_ptr: handle_out receives FP8FLOW_IPC_HANDLE_BYTES opaque bytes and *offset_out the
+ * byte offset of dev_ptr inside that allocation (caching allocators sub-allocate).
+ * fp8flow_ipc_open maps a handle exported by ANOTHER process (peer access enabled lazily) and
+ * returns the allocation's base in *base_out (add the exporter's offset); fp8flow_ipc_close unmaps
+ * it.  Errors: FP8FLOW_ERR_NULL, FP8FLOW_ERR_CUDA. */
+FP8FLOW_API int fp8flow_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+FP8FLOW_API int fp8flow_ipc_open(const void* handle, void** base_out);
+FP8FLOW_API int fp8flow_ipc_close(void* base);
+
+/* fp8flow_peer_barrier -- device-side barrier of n ranks over peer flags (no host sync).
+ *   peer_signal  host array [n] of device pointers; entry d = rank d's signal buffer of n + 1
+ *                uint32, zero-initialised once by its owner before first use (slot s = the last
+ *                epoch rank s announced; slot n = the owner's epoch counter, advanced on device)
+ *   status       device int32 or NULL: 0 on success, 1 if the peers did not arrive within
+ *                timeout_ms (the kernel then returns instead of hanging).
+ * Every rank must call it the same number of times. */
+FP8FLOW_API int fp8flow_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int32_t* status,
+                                     uint32_t timeout_ms, void* stream);
+
+/* fp8flow_peer_gather -- all-gather by pulls: dst[r*bytes_per_rank ...] = peer_src[r][0 .. bytes_per_rank)
+ * (e.g. every rank's topk_idx for the dispatch plan).  bytes_per_rank % 16 == 0, all pointers
+ * 16-byte aligned, dst device [n*bytes_per_rank]. */
+FP8FLOW_API int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
+                                    void* stream);
+
+/* fp8flow_dispatch_permute_pad -- the receive side of the FP8 dispatch fused with A3's move: every
+ *   token routed to one of this rank's experts is read ONCE from its owner (codes + scale bytes)
+ *   and written to all of its local expert rows; PAD rows get code 0x00 / scale 0x00.  The result
+ *   is bit-identical to fp8flow_permute_pad on the rank-order concatenation of all ranks' tokens.
+ *   peer_q    host array [n]: rank r's codes [tokens_per_rank][hidden] (as from A1)
+ *   peer_s    host array [n]: rank r's scales [hidden/128][ld_s_tok] (MN-major, as from A1)
+ *   row_map, src_of_row, expert_offsets: from fp8flow_permute_plan over the GATHERED topk_idx
+ *             [n*tokens_per_rank][top_k] with this rank's expert range (global token ids)
+ *   q_out [max_rows][hidden], s_out [hidden/128][max_rows] (rows >= expert_offsets[E_loc] untouched)
+ *   hidden % 128 == 0, q pointers 16-byte aligned, 1 <= top_k <= 16, ld_s_tok >= tokens_per_rank. */
+FP8FLOW_API int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s,
+                                             int64_t ld_s_tok, int32_t n, int64_t tokens_per_rank, int64_t hidden,
+                                             const int32_t* row_map, int32_t top_k, const int32_t* src_of_row,
+                                             const int32_t* expert_offsets, int32_t num_local_experts,
+                                             int64_t max_rows, uint8_t* q_out, uint8_t* s_out, void* stream);
+
+/* fp8flow_combine_unpermute -- the owner side of the BF16 combine fused with A4: for the caller's
+ *   tokens t (global id token_begin + t),
+ *     y[t][h] = BF16_RNE( sum_k p[t][k] * x_d[row_map_d[token_begin + t][k]][h] ),
+ *     d = topk_idx[t][k] / experts_per_rank,
+ *   fp32 fmaf in k order from +0 (p = 1 when probs is NULL) -- A4's arithmetic, so the result is
+ *   bit-identical to fp8flow_unpermute_unpad over the concatenated expert outputs.  Terms whose
+ *   expert id is outside [0, n*experts_per_rank) or whose row is -1 are skipped.
+ *   peer_x       host array [n]: rank d's expert outputs, BF16 [rows_d][hidden], 16-byte aligned
+ *   peer_row_map host array [n]: rank d's plan row_map [n*tokens_per_rank][top_k] (device int32)
+ *   topk_idx [num_tokens][top_k], probs fp32 [num_tokens][top_k] or NULL, y BF16 [num_tokens][hidden].
+ *   hidden % 8 == 0, 1 <= top_k <= 16. */
+FP8FLOW_API int fp8flow_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
+                                          int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank,
+                                          const float* probs, int64_t token_begin, int64_t num_tokens, int32_t top_k,
+                                          void* y_bf16, void* stream);
+
 /* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
  * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */
 FP8FLOW_API int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void* stream);

@@ -293,4 +293,119 @@ int fp8flow_checksum64(const void* buf, int64_t nbytes, uint64_t* out_dev, void*
   return launched(launch_checksum64(buf, nbytes, out_dev, static_cast<cudaStream_t>(stream), sms));
 }
 
+// ------------------------------------------------------------------------------------- NEXT-3
+namespace {
+typedef int (*PFN_cuMemGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+int peer_table_ok(const void* const* tab, int32_t n, bool need16) {
+  if (!tab) return FP8FLOW_ERR_NULL;
+  for (int r = 0; r < n; ++r) {
+    if (!tab[r]) return FP8FLOW_ERR_NULL;
+    if (need16 && !aligned16(tab[r])) return FP8FLOW_ERR_ALIGN;
+  }
+  return FP8FLOW_OK;
+}
+}  // namespace
+
+int fp8flow_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == FP8FLOW_IPC_HANDLE_BYTES, "IPC handle size");
+  if (!dev_ptr || !handle_out || !offset_out) return FP8FLOW_ERR_NULL;
+  static PFN_cuMemGetAddressRange get_range = nullptr;
+  if (!get_range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &qres);
+    if (e != cudaSuccess || qres != cudaDriverEntryPointSuccess || !p) return fail_cuda(e != cudaSuccess ? e : cudaErrorNotSupported);
+    get_range = reinterpret_cast<PFN_cuMemGetAddressRange>(p);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0) return fail_cuda(cudaErrorInvalidValue);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail_cuda(e);
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = static_cast<int64_t>(reinterpret_cast<unsigned long long>(dev_ptr) - base);
+  return FP8FLOW_OK;
+}
+
+int fp8flow_ipc_open(const void* handle, void** base_out) {
+  if (!handle || !base_out) return FP8FLOW_ERR_NULL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? FP8FLOW_OK : fail_cuda(e);
+}
+
+int fp8flow_ipc_close(void* base) {
+  if (!base) return FP8FLOW_ERR_NULL;
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  return e == cudaSuccess ? FP8FLOW_OK : fail_cuda(e);
+}
+
+int fp8flow_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int32_t* status, uint32_t timeout_ms,
+                         void* stream) {
+  if (n < 1 || n > FP8FLOW_MAX_RANKS || rank < 0 || rank >= n) return FP8FLOW_ERR_ARG;
+  int st = peer_table_ok(peer_signal, n, false);
+  if (st != FP8FLOW_OK) return st;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_peer_barrier(peer_signal, rank, n, status, timeout_ms, static_cast<cudaStream_t>(stream)));
+}
+
+int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst, void* stream) {
+  if (n < 1 || n > FP8FLOW_MAX_RANKS) return FP8FLOW_ERR_ARG;
+  if (bytes_per_rank < 0 || bytes_per_rank % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (bytes_per_rank == 0) return FP8FLOW_OK;
+  int st = peer_table_ok(peer_src, n, true);
+  if (st != FP8FLOW_OK) return st;
+  if (!dst) return FP8FLOW_ERR_NULL;
+  if (!aligned16(dst)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_peer_gather(peer_src, n, bytes_per_rank, dst, static_cast<cudaStream_t>(stream), sms));
+}
+
+int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s, int64_t ld_s_tok,
+                                 int32_t n, int64_t tokens_per_rank, int64_t hidden, const int32_t* row_map,
+                                 int32_t top_k, const int32_t* src_of_row, const int32_t* expert_offsets,
+                                 int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
+                                 void* stream) {
+  if (n < 1 || n > FP8FLOW_MAX_RANKS) return FP8FLOW_ERR_ARG;
+  if (top_k < 1 || top_k > 16 || num_local_experts < 1 || num_local_experts > 1024) return FP8FLOW_ERR_ARG;
+  if (tokens_per_rank < 0 || hidden <= 0 || hidden % 128 != 0 || max_rows < 0) return FP8FLOW_ERR_SHAPE;
+  if (ld_s_tok < tokens_per_rank) return FP8FLOW_ERR_SHAPE;
+  if (tokens_per_rank * n > INT32_MAX) return FP8FLOW_ERR_SHAPE;
+  if (tokens_per_rank == 0) return FP8FLOW_OK;  // no tokens: every expert is empty, no rows to write
+  int st = peer_table_ok(reinterpret_cast<const void* const*>(peer_q), n, true);
+  if (st != FP8FLOW_OK) return st;
+  if ((st = peer_table_ok(reinterpret_cast<const void* const*>(peer_s), n, false)) != FP8FLOW_OK) return st;
+  if (!row_map || !src_of_row || !expert_offsets || !q_out || !s_out) return FP8FLOW_ERR_NULL;
+  if (!aligned16(q_out)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_dispatch_permute_pad(peer_q, peer_s, ld_s_tok, n, tokens_per_rank, hidden, row_map, top_k,
+                                              src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out,
+                                              static_cast<cudaStream_t>(stream), sms));
+}
+
+int fp8flow_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
+                              int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank, const float* probs,
+                              int64_t token_begin, int64_t num_tokens, int32_t top_k, void* y_bf16, void* stream) {
+  if (n < 1 || n > FP8FLOW_MAX_RANKS || experts_per_rank < 1) return FP8FLOW_ERR_ARG;
+  if (top_k < 1 || top_k > 16) return FP8FLOW_ERR_ARG;
+  if (num_tokens < 0 || token_begin < 0 || hidden <= 0 || hidden % 8 != 0) return FP8FLOW_ERR_SHAPE;
+  if (num_tokens == 0) return FP8FLOW_OK;
+  int st = peer_table_ok(peer_x, n, true);
+  if (st != FP8FLOW_OK) return st;
+  if ((st = peer_table_ok(reinterpret_cast<const void* const*>(peer_row_map), n, false)) != FP8FLOW_OK) return st;
+  if (!topk_idx || !y_bf16) return FP8FLOW_ERR_NULL;
+  if (!aligned16(y_bf16)) return FP8FLOW_ERR_ALIGN;
+  int sms = 0;
+  if ((st = device(&sms)) != FP8FLOW_OK) return st;
+  return launched(launch_combine_unpermute(peer_x, peer_row_map, n, hidden, topk_idx, experts_per_rank, probs,
+                                           token_begin, num_tokens, top_k, y_bf16, static_cast<cudaStream_t>(stream),
+                                           sms));
+}
+
 }  // extern "C"

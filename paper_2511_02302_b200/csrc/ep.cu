@@ -1,0 +1,343 @@
+// ep.cu -- NEXT-3: expert-parallel FP8 dispatch fused with A3's permute + pad on the receive side,
+// and the BF16 combine fused with A4's unpermute, over peer memory (NVLink 5 / NVSwitch: CUDA IPC
+// mappings of the other ranks' buffers; plain local pointers when several ranks share a device).
+//
+// Paper: P:245 (routing -> dispatch -> permutation -> experts -> unpermutation -> combination);
+// P:128 (dispatch ships the row-wise FP8 format); P:347 ("the need to transmit both the FP8 tensor
+// and its corresponding scaling factors doubles the number of data buffers and synchronizations");
+// P:260 (BF16 at the combine boundary).  Reading R34: rank g's dispatched rows are
+// A3 over all ranks' tokens gathered in rank order, restricted to g's experts; combine is A4 over the
+// concatenated expert outputs (fp32 FMA in k order, BF16 RNE).
+//
+// B200 design (NEXT-3):
+//  * PULL, not push: the receiver reads each routed token ONCE from its owner over NVLink and fans
+//    it out to all of its local expert rows in HBM, so NVLink carries unique (token, rank) bytes
+//    (~2x fewer than one message per (token, expert) pair at DSv3 routing) and no intermediate
+//    receive buffer is written and re-read (the permute is fused into the receive).
+//  * codes and scales in one kernel, one synchronisation (the barrier before it), no staging
+//    buffer pair as in P:347.
+//  * peer pointers travel by value in the kernel parameters (<= 64 ranks), so every launch is
+//    CUDA-graph capturable; the barrier keeps its epoch on the device.
+//  * plain 128-bit loads/stores (ld.global.nc) rather than bulk copies: valid on any peer mapping.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fp8flow {
+
+constexpr int kEpThreads = 256;
+constexpr int kEpWarps = kEpThreads / 32;
+constexpr int kCopyU = 16;  // uint4 per lane per pass of the token copy (8 KB per warp pass)
+constexpr int kScaleTiles = 8;  // 1x128 tiles per scale work item
+
+struct PeerPtrs {
+  const void* p[kMaxRanks];
+};
+struct PeerPtrs2 {
+  const void* a[kMaxRanks];
+  const void* b[kMaxRanks];
+};
+
+// ---------------------------------------------------------------------------------------------
+// all-gather by pulls: out[r * bytes + i] = peer[r][i]
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kEpThreads) peer_gather_kernel(PeerPtrs src, int n, int64_t vec_per_rank,
+                                                                 uint4* __restrict__ out) {
+  const int64_t total = vec_per_rank * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / vec_per_rank);
+    const int64_t j = i - r * vec_per_rank;
+    out[i] = ld_nc_v4(static_cast<const uint4*>(src.p[r]) + j);
+  }
+}
+
+cudaError_t launch_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
+                               cudaStream_t stream, int num_sms) {
+  PeerPtrs pp{};
+  for (int r = 0; r < n; ++r) pp.p[r] = peer_src[r];
+  const int64_t vec = bytes_per_rank / 16;
+  int64_t grid = (vec * n + kEpThreads - 1) / kEpThreads;
+  if (grid > 4LL * num_sms) grid = 4LL * num_sms;
+  if (grid < 1) grid = 1;
+  peer_gather_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec, static_cast<uint4*>(dst));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// device barrier over peer flags.  Rank r's signal buffer holds n + 1 uint32: slot s = the last
+// epoch rank s announced to r, slot n = r's own epoch counter (advanced only by r).  Every call
+// advances the epoch, stores it (release, system scope) into slot r of every peer, then waits
+// (acquire) until every slot of its own buffer has reached it.  Bounded: after ~timeout_ms the
+// kernel gives up and writes 1 to *status (0 on success).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kMaxRanks) peer_barrier_kernel(PeerPtrs sig, int rank, int n, int32_t* status,
+                                                                 uint64_t timeout_ns) {
+  __shared__ uint32_t epoch_s;
+  __shared__ int failed;
+  uint32_t* mine = static_cast<uint32_t*>(const_cast<void*>(sig.p[rank]));
+  if (threadIdx.x == 0) {
+    epoch_s = mine[n] + 1;
+    mine[n] = epoch_s;
+    failed = 0;
+  }
+  __syncthreads();
+  const uint32_t epoch = epoch_s;
+  const int d = threadIdx.x;
+  if (d < n) {
+    __threadfence_system();  // everything this stream wrote before the barrier, visible system-wide
+    st_release_sys(static_cast<uint32_t*>(const_cast<void*>(sig.p[d])) + rank, epoch);
+    const uint64_t t0 = globaltimer_ns();
+    while (static_cast<int32_t>(ld_acquire_sys(mine + d) - epoch) < 0) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        failed = 1;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && status != nullptr) *status = failed;
+}
+
+cudaError_t launch_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int32_t* status,
+                                uint32_t timeout_ms, cudaStream_t stream) {
+  PeerPtrs pp{};
+  for (int r = 0; r < n; ++r) pp.p[r] = peer_signal[r];
+  peer_barrier_kernel<<<1, kMaxRanks, 0, stream>>>(pp, rank, n, status,
+                                                   static_cast<uint64_t>(timeout_ms) * 1000000ull);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// dispatch + permute + pad (receive side).  Three kinds of warp work in one launch:
+//   scales: per (32-token chunk, 8 tiles): each lane loads its token's 8 scale bytes first (one
+//           32-byte sector per tile for the warp), then scatters them to every local row;
+//   codes : per global token with >= 1 local row: the warp pulls its H code bytes once (128-bit
+//           non-coherent loads, up to 8 KB in flight per warp) and stores them to every local row;
+//   PAD   : per local expert, the trailing PAD rows (src_of_row < 0) get code 0x00 and scale 0x00.
+// Scale and PAD items are taken by the grid's first and last warps; code items by all warps.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kEpThreads) dispatch_permute_kernel(
+    PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
+    const int32_t* __restrict__ src_of_row, const int32_t* __restrict__ offsets, int E_loc, int64_t max_rows,
+    uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * kEpWarps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEpWarps + (threadIdx.x >> 5);
+  const int64_t T = Tpr * n;
+  const int64_t n_tiles = H / 128;
+
+  // ---- scales: item = (chunk of 32 consecutive global tokens, group of kScaleTiles 1x128 tiles).
+  // Lane l owns token c*32 + l: its kScaleTiles scale bytes are loaded first (one 32-byte sector
+  // per tile for the warp), then scattered to each of the token's local rows.
+  const int64_t n_tg = (n_tiles + kScaleTiles - 1) / kScaleTiles;
+  const int64_t n_items = ((T + 31) / 32) * n_tg;
+  for (int64_t it = gw; it < n_items; it += W) {
+    const int64_t c = it / n_tg;
+    const int64_t j0 = (it - c * n_tg) * kScaleTiles;
+    const int64_t gt = c * 32 + lane;
+    int32_t rows[16];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      rows[k] = (gt < T && k < K) ? __ldg(row_map + gt * K + k) : -1;
+      any |= rows[k] >= 0;
+    }
+    if (!__any_sync(0xffffffffu, any)) continue;
+    if (any) {
+      const int src_rank = static_cast<int>(gt / Tpr);
+      const uint8_t* s_src = static_cast<const uint8_t*>(peer.b[src_rank]) + (gt - src_rank * Tpr);
+      uint8_t v[kScaleTiles];
+#pragma unroll
+      for (int j = 0; j < kScaleTiles; ++j) v[j] = (j0 + j < n_tiles) ? s_src[(j0 + j) * ld_s_tok] : 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (rows[k] >= 0) {
+#pragma unroll
+          for (int j = 0; j < kScaleTiles; ++j)
+            if (j0 + j < n_tiles) s_out[(j0 + j) * max_rows + rows[k]] = v[j];
+        }
+      }
+    }
+  }
+
+  // ---- PAD rows: expert e from the last warp down
+  for (int64_t e = W - 1 - gw; e < E_loc; e += W) {
+    const int64_t lo = offsets[e], hi = offsets[e + 1];
+    for (int64_t r = hi - 1; r >= lo; --r) {
+      if (src_of_row[r] >= 0) break;
+      for (int64_t i = lane * 16; i < H; i += 32 * 16) st_v4(q_out + r * H + i, make_uint4(0, 0, 0, 0));
+      for (int64_t j = lane; j < n_tiles; j += 32) s_out[j * max_rows + r] = 0;
+    }
+  }
+
+  // ---- codes: one global token per warp item
+  const int64_t nvec = H / 16;
+  for (int64_t gt = gw; gt < T; gt += W) {
+    const int32_t my_row = lane < K ? __ldg(row_map + gt * K + lane) : -1;
+    const uint32_t valid = __ballot_sync(0xffffffffu, my_row >= 0);
+    if (valid == 0) continue;
+    const int src_rank = static_cast<int>(gt / Tpr);
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(peer.a[src_rank]) +
+                                                      (gt - src_rank * Tpr) * H);
+    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kCopyU) {
+      uint4 buf[kCopyU];
+#pragma unroll
+      for (int u = 0; u < kCopyU; ++u) {
+        const int64_t v = v0 + lane + 32 * u;
+        if (v < nvec) buf[u] = ld_nc_v4(src + v);
+      }
+      for (uint32_t m = valid; m != 0; m &= m - 1) {
+        const int k = __ffs(m) - 1;
+        const int32_t r = __shfl_sync(0xffffffffu, my_row, k);
+        uint4* dst = reinterpret_cast<uint4*>(q_out + static_cast<int64_t>(r) * H);
+#pragma unroll
+        for (int u = 0; u < kCopyU; ++u) {
+          const int64_t v = v0 + lane + 32 * u;
+          if (v < nvec) st_v4(dst + v, buf[u]);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s, int64_t ld_s_tok,
+                                        int32_t n, int64_t tokens_per_rank, int64_t hidden, const int32_t* row_map,
+                                        int32_t top_k, const int32_t* src_of_row, const int32_t* expert_offsets,
+                                        int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
+                                        cudaStream_t stream, int num_sms) {
+  PeerPtrs2 pp{};
+  for (int r = 0; r < n; ++r) {
+    pp.a[r] = peer_q[r];
+    pp.b[r] = peer_s[r];
+  }
+  static const int occ = occupancy_of(dispatch_permute_kernel, kEpThreads, 0);
+  const int64_t T = tokens_per_rank * n;
+  const int64_t need = (T + kEpWarps - 1) / kEpWarps;
+  const int64_t grid = one_wave_grid(occ, num_sms, need > num_local_experts ? need : num_local_experts);
+  dispatch_permute_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(
+      pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
+      max_rows, q_out, s_out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// combine + unpermute (owner side): warp per owned token; lane k resolves (rank, row, gate) of its
+// expert; column passes of 2 x 8 BF16 per lane, rows taken four at a time so 8 x 16 B loads per
+// lane are in flight, then acc = fmaf(p_k, x_k, acc) strictly in k order; BF16 RNE 128-bit stores.
+// ---------------------------------------------------------------------------------------------
+constexpr int kCombU = 2;   // 16-byte chunks per lane per pass
+constexpr int kCombKB = 8;  // rows loaded together
+
+__global__ void __launch_bounds__(kEpThreads) combine_kernel(PeerPtrs2 peer, int n, int64_t H,
+                                                             const int32_t* __restrict__ topk_idx, int E_per,
+                                                             const float* __restrict__ probs, int64_t token_begin,
+                                                             int64_t T, int K, __nv_bfloat16* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * kEpWarps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEpWarps + (threadIdx.x >> 5);
+  const int64_t nchunk = H / 8;
+  for (int64_t t = gw; t < T; t += W) {
+    // lane k: the expert's rank and row on that rank (a 4-byte load from the rank's plan)
+    const uint8_t* my_base = nullptr;
+    float my_p = 0.0f;
+    if (lane < K) {
+      const int e = __ldg(topk_idx + t * K + lane);
+      const int d = e / E_per;
+      if (e >= 0 && d < n) {
+        const int32_t r = static_cast<const int32_t*>(peer.b[d])[(token_begin + t) * K + lane];
+        if (r >= 0) {
+          my_base = static_cast<const uint8_t*>(peer.a[d]) + static_cast<int64_t>(r) * H * 2;
+          my_p = probs != nullptr ? __ldg(probs + t * K + lane) : 1.0f;
+        }
+      }
+    }
+    const uint32_t valid = __ballot_sync(0xffffffffu, my_base != nullptr);
+    const int nk = __popc(valid);
+    // compact the valid terms to lanes 0..nk-1, k order preserved
+    const int from = static_cast<int>(__fns(valid, 0, lane + 1)) & 31;
+    const uint64_t cb = __shfl_sync(0xffffffffu, reinterpret_cast<uint64_t>(my_base), from);
+    const float cp = __shfl_sync(0xffffffffu, my_p, from);
+    for (int64_t c0 = 0; c0 < nchunk; c0 += 32 * kCombU) {
+      float acc[kCombU][8];
+#pragma unroll
+      for (int u = 0; u < kCombU; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[u][j] = 0.0f;
+      for (int i0 = 0; i0 < nk; i0 += kCombKB) {
+        uint4 v[kCombKB][kCombU];
+        float p[kCombKB];
+#pragma unroll
+        for (int b = 0; b < kCombKB; ++b) {
+          const uint64_t base = __shfl_sync(0xffffffffu, cb, (i0 + b) & 31);
+          p[b] = __shfl_sync(0xffffffffu, cp, (i0 + b) & 31);
+#pragma unroll
+          for (int u = 0; u < kCombU; ++u) {
+            const int64_t c = c0 + lane + 32 * u;
+            if (i0 + b < nk && c < nchunk) v[b][u] = ld_nc_v4(reinterpret_cast<const uint8_t*>(base) + c * 16);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kCombKB; ++b) {
+          if (i0 + b < nk) {
+#pragma unroll
+            for (int u = 0; u < kCombU; ++u) {
+              const uint32_t w[4] = {v[b][u].x, v[b][u].y, v[b][u].z, v[b][u].w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                acc[u][2 * j] = __fmaf_rn(p[b], bf16lo_to_f32(w[j]), acc[u][2 * j]);
+                acc[u][2 * j + 1] = __fmaf_rn(p[b], bf16hi_to_f32(w[j]), acc[u][2 * j + 1]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCombU; ++u) {
+        const int64_t c = c0 + lane + 32 * u;
+        if (c < nchunk) {
+          uint32_t o[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 bb = __floats2bfloat162_rn(acc[u][2 * j], acc[u][2 * j + 1]);
+            o[j] = *reinterpret_cast<uint32_t*>(&bb);
+          }
+          st_v4(y + t * H + c * 8, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
+                                     int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank,
+                                     const float* probs, int64_t token_begin, int64_t num_tokens, int32_t top_k,
+                                     void* y, cudaStream_t stream, int num_sms) {
+  PeerPtrs2 pp{};
+  for (int r = 0; r < n; ++r) {
+    pp.a[r] = peer_x[r];
+    pp.b[r] = peer_row_map[r];
+  }
+  static const int occ = occupancy_of(combine_kernel, kEpThreads, 0);
+  const int64_t grid = one_wave_grid(occ, num_sms, (num_tokens + kEpWarps - 1) / kEpWarps);
+  combine_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(
+      pp, n, hidden, topk_idx, experts_per_rank, probs, token_begin, num_tokens, top_k,
+      static_cast<__nv_bfloat16*>(y));
+  return cudaGetLastError();
+}
+
+}  // namespace fp8flow

@@ -7,6 +7,8 @@
 
 namespace fp8flow {
 
+constexpr int kMaxRanks = 64;  // FP8FLOW_MAX_RANKS
+
 struct DeviceInfo {
   int device;
   int num_sms;
@@ -80,6 +82,20 @@ cudaError_t launch_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma,
 cudaError_t launch_swiglu_bwd_quant(const void* h, const void* dA, int64_t rows_max, const int32_t* rows_dev,
                                     int64_t ffn, uint8_t* q, uint8_t* s, int64_t ld_s, cudaStream_t stream,
                                     int num_sms);
+
+cudaError_t launch_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
+                               cudaStream_t stream, int num_sms);
+cudaError_t launch_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int32_t* status,
+                                uint32_t timeout_ms, cudaStream_t stream);
+cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s, int64_t ld_s_tok,
+                                        int32_t n, int64_t tokens_per_rank, int64_t hidden, const int32_t* row_map,
+                                        int32_t top_k, const int32_t* src_of_row, const int32_t* expert_offsets,
+                                        int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
+                                        cudaStream_t stream, int num_sms);
+cudaError_t launch_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
+                                     int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank,
+                                     const float* probs, int64_t token_begin, int64_t num_tokens, int32_t top_k,
+                                     void* y, cudaStream_t stream, int num_sms);
 
 cudaError_t launch_checksum64(const void* buf, int64_t nbytes, uint64_t* out, cudaStream_t stream, int num_sms);
 

@@ -47,7 +47,18 @@ SIGNATURES = {
     "fp8flow_swiglu_quant_dual": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
     "fp8flow_gemm_blockscaled": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _P, _I32, _P]),
     "fp8flow_gemm_wgrad": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _I32, _P, _I32, _P]),
+    "fp8flow_ipc_get_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    "fp8flow_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "fp8flow_ipc_close": (ctypes.c_int, [_P]),
+    "fp8flow_peer_barrier": (ctypes.c_int, [_P, _I32, _I32, _P, ctypes.c_uint32, _P]),
+    "fp8flow_peer_gather": (ctypes.c_int, [_P, _I32, _I64, _P, _P]),
+    "fp8flow_dispatch_permute_pad": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P, _I32, _P, _P, _I32, _I64,
+                                                    _P, _P, _P]),
+    "fp8flow_combine_unpermute": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _I32, _P, _I64, _I64, _I32, _P, _P]),
 }
+
+IPC_HANDLE_BYTES = 64
+MAX_RANKS = 64
 
 
 class Fp8FlowError(RuntimeError):
@@ -251,6 +262,72 @@ def fp8flow_checksum64(buf: torch.Tensor, out: torch.Tensor, stream=None) -> Non
     _check(lib().fp8flow_checksum64(_ptr(buf), buf.numel() * buf.element_size(), _ptr(out), _stream(stream)),
            "fp8flow_checksum64")
 
+
+# ----------------------------------------------------------------------------------- NEXT-3
+def _table(ptrs) -> ctypes.Array:
+    """Host array of device pointers (ints, or CUDA tensors whose data_ptr is taken)."""
+    vals = [p.data_ptr() if isinstance(p, torch.Tensor) else int(p) for p in ptrs]
+    return (ctypes.c_void_p * len(vals))(*vals)
+
+
+def fp8flow_ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, byte offset of t inside it)."""
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    off = ctypes.c_int64(0)
+    _check(lib().fp8flow_ipc_get_handle(_ptr(t), h, ctypes.byref(off)), "fp8flow_ipc_get_handle")
+    return h.raw, off.value
+
+
+def fp8flow_ipc_open(handle: bytes) -> int:
+    """Maps another process's allocation; returns its base device address in this process."""
+    base = ctypes.c_void_p(0)
+    buf = ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+    _check(lib().fp8flow_ipc_open(buf, ctypes.byref(base)), "fp8flow_ipc_open")
+    return int(base.value)
+
+
+def fp8flow_ipc_close(base: int) -> None:
+    _check(lib().fp8flow_ipc_close(ctypes.c_void_p(base)), "fp8flow_ipc_close")
+
+
+def fp8flow_peer_barrier(peer_signal, rank: int, status: torch.Tensor | None = None, timeout_ms: int = 10000,
+                         stream=None) -> None:
+    """peer_signal: n device pointers to the ranks' uint32 [n+1] signal buffers (zeroed once)."""
+    n = len(peer_signal)
+    _check(lib().fp8flow_peer_barrier(_table(peer_signal), rank, n, _ptr(status), timeout_ms, _stream(stream)),
+           "fp8flow_peer_barrier")
+
+
+def fp8flow_peer_gather(peer_src, bytes_per_rank: int, dst: torch.Tensor, stream=None) -> None:
+    n = len(peer_src)
+    _check(lib().fp8flow_peer_gather(_table(peer_src), n, bytes_per_rank, _ptr(dst), _stream(stream)),
+           "fp8flow_peer_gather")
+
+
+def fp8flow_dispatch_permute_pad(peer_q, peer_s, ld_s_tok: int, tokens_per_rank: int, hidden: int,
+                                 row_map: torch.Tensor, src_of_row: torch.Tensor, expert_offsets: torch.Tensor,
+                                 q_out: torch.Tensor, s_out: torch.Tensor, stream=None) -> None:
+    """peer_q / peer_s: n device pointers (or tensors) of the ranks' A1 outputs; row_map etc. from
+    fp8flow_permute_plan over the gathered topk_idx [n*tokens_per_rank, K]."""
+    n = len(peer_q)
+    assert len(peer_s) == n
+    _check(lib().fp8flow_dispatch_permute_pad(_table(peer_q), _table(peer_s), ld_s_tok, n, tokens_per_rank, hidden,
+                                              _ptr(row_map), row_map.shape[1], _ptr(src_of_row),
+                                              _ptr(expert_offsets), expert_offsets.numel() - 1, q_out.shape[0],
+                                              _ptr(_u8(q_out)), _ptr(_u8(s_out)), _stream(stream)),
+           "fp8flow_dispatch_permute_pad")
+
+
+def fp8flow_combine_unpermute(peer_x, peer_row_map, hidden: int, topk_idx: torch.Tensor, experts_per_rank: int,
+                              probs: torch.Tensor | None, token_begin: int, y: torch.Tensor, stream=None) -> None:
+    """peer_x: n device pointers to BF16 expert outputs; peer_row_map: n device pointers to the
+    ranks' plan row_maps; topk_idx/probs [T, K] of the caller's tokens; y bf16 [T, hidden]."""
+    n = len(peer_x)
+    assert y.dtype == torch.bfloat16
+    T, K = topk_idx.shape
+    _check(lib().fp8flow_combine_unpermute(_table(peer_x), _table(peer_row_map), n, hidden, _ptr(topk_idx),
+                                           experts_per_rank, _ptr(probs), token_begin, T, K, _ptr(y),
+                                           _stream(stream)), "fp8flow_combine_unpermute")
 
 # ----------------------------------------------------------------------------------- sizes
 def transpose_out_shapes(rows: int, cols: int, num_segs: int = 1):

@@ -75,6 +75,21 @@ def swiglu_quant_dual_bytes(seg_lengths, ffn: int) -> int:
     return m * (4 * ffn + ffn + ffn) + m * (ffn // 128) + blocks * ffn
 
 
+def dispatch_permute_bytes(unique_recv_tokens: int, padded_rows: int, total_tokens: int, top_k: int,
+                           hidden: int) -> int:
+    """NEXT-3 dispatch + permute (receive side): every routed token's codes + scales read once from
+    its owner (NVLink on the 8-GPU box, HBM when the ranks share a device), every local row (incl.
+    PAD) written once, the global plan's row_map read."""
+    row = hidden + hidden // 128
+    return unique_recv_tokens * row + padded_rows * row + total_tokens * top_k * 4
+
+
+def combine_bytes(num_tokens: int, top_k: int, hidden: int, with_probs: bool = True) -> int:
+    """NEXT-3 combine: top_k BF16 expert rows pulled per owned token, the BF16 output written,
+    topk_idx + the experts' row_map entries (+ gates) read."""
+    return num_tokens * top_k * hidden * 2 + num_tokens * hidden * 2 + num_tokens * top_k * (8 + (4 if with_probs else 0))
+
+
 def measured_peaks(root: str) -> dict:
     """HBM copy bandwidth to use as the roofline denominator: the driver-measured figure when
     MEASURED_PEAKS.json exists, else the profiling guide's fallback (6650 GB/s)."""

@@ -74,6 +74,13 @@ def activations_bf16_device(rows: int, cols: int, seed: int, device, outlier_fra
     return (z.mul_(gain).mul_(ch)).to(torch.bfloat16)
 
 
+def normal_bf16_device(rows: int, cols: int, seed: int, device, sigma: float = 1.0) -> torch.Tensor:
+    """N(0, sigma^2) in BF16 drawn on the device (Philox) for large bench-only buffers."""
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) & 0xFFFFFFFFFFFFFFFF)
+    return (torch.randn(rows, cols, generator=g, device=device, dtype=torch.float32) * sigma).to(torch.bfloat16)
+
+
 def normal_bf16(rows: int, cols: int, seed: int, sigma: float = 1.0) -> torch.Tensor:
     g = _gen(seed)
     return (torch.randn(rows, cols, generator=g, dtype=torch.float32) * sigma).to(torch.bfloat16)

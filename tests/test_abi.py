@@ -115,6 +115,41 @@ def test_validation_of_next_row_entry_points(L):
     assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, None, 4, a16, 1, None) == 1
 
 
+def test_validation_of_next3_entry_points(L):
+    """NEXT-3 peer-memory entry points reject bad arguments synchronously (no device touched)."""
+    P = ctypes.c_void_p
+    a16 = P(16)
+    tab2 = (P * 2)(16, 32)
+    tab_null = (P * 2)(16, None)
+    tab_mis = (P * 2)(16, 40)
+    # IPC helpers: NULL arguments
+    assert L.fp8flow_ipc_get_handle(None, None, None) == 1
+    assert L.fp8flow_ipc_open(None, None) == 1
+    assert L.fp8flow_ipc_close(None) == 1
+    # barrier: rank outside [0, n), n outside [1, 64], NULL table / entry
+    assert L.fp8flow_peer_barrier(tab2, 2, 2, None, 100, None) == 4
+    assert L.fp8flow_peer_barrier(tab2, 0, 65, None, 100, None) == 4
+    assert L.fp8flow_peer_barrier(None, 0, 2, None, 100, None) == 1
+    assert L.fp8flow_peer_barrier(tab_null, 0, 2, None, 100, None) == 1
+    # gather: bytes % 16, empty no-op, misaligned peer
+    assert L.fp8flow_peer_gather(tab2, 2, 24, a16, None) == 2
+    assert L.fp8flow_peer_gather(tab2, 2, 0, None, None) == 0
+    assert L.fp8flow_peer_gather(tab_mis, 2, 32, a16, None) == 3
+    # dispatch: top_k, hidden % 128, ld_s < tokens, NULL plan
+    assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 7168, a16, 17, a16, a16, 32, 1024, a16, a16,
+                                          None) == 4
+    assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 100, a16, 8, a16, a16, 32, 1024, a16, a16,
+                                          None) == 2
+    assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 32, 2, 64, 7168, a16, 8, a16, a16, 32, 1024, a16, a16,
+                                          None) == 2
+    assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 7168, None, 8, a16, a16, 32, 1024, a16, a16,
+                                          None) == 1
+    # combine: experts_per_rank, hidden % 8, empty no-op, NULL peer entry
+    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7168, a16, 0, None, 0, 4, 8, a16, None) == 4
+    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7164, a16, 32, None, 0, 4, 8, a16, None) == 2
+    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7168, a16, 32, None, 0, 0, 8, a16, None) == 0
+    assert L.fp8flow_combine_unpermute(tab_null, tab2, 2, 7168, a16, 32, None, 0, 4, 8, a16, None) == 1
+
 def test_no_device_means_error_not_fallback(L):
     import torch
 

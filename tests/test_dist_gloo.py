@@ -90,3 +90,61 @@ def test_expert_shard_is_what_dispatch_would_deliver(group):
     # every token's experts are distinct (precondition of the plan) and routing is group-limited
     assert all(len(set(r)) == 8 for r in idx.numpy()[:200])
     assert all(len({e // 32 for e in r}) <= 4 for r in idx.numpy()[:200])
+
+
+# ------------------------------------------------------------------ NEXT-3 peer-table plumbing
+def _ep_worker(rank, world, port, q):
+    """The IpcPeers exchange with fake handles: every rank publishes {name: (handle, offset)} over
+    gloo's all_gather_object and resolves the peer table with a recording open function."""
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch.distributed as dist
+
+    from paper_2511_02302_b200 import ep
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # names q and s live in one allocation (same handle, different offsets), x in another
+    mine = {"q": (b"A%d" % rank, 0), "s": (b"A%d" % rank, 4096), "x": (b"B%d" % rank, 64)}
+    records = [None] * world
+    dist.all_gather_object(records, mine)
+    opened = []
+
+    def fake_open(h):
+        opened.append(h)
+        return 1_000_000 * (1 + int(h[1:])) + (0 if h[:1] == b"A" else 500_000)
+
+    local = {"q": 11, "s": 22, "x": 33}
+    tables, bases = ep.resolve_tables(records, rank, local, fake_open)
+    dist.destroy_process_group()
+    q.put((rank, tables, sorted(opened), sorted(bases)))
+
+
+def test_two_rank_gloo_peer_table_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, t0, o0, b0), (r1, t1, o1, b1) = out
+    # own entries are local pointers; peers' = opened base + the exporter's offset
+    assert t0 == {"q": [11, 2_000_000], "s": [22, 2_004_096], "x": [33, 2_500_064]}
+    assert t1 == {"q": [1_000_000, 11], "s": [1_004_096, 22], "x": [1_500_064, 33]}
+    assert o0 == [b"A1", b"B1"] and o1 == [b"A0", b"B0"]          # each distinct handle opened once
+    assert b0 == [2_000_000, 2_500_000] and b1 == [1_000_000, 1_500_000]
+
+
+def test_expert_and_token_ranges():
+    from paper_2511_02302_b200 import ep
+
+    assert [ep.expert_range(r, 8, 256) for r in (0, 7)] == [(0, 32), (224, 32)]
+    assert ep.token_range(3, 2048) == (6144, 8192)
+    with pytest.raises(ValueError):
+        ep.expert_range(0, 3, 256)
+    from paper_2511_02302_b200 import roofline as RL
+
+    assert RL.dispatch_permute_bytes(10, 32, 100, 8, 256) == 10 * 258 + 32 * 258 + 100 * 8 * 4
+    assert RL.combine_bytes(4, 8, 128, True) == 4 * 8 * 256 + 4 * 256 + 4 * 8 * 12
