@@ -18,7 +18,10 @@
 //    buffer pair as in P:347.
 //  * peer pointers travel by value in the kernel parameters (<= 64 ranks), so every launch is
 //    CUDA-graph capturable; the barrier keeps its epoch on the device.
-//  * plain 128-bit loads/stores (ld.global.nc) rather than bulk copies: valid on any peer mapping.
+//  * the dispatch pulls whole tokens with 1D bulk copies (cp.async.bulk global -> shared, peer VA
+//    through UVA) and writes rows with bulk stores; the combine and the LSU dispatch variant use
+//    plain 128-bit non-coherent loads.
+#include "async.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -131,7 +134,7 @@ cudaError_t launch_peer_barrier(void* const* peer_signal, int32_t rank, int32_t 
 //   PAD   : per local expert, the trailing PAD rows (src_of_row < 0) get code 0x00 and scale 0x00.
 // Scale and PAD items are taken by the grid's first and last warps; code items by all warps.
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kEpThreads) dispatch_permute_kernel(
+__global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
     PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
     const int32_t* __restrict__ src_of_row, const int32_t* __restrict__ offsets, int E_loc, int64_t max_rows,
     uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out) {
@@ -215,6 +218,133 @@ __global__ void __launch_bounds__(kEpThreads) dispatch_permute_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// dispatch + permute + pad on the bulk-copy engine (default).  Two CTAs per SM; CTA c owns global
+// tokens c, c+G, c+2G, ...
+//   1. all warps compact the CTA's routed tokens (row_map read 32 tokens at a time, ballot, one
+//      shared atomic per batch) into a shared list {token, its top_k rows};
+//   2. warp 0 / lane 0 streams the list through a ring of token slots: a 1D bulk copy pulls a
+//      token's H code bytes from its owner into a slot (mbarrier-completed, `lead` tokens ahead),
+//      then one 1D bulk store per local row writes it out (one bulk group per token; a slot is
+//      refilled once its stores have read it) -- up to ~25 tokens (180 KB) in flight per SM with
+//      no register staging and no per-16-byte LSU instructions;
+//   3. warps 1-7 meanwhile gather the scale bytes row by row over the CTA's share of the output
+//      rows (coalesced stores; PAD rows 0x00), then zero the PAD rows' codes (32-row chunks).
+// ---------------------------------------------------------------------------------------------
+constexpr int kDispMaxSlots = 32;
+constexpr int kDispStoreSlack = 4;
+constexpr size_t kDispSmemBudget = 220 * 1024;
+constexpr int kDispListStride = 17;  // token id + up to 16 rows
+
+__global__ void __launch_bounds__(256) dispatch_engine_kernel(
+    PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
+    const int32_t* __restrict__ src_of_row, const int32_t* __restrict__ offsets, int E_loc, int64_t max_rows,
+    uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out, int nslots, int list_cap) {
+  extern __shared__ __align__(128) uint8_t smem_disp[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_disp);
+  int32_t* list_n = reinterpret_cast<int32_t*>(full + kDispMaxSlots);
+  int32_t* list = list_n + 4;
+  uint8_t* slots = smem_disp + ((8 * kDispMaxSlots + 16 + 4 * static_cast<int64_t>(list_cap) * kDispListStride + 127) / 128) * 128;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G = gridDim.x, cta = blockIdx.x;
+  const int64_t T = Tpr * n;
+  const int64_t n_tiles = H / 128;
+
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) mbar_init(&full[i], 1);
+    mbar_init_fence();
+    *list_n = 0;
+  }
+  __syncthreads();
+  // every warp compacts 32-token batches (warp w: batches w, w+8, ...); list order is irrelevant
+  // to the result (each row's content is fixed by row_map), so slots are taken with one shared
+  // atomic per batch
+  for (int64_t i0 = static_cast<int64_t>(warp) * 32; cta + i0 * G < T; i0 += 32 * 8) {
+    const int64_t gt = cta + (i0 + lane) * G;
+    int32_t rows[16];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      rows[k] = (gt < T && k < K) ? __ldg(row_map + gt * K + k) : -1;
+      any |= rows[k] >= 0;
+    }
+    const uint32_t mask = __ballot_sync(0xffffffffu, any);
+    int base = 0;
+    if (lane == 0 && mask != 0) base = atomicAdd(list_n, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (any) {
+      int32_t* e = list + (base + __popc(mask & ((1u << lane) - 1u))) * kDispListStride;
+      e[0] = static_cast<int32_t>(gt);
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k < K) e[1 + k] = rows[k];
+    }
+  }
+  __syncthreads();
+  const int N = *list_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int lead = nslots - kDispStoreSlack;
+      uint32_t phase_bits = 0;
+      for (int nn = 0; nn < N + lead; ++nn) {
+        const int m = nn - lead;
+        if (m >= 0) {  // store stage: token m is in slot m % nslots
+          const int slot = m % nslots;
+          mbar_wait(&full[slot], (phase_bits >> slot) & 1u);
+          phase_bits ^= 1u << slot;
+          const int32_t* e = list + m * kDispListStride;
+          for (int k = 0; k < K; ++k)
+            if (e[1 + k] >= 0)
+              bulk_store_1d(q_out + static_cast<int64_t>(e[1 + k]) * H, slots + static_cast<int64_t>(slot) * H,
+                            static_cast<uint32_t>(H));
+          bulk_commit();
+        }
+        if (nn < N) {  // load stage
+          const int slot = nn % nslots;
+          if (nn >= nslots) bulk_wait_read<kDispStoreSlack>();  // token nn - nslots's stores have read it
+          const int64_t gt = list[nn * kDispListStride];
+          const int src_rank = static_cast<int>(gt / Tpr);
+          mbar_expect_tx(&full[slot], static_cast<uint32_t>(H));
+          bulk_load_1d(slots + static_cast<int64_t>(slot) * H,
+                       static_cast<const uint8_t*>(peer.a[src_rank]) + (gt - src_rank * Tpr) * H,
+                       static_cast<uint32_t>(H), &full[slot]);
+        }
+      }
+      bulk_wait_all();
+    }
+  } else {
+    // scales, row-major like A3's move: the CTA's contiguous share of the output rows, (row, tile)
+    // pairs with consecutive threads on consecutive rows (coalesced stores); a row's byte comes
+    // from its source token's owner (src_of_row holds the global token id), PAD rows get 0x00
+    const int64_t R_all = offsets[E_loc];
+    const int64_t rb = cta * R_all / G;
+    const int nr = static_cast<int>((cta + 1) * R_all / G - rb);
+    const int tpr = static_cast<int>(Tpr);
+    for (int p = tid - 32; p < nr * static_cast<int>(n_tiles); p += 224) {
+      const int tl = p / nr;
+      const int64_t r = rb + (p - tl * nr);
+      const int32_t src = __ldg(src_of_row + r);
+      uint8_t v = 0;
+      if (src >= 0) {
+        const int src_rank = src / tpr;
+        v = __ldg(static_cast<const uint8_t*>(peer.b[src_rank]) + static_cast<int64_t>(tl) * ld_s_tok + (src - src_rank * tpr));
+      }
+      s_out[static_cast<int64_t>(tl) * max_rows + r] = v;
+    }
+    // PAD rows: 32-row chunks over the grid's warps 1..7
+    const int64_t R = offsets[E_loc];
+    for (int64_t c = cta * 7 + (warp - 1); c * 32 < R; c += G * 7) {
+      const int64_t r0 = c * 32;
+      const bool pad = r0 + lane < R && src_of_row[r0 + lane] < 0;
+      for (uint32_t msk = __ballot_sync(0xffffffffu, pad); msk != 0; msk &= msk - 1) {
+        const int64_t r = r0 + __ffs(msk) - 1;
+        for (int64_t i = lane * 16; i < H; i += 32 * 16) st_v4(q_out + r * H + i, make_uint4(0, 0, 0, 0));
+      }
+    }
+  }
+}
+
 cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s, int64_t ld_s_tok,
                                         int32_t n, int64_t tokens_per_rank, int64_t hidden, const int32_t* row_map,
                                         int32_t top_k, const int32_t* src_of_row, const int32_t* expert_offsets,
@@ -225,13 +355,37 @@ cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint
     pp.a[r] = peer_q[r];
     pp.b[r] = peer_s[r];
   }
-  static const int occ = occupancy_of(dispatch_permute_kernel, kEpThreads, 0);
   const int64_t T = tokens_per_rank * n;
-  const int64_t need = (T + kEpWarps - 1) / kEpWarps;
-  const int64_t grid = one_wave_grid(occ, num_sms, need > num_local_experts ? need : num_local_experts);
-  dispatch_permute_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(
+  if (tune_int("EP_DISPATCH_LSU", 0)) {  // register-copy variant, kept for comparison
+    static const int occ = occupancy_of(dispatch_permute_lsu_kernel, kEpThreads, 0);
+    const int64_t need = (T + kEpWarps - 1) / kEpWarps;
+    const int64_t grid = one_wave_grid(occ, num_sms, need > num_local_experts ? need : num_local_experts);
+    dispatch_permute_lsu_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(
+        pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
+        max_rows, q_out, s_out);
+    return cudaGetLastError();
+  }
+  // CTAS_PER_SM_DISP co-resident CTAs per SM (smem budget split); more CTAs (queued) when a CTA
+  // would own more than 256 tokens
+  const int ctas = tune_int("CTAS_PER_SM_DISP", 2) > 0 ? tune_int("CTAS_PER_SM_DISP", 2) : 1;
+  const size_t budget = kDispSmemBudget / ctas;
+  int64_t grid = static_cast<int64_t>(num_sms) * ctas;
+  if ((T + grid - 1) / grid > 256) grid = (T + 255) / 256;
+  const int list_cap = static_cast<int>((T + grid - 1) / grid);
+  const size_t head = ((8 * kDispMaxSlots + 16 + 4 * static_cast<size_t>(list_cap) * kDispListStride + 127) / 128) * 128;
+  if (head + static_cast<size_t>(hidden) * (kDispStoreSlack + 2) > budget) return cudaErrorInvalidValue;
+  int nslots = static_cast<int>((budget - head) / hidden);
+  if (nslots > kDispMaxSlots) nslots = kDispMaxSlots;
+  const size_t smem = head + static_cast<size_t>(hidden) * nslots;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dispatch_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kDispSmemBudget));
+    attr = true;
+  }
+  dispatch_engine_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
       pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
-      max_rows, q_out, s_out);
+      max_rows, q_out, s_out, nslots, list_cap);
   return cudaGetLastError();
 }
 
