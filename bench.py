@@ -507,13 +507,10 @@ def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20) -> dict:
     return out
 
 
-def ep_measure(device, peak: float, reps: int = 20) -> dict:
-    """NEXT-3 on one GPU: the 8 expert-parallel ranks of the DeepSeek-V3 layer (2048 tokens each,
-    16384 in all, top-8 of 256 experts, 32 per rank) held as virtual ranks on this device, so the
-    peer reads are HBM reads here (NVLink reads on the 8-GPU box).  Times rank 0's receive side
-    (dispatch + fused permute/pad kernel alone, and with the routing gather + plan) and its BF16
-    combine over the 8 ranks' expert outputs; outputs are checked against A3 / A4 on the
-    concatenation (both oracle-parity-tested)."""
+def ep_setup(device) -> dict:
+    """NEXT-3 state on one GPU: the 8 expert-parallel ranks of the DeepSeek-V3 layer (2048 tokens
+    each, 16384 in all, top-8 of 256 experts, 32 per rank) held as virtual ranks on this device:
+    their A1 outputs and routing, every rank's plan and dispatched rows, BF16 expert outputs."""
     from paper_2511_02302_b200 import ep
     from paper_2511_02302_b200 import fp8flow as F
 
@@ -564,6 +561,18 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
         ranks[g]["row_map"] = plans[g]["row_map"]
     peers = ep.LocalPeers(ranks)
     y = torch.empty(tpr, HIDDEN, dtype=torch.bfloat16, device=device)
+    return dict(F=F, ep=ep, n=n, tpr=tpr, E=E, ranks=ranks, plans=plans, peers=peers, receive=receive, y=y)
+
+
+def ep_measure(device, peak: float, reps: int = 20) -> dict:
+    """NEXT-3 on one GPU (ep_setup's virtual ranks, so the peer reads are HBM reads here and NVLink
+    reads on the 8-GPU box).  Times rank 0's receive side (dispatch + fused permute/pad kernel
+    alone, and with the routing gather + plan) and its BF16 combine over the 8 ranks' expert
+    outputs; outputs are checked against A3 / A4 on the concatenation (both oracle-parity-tested)."""
+    st = ep_setup(device)
+    F, ep, n, tpr, E = st["F"], st["ep"], st["n"], st["tpr"], st["E"]
+    ranks, plans, peers, receive, y = st["ranks"], st["plans"], st["peers"], st["receive"], st["y"]
+    i32 = torch.int32
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 

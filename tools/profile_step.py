@@ -1,6 +1,6 @@
 """Profiling driver (not product): warms up bench.py's step, then runs ONE serial pass of the
-step's 9 launches plus the NEXT-row kernels (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM
-on a 2048-row slice) between cudaProfilerStart/Stop, so that
+step's 9 launches plus the NEXT-row kernels (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM,
+NEXT-3 dispatch and combine of rank 0 of 8 virtual EP ranks) between cudaProfilerStart/Stop, so that
     ncu --set full --profile-from-start off ... python tools/profile_step.py
 captures exactly one launch of each kernel, in this order."""
 import os
@@ -15,7 +15,7 @@ import synth  # noqa: E402
 
 ORDER = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
          "A2_transpose_xperm", "A2_transpose_a", "NEXT1_swiglu_bwd_quant", "NEXT1_swiglu_quant_dual",
-         "NEXT2_gemm_fc1_fprop"]
+         "NEXT2_gemm_fc1_fprop", "NEXT3_dispatch_permute_pad", "NEXT3_combine_unpermute"]
 
 
 def main():
@@ -33,10 +33,15 @@ def main():
     Dg = torch.empty(hw.R, 2 * bench.FFN, dtype=torch.bfloat16, device=dev)
     rows_dev = ds.off[E:]
 
+    st = bench.ep_setup(dev)  # NEXT-3: 8 virtual EP ranks on this device
+
     def extra():
         F.fp8flow_swiglu_bwd_quant(ds.h, dA, qb, sbw, rows_dev=rows_dev)
         F.fp8flow_swiglu_quant_dual(ds.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off)
         F.fp8flow_gemm_blockscaled(ds.x_perm, ds.s_perm, W, sW, Dg, seg_offsets=ds.off)
+        st["receive"](0, kernel_only=True)
+        st["ep"].combine(st["peers"], 0, st["tpr"], bench.HIDDEN, st["E"], st["ranks"][0]["topk"],
+                         st["ranks"][0]["probs"], st["y"])
 
     for _ in range(3):
         ds.launch_ops(record=False)
