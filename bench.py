@@ -574,13 +574,15 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
     ranks, plans, peers, receive, y = st["ranks"], st["plans"], st["peers"], st["receive"], st["y"]
     i32 = torch.int32
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
     def med(fn):
         fn()
         ts = []
         for _ in range(reps):
-            flush.fill_(1)
+            flush.fill_(1)      # evict, then read clean unrelated lines: no dirty write-back is
+            clean.sum()         # left for the timed kernel to pay (as DeviceStep.flush_l2)
             torch.cuda._sleep(1_000_000)
             ev[0].record()
             fn()
