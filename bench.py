@@ -629,6 +629,108 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
                                                with_gather_and_plan_us=round(ms_all * 1e3, 2), note=note),
             "NEXT3_combine_unpermute": line(ms_c, nb_c, rank=0, tokens=tpr, parity=ok_c, note=note)}
 
+def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) -> dict:
+    """NEXT-3 across the job's ranks (one process per GPU: peer reads cross NVLink on the 8-GPU box;
+    with FP8FLOW_DIST_BACKEND=gloo several ranks share one GPU through CUDA IPC).  Weak scaling:
+    2048 tokens per rank, 256 experts split evenly.  Times every rank's fused dispatch + permute/pad
+    kernel and its combine (max over ranks) after host barriers; checks rank r's dispatch against A3
+    on the all-gathered tokens and its combine against A4 on the all-gathered expert outputs.
+    Collective: a handle exchange and the checks' all-gathers, all outside the timed kernels."""
+    from paper_2511_02302_b200 import ep
+    from paper_2511_02302_b200 import fp8flow as F
+
+    tpr, E = T_GLOBAL // D.NUM_GROUPS, N_EXPERTS
+    T = tpr * world
+    e0, per = ep.expert_range(rank, world, E)
+    idx, probs = synth.routing(T, synth.BASE_SEED)
+    x = synth.activations_bf16_device(tpr, HIDDEN, synth.BASE_SEED + 100 + rank, device)
+    q = torch.empty(tpr, HIDDEN, dtype=torch.uint8, device=device)
+    s_ = torch.empty(HIDDEN // 128, tpr, dtype=torch.uint8, device=device)
+    F.fp8flow_quantize_rowwise(x, q, s_)
+    del x
+    topk = idx[rank * tpr:(rank + 1) * tpr].contiguous().to(device)
+    pr = probs[rank * tpr:(rank + 1) * tpr].contiguous().to(device)
+    mr = F.permute_max_rows(T, TOP_K, per)
+    i32 = torch.int32
+    topk_all = torch.empty(T, TOP_K, dtype=i32, device=device)
+    row_map = torch.empty(T, TOP_K, dtype=i32, device=device)
+    src = torch.empty(mr, dtype=i32, device=device)
+    off = torch.empty(per + 1, dtype=i32, device=device)
+    ws = torch.empty(F.fp8flow_permute_workspace_bytes(T, TOP_K, per), dtype=torch.uint8, device=device)
+    q_out = torch.empty(mr, HIDDEN, dtype=torch.uint8, device=device)
+    s_out = torch.empty(HIDDEN // 128, mr, dtype=torch.uint8, device=device)
+    xo = synth.normal_bf16_device(mr, HIDDEN, synth.BASE_SEED + 200 + rank, device)
+    y = torch.empty(tpr, HIDDEN, dtype=torch.bfloat16, device=device)
+    torch.cuda.synchronize(device)
+    peers = ep.IpcPeers({"q": q, "s": s_, "topk": topk, "x": xo, "row_map": row_map})
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps + 1):
+            flush.fill_(1)
+            clean.sum()
+            torch.cuda.synchronize(device)
+            D.barrier(device)               # every rank's inputs complete before any peer reads
+            ev[0].record()
+            fn()
+            ev[1].record()
+            ev[1].synchronize()
+            D.barrier(device)               # no rank overwrites what a peer may still read
+            ts.append(ev[0].elapsed_time(ev[1]))
+        return D.max_over_ranks(statistics.median(ts[1:]), device)
+
+    # plan once (the dispatch kernel then re-runs on the same plan)
+    ep.dispatch_permute(peers, rank, tpr, HIDDEN, TOP_K, E, tpr, topk_all, row_map, src, off, ws, q_out, s_out)
+    torch.cuda.synchronize(device)
+    ms_plan_disp = timed(lambda: ep.dispatch_permute(peers, rank, tpr, HIDDEN, TOP_K, E, tpr, topk_all, row_map,
+                                                     src, off, ws, q_out, s_out))
+    ms_disp = timed(lambda: F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), tpr, tpr, HIDDEN,
+                                                           row_map, src, off, q_out, s_out))
+    ms_comb = timed(lambda: ep.combine(peers, rank, tpr, HIDDEN, E, topk, pr, y))
+    # checks (outside the timing): gather every rank's tokens / expert outputs / plans
+    gq = [torch.empty_like(q) for _ in range(world)]
+    gs = [torch.empty_like(s_) for _ in range(world)]
+    gx = [torch.empty_like(xo) for _ in range(world)]
+    gr = [torch.empty_like(row_map) for _ in range(world)]
+    cdev = torch.device("cpu") if D.dist.get_backend() == "gloo" else device
+    for lst, t in ((gq, q), (gs, s_), (gx, xo), (gr, row_map)):
+        buf = [b.to(cdev) for b in lst]
+        D.dist.all_gather(buf, t.to(cdev))
+        for i in range(world):
+            lst[i].copy_(buf[i])
+    R = int(off[-1].item())
+    ref_q, ref_s = torch.empty_like(q_out), torch.empty_like(s_out)
+    F.fp8flow_permute_pad(torch.cat(gq), torch.cat(gs, dim=1).contiguous(), src, off, ref_q, ref_s)
+    rm_glob = torch.full((tpr, TOP_K), -1, dtype=i32, device=device)
+    for g in range(world):
+        rmg = gr[g][rank * tpr:(rank + 1) * tpr]
+        rm_glob = torch.where(rmg >= 0, rmg + g * mr, rm_glob)
+    y_ref = torch.empty_like(y)
+    F.fp8flow_unpermute_unpad(torch.cat(gx), rm_glob.contiguous(), pr, y_ref)
+    torch.cuda.synchronize(device)
+    ok_d = bool(torch.equal(ref_q[:R], q_out[:R]) and torch.equal(ref_s[:, :R], s_out[:, :R]))
+    ok_c = bool(torch.equal(y.view(torch.int16), y_ref.view(torch.int16)))
+    ok = D.sum_over_ranks(float(ok_d and ok_c), device) == world
+    uniq = int(np.count_nonzero((row_map.cpu().numpy() >= 0).any(axis=1)))
+    nb_d = D.sum_over_ranks(RL.dispatch_permute_bytes(uniq, R, T, TOP_K, HIDDEN), device)
+    nb_c = D.sum_over_ranks(RL.combine_bytes(tpr, TOP_K, HIDDEN, True), device)
+    D.barrier(device)
+    peers.close()
+
+    def line(ms, nb, **kw):
+        return {"us": round(ms * 1e3, 2), "bytes_all_ranks": int(nb), "gbs_all_ranks": round(nb / ms / 1e6, 1),
+                "gbs_per_gpu": round(nb / ms / 1e6 / world, 1), **kw}
+
+    shared = D.dist.get_backend() == "gloo"
+    note = (f"{world} ranks, one process per {'rank, all sharing one GPU (time-sliced contexts: not a link or HBM measurement)' if shared else 'GPU'} "
+            f"(CUDA IPC peer tables); time = max over ranks; {tpr} tokens per rank, {per} experts per rank")
+    return {"NEXT3_dispatch_permute_pad": line(ms_disp, nb_d, with_gather_and_plan_us=round(ms_plan_disp * 1e3, 2),
+                                               note=note),
+            "NEXT3_combine_unpermute": line(ms_comb, nb_c, note=note), "parity": ok}
+
 def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
     """NEXT-2: the block-scaled FP8 grouped GEMMs that consume the step's outputs directly -- fc1
     Fprop on A3's X_perm (FP8 codes + 1x128 scales, 32 expert groups) and fc2 Fprop on A5's A --
@@ -803,6 +905,7 @@ def main():
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ep", action="store_true", help="skip the N>1 NEXT-3 dispatch/combine measurement")
     ap.add_argument("--sweep", action="store_true", help="config 5: transpose vs naive bandwidth sweep (one JSON line)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
@@ -891,6 +994,12 @@ def main():
 
     parity = None if args.no_verify else verify(ds)
     sums = D.gather_checksums(ds.checksums(), device)
+    next3_dist = None
+    if world > 1 and not args.no_ep:
+        try:
+            next3_dist = ep_measure_dist(device, peak, rank, world)
+        except Exception as e:  # noqa: BLE001 -- reported in the line, never fatal to the headline
+            next3_dist = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -922,6 +1031,8 @@ def main():
         if world == 1:
             line["cfg2"] = cfg2_measure(device, peak)
             line["next_ops"] = next_ops_measure(ds, peak)
+        if next3_dist is not None:
+            line["next3_multi_rank"] = next3_dist
         print(json.dumps(line), flush=True)
     D.barrier(device)
     if D.dist.is_initialized():
