@@ -662,7 +662,17 @@ def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) 
     xo = synth.normal_bf16_device(mr, HIDDEN, synth.BASE_SEED + 200 + rank, device)
     y = torch.empty(tpr, HIDDEN, dtype=torch.bfloat16, device=device)
     torch.cuda.synchronize(device)
-    peers = ep.IpcPeers({"q": q, "s": s_, "topk": topk, "x": xo, "row_map": row_map})
+    # the one step that can fail on a new machine (IPC / peer access): every rank agrees before any
+    # rank enters the barriers of the timed loop, so a failure cannot leave ranks waiting
+    err = None
+    try:
+        peers = ep.IpcPeers({"q": q, "s": s_, "topk": topk, "x": xo, "row_map": row_map})
+    except Exception as e:  # noqa: BLE001
+        peers, err = None, f"rank {rank}: {type(e).__name__}: {e}"[:300]
+    if D.sum_over_ranks(0.0 if err is None else 1.0, device) > 0:
+        if peers is not None:
+            peers.close()   # nothing has read through the mappings yet
+        return {"error": err or "peer mapping failed on another rank"}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]

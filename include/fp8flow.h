@@ -311,7 +311,10 @@ FP8FLOW_API int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int6
  *   row_map, src_of_row, expert_offsets: from fp8flow_permute_plan over the GATHERED topk_idx
  *             [n*tokens_per_rank][top_k] with this rank's expert range (global token ids)
  *   q_out [max_rows][hidden], s_out [hidden/128][max_rows] (rows >= expert_offsets[E_loc] untouched)
- *   hidden % 128 == 0, q pointers 16-byte aligned, 1 <= top_k <= 16, ld_s_tok >= tokens_per_rank. */
+ *   hidden % 128 == 0, q pointers 16-byte aligned, 1 <= top_k <= 16, ld_s_tok >= tokens_per_rank.
+ *   Kernel choice (same result): when every peer_q lives on the calling device, a bulk-copy engine
+ *   (cp.async.bulk token pulls into shared memory, bulk stores per row); when any lives on another
+ *   device, register copies with plain 128-bit loads (valid on every peer mapping). */
 FP8FLOW_API int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s,
                                              int64_t ld_s_tok, int32_t n, int64_t tokens_per_rank, int64_t hidden,
                                              const int32_t* row_map, int32_t top_k, const int32_t* src_of_row,

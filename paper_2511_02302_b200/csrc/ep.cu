@@ -356,7 +356,26 @@ cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint
     pp.b[r] = peer_s[r];
   }
   const int64_t T = tokens_per_rank * n;
-  if (tune_int("EP_DISPATCH_LSU", 0)) {  // register-copy variant, kept for comparison
+  // The bulk-copy engine reads peers with cp.async.bulk; that is verified only for buffers on the
+  // calling device (virtual ranks, processes sharing a GPU).  When any peer's codes live on another
+  // device (NVLink), the register-copy kernel -- plain 128-bit loads, valid on every peer
+  // mapping -- is used instead.  FP8FLOW_EP_DISPATCH_LSU=1 forces it, =0 forces the engine.
+  const int force = tune_int("EP_DISPATCH_LSU", 2);
+  bool remote = false;
+  if (force == 2) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (int r = 0; r < n && !remote; ++r) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, peer_q[r]) != cudaSuccess) {
+        cudaGetLastError();
+        remote = true;  // unknown mapping: take the path that is valid everywhere
+      } else if (a.device != dev) {
+        remote = true;
+      }
+    }
+  }
+  if (force == 1 || (force == 2 && remote)) {
     static const int occ = occupancy_of(dispatch_permute_lsu_kernel, kEpThreads, 0);
     const int64_t need = (T + kEpWarps - 1) / kEpWarps;
     const int64_t grid = one_wave_grid(occ, num_sms, need > num_local_experts ? need : num_local_experts);

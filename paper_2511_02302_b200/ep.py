@@ -63,9 +63,15 @@ class IpcPeers:
     def __init__(self, buffers: dict[str, torch.Tensor], group=None):
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        mine = {name: F.fp8flow_ipc_get_handle(t) for name, t in buffers.items()}
+        try:
+            mine = {name: F.fp8flow_ipc_get_handle(t) for name, t in buffers.items()}
+        except F.Fp8FlowError:
+            mine = None  # still join the collective, so no rank is left waiting in it
         records: list = [None] * self.world
         dist.all_gather_object(records, mine, group=group)
+        bad = [r for r, rec in enumerate(records) if rec is None]
+        if bad:
+            raise F.Fp8FlowError(f"CUDA IPC export failed on rank(s) {bad}")
         local = {name: t.data_ptr() for name, t in buffers.items()}
         self.tables, self._bases = resolve_tables(records, self.rank, local, F.fp8flow_ipc_open)
         self._keep = buffers

@@ -69,9 +69,13 @@ def run_dispatch(F, ranks, ld, rank, tpr, H, E, K, align=16):
     return dict(topk_all=topk_all, row_map=row_map, src=src, off=off, q_out=q_out, s_out=s_out, max_rows=max_rows)
 
 
+@pytest.mark.parametrize("kernel", ["engine", "lsu"])
 @pytest.mark.parametrize("n,tpr,H,E,K", [(1, 300, 1024, 16, 4), (2, 256, 7168, 32, 8), (4, 100, 1152, 64, 8),
                                          (8, 64, 7168, 256, 8), (2, 0, 256, 8, 2)])
-def test_dispatch_permute_parity(F, orc, n, tpr, H, E, K):
+def test_dispatch_permute_parity(F, orc, n, tpr, H, E, K, kernel, monkeypatch):
+    """Both dispatch kernels: the bulk-copy engine (peers on this device) and the register-copy
+    kernel the launcher takes when a peer lives on another GPU (NVLink)."""
+    monkeypatch.setenv("FP8FLOW_EP_DISPATCH_LSU", "1" if kernel == "lsu" else "0")
     ranks, ld = make_ranks(F, n, tpr, H, E, K, 1000 + n * tpr)
     qs = [host(r["q"]) for r in ranks]
     ss = [host(r["s"]) for r in ranks]
@@ -201,9 +205,9 @@ def _free_port():
     return p
 
 
-def _ipc_worker(rank, world, port, q):
+def _ipc_worker(rank, world, port, q, lsu="2"):
     try:
-        os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+        os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), "FP8FLOW_EP_DISPATCH_LSU": lsu})
         import torch.distributed as dist
 
         import oracle
@@ -262,13 +266,16 @@ def _ipc_worker(rank, world, port, q):
         del e
 
 
-def test_two_processes_over_cuda_ipc(F):
+@pytest.mark.parametrize("lsu", ["2", "1"])
+def test_two_processes_over_cuda_ipc(F, lsu):
+    """lsu "2": the launcher's own choice (same device -> bulk-copy engine); "1": the register-copy
+    kernel used across GPUs."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, lsu)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
