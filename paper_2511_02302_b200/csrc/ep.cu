@@ -30,7 +30,7 @@ namespace fp8flow {
 constexpr int kEpThreads = 256;
 constexpr int kEpWarps = kEpThreads / 32;
 constexpr int kCopyU = 16;  // uint4 per lane per pass of the token copy (8 KB per warp pass)
-constexpr int kScaleTiles = 8;  // 1x128 tiles per scale work item
+constexpr int kScaleUnroll = 4;  // (tile, row) scale pairs per thread with loads in flight together
 
 struct PeerPtrs {
   const void* p[kMaxRanks];
@@ -126,13 +126,15 @@ cudaError_t launch_peer_barrier(void* const* peer_signal, int32_t rank, int32_t 
 }
 
 // ---------------------------------------------------------------------------------------------
-// dispatch + permute + pad (receive side).  Three kinds of warp work in one launch:
-//   scales: per (32-token chunk, 8 tiles): each lane loads its token's 8 scale bytes first (one
-//           32-byte sector per tile for the warp), then scatters them to every local row;
+// dispatch + permute + pad (receive side), register-copy kernel (the path across GPUs).  Three
+// kinds of work in one launch, each spread over the whole grid:
 //   codes : per global token with >= 1 local row: the warp pulls its H code bytes once (128-bit
 //           non-coherent loads, up to 8 KB in flight per warp) and stores them to every local row;
-//   PAD   : per local expert, the trailing PAD rows (src_of_row < 0) get code 0x00 and scale 0x00.
-// Scale and PAD items are taken by the grid's first and last warps; code items by all warps.
+//   scales: (tile, row) pairs row-major over all threads (coalesced stores), 4 gathers in flight
+//           per thread; PAD rows 0x00;
+//   PAD   : per 32 output rows, the PAD rows' codes 0x00.
+// (Measured on the way: PAD rows handled per expert by 32 warps, or scales per 32-token chunk
+// before the codes, each cost ~15 us of serial latency at DSv3 sizes.)
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
     PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
@@ -143,77 +145,88 @@ __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEpWarps + (threadIdx.x >> 5);
   const int64_t T = Tpr * n;
   const int64_t n_tiles = H / 128;
+  const int64_t R = offsets[E_loc];
 
-  // ---- scales: item = (chunk of 32 consecutive global tokens, group of kScaleTiles 1x128 tiles).
-  // Lane l owns token c*32 + l: its kScaleTiles scale bytes are loaded first (one 32-byte sector
-  // per tile for the warp), then scattered to each of the token's local rows.
-  const int64_t n_tg = (n_tiles + kScaleTiles - 1) / kScaleTiles;
-  const int64_t n_items = ((T + 31) / 32) * n_tg;
-  for (int64_t it = gw; it < n_items; it += W) {
-    const int64_t c = it / n_tg;
-    const int64_t j0 = (it - c * n_tg) * kScaleTiles;
-    const int64_t gt = c * 32 + lane;
+  // ---- codes: warp gw owns tokens gw, gw+W, ...; their row_map rows are read 32 tokens at a time
+  // (lane l: token gw + (i0+l)W), a ballot marks the routed ones; per routed token the warp pulls
+  // its H code bytes once (16-byte non-coherent loads, up to 8 KB in flight per warp) and stores
+  // them to every local row.
+  const int64_t nvec = H / 16;
+  for (int64_t i0 = 0; gw + i0 * W < T; i0 += 32) {
+    const int64_t my_gt = gw + (i0 + lane) * W;
     int32_t rows[16];
     bool any = false;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      rows[k] = (gt < T && k < K) ? __ldg(row_map + gt * K + k) : -1;
+      rows[k] = (my_gt < T && k < K) ? __ldg(row_map + my_gt * K + k) : -1;
       any |= rows[k] >= 0;
     }
-    if (!__any_sync(0xffffffffu, any)) continue;
-    if (any) {
+    for (uint32_t mask = __ballot_sync(0xffffffffu, any); mask != 0; mask &= mask - 1) {
+      const int j = __ffs(mask) - 1;
+      const int64_t gt = gw + (i0 + j) * W;
       const int src_rank = static_cast<int>(gt / Tpr);
-      const uint8_t* s_src = static_cast<const uint8_t*>(peer.b[src_rank]) + (gt - src_rank * Tpr);
-      uint8_t v[kScaleTiles];
-#pragma unroll
-      for (int j = 0; j < kScaleTiles; ++j) v[j] = (j0 + j < n_tiles) ? s_src[(j0 + j) * ld_s_tok] : 0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (rows[k] >= 0) {
-#pragma unroll
-          for (int j = 0; j < kScaleTiles; ++j)
-            if (j0 + j < n_tiles) s_out[(j0 + j) * max_rows + rows[k]] = v[j];
-        }
-      }
-    }
-  }
-
-  // ---- PAD rows: expert e from the last warp down
-  for (int64_t e = W - 1 - gw; e < E_loc; e += W) {
-    const int64_t lo = offsets[e], hi = offsets[e + 1];
-    for (int64_t r = hi - 1; r >= lo; --r) {
-      if (src_of_row[r] >= 0) break;
-      for (int64_t i = lane * 16; i < H; i += 32 * 16) st_v4(q_out + r * H + i, make_uint4(0, 0, 0, 0));
-      for (int64_t j = lane; j < n_tiles; j += 32) s_out[j * max_rows + r] = 0;
-    }
-  }
-
-  // ---- codes: one global token per warp item
-  const int64_t nvec = H / 16;
-  for (int64_t gt = gw; gt < T; gt += W) {
-    const int32_t my_row = lane < K ? __ldg(row_map + gt * K + lane) : -1;
-    const uint32_t valid = __ballot_sync(0xffffffffu, my_row >= 0);
-    if (valid == 0) continue;
-    const int src_rank = static_cast<int>(gt / Tpr);
-    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(peer.a[src_rank]) +
-                                                      (gt - src_rank * Tpr) * H);
-    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kCopyU) {
-      uint4 buf[kCopyU];
-#pragma unroll
-      for (int u = 0; u < kCopyU; ++u) {
-        const int64_t v = v0 + lane + 32 * u;
-        if (v < nvec) buf[u] = ld_nc_v4(src + v);
-      }
-      for (uint32_t m = valid; m != 0; m &= m - 1) {
-        const int k = __ffs(m) - 1;
-        const int32_t r = __shfl_sync(0xffffffffu, my_row, k);
-        uint4* dst = reinterpret_cast<uint4*>(q_out + static_cast<int64_t>(r) * H);
+      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(peer.a[src_rank]) +
+                                                        (gt - src_rank * Tpr) * H);
+      for (int64_t v0 = 0; v0 < nvec; v0 += 32 * kCopyU) {
+        uint4 buf[kCopyU];
 #pragma unroll
         for (int u = 0; u < kCopyU; ++u) {
           const int64_t v = v0 + lane + 32 * u;
-          if (v < nvec) st_v4(dst + v, buf[u]);
+          if (v < nvec) buf[u] = ld_nc_v4(src + v);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int32_t r = __shfl_sync(0xffffffffu, rows[k], j);
+          if (r >= 0) {
+            uint4* dst = reinterpret_cast<uint4*>(q_out + static_cast<int64_t>(r) * H);
+#pragma unroll
+            for (int u = 0; u < kCopyU; ++u) {
+              const int64_t v = v0 + lane + 32 * u;
+              if (v < nvec) st_v4(dst + v, buf[u]);
+            }
+          }
         }
       }
+    }
+  }
+
+  // ---- scales, row-major over the grid's threads: pair p = (tile, row), consecutive threads on
+  // consecutive rows (coalesced stores); kScaleUnroll pairs per thread have their loads in flight
+  // together; PAD rows get 0x00
+  const int64_t nthr = W * 32;
+  const int64_t pairs = R * n_tiles;
+  const int tpr = static_cast<int>(Tpr);
+  for (int64_t p0 = gw * 32 + lane; p0 < pairs; p0 += nthr * kScaleUnroll) {
+    int32_t srcv[kScaleUnroll];
+    int64_t rr[kScaleUnroll], tl[kScaleUnroll];
+#pragma unroll
+    for (int u = 0; u < kScaleUnroll; ++u) {
+      const int64_t p = p0 + u * nthr;
+      tl[u] = p / R;
+      rr[u] = p - tl[u] * R;
+      srcv[u] = p < pairs ? __ldg(src_of_row + rr[u]) : -2;
+    }
+    uint8_t v[kScaleUnroll];
+#pragma unroll
+    for (int u = 0; u < kScaleUnroll; ++u) {
+      v[u] = 0;
+      if (srcv[u] >= 0) {
+        const int src_rank = srcv[u] / tpr;
+        v[u] = __ldg(static_cast<const uint8_t*>(peer.b[src_rank]) + tl[u] * ld_s_tok + (srcv[u] - src_rank * tpr));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kScaleUnroll; ++u)
+      if (srcv[u] != -2) s_out[tl[u] * max_rows + rr[u]] = v[u];
+  }
+
+  // ---- PAD rows' codes: 32-row chunks from the last warp down
+  for (int64_t c = W - 1 - gw; c * 32 < R; c += W) {
+    const int64_t r0 = c * 32;
+    const bool pad = r0 + lane < R && src_of_row[r0 + lane] < 0;
+    for (uint32_t m = __ballot_sync(0xffffffffu, pad); m != 0; m &= m - 1) {
+      const int64_t r = r0 + __ffs(m) - 1;
+      for (int64_t i = lane * 16; i < H; i += 32 * 16) st_v4(q_out + r * H + i, make_uint4(0, 0, 0, 0));
     }
   }
 }
