@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
 }
 
 // ---------------------------------------------------------------------------------------------
-// dispatch + permute + pad on the bulk-copy engine (default).  Two CTAs per SM; CTA c owns global
+// dispatch + permute + pad on the bulk-copy engine (same-device peers).  Four CTAs per SM (one producer
+// thread each: 1 CTA/SM 54 us, 2: 34.7, 3: 33.6, 4: 32.8 at DSv3 sizes; store slack 2/4/8 made no
+// difference -- the single issuing thread per CTA is what bounds it); CTA c owns global
 // tokens c, c+G, c+2G, ...
 //   1. all warps compact the CTA's routed tokens (row_map read 32 tokens at a time, ballot, one
 //      shared atomic per batch) into a shared list {token, its top_k rows};
@@ -249,6 +251,7 @@ constexpr int kDispStoreSlack = 4;
 constexpr size_t kDispSmemBudget = 220 * 1024;
 constexpr int kDispListStride = 17;  // token id + up to 16 rows
 
+template <int SLACK>
 __global__ void __launch_bounds__(256) dispatch_engine_kernel(
     PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
     const int32_t* __restrict__ src_of_row, const int32_t* __restrict__ offsets, int E_loc, int64_t max_rows,
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(256) dispatch_engine_kernel(
 
   if (warp == 0) {
     if (lane == 0) {
-      const int lead = nslots - kDispStoreSlack;
+      const int lead = nslots - SLACK;
       uint32_t phase_bits = 0;
       for (int nn = 0; nn < N + lead; ++nn) {
         const int m = nn - lead;
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(256) dispatch_engine_kernel(
         }
         if (nn < N) {  // load stage
           const int slot = nn % nslots;
-          if (nn >= nslots) bulk_wait_read<kDispStoreSlack>();  // token nn - nslots's stores have read it
+          if (nn >= nslots) bulk_wait_read<SLACK>();  // token nn - nslots's stores have read it
           const int64_t gt = list[nn * kDispListStride];
           const int src_rank = static_cast<int>(gt / Tpr);
           mbar_expect_tx(&full[slot], static_cast<uint32_t>(H));
@@ -399,7 +402,7 @@ cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint
   }
   // CTAS_PER_SM_DISP co-resident CTAs per SM (smem budget split); more CTAs (queued) when a CTA
   // would own more than 256 tokens
-  const int ctas = tune_int("CTAS_PER_SM_DISP", 2) > 0 ? tune_int("CTAS_PER_SM_DISP", 2) : 1;
+  const int ctas = tune_int("CTAS_PER_SM_DISP", 4) > 0 ? tune_int("CTAS_PER_SM_DISP", 4) : 1;
   const size_t budget = kDispSmemBudget / ctas;
   int64_t grid = static_cast<int64_t>(num_sms) * ctas;
   if ((T + grid - 1) / grid > 256) grid = (T + 255) / 256;
@@ -409,15 +412,24 @@ cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint
   int nslots = static_cast<int>((budget - head) / hidden);
   if (nslots > kDispMaxSlots) nslots = kDispMaxSlots;
   const size_t smem = head + static_cast<size_t>(hidden) * nslots;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dispatch_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kDispSmemBudget));
-    attr = true;
-  }
-  dispatch_engine_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
-      pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
-      max_rows, q_out, s_out, nslots, list_cap);
+  const int slack = tune_int("DISP_SLACK", kDispStoreSlack);
+#define FP8FLOW_DISP_LAUNCH(SL)                                                                             \
+  do {                                                                                                      \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      cudaFuncSetAttribute(dispatch_engine_kernel<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                           static_cast<int>(kDispSmemBudget));                                              \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    if (nslots < SL + 2) return cudaErrorInvalidValue;                                                     \
+    dispatch_engine_kernel<SL><<<static_cast<unsigned>(grid), 256, smem, stream>>>(                         \
+        pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts, \
+        max_rows, q_out, s_out, nslots, list_cap);                                                          \
+  } while (0)
+  if (slack == 2) FP8FLOW_DISP_LAUNCH(2);
+  else if (slack == 8) FP8FLOW_DISP_LAUNCH(8);
+  else FP8FLOW_DISP_LAUNCH(4);
+#undef FP8FLOW_DISP_LAUNCH
   return cudaGetLastError();
 }
 
