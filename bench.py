@@ -977,6 +977,8 @@ def main():
     max_total_ms = D.max_over_ranks(total_ms, device)
     all_bytes = D.sum_over_ranks(step_bytes * args.steps, device)
     value = all_bytes / (max_total_ms / 1e3) / 1e9
+    # EP load imbalance: the heaviest expert group's bytes over the mean (routing skew)
+    imbalance = D.max_over_ranks(float(step_bytes), device) / (all_bytes / args.steps / world)
     op_ms = {op: statistics.mean(p[i] for p in per_step) for i, op in enumerate(OPS)}
     ops = {op: {"us": round(op_ms[op] * 1e3, 2), "bytes": op_bytes[op],
                 "gbs": round(op_bytes[op] / op_ms[op] / 1e6, 1),
@@ -1029,6 +1031,7 @@ def main():
             "data": "synthetic (seeded; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
             "frac_of_hbm_peak": round(value / world / peak, 3),
             "per_gpu_gbs": round(value / world, 1),
+            "load_imbalance": round(imbalance, 3),
             "step_us_quantiles": {q: round(float(np.percentile(step_ms, p)) * 1e3, 1)
                                   for q, p in (("p10", 10), ("p50", 50), ("p90", 90))},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ops[dom]["gbs"], "peak": peak, "unit": "GB/s",
