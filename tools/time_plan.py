@@ -50,4 +50,10 @@ for name, topk in [("step group 0 (received tokens)", torch.from_numpy(sh.topk_i
         res[fused] = (rm.clone(), off.clone())
         print(f"plan {name} T={T}: fused={fused} {ms * 1e3:7.2f} us", flush=True)
     assert torch.equal(res["1"][0], res["0"][0]) and torch.equal(res["1"][1], res["0"][1])
+    os.environ["FP8FLOW_PLAN_FUSED"] = "1"
+    for stop in ("1", "2", "3"):
+        os.environ["FP8FLOW_PLAN_STOP"] = stop
+        ms = timed(lambda: F.fp8flow_permute_plan(topk, 0, E, 16, rm, src, off, ws))
+        print(f"plan {name}: fused, ends after stage {stop}: {ms * 1e3:7.2f} us", flush=True)
+    os.environ["FP8FLOW_PLAN_STOP"] = "0"
 print("paths agree")
