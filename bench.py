@@ -629,6 +629,49 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
                                                with_gather_and_plan_us=round(ms_all * 1e3, 2), note=note),
             "NEXT3_combine_unpermute": line(ms_c, nb_c, rank=0, tokens=tpr, parity=ok_c, note=note)}
 
+def nccl_dispatch_baseline(F, rank, world, tpr, E, q, s_, topk, device, out):
+    """The baseline NEXT-3 replaces: an all-to-all collective followed by a separate permute -- a
+    rank packs its tokens for every destination rank (index_select of codes, token-major scale
+    bytes, routing rows), exchanges the counts (host sync) and the payloads with
+    torch.distributed all_to_all_single (NCCL on the GPU box), then runs A3's plan + move on what
+    it received.  Writes into out = dict(q_out, s_out, off) so the result can be compared with the
+    fused pull (they must be identical)."""
+    e0, per = E // world * rank, E // world
+    dest = (topk // per)                                                   # [tpr, K] destination rank
+    gloo = D.dist.get_backend() == "gloo"
+    cdev = torch.device("cpu") if gloo else device
+    sel = [torch.nonzero((dest == d).any(dim=1)).flatten() for d in range(world)]
+    send_counts = torch.tensor([int(x.shape[0]) for x in sel], dtype=torch.int64, device=cdev)
+    recv_counts = torch.empty_like(send_counts)
+    D.dist.all_to_all_single(recv_counts, send_counts)
+    idx = torch.cat(sel)
+    sc, rc = send_counts.tolist(), recv_counts.tolist()
+    payload_q = q.index_select(0, idx)
+    payload_s = s_[:, :tpr].t().index_select(0, idx).contiguous()           # token-major scale bytes
+    payload_t = topk.index_select(0, idx)
+    nr = sum(rc)
+    rq = torch.empty(nr, HIDDEN, dtype=torch.uint8, device=device)
+    rs = torch.empty(nr, HIDDEN // 128, dtype=torch.uint8, device=device)
+    rt = torch.empty(nr, topk.shape[1], dtype=torch.int32, device=device)
+    for send, recv in ((payload_q, rq), (payload_s, rs), (payload_t, rt)):
+        if gloo:
+            r_cpu = recv.cpu()
+            D.dist.all_to_all_single(r_cpu, send.cpu(), rc, sc)
+            recv.copy_(r_cpu)
+        else:
+            D.dist.all_to_all_single(recv, send, rc, sc)
+    # separate permute on the receive side (A3 plan + move over the received tokens, rank order)
+    mr = out["q_out"].shape[0]
+    row_map = torch.empty(max(nr, 1), topk.shape[1], dtype=torch.int32, device=device)[:nr]
+    src = torch.empty(mr, dtype=torch.int32, device=device)
+    ws = torch.empty(F.fp8flow_permute_workspace_bytes(nr, topk.shape[1], per), dtype=torch.uint8, device=device)
+    F.fp8flow_permute_plan(rt, e0, per, ALIGN, row_map, src, out["off"], ws)
+    ld = (nr + 15) // 16 * 16
+    rs_mn = torch.zeros(HIDDEN // 128, max(ld, 16), dtype=torch.uint8, device=device)
+    rs_mn[:, :nr] = rs.t()
+    F.fp8flow_permute_pad(rq, rs_mn, src, out["off"], out["q_out"], out["s_out"])
+
+
 def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) -> dict:
     """NEXT-3 across the job's ranks (one process per GPU: peer reads cross NVLink on the 8-GPU box;
     with FP8FLOW_DIST_BACKEND=gloo several ranks share one GPU through CUDA IPC).  Weak scaling:
@@ -700,6 +743,16 @@ def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) 
     ms_disp = timed(lambda: F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), tpr, tpr, HIDDEN,
                                                            row_map, src, off, q_out, s_out))
     ms_comb = timed(lambda: ep.combine(peers, rank, tpr, HIDDEN, E, topk, pr, y))
+    # the NCCL baseline on the same data (all-to-all of codes + scales + routing, then A3)
+    base_out = {"q_out": torch.empty_like(q_out), "s_out": torch.empty_like(s_out), "off": torch.empty_like(off)}
+    ms_base, base_err = None, None
+    try:
+        nccl_dispatch_baseline(F, rank, world, tpr, E, q, s_, topk, device, base_out)
+        torch.cuda.synchronize(device)
+    except Exception as e:  # noqa: BLE001
+        base_err = f"rank {rank}: {type(e).__name__}: {e}"[:300]
+    if D.sum_over_ranks(0.0 if base_err is None else 1.0, device) == 0:
+        ms_base = timed(lambda: nccl_dispatch_baseline(F, rank, world, tpr, E, q, s_, topk, device, base_out))
     # checks (outside the timing): gather every rank's tokens / expert outputs / plans
     gq = [torch.empty_like(q) for _ in range(world)]
     gs = [torch.empty_like(s_) for _ in range(world)]
@@ -723,7 +776,11 @@ def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) 
     torch.cuda.synchronize(device)
     ok_d = bool(torch.equal(ref_q[:R], q_out[:R]) and torch.equal(ref_s[:, :R], s_out[:, :R]))
     ok_c = bool(torch.equal(y.view(torch.int16), y_ref.view(torch.int16)))
+    ok_b = ms_base is not None and bool(torch.equal(base_out["off"], off) and
+                                        torch.equal(base_out["q_out"][:R], q_out[:R]) and
+                                        torch.equal(base_out["s_out"][:, :R], s_out[:, :R]))
     ok = D.sum_over_ranks(float(ok_d and ok_c), device) == world
+    ok_base = D.sum_over_ranks(float(ok_b), device) == world
     uniq = int(np.count_nonzero((row_map.cpu().numpy() >= 0).any(axis=1)))
     nb_d = D.sum_over_ranks(RL.dispatch_permute_bytes(uniq, R, T, TOP_K, HIDDEN), device)
     nb_c = D.sum_over_ranks(RL.combine_bytes(tpr, TOP_K, HIDDEN, True), device)
@@ -739,7 +796,12 @@ def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) 
             f"(CUDA IPC peer tables); time = max over ranks; {tpr} tokens per rank, {per} experts per rank")
     return {"NEXT3_dispatch_permute_pad": line(ms_disp, nb_d, with_gather_and_plan_us=round(ms_plan_disp * 1e3, 2),
                                                note=note),
-            "NEXT3_combine_unpermute": line(ms_comb, nb_c, note=note), "parity": ok}
+            "NEXT3_combine_unpermute": line(ms_comb, nb_c, note=note), "parity": ok,
+            "baseline_all_to_all_then_permute": (
+                {"us": round(ms_base * 1e3, 2), "same_output": ok_base,
+                 "what": "torch.distributed all_to_all_single of the packed FP8 codes, token-major scale bytes "
+                         "and routing rows (counts exchanged first, host sync), then A3 plan + move on the "
+                         "received tokens"} if ms_base is not None else {"error": base_err or "failed on a rank"})}
 
 def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
     """NEXT-2: the block-scaled FP8 grouped GEMMs that consume the step's outputs directly -- fc1
