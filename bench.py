@@ -1121,7 +1121,8 @@ SWEEP_SHAPES = [(128, 128), (256, 256), (512, 512), (1024, 1024), (2048, 2048), 
 def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
     """Config 5: scaling-aware transpose vs the naive dequant -> transpose -> requant comparator,
     128^2 .. 65536x7168, the same shape on every GPU (weak scaling).  Latency per launch (L2
-    flushed before each), GB/s on A2's algorithmic bytes, naive/direct latency ratio."""
+    flushed before each), GB/s on A2's algorithmic bytes, naive/direct latency ratio; plus
+    A1 alone and the one-pass quantize + transpose (NEXT-1 dual) on the same shape."""
     from paper_2511_02302_b200 import fp8flow as F
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -1148,10 +1149,16 @@ def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
         q = torch.empty(rows, cols, dtype=torch.uint8, device=device)
         s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=device)
         F.fp8flow_quantize_rowwise(x, q, s)
-        del x
         qT = torch.empty(rows * cols, dtype=torch.uint8, device=device)
         sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
         ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, 1), dtype=torch.uint8, device=device)
+        # the metric's two ops on the same shape: A1 alone and the quantize + transpose dual kernel
+        # (BF16 read once -> row-wise and column-wise FP8), L2 flushed the same way
+        t_q = D.max_over_ranks(timed(lambda: F.fp8flow_quantize_rowwise(x, q, s)), device)
+        q2, s2 = torch.empty_like(q), torch.empty_like(s)
+        qT2, sT2 = torch.empty_like(qT), torch.empty_like(sT)
+        t_dual = D.max_over_ranks(timed(lambda: F.fp8flow_quantize_dual(x, q2, s2, qT2, sT2)), device)
+        del x, q2, s2, qT2, sT2
         t_d = timed(lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT))
         t_n = timed(lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws))
         t_d = D.max_over_ranks(t_d, device)
@@ -1182,7 +1189,11 @@ def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
                     "direct_gbs_per_gpu": round(nb / t_d / 1e6, 1), "direct_frac": round(nb / t_d / 1e6 / peak, 3),
                     "naive_effective_gbs_per_gpu": round(nb / t_n / 1e6, 1),
                     "naive_actual_gbs_per_gpu": round(RL.naive_transpose_actual_bytes([rows], cols) / t_n / 1e6, 1),
-                    "direct_gbs_all_gpus": round(world * nb / t_d / 1e6, 1)})
+                    "direct_gbs_all_gpus": round(world * nb / t_d / 1e6, 1),
+                    "quantize_us": round(t_q * 1e3, 2),
+                    "quantize_frac": round(RL.quantize_bytes(rows, cols) / t_q / 1e6 / peak, 3),
+                    "quantize_transpose_dual_us": round(t_dual * 1e3, 2),
+                    "quantize_transpose_dual_frac": round(RL.quantize_dual_bytes([rows], cols) / t_dual / 1e6 / peak, 3)})
         del q, s, qT, sT, ws
     return out
 
