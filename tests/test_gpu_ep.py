@@ -326,3 +326,73 @@ def test_dispatch_combine_edge_cases(F, orc, kernel, monkeypatch):
             torch.cuda.synchronize()
             y_ref = orc.combine(xs, rms, ts[g], E // n, probs=host(ranks[g]["probs"]), token_begin=g * tpr)
             assert np.array_equal(host(y.view(torch.int16)).view(np.uint16), y_ref)
+
+
+def test_next3_sequence_captures_into_a_cuda_graph(F):
+    """Barrier -> routing gather -> plan -> fused dispatch, then combine: every launch is graph-
+    capturable (peer tables by value, sizes on the device, the barrier's epoch on the device); a
+    replay reproduces the eager outputs bit for bit."""
+    from paper_2511_02302_b200 import ep
+
+    n, tpr, H, E, K = 2, 256, 1024, 16, 4
+    ranks, ld = make_ranks(F, n, tpr, H, E, K, 4321)
+    for r in ranks:
+        r["sig"] = ep.signal_buffer(n, "cuda")
+    _, per = ep.expert_range(0, n, E)
+    mr = F.permute_max_rows(n * tpr, K, per)
+    bufs = []
+    for g in range(n):
+        b = dict(topk_all=torch.empty(n * tpr, K, dtype=torch.int32, device="cuda"),
+                 row_map=torch.empty(n * tpr, K, dtype=torch.int32, device="cuda"),
+                 src=torch.empty(mr, dtype=torch.int32, device="cuda"),
+                 off=torch.empty(per + 1, dtype=torch.int32, device="cuda"),
+                 ws=torch.empty(F.fp8flow_permute_workspace_bytes(n * tpr, K, per), dtype=torch.uint8, device="cuda"),
+                 q_out=torch.zeros(mr, H, dtype=torch.uint8, device="cuda"),
+                 s_out=torch.zeros(H // 128, mr, dtype=torch.uint8, device="cuda"),
+                 y=torch.zeros(tpr, H, dtype=torch.bfloat16, device="cuda"),
+                 st=torch.full((1,), -1, dtype=torch.int32, device="cuda"))
+        bufs.append(b)
+        ranks[g]["x"] = synth.normal_bf16(mr, H, 90 + g).cuda()
+        ranks[g]["row_map"] = b["row_map"]
+    peers = ep.LocalPeers(ranks)
+    streams = [torch.cuda.Stream() for _ in range(n)]
+
+    def layer(g, stream):
+        b = bufs[g]
+        F.fp8flow_peer_barrier(peers.table("sig"), g, b["st"], timeout_ms=2000, stream=stream)
+        ep.dispatch_permute(peers, g, tpr, H, K, E, ld, b["topk_all"], b["row_map"], b["src"], b["off"], b["ws"],
+                            b["q_out"], b["s_out"], stream=stream)
+
+    def combine(g, stream):
+        ep.combine(peers, g, tpr, H, E, ranks[g]["topk"], ranks[g]["probs"], bufs[g]["y"], stream=stream)
+
+    torch.cuda.synchronize()
+    for g in range(n):                       # eager, ranks on their own streams (the barrier needs both)
+        layer(g, streams[g])
+    torch.cuda.synchronize()
+    for g in range(n):
+        combine(g, streams[g])
+    torch.cuda.synchronize()
+    eager = [{k: bufs[g][k].clone() for k in ("row_map", "off", "q_out", "s_out", "y")} for g in range(n)]
+    for g in range(n):
+        for k in ("q_out", "s_out", "y"):
+            bufs[g][k].zero_()
+    # capture rank g's sequence into its own graph, then replay both graphs concurrently
+    graphs = []
+    for g in range(n):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=streams[g]):
+            layer(g, streams[g])
+        graphs.append(gr)
+    torch.cuda.synchronize()
+    for g in range(n):
+        with torch.cuda.stream(streams[g]):
+            graphs[g].replay()
+    torch.cuda.synchronize()
+    for g in range(n):
+        combine(g, streams[g])
+    torch.cuda.synchronize()
+    for g in range(n):
+        assert bufs[g]["st"].item() == 0
+        for k, v in eager[g].items():
+            assert torch.equal(bufs[g][k], v), (g, k)
