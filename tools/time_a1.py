@@ -35,7 +35,7 @@ def timed(fn):
 for rows, cols in [(2048, 7168), (4096, 7168), (16384, 7168)]:
     x = synth.activations_bf16_device(rows, cols, 5, dev)
     outs = {}
-    for var, sched in [("0", "0"), ("1", "2"), ("0", "2")]:
+    for var, sched in [("0", "0"), ("1", "0")]:
         os.environ["FP8FLOW_A1_VARIANT"] = var
         os.environ["FP8FLOW_SCHED_A1"] = sched
         q = torch.empty(rows, cols, dtype=torch.uint8, device=dev)
@@ -45,7 +45,7 @@ for rows, cols in [(2048, 7168), (4096, 7168), (16384, 7168)]:
         outs[(var, sched)] = (q.clone(), s.clone())
         print(f"A1 {rows}x{cols} variant {var} sched {sched}: {ms * 1e3:7.2f} us  {nb / ms / 1e6:7.1f} GB/s  "
               f"frac {nb / ms / 1e6 / peak:.3f}", flush=True)
-    ref = outs[("0", "2")]
+    ref = outs[("0", "0")]
     for k, (q, s) in outs.items():
         assert torch.equal(q, ref[0]) and torch.equal(s, ref[1]), f"variant {k} differs"
 print("variants bit-identical")
