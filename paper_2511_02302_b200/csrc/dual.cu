@@ -74,11 +74,14 @@ __device__ __forceinline__ uint32_t quant_rows(const uint2 (&w)[N], uint32_t (&c
   uint32_t mine = 0;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    const uint32_t m = max(max(w[i].x & 0x7FFFu, (w[i].x >> 16) & 0x7FFFu), max(w[i].y & 0x7FFFu, (w[i].y >> 16) & 0x7FFFu));
+    const uint32_t m2 = __vmaxu2(w[i].x & 0x7FFF7FFFu, w[i].y & 0x7FFF7FFFu);  // packed 16-bit max
+    const uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
     const uint32_t sb = scale_byte_from_bf16_mag(__reduce_max_sync(0xffffffffu, m));
     const float inv = inv_scale_from_byte(sb);
-    c[i] = cvt_e4m3x2_f32(bf16lo_to_f32(w[i].x) * inv, bf16hi_to_f32(w[i].x) * inv) |
-           (cvt_e4m3x2_f32(bf16lo_to_f32(w[i].y) * inv, bf16hi_to_f32(w[i].y) * inv) << 16);
+    const float2 iv = make_float2(inv, inv);
+    const float2 px = __fmul2_rn(make_float2(bf16lo_to_f32(w[i].x), bf16hi_to_f32(w[i].x)), iv);
+    const float2 py = __fmul2_rn(make_float2(bf16lo_to_f32(w[i].y), bf16hi_to_f32(w[i].y)), iv);
+    c[i] = cvt_e4m3x2_f32(px.x, px.y) | (cvt_e4m3x2_f32(py.x, py.y) << 16);
     mine = (lane & (N - 1)) == i ? sb : mine;
   }
   return mine;
