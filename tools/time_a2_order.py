@@ -13,6 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2511_02302_b200 import fp8flow as F, roofline as RL  # noqa: E402
 
+KNOB = os.environ.get("A2_KNOB", "FP8FLOW_A2_VARIANT")      # FP8FLOW_A2_COLMAJOR for the order experiment
+VARIANTS = os.environ.get("A2_VALUES", "0,1,2,3").split(",")
 dev = torch.device("cuda:0")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 clean = torch.ones(64 << 20, dtype=torch.float32, device=dev)
@@ -51,14 +53,15 @@ for name, rows, cols, sg in cases:
     nseg = 1 if sg is None else len(sg)
     nb = RL.transpose_bytes([rows] if sg is None else [int(v) for v in sg], cols)
     outs = {}
-    for order in ("0", "1"):
-        os.environ["FP8FLOW_A2_COLMAJOR"] = order
+    for order in VARIANTS:
+        os.environ[KNOB] = order
         qT = torch.zeros(rows * cols, dtype=torch.uint8, device=dev)
         sT = torch.zeros(rows // 128 + nseg, cols, dtype=torch.uint8, device=dev)
         ms = timed(lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT, seg_offsets=off))
         outs[order] = (qT, sT)
-        print(f"A2 {name}: colmajor={order} {ms * 1e3:8.2f} us  {nb / ms / 1e6:7.1f} GB/s  frac {nb / ms / 1e6 / peak:.3f}",
+        print(f"A2 {name}: {KNOB}={order} {ms * 1e3:8.2f} us  {nb / ms / 1e6:7.1f} GB/s  frac {nb / ms / 1e6 / peak:.3f}",
               flush=True)
-    assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1]), name
+    for k in outs:
+        assert torch.equal(outs["0"][0], outs[k][0]) and torch.equal(outs["0"][1], outs[k][1]), (name, k)
     del q, s, outs
-print("orders bit-identical")
+print("variants bit-identical")
