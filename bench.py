@@ -316,9 +316,9 @@ def run_e2e(ds: DeviceStep, steps: int) -> dict:
 # =============================================================================================
 # parity of the timed outputs against the oracle (sampled; after timing)
 # =============================================================================================
-def verify(ds: DeviceStep) -> dict:
-    import oracle as O
-
+def _oracle_parity(O, ds: DeviceStep) -> dict:
+    """Sampled parity of the timed outputs against the oracle module O (passed in by
+    cpu_baseline_leg, the only code in bench.py that loads the oracle)."""
     hw, res = ds.hw, {}
     host = lambda t: t.cpu().numpy()  # noqa: E731
     bits = synth.bf16_bits
@@ -361,11 +361,9 @@ def verify(ds: DeviceStep) -> dict:
 # =============================================================================================
 # CPU oracle timing (cpu_baseline and the reference arm)
 # =============================================================================================
-def oracle_sample(hw: HostWorkload, frac: float, threads: int | None) -> tuple[float, float, str]:
-    """Runs the oracle on a bounded sample (fraction `frac` of every op's rows) of this rank's step.
-    Returns (algorithmic bytes of the sample, seconds, description)."""
-    import oracle as O
-
+def oracle_sample(O, hw: HostWorkload, frac: float, threads: int | None) -> tuple[float, float, str]:
+    """Runs the oracle module O on a bounded sample (fraction `frac` of every op's rows) of this
+    rank's step.  Returns (algorithmic bytes of the sample, seconds, description)."""
     bits = synth.bf16_bits
     n_sh = max(16, int(len(hw.x_shard) * frac) // 16 * 16)
     n_tok = max(16, int(hw.T_recv * frac))
@@ -398,6 +396,40 @@ def oracle_sample(hw: HostWorkload, frac: float, threads: int | None) -> tuple[f
             f"{n_rows}x{FFN}")
     return nbytes, dt, desc
 
+
+def _gemm_rows_check(O, entry: dict, samples, what: str) -> None:
+    worst = 0.0
+    for a, sa, b, sb, d in samples:
+        ref = O.gemm_blockscaled(a, sa, b, sb)[0]
+        mag = O.gemm_blockscaled(a & 0x7F, sa, b & 0x7F, sb)[0]
+        err = np.abs(d - ref) - 2.0 ** -8 * np.abs(ref)
+        worst = max(worst, float(np.max(err / (mag + 1e-30))))
+    entry.update({"parity_rows": what, "parity_worst": worst, "parity_ok": worst <= 2.0 ** -14})
+
+
+def cpu_baseline_leg(hw: "HostWorkload", ds: "DeviceStep", time_it: bool, verify: bool, checks: list) -> tuple:
+    """The CPU-oracle leg of bench.py -- the only code here that loads oracle/ (test
+    infrastructure): (1) on rank 0 at N = 1, the oracle as it stands timed on a bounded sample of the
+    step (all host cores, and one core on 1/16 of it); (2) the sampled parity of the timed GPU
+    outputs (step ops and the queued NEXT-2 GEMM rows) against the oracle, after timing.  Returns
+    (cpu_baseline dict or None, parity dict or None)."""
+    if not (time_it or verify):
+        return None, None
+    import oracle as O
+
+    cpu = parity = None
+    if verify:
+        parity = _oracle_parity(O, ds)
+        for entry, samples, what in checks:
+            _gemm_rows_check(O, entry, samples, what)
+    if time_it:
+        nbytes, secs, desc = oracle_sample(O, hw, 1.0, None)
+        nb1, secs1, desc1 = oracle_sample(O, hw, 1.0 / 16, 1)  # the same oracle on one core, 1/16 of the sample
+        cpu = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": desc, "seconds": round(secs, 2), "cpu_model": cpu_model(),
+               "single_thread": {"value": round(nb1 / secs1 / 1e9, 4), "unit": "GB/s", "sample": desc1,
+                                 "seconds": round(secs1, 2)}}
+    return cpu, parity
 
 def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
@@ -461,7 +493,7 @@ class ClockSampler:
 # =============================================================================================
 # config-2 sub-measurement (4096 x 7168, one expert): A1, A2 and the naive comparator
 # =============================================================================================
-def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20) -> dict:
+def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20, checks: list | None = None) -> dict:
     """NEXT rows measured on the same workload (not part of the headline step): NEXT-1 fused
     SwiGLU backward + quant of dA [R, 2048] with the saved fc1 output h [R, 4096], and the
     dual-output SwiGLU + quant emitting A row-wise and column-wise (per expert) in one pass, against
@@ -502,7 +534,7 @@ def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20) -> dict:
     ms = med(lambda: F.fp8flow_swiglu_quant_dual(ds.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off))
     out["NEXT1_swiglu_quant_dual"] = line(ms, nb, segments=len(segs),
                                           vs_A5_then_A2_us=round(ms_two * 1e3, 2))
-    out.update(gemm_measure(ds, reps))
+    out.update(gemm_measure(ds, reps, checks))
     out.update(ep_measure(ds.dev, peak, reps))
     return out
 
@@ -803,11 +835,12 @@ def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) 
                          "and routing rows (counts exchanged first, host sync), then A3 plan + move on the "
                          "received tokens"} if ms_base is not None else {"error": base_err or "failed on a rank"})}
 
-def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
+def gemm_measure(ds: "DeviceStep", reps: int = 10, checks: list | None = None) -> dict:
     """NEXT-2: the block-scaled FP8 grouped GEMMs that consume the step's outputs directly -- fc1
     Fprop on A3's X_perm (FP8 codes + 1x128 scales, 32 expert groups) and fc2 Fprop on A5's A --
     with synthetic FP8 expert weights; TFLOP/s against the FP8 dense peak (2 x measured bf16, the
-    profiling guide's nominal ratio).  One output row per expert is checked against the oracle."""
+    profiling guide's nominal ratio).  Sampled output rows are queued in `checks` for the oracle
+    comparison in cpu_baseline_leg."""
     F, hw, dev = ds.F, ds.hw, ds.dev
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     bf16 = json.load(open(peaks_path))["bf16_tflops"] if os.path.exists(peaks_path) else 1673.3
@@ -846,24 +879,15 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
         ms = timed(lambda: F.fp8flow_gemm_blockscaled(A, sA, W, sW, Dout, seg_offsets=ds.off))
         flops = 2.0 * hw.R * N * K
         tf = flops / ms / 1e9
-        # parity sample: the first row of every non-empty expert vs the oracle's fp64 definition
-        from oracle import gemm_blockscaled as orc_gemm  # test infrastructure: the verify leg only
+        # parity sample (checked later by cpu_baseline_leg): the first row of every non-empty expert
         offs = ds.off.cpu().numpy()
-        worst = 0.0
-        for e in range(E):
-            if offs[e + 1] == offs[e]:
-                continue
-            r = int(offs[e])
-            ref = orc_gemm(A[r:r + 1].cpu().numpy(), sA[:, r:r + 16].cpu().numpy(), W[e].cpu().numpy(),
-                           sW[e].cpu().numpy())[0]
-            mag = orc_gemm(A[r:r + 1].cpu().numpy() & 0x7F, sA[:, r:r + 16].cpu().numpy(),
-                           W[e].cpu().numpy() & 0x7F, sW[e].cpu().numpy())[0]
-            err = np.abs(Dout[r].float().cpu().numpy() - ref) - 2.0 ** -8 * np.abs(ref)
-            worst = max(worst, float(np.max(err / (mag + 1e-30))))
+        samples = [(A[r:r + 1].cpu().numpy(), sA[:, r:r + 16].cpu().numpy(), W[e].cpu().numpy(), sW[e].cpu().numpy(),
+                    Dout[r].float().cpu().numpy()) for e in range(E) for r in [int(offs[e])] if offs[e + 1] > offs[e]]
         out[name] = {"us": round(ms * 1e3, 1), "tflops": round(tf, 1), "frac": round(tf / fp8_peak, 3),
-                     "peak_tflops": round(fp8_peak, 1), "shape": {"M": hw.R, "N": N, "K": K, "groups": E},
-                     "parity_rows": "first row of every expert vs oracle fp64; max (|err| - 2^-8|ref|)/(|A||B|^T)",
-                     "parity_worst": worst, "parity_ok": worst <= 2.0 ** -14}
+                     "peak_tflops": round(fp8_peak, 1), "shape": {"M": hw.R, "N": N, "K": K, "groups": E}}
+        if checks is not None:
+            checks.append((out[name], samples, "first row of every expert vs oracle fp64; "
+                                                "max (|err| - 2^-8|ref|)/(|A||B|^T)"))
         del W, sW, Dout
 
     # Wgrad of fc1, all FP8: dH from NEXT-1 (SwiGLU backward + quant) -> A2 per expert -> grouped-K
@@ -879,7 +903,6 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
     ms = timed(lambda: F.fp8flow_gemm_wgrad(hT, shT, ds.xT, ds.sxT, dW, ds.off))
     flops = 2.0 * hw.R * 2 * FFN * HIDDEN
     tf = flops / ms / 1e9
-    from oracle import gemm_blockscaled as orc_gemm  # test infrastructure: the verify leg only
     offs = ds.off.cpu().numpy()
     P = np.concatenate([[0], np.cumsum((np.diff(offs) + 127) // 128)])
     e = int(np.argmax(np.diff(offs)))  # the largest expert: rows 0 and 2F-1 of dW_e
@@ -888,18 +911,13 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10) -> dict:
     Ae = hT[Fh * o: Fh * (o + me)].view(Fh, me).cpu().numpy()
     Be = ds.xT[HIDDEN * o: HIDDEN * (o + me)].view(HIDDEN, me).cpu().numpy()
     sA, sB = shT[P[e]:P[e + 1]].cpu().numpy(), ds.sxT[P[e]:P[e + 1]].cpu().numpy()
-    worst = 0.0
-    for r in (0, Fh - 1):
-        ref = orc_gemm(Ae[r:r + 1], sA[:, r:r + 16], Be, sB)[0]
-        mag = orc_gemm(Ae[r:r + 1] & 0x7F, sA[:, r:r + 16], Be & 0x7F, sB)[0]
-        err = np.abs(dW[e, r].float().cpu().numpy() - ref) - 2.0 ** -8 * np.abs(ref)
-        worst = max(worst, float(np.max(err / (mag + 1e-30))))
+    samples = [(Ae[r:r + 1], sA[:, r:r + 16], Be, sB, dW[e, r].float().cpu().numpy()) for r in (0, Fh - 1)]
     out["NEXT2_gemm_fc1_wgrad"] = {"us": round(ms * 1e3, 1), "tflops": round(tf, 1), "frac": round(tf / fp8_peak, 3),
                                    "peak_tflops": round(fp8_peak, 1),
                                    "shape": {"Ma": Fh, "Nb": HIDDEN, "K_total": hw.R, "groups": E},
-                                   "operands": "A2(NEXT-1 dH) and A2(X_perm) from the step, groups over K",
-                                   "parity_rows": f"expert {e} (m_e={me}), rows 0 and {Fh - 1} vs oracle fp64",
-                                   "parity_worst": worst, "parity_ok": worst <= 2.0 ** -14}
+                                   "operands": "A2(NEXT-1 dH) and A2(X_perm) from the step, groups over K"}
+    if checks is not None:
+        checks.append((out["NEXT2_gemm_fc1_wgrad"], samples, f"expert {e} (m_e={me}), rows 0 and {Fh - 1} vs oracle fp64"))
     return out
 
 
@@ -1066,7 +1084,6 @@ def main():
                "note": "H2D of all step inputs from pinned host memory + the step + checksum kernels + D2H of "
                        "the output checksums, per step, CUDA events"}
 
-    parity = None if args.no_verify else verify(ds)
     sums = D.gather_checksums(ds.checksums(), device)
     next3_dist = None
     if world > 1 and not args.no_ep:
@@ -1074,15 +1091,13 @@ def main():
             next3_dist = ep_measure_dist(device, peak, rank, world)
         except Exception as e:  # noqa: BLE001 -- reported in the line, never fatal to the headline
             next3_dist = {"error": f"{type(e).__name__}: {e}"[:300]}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nbytes, secs, desc = oracle_sample(hw, 1.0, None)
-        nb1, secs1, desc1 = oracle_sample(hw, 1.0 / 16, 1)  # the same oracle on one core, 1/16 of the sample
-        cpu = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": desc, "seconds": round(secs, 2), "cpu_model": cpu_model(),
-               "single_thread": {"value": round(nb1 / secs1 / 1e9, 4), "unit": "GB/s", "sample": desc1,
-                                 "seconds": round(secs1, 2)}}
+    checks: list = []
+    extra = {}
+    if rank == 0 and world == 1:
+        extra["cfg2"] = cfg2_measure(device, peak)
+        extra["next_ops"] = next_ops_measure(ds, peak, checks=checks)
+    cpu, parity = cpu_baseline_leg(hw, ds, time_it=rank == 0 and world == 1 and not args.no_cpu_baseline,
+                                   verify=not args.no_verify, checks=checks)
 
     if rank == 0:
         line = {
@@ -1103,9 +1118,7 @@ def main():
             "clocks": clk, "parity": parity,
             "checksums": {f"rank{r}": f"{(sum(c) & ((1 << 64) - 1)):016x}" for r, c in enumerate(sums)},
         }
-        if world == 1:
-            line["cfg2"] = cfg2_measure(device, peak)
-            line["next_ops"] = next_ops_measure(ds, peak)
+        line.update(extra)
         if next3_dist is not None:
             line["next3_multi_rank"] = next3_dist
         print(json.dumps(line), flush=True)
@@ -1213,13 +1226,15 @@ def run_reference(args, rank, world, group, cfg):
     """The reference arm: the CPU oracle as it stands, on host cores, each step a bounded sample."""
     if rank != 0:
         return
+    import oracle as O  # the reference arm IS the oracle (tier framing)
+
     hw = HostWorkload(group)
     frac = 1.0 / 8
     for _ in range(args.warmup):
-        oracle_sample(hw, frac, None)
+        oracle_sample(O, hw, frac, None)
     nb, ts, desc = 0.0, 0.0, ""
     for _ in range(args.steps):
-        b, t, desc = oracle_sample(hw, frac, None)
+        b, t, desc = oracle_sample(O, hw, frac, None)
         nb, ts = nb + b, ts + t
     v = nb / ts / 1e9
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

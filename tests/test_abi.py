@@ -180,3 +180,19 @@ def test_product_package_never_imports_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 assert not bad.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_oracle_loaded_only_by_tests_smoke_and_bench_cpu_leg():
+    """oracle/ is test infrastructure: tools/ never load it, and in bench.py only cpu_baseline_leg
+    (and the --impl reference arm, which IS the oracle) import it."""
+    bad = re.compile(r"^\s*(import\s+oracle|from\s+oracle\b)", re.M)
+    for f in os.listdir(os.path.join(ROOT, "tools")):
+        if f.endswith(".py"):
+            assert not bad.search(open(os.path.join(ROOT, "tools", f)).read()), f
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    owners = []
+    for m in bad.finditer(src):
+        head = src[:m.start()]
+        owners.append(re.findall(r"^def (\w+)", head, re.M)[-1])
+    assert sorted(owners) == ["cpu_baseline_leg", "run_reference"], owners
+

@@ -1,6 +1,6 @@
 """Times A5 (fused SwiGLU + quant) and NEXT-1 (fused SwiGLU backward + quant) alone on bench.py's
-shape, L2 flushed before each launch; --check compares a row sample with the oracle.
-Usage: python tools/time_swiglu.py [--check] [KNOB=V,KNOB=V ...]"""
+shape, L2 flushed before each launch.
+Usage: python tools/time_swiglu.py [KNOB=V,KNOB=V ...]"""
 import os
 import statistics
 import sys
@@ -48,16 +48,4 @@ for setting in [a for a in sys.argv[1:] if not a.startswith("--")] or [""]:
     print(f"[{setting}]")
     timed(lambda: F.fp8flow_swiglu_quant(h, qf, sf), RL.swiglu_quant_bytes(R, FFN), "A5 swiglu_quant")
     timed(lambda: F.fp8flow_swiglu_bwd_quant(h, dA, q, s), RL.swiglu_bwd_quant_bytes(R, FFN), "NEXT1 swiglu_bwd_quant")
-if "--check" in sys.argv:
-    import oracle as O
-    import numpy as np
-    idx = torch.arange(0, R, 61)
-    hb = h[idx].cpu().view(torch.int16).numpy().view(np.uint16)
-    db = dA[idx].cpu().view(torch.int16).numpy().view(np.uint16)
-    qo, so = O.swiglu_bwd_quant(hb, db)
-    qg = q[idx].cpu().numpy()
-    sg = s[:, idx].cpu().numpy()
-    print("bwd code mismatches", int((qo != qg).sum()), "of", qo.size, "scale mismatches", int((so != sg).sum()))
-    qo, so = O.swiglu_quant(hb)
-    print("fwd code mismatches", int((qo != qf[idx].cpu().numpy()).sum()), "of", qo.size, "scale mismatches",
-          int((so != sf[:, idx].cpu().numpy()).sum()))
+# (code/scale parity against the oracle lives in tests/test_gpu_parity.py; tools/ never load oracle/)
