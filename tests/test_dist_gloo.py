@@ -148,3 +148,46 @@ def test_expert_and_token_ranges():
 
     assert RL.dispatch_permute_bytes(10, 32, 100, 8, 256) == 10 * 258 + 32 * 258 + 100 * 8 * 4
     assert RL.combine_bytes(4, 8, 128, True) == 4 * 8 * 256 + 4 * 256 + 4 * 8 * 12
+
+
+def _ipc_fail_worker(rank, world, port, q):
+    """IpcPeers when one rank cannot export a handle: every rank still joins the all-gather and
+    every rank raises (no rank is left waiting in a collective)."""
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_02302_b200 import ep
+    from paper_2511_02302_b200 import fp8flow as F
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def fake_get(t):
+        if rank == 1:
+            raise F.Fp8FlowError("export failed (simulated)")
+        return b"H" * 64, 0
+
+    F.fp8flow_ipc_get_handle = fake_get          # this process only (spawned)
+    F.fp8flow_ipc_open = lambda h: 1000
+    raised = None
+    try:
+        ep.IpcPeers({"q": torch.zeros(4)})
+    except F.Fp8FlowError as e:
+        raised = str(e)
+    dist.barrier()                               # both ranks reach this: nobody hung in all_gather
+    dist.destroy_process_group()
+    q.put((rank, raised))
+
+
+def test_ipc_export_failure_raises_on_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(msg is not None and "rank(s) [1]" in msg for _, msg in out), out
