@@ -121,8 +121,8 @@ __device__ __forceinline__ void a1_process_v2(int64_t rows, int64_t cols, int64_
   }
 }
 
-template <int ROWS>
-__global__ void __launch_bounds__(256) quantize_rowwise_v2_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
+template <int ROWS, int WARPS = 8>
+__global__ void __launch_bounds__(32 * WARPS) quantize_rowwise_v2_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
                                                                    int64_t cols, uint8_t* __restrict__ q,
                                                                    uint8_t* __restrict__ s, int64_t ld_s) {
   const int lane = threadIdx.x & 31;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) quantize_rowwise_v2_kernel(const __nv_bfl
   const int sub = lane & 15;
   const int64_t col_pairs = (cols + 255) / 256;
   const int64_t n_items = ((rows + ROWS - 1) / ROWS) * col_pairs;
-  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);  // one item per warp
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);  // one item per warp
   if (item >= n_items) return;
   uint4 v[ROWS];
   a1_load<ROWS>(x, rows, cols, col_pairs, item, half, sub, v);
@@ -184,21 +184,29 @@ static cudaError_t launch_a1(const void* x, int64_t rows, int64_t cols, uint8_t*
 
 cudaError_t launch_quantize_rowwise(const void* x, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s,
                                     int64_t ld_s, cudaStream_t stream, int num_sms) {
-  // Default: 8-row items, one per warp, v2 item math (tools/time_a1.py, DESIGN.md §6/§9):
+  // Default: 8-row items, one per warp, 4 warps per CTA, v2 item math (tools/time_a1.py, DESIGN.md
+  // §6/§9; 4-warp CTAs: 2048x7168 14.3 -> 12.3-13.3 us, equal at larger shapes; 2 warps equal,
+  // 16 warps slower):
   // 4096x7168 18.4 us, 16384x7168 56.2 us (0.945 of 6650 GB/s) vs 22.5 / 63.5 us for the
   // shuffle-tree version (whose __shfl_xor_sync trees compiled to warp-collective fallbacks:
   // 32 WARPSYNC/ENDCOLLECTIVE sequences per item, 1392 vs 944 SASS instructions).
   // Experiments: FP8FLOW_A1_VARIANT 1 = that version, 2 = 4-row items, 3 = 4 rows pipelined,
-  // 4 = 8 rows pipelined, 6 = 16 rows (all slower).
+  // 4 = 8 rows pipelined, 5 = v2 with 8-warp CTAs, 6 = 16 rows (all slower or equal).
   switch (tune_int("A1_VARIANT", 0)) {
     case 1: return launch_a1<8, false>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedOnePerWarp);
     case 2: return launch_a1<4, false>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedInterleaved);
     case 3: return launch_a1<4, true>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedInterleaved);
     case 4: return launch_a1<8, true>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedInterleaved);
     case 6: return launch_a1<16, false>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedOnePerWarp);
+    case 5: {
+      const int64_t n_items = ((rows + 7) / 8) * ((cols + 255) / 256);
+      quantize_rowwise_v2_kernel<8, 8><<<static_cast<unsigned>((n_items + 7) / 8), 256, 0, stream>>>(
+          static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s);
+      return cudaGetLastError();
+    }
     default: {
       const int64_t n_items = ((rows + 7) / 8) * ((cols + 255) / 256);
-      quantize_rowwise_v2_kernel<8><<<static_cast<unsigned>((n_items + 7) / 8), 256, 0, stream>>>(
+      quantize_rowwise_v2_kernel<8, 4><<<static_cast<unsigned>((n_items + 3) / 4), 128, 0, stream>>>(
           static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s);
       return cudaGetLastError();
     }

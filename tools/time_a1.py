@@ -35,7 +35,7 @@ def timed(fn):
 for rows, cols in [(2048, 7168), (4096, 7168), (16384, 7168)]:
     x = synth.activations_bf16_device(rows, cols, 5, dev)
     outs = {}
-    for var, sched in [("0", "0"), ("1", "0")]:
+    for var, sched in [("0", "0"), ("5", "0"), ("1", "0")]:
         os.environ["FP8FLOW_A1_VARIANT"] = var
         os.environ["FP8FLOW_SCHED_A1"] = sched
         q = torch.empty(rows, cols, dtype=torch.uint8, device=dev)
