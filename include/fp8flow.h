@@ -297,8 +297,9 @@ FP8FLOW_API int fp8flow_peer_barrier(void* const* peer_signal, int32_t rank, int
                                      uint32_t timeout_ms, void* stream);
 
 /* fp8flow_peer_gather -- all-gather by pulls: dst[r*bytes_per_rank ...] = peer_src[r][0 .. bytes_per_rank)
- * (e.g. every rank's topk_idx for the dispatch plan).  bytes_per_rank % 16 == 0, all pointers
- * 16-byte aligned, dst device [n*bytes_per_rank]. */
+ * (e.g. every rank's topk_idx for the dispatch plan).  bytes_per_rank % 4 == 0 (16-byte copies
+ * when bytes_per_rank % 16 == 0, else 4-byte words), all pointers 16-byte aligned, dst device
+ * [n*bytes_per_rank]. */
 FP8FLOW_API int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
                                     void* stream);
 

@@ -355,7 +355,7 @@ int fp8flow_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int3
 
 int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst, void* stream) {
   if (n < 1 || n > FP8FLOW_MAX_RANKS) return FP8FLOW_ERR_ARG;
-  if (bytes_per_rank < 0 || bytes_per_rank % 16 != 0) return FP8FLOW_ERR_SHAPE;
+  if (bytes_per_rank < 0 || bytes_per_rank % 4 != 0) return FP8FLOW_ERR_SHAPE;
   if (bytes_per_rank == 0) return FP8FLOW_OK;
   int st = peer_table_ok(peer_src, n, true);
   if (st != FP8FLOW_OK) return st;

@@ -43,14 +43,19 @@ struct PeerPtrs2 {
 // ---------------------------------------------------------------------------------------------
 // all-gather by pulls: out[r * bytes + i] = peer[r][i]
 // ---------------------------------------------------------------------------------------------
+template <typename V>
 __global__ void __launch_bounds__(kEpThreads) peer_gather_kernel(PeerPtrs src, int n, int64_t vec_per_rank,
-                                                                 uint4* __restrict__ out) {
+                                                                 V* __restrict__ out) {
   const int64_t total = vec_per_rank * n;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(i / vec_per_rank);
     const int64_t j = i - r * vec_per_rank;
-    out[i] = ld_nc_v4(static_cast<const uint4*>(src.p[r]) + j);
+    if constexpr (sizeof(V) == 16) {
+      out[i] = ld_nc_v4(static_cast<const uint4*>(src.p[r]) + j);
+    } else {
+      out[i] = __ldg(static_cast<const V*>(src.p[r]) + j);
+    }
   }
 }
 
@@ -58,11 +63,16 @@ cudaError_t launch_peer_gather(const void* const* peer_src, int32_t n, int64_t b
                                cudaStream_t stream, int num_sms) {
   PeerPtrs pp{};
   for (int r = 0; r < n; ++r) pp.p[r] = peer_src[r];
-  const int64_t vec = bytes_per_rank / 16;
+  const bool v16 = bytes_per_rank % 16 == 0;  // else 4-byte words (the ABI requires bytes % 4 == 0)
+  const int64_t vec = bytes_per_rank / (v16 ? 16 : 4);
   int64_t grid = (vec * n + kEpThreads - 1) / kEpThreads;
   if (grid > 4LL * num_sms) grid = 4LL * num_sms;
   if (grid < 1) grid = 1;
-  peer_gather_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec, static_cast<uint4*>(dst));
+  if (v16)
+    peer_gather_kernel<uint4><<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec, static_cast<uint4*>(dst));
+  else
+    peer_gather_kernel<uint32_t><<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec,
+                                                                                        static_cast<uint32_t*>(dst));
   return cudaGetLastError();
 }
 

@@ -131,8 +131,8 @@ def test_validation_of_next3_entry_points(L):
     assert L.fp8flow_peer_barrier(tab2, 0, 65, None, 100, None) == 4
     assert L.fp8flow_peer_barrier(None, 0, 2, None, 100, None) == 1
     assert L.fp8flow_peer_barrier(tab_null, 0, 2, None, 100, None) == 1
-    # gather: bytes % 16, empty no-op, misaligned peer
-    assert L.fp8flow_peer_gather(tab2, 2, 24, a16, None) == 2
+    # gather: bytes % 4, empty no-op, misaligned peer
+    assert L.fp8flow_peer_gather(tab2, 2, 22, a16, None) == 2
     assert L.fp8flow_peer_gather(tab2, 2, 0, None, None) == 0
     assert L.fp8flow_peer_gather(tab_mis, 2, 32, a16, None) == 3
     # dispatch: top_k, hidden % 128, ld_s < tokens, NULL plan

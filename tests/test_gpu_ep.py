@@ -289,13 +289,15 @@ def test_two_processes_over_cuda_ipc(F, lsu):
 @pytest.mark.parametrize("kernel", ["engine", "lsu"])
 def test_dispatch_combine_edge_cases(F, orc, kernel, monkeypatch):
     """A rank that receives nothing (every token routed to the other rank's experts), top_k = 1 and
-    top_k = 16, and a rank whose experts all stay empty: both dispatch kernels and the combine stay
-    bit-exact against the oracle."""
+    top_k = 16, an odd token count (routing bytes not a multiple of 16): both dispatch kernels and
+    the combine stay bit-exact against the oracle."""
     from paper_2511_02302_b200 import ep
 
     monkeypatch.setenv("FP8FLOW_EP_DISPATCH_LSU", "1" if kernel == "lsu" else "0")
     H = 512
-    for n, tpr, E, K, force in [(2, 64, 8, 2, "low"), (2, 48, 32, 1, None), (2, 40, 64, 16, None)]:
+    # (37 tokens x top-1 = 148 routing bytes per rank: the routing gather's 4-byte-word path)
+    for n, tpr, E, K, force in [(2, 64, 8, 2, "low"), (2, 48, 32, 1, None), (2, 40, 64, 16, None),
+                                (2, 37, 16, 1, None)]:
         ranks, ld = make_ranks(F, n, tpr, H, E, K, 555 + K)
         if force == "low":   # every token picks experts of rank 0 only: rank 1 receives nothing
             for r in ranks:
