@@ -42,7 +42,10 @@ from paper_2511_02302_b200 import dist as D  # noqa: E402
 from paper_2511_02302_b200 import roofline as RL  # noqa: E402
 
 METRIC = "scaling-aware transpose + quantize GB/s and % of HBM peak at 1/2/4/8 B200"
-T_GLOBAL, HIDDEN, FFN, N_EXPERTS, TOP_K, ALIGN = 16384, synth.HIDDEN, synth.FFN, synth.NUM_EXPERTS, synth.TOP_K, 16
+# DeepSeek-V3 layer: 16384 tokens.  FP8FLOW_BENCH_TOKENS shrinks it for the multi-rank smoke test
+# only (tests/test_gpu_bench_multirank.py); the line's config always reports the token count used.
+T_GLOBAL = int(os.environ.get("FP8FLOW_BENCH_TOKENS", "16384"))
+HIDDEN, FFN, N_EXPERTS, TOP_K, ALIGN = synth.HIDDEN, synth.FFN, synth.NUM_EXPERTS, synth.TOP_K, 16
 KERNELS_PER_STEP = 9    # A1, plan x2 (count, place), move, A5, A4, A1(dY), A2 x2
 OPS = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
        "A2_transpose_xperm", "A2_transpose_a"]
@@ -1007,7 +1010,7 @@ def main():
             sys.exit(2)
     group = D.expert_group(rank)
     cfg = {"workload": "DeepSeek-V3 MoE layer hot path, one EP8 expert-group shard per GPU (32 of 256 experts), "
-                       "16384 tokens top-8, hidden 7168, expert FFN 2x2048: A1 x2, A3 plan+move, A5, A4, A2 x2",
+                       f"{T_GLOBAL} tokens top-8, hidden 7168, expert FFN 2x2048: A1 x2, A3 plan+move, A5, A4, A2 x2",
            "tokens": T_GLOBAL, "hidden": HIDDEN, "ffn": FFN, "experts": N_EXPERTS, "top_k": TOP_K,
            "local_experts": N_EXPERTS // D.NUM_GROUPS, "align": ALIGN, "routing": "DSv3 group-limited top-8, "
            "skewed expert bias N(0,1) + Gumbel, seed 2511023020", "parallelism": f"ep-group shard x{world} (weak)"}
