@@ -189,6 +189,43 @@ class DeviceStep:
         if record:
             ev[8].record()
 
+    def op_fns(self) -> dict:
+        """The step's ops as separate launches (same arguments as launch_ops), keyed like OPS."""
+        F, hw = self.F, self.hw
+        return {
+            "A1_quantize_x": lambda: F.fp8flow_quantize_rowwise(self.x_shard, self.q_x, self.s_x),
+            "A3_plan": lambda: F.fp8flow_permute_plan(self.topk, hw.e0, hw.E_loc, ALIGN, self.row_map, self.src,
+                                                      self.off, self.ws),
+            "A3_move": lambda: F.fp8flow_permute_pad(self.q_recv, self.s_recv, self.src, self.off, self.x_perm,
+                                                     self.s_perm),
+            "A5_swiglu_quant": lambda: F.fp8flow_swiglu_quant(self.h, self.q_a, self.s_a,
+                                                              rows_dev=self.off[hw.E_loc:]),
+            "A4_unpermute": lambda: F.fp8flow_unpermute_unpad(self.y, self.row_map, self.probs, self.y_tok),
+            "A1_quantize_dy": lambda: F.fp8flow_quantize_rowwise(self.dy_shard, self.q_dy, self.s_dy),
+            "A2_transpose_xperm": lambda: F.fp8flow_scaling_aware_transpose(self.x_perm, self.s_perm, self.xT,
+                                                                            self.sxT, seg_offsets=self.off),
+            "A2_transpose_a": lambda: F.fp8flow_scaling_aware_transpose(self.q_a, self.s_a, self.aT, self.saT,
+                                                                        seg_offsets=self.off),
+        }
+
+    def isolated_us(self, reps: int = 10) -> dict:
+        """Each op alone after a clean L2 flush (median of reps): the kernel's own speed, without
+        the write-back of the previous kernels' dirty lines that the serial pass includes."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        out = {}
+        for op, fn in self.op_fns().items():
+            ts = []
+            for _ in range(reps):
+                self.flush_l2()
+                torch.cuda._sleep(1_000_000)
+                ev[0].record()
+                fn()
+                ev[1].record()
+                ev[1].synchronize()
+                ts.append(ev[0].elapsed_time(ev[1]))
+            out[op] = statistics.median(ts) * 1e3
+        return out
+
     def flush_l2(self) -> None:
         """Write a 256 MiB buffer (evicts everything), then read another 256 MiB buffer so the L2 is
         left holding CLEAN unrelated lines: the timed kernels neither hit in L2 nor pay the
@@ -1067,6 +1104,10 @@ def main():
                 "gbs": round(op_bytes[op] / op_ms[op] / 1e6, 1),
                 "frac": round(op_bytes[op] / op_ms[op] / 1e6 / peak, 3),
                 "share": round(op_ms[op] / statistics.mean(serial_ms), 3)} for op in OPS}
+    iso = ds.isolated_us()
+    for op in OPS:
+        ops[op]["isolated_us"] = round(iso[op], 2)
+        ops[op]["isolated_frac"] = round(op_bytes[op] / iso[op] / 1e3 / peak, 3)
     dom = max(OPS, key=lambda o: op_ms[o])
     traffic = ncu_traffic(dom)
     cfg.update({"expert_group": group, "recv_tokens": hw.T_recv, "padded_rows": hw.R, "valid_rows": hw.valid_rows,
@@ -1074,7 +1115,8 @@ def main():
                       "read so the L2 holds clean unrelated lines",
                 "timing": "CUDA events; the step's dependency DAG on 4 streams (plan->move->A2(X) | A1,A1 | "
                           "A5->A2(A) | A4) captured once into a CUDA graph and replayed behind a spin kernel each "
-                          "step; per-op breakdown from the same steps launched serially on one stream",
+                          "step; per-op breakdown from the same steps launched serially on one stream "
+                          "(ops.*.us), and each op alone after a clean L2 flush (ops.*.isolated_us)",
                 "serial_ms_per_step": round(statistics.mean(serial_ms), 4)})
 
     e2e = None
