@@ -30,7 +30,7 @@ namespace fp8flow {
 constexpr int kEpThreads = 256;
 constexpr int kEpWarps = kEpThreads / 32;
 constexpr int kCopyU = 16;  // uint4 per lane per pass of the token copy (8 KB per warp pass)
-constexpr int kScaleUnroll = 4;  // (tile, row) scale pairs per thread with loads in flight together
+constexpr int kScaleChunk = 16;  // scale bytes per token with loads in flight together (LSU dispatch)
 
 struct PeerPtrs {
   const void* p[kMaxRanks];
@@ -140,9 +140,9 @@ cudaError_t launch_peer_barrier(void* const* peer_signal, int32_t rank, int32_t 
 // kinds of work in one launch, each spread over the whole grid:
 //   codes : per global token with >= 1 local row: the warp pulls its H code bytes once (128-bit
 //           non-coherent loads, up to 8 KB in flight per warp) and stores them to every local row;
-//   scales: (tile, row) pairs row-major over all threads (coalesced stores), 4 gathers in flight
-//           per thread; PAD rows 0x00;
-//   PAD   : per 32 output rows, the PAD rows' codes 0x00.
+//   scales: per batch of 32 consecutive tokens, one 32-byte sector per tile from the owner for
+//           the whole batch (the link-efficient gather), scattered to each token's local rows;
+//   PAD   : per 32 output rows, the PAD rows' codes and scale bytes 0x00.
 // (Measured on the way: PAD rows handled per expert by 32 warps, or scales per 32-token chunk
 // before the codes, each cost ~15 us of serial latency at DSv3 sizes.)
 // ---------------------------------------------------------------------------------------------
@@ -157,13 +157,21 @@ __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
   const int64_t n_tiles = H / 128;
   const int64_t R = offsets[E_loc];
 
-  // ---- codes: warp gw owns tokens gw, gw+W, ...; their row_map rows are read 32 tokens at a time
-  // (lane l: token gw + (i0+l)W), a ballot marks the routed ones; per routed token the warp pulls
-  // its H code bytes once (16-byte non-coherent loads, up to 8 KB in flight per warp) and stores
-  // them to every local row.
+  // warp roles: the first S warps gather the scale bytes (by 32-token batches, below), the other
+  // Wc warps copy the codes -- so the scale batches' few serial link round trips overlap the
+  // code copies instead of adding to them
+  const int64_t n_batches = (T + 31) / 32;
+  const int64_t S = W >= 8 ? min64(n_batches, W / 4) : 0;
+  const int64_t Wc = W - S;
+  const int64_t gc = gw - S;  // code-warp index (< 0: a scale warp)
+
+  // ---- codes: code warp gc owns tokens gc, gc+Wc, ...; their row_map rows are read 32 tokens at a
+  // time (lane l: token gc + (i0+l)Wc), a ballot marks the routed ones; per routed token the warp
+  // pulls its H code bytes once (16-byte non-coherent loads, up to 8 KB in flight per warp) and
+  // stores them to every local row.
   const int64_t nvec = H / 16;
-  for (int64_t i0 = 0; gw + i0 * W < T; i0 += 32) {
-    const int64_t my_gt = gw + (i0 + lane) * W;
+  for (int64_t i0 = 0; gc >= 0 && gc + i0 * Wc < T; i0 += 32) {
+    const int64_t my_gt = gc + (i0 + lane) * Wc;
     int32_t rows[16];
     bool any = false;
 #pragma unroll
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
     }
     for (uint32_t mask = __ballot_sync(0xffffffffu, any); mask != 0; mask &= mask - 1) {
       const int j = __ffs(mask) - 1;
-      const int64_t gt = gw + (i0 + j) * W;
+      const int64_t gt = gc + (i0 + j) * Wc;
       const int src_rank = static_cast<int>(gt / Tpr);
       const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(peer.a[src_rank]) +
                                                         (gt - src_rank * Tpr) * H);
@@ -200,43 +208,48 @@ __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
     }
   }
 
-  // ---- scales, row-major over the grid's threads: pair p = (tile, row), consecutive threads on
-  // consecutive rows (coalesced stores); kScaleUnroll pairs per thread have their loads in flight
-  // together; PAD rows get 0x00
-  const int64_t nthr = W * 32;
-  const int64_t pairs = R * n_tiles;
-  const int tpr = static_cast<int>(Tpr);
-  for (int64_t p0 = gw * 32 + lane; p0 < pairs; p0 += nthr * kScaleUnroll) {
-    int32_t srcv[kScaleUnroll];
-    int64_t rr[kScaleUnroll], tl[kScaleUnroll];
+  // ---- scales, by batches of 32 consecutive global tokens (scale warp gw: batches gw, gw+S, ...; all
+  // warps when the grid is tiny): lane l
+  // owns token 32c+l, so for every 1x128 tile the warp's 32 scale-byte reads from the owner fall in
+  // ONE 32-byte sector -- 56 link transactions per 32 tokens, where a row-by-row gather costs one
+  // per (row, tile) (~30x more transactions over NVLink for DSv3 routing); each lane then writes
+  // its token's bytes to the token's local rows (local HBM).  kScaleChunk loads in flight per lane.
+  const int64_t scale_stride = S > 0 ? S : W;
+  for (int64_t c = gw; (S == 0 || gw < S) && c * 32 < T; c += scale_stride) {
+    const int64_t gt = c * 32 + lane;
+    int32_t rows[16];
+    bool any = false;
 #pragma unroll
-    for (int u = 0; u < kScaleUnroll; ++u) {
-      const int64_t p = p0 + u * nthr;
-      tl[u] = p / R;
-      rr[u] = p - tl[u] * R;
-      srcv[u] = p < pairs ? __ldg(src_of_row + rr[u]) : -2;
+    for (int k = 0; k < 16; ++k) {
+      rows[k] = (gt < T && k < K) ? __ldg(row_map + gt * K + k) : -1;
+      any |= rows[k] >= 0;
     }
-    uint8_t v[kScaleUnroll];
+    if (!__any_sync(0xffffffffu, any)) continue;
+    const int src_rank = any ? static_cast<int>(gt / Tpr) : 0;
+    const uint8_t* sp = static_cast<const uint8_t*>(peer.b[src_rank]) + (any ? gt - src_rank * Tpr : 0);
+    for (int64_t j0 = 0; j0 < n_tiles; j0 += kScaleChunk) {
+      uint32_t v[kScaleChunk];
 #pragma unroll
-    for (int u = 0; u < kScaleUnroll; ++u) {
-      v[u] = 0;
-      if (srcv[u] >= 0) {
-        const int src_rank = srcv[u] / tpr;
-        v[u] = __ldg(static_cast<const uint8_t*>(peer.b[src_rank]) + tl[u] * ld_s_tok + (srcv[u] - src_rank * tpr));
+      for (int j = 0; j < kScaleChunk; ++j) v[j] = (any && j0 + j < n_tiles) ? __ldg(sp + (j0 + j) * ld_s_tok) : 0u;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (rows[k] >= 0) {
+#pragma unroll
+          for (int j = 0; j < kScaleChunk; ++j)
+            if (j0 + j < n_tiles) s_out[(j0 + j) * max_rows + rows[k]] = static_cast<uint8_t>(v[j]);
+        }
       }
     }
-#pragma unroll
-    for (int u = 0; u < kScaleUnroll; ++u)
-      if (srcv[u] != -2) s_out[tl[u] * max_rows + rr[u]] = v[u];
   }
 
-  // ---- PAD rows' codes: 32-row chunks from the last warp down
+  // ---- PAD rows (codes 0x00, scale bytes 0x00): 32-row chunks from the last warp down
   for (int64_t c = W - 1 - gw; c * 32 < R; c += W) {
     const int64_t r0 = c * 32;
     const bool pad = r0 + lane < R && src_of_row[r0 + lane] < 0;
     for (uint32_t m = __ballot_sync(0xffffffffu, pad); m != 0; m &= m - 1) {
       const int64_t r = r0 + __ffs(m) - 1;
       for (int64_t i = lane * 16; i < H; i += 32 * 16) st_v4(q_out + r * H + i, make_uint4(0, 0, 0, 0));
+      for (int64_t j = lane; j < n_tiles; j += 32) s_out[j * max_rows + r] = 0;
     }
   }
 }
