@@ -669,6 +669,14 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
     uniq = int(np.count_nonzero((p0["row_map"].cpu().numpy() >= 0).any(axis=1)))
     nb_d = RL.dispatch_permute_bytes(uniq, R0, T_GLOBAL, TOP_K, HIDDEN)
     ms_k = med(lambda: receive(0, kernel_only=True))
+    # the register-copy kernel the launcher takes when peers live on other GPUs, on the same data
+    prev = os.environ.get("FP8FLOW_EP_DISPATCH_LSU")
+    os.environ["FP8FLOW_EP_DISPATCH_LSU"] = "1"
+    ms_lsu = med(lambda: receive(0, kernel_only=True))
+    if prev is None:
+        del os.environ["FP8FLOW_EP_DISPATCH_LSU"]
+    else:
+        os.environ["FP8FLOW_EP_DISPATCH_LSU"] = prev
     ms_all = med(lambda: receive(0))
     nb_c = RL.combine_bytes(tpr, TOP_K, HIDDEN, True)
     ms_c = med(lambda: ep.combine(peers, 0, tpr, HIDDEN, E, ranks[0]["topk"], ranks[0]["probs"], y))
@@ -698,7 +706,8 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
 
     note = "8 virtual EP ranks on one GPU: peer reads are local HBM here, NVLink on the 8-GPU box"
     return {"NEXT3_dispatch_permute_pad": line(ms_k, nb_d, rank=0, recv_tokens=uniq, rows=R0, parity=ok_d,
-                                               with_gather_and_plan_us=round(ms_all * 1e3, 2), note=note),
+                                               with_gather_and_plan_us=round(ms_all * 1e3, 2),
+                                               cross_gpu_kernel_us=round(ms_lsu * 1e3, 2), note=note),
             "NEXT3_combine_unpermute": line(ms_c, nb_c, rank=0, tokens=tpr, parity=ok_c, note=note)}
 
 def nccl_dispatch_baseline(F, rank, world, tpr, E, q, s_, topk, device, out):
