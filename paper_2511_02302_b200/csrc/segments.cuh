@@ -38,14 +38,19 @@ template <int NT, typename Smem>
 __device__ __forceinline__ void load_segments(Smem& sm, const int32_t* seg_offsets, int32_t num_segs,
                                               int64_t rows) {
   const int tid = threadIdx.x;
-  if (seg_offsets == nullptr) {
+  if (seg_offsets == nullptr) {  // one segment: no scan, one barrier
     if (tid == 0) {
+      const int32_t nb = static_cast<int32_t>((rows + kTile - 1) / kTile);
       sm.seg_off[0] = 0;
       sm.seg_off[1] = static_cast<int32_t>(rows);
+      sm.blk_prefix[0] = 0;
+      sm.blk_prefix[1] = nb;
+      sm.total_rb = nb;
     }
-  } else {
-    for (int i = tid; i <= num_segs; i += NT) sm.seg_off[i] = seg_offsets[i];
+    __syncthreads();
+    return;
   }
+  for (int i = tid; i <= num_segs; i += NT) sm.seg_off[i] = seg_offsets[i];
   __syncthreads();
   // 4 consecutive segments per thread (num_segs <= 1024)
   int nb[4], tsum = 0;
