@@ -42,6 +42,7 @@ from paper_2511_02302_b200 import dist as D  # noqa: E402
 from paper_2511_02302_b200 import roofline as RL  # noqa: E402
 
 METRIC = "scaling-aware transpose + quantize GB/s and % of HBM peak at 1/2/4/8 B200"
+NVTX = os.environ.get("FP8FLOW_NVTX", "0") == "1"   # profiling runs only (e.g. ncu --nvtx)
 # DeepSeek-V3 layer: 16384 tokens.  FP8FLOW_BENCH_TOKENS shrinks it for the multi-rank smoke test
 # only (tests/test_gpu_bench_multirank.py); the line's config always reports the token count used.
 T_GLOBAL = int(os.environ.get("FP8FLOW_BENCH_TOKENS", "16384"))
@@ -161,6 +162,12 @@ class DeviceStep:
         self.ev_side = [torch.cuda.Event() for _ in range(3)]
 
     def launch_ops(self, record: bool) -> None:
+        if NVTX:  # opt-in NVTX ranges per op for profiler filtering (host calls; off when timing)
+            for i, (op, fn) in enumerate(self.op_fns().items()):
+                torch.cuda.nvtx.range_push(op)
+                fn()
+                torch.cuda.nvtx.range_pop()
+            return
         F, hw, ev = self.F, self.hw, self.events
         if record:
             ev[0].record()

@@ -1,0 +1,79 @@
+"""Determinism: the same inputs give byte-identical outputs run after run and
+whatever the launch configuration -- the permute plan orders rows without atomics deciding the
+order, A4 accumulates in k order, the NEXT-3 dispatch's shared token list may be filled in any
+order (each row's content is fixed by row_map), and the concurrent / graph-replayed step equals
+the serial launch sequence."""
+import os
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+@pytest.fixture(scope="module")
+def step():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import bench
+
+    dev = torch.device("cuda", 0)
+    hw = bench.HostWorkload(1)            # expert group 1 (the bench times group 0)
+    return bench.DeviceStep(hw, dev)
+
+
+def test_step_outputs_repeat_bit_for_bit(step):
+    step.launch_ops(record=False)
+    torch.cuda.synchronize()
+    first = step.checksums()
+    for _ in range(3):
+        step.launch_ops(record=False)
+        torch.cuda.synchronize()
+        assert step.checksums() == first
+    step.launch_ops_concurrent()          # 4-stream DAG
+    torch.cuda.synchronize()
+    assert step.checksums() == first
+    step.capture_graph()
+    step.timed_step_graph()               # CUDA-graph replay
+    torch.cuda.synchronize()
+    assert step.checksums() == first
+
+
+def test_step_outputs_independent_of_launch_knobs(step, monkeypatch):
+    step.launch_ops(record=False)
+    torch.cuda.synchronize()
+    ref = step.checksums()
+    for knob, val in (("FP8FLOW_CTAS_PER_SM_A3", "1"), ("FP8FLOW_CTAS_PER_SM_A4", "1"), ("FP8FLOW_PLAN_FUSED", "0"),
+                      ("FP8FLOW_A2_VARIANT", "3"), ("FP8FLOW_A1_VARIANT", "2")):
+        monkeypatch.setenv(knob, val)
+        step.launch_ops(record=False)
+        torch.cuda.synchronize()
+        assert step.checksums() == ref, knob
+        monkeypatch.delenv(knob)
+
+
+def test_next3_dispatch_independent_of_grid_shape(monkeypatch):
+    """The dispatch engine's per-CTA token lists are filled through shared atomics: any CTA count
+    (hence any list order) and the register-copy kernel give the same bytes."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from test_gpu_ep import make_ranks, run_dispatch
+    from paper_2511_02302_b200 import fp8flow as F
+
+    n, tpr, H, E, K = 4, 512, 2048, 64, 8
+    ranks, ld = make_ranks(F, n, tpr, H, E, K, 9090)
+    outs = []
+    for knobs in ({}, {"FP8FLOW_CTAS_PER_SM_DISP": "1"}, {"FP8FLOW_CTAS_PER_SM_DISP": "3"},
+                  {"FP8FLOW_EP_DISPATCH_LSU": "1"}):
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        o = run_dispatch(F, ranks, ld, 1, tpr, H, E, K)
+        outs.append((o["q_out"].clone(), o["s_out"].clone(), o["row_map"].clone()))
+        for k in knobs:
+            monkeypatch.delenv(k)
+    for q, s, rm in outs[1:]:
+        assert torch.equal(q, outs[0][0]) and torch.equal(s, outs[0][1]) and torch.equal(rm, outs[0][2])
