@@ -163,10 +163,14 @@ class DeviceStep:
 
     def launch_ops(self, record: bool) -> None:
         if NVTX:  # opt-in NVTX ranges per op for profiler filtering (host calls; off when timing)
+            if record:
+                self.events[0].record()
             for i, (op, fn) in enumerate(self.op_fns().items()):
                 torch.cuda.nvtx.range_push(op)
                 fn()
                 torch.cuda.nvtx.range_pop()
+                if record:
+                    self.events[i + 1].record()
             return
         F, hw, ev = self.F, self.hw, self.events
         if record:
