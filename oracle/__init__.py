@@ -21,6 +21,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fp8flow_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tests/test_oracle_mutations.py points this at a deliberately broken build of the same source to
+# show that the pins catch the mutation; never set otherwise.
+_LIB_OVERRIDE = os.environ.get("FP8FLOW_ORACLE_LIB")
 _lock = threading.Lock()
 _lib = None
 
@@ -40,8 +43,11 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            build()
-            L = ctypes.CDLL(_LIB)
+            if _LIB_OVERRIDE:
+                L = ctypes.CDLL(_LIB_OVERRIDE)
+            else:
+                build()
+                L = ctypes.CDLL(_LIB)
             P = ctypes.c_void_p
             I64 = ctypes.c_int64
             I32 = ctypes.c_int32

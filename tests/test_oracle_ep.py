@@ -124,3 +124,23 @@ def test_combine_two_ranks_equals_a4_over_concatenation(orc):
         y = orc.combine(xs, [p[0] for p in plans], ts[g], E // n, probs=ps[g], token_begin=g * tpr)
         ref = orc.unpermute(x_cat, rm_glob[g * tpr:(g + 1) * tpr], ps[g])
         assert np.array_equal(y, ref)
+
+
+def test_combine_k_order_half_ulp_tie(orc):
+    """R34 / R21: combine sums a token's K terms in fp32 in k order across the ranks that hold
+    them (no per-rank partial sums).  Same hand-built terms as the A4 pin
+    (test_unpermute_k_order_half_ulp_tie): 1, 2^-8, 2^-24, 2^-24 in k order -> BF16 0x3F80;
+    the reversed listing -> 0x3F81.  Two ranks, two experts each; each rank holds two of the
+    terms, so the order crosses ranks."""
+    H = 128
+    one, e8, e24 = 0x3F80, 0x3B80, 0x3380
+    # rank 0 holds experts 0, 1; rank 1 holds experts 2, 3.  Rows: x_0 = [1, 2^-24], x_1 = [2^-8, 2^-24]
+    x0 = np.repeat(np.array([one, e24], np.uint16)[:, None], H, axis=1)
+    x1 = np.repeat(np.array([e8, e24], np.uint16)[:, None], H, axis=1)
+    # token 0: experts [0, 2, 1, 3] -> terms 1, 2^-8, 2^-24, 2^-24; token 1: the reverse listing
+    topk = np.array([[0, 2, 1, 3], [3, 1, 2, 0]], np.int32)
+    rm0 = np.array([[0, -1, 1, -1], [-1, 1, -1, 0]], np.int32)     # rows on rank 0 (experts 0, 1)
+    rm1 = np.array([[-1, 0, -1, 1], [1, -1, 0, -1]], np.int32)     # rows on rank 1 (experts 2, 3)
+    for probs in (None, np.ones((2, 4), np.float32)):
+        y = orc.combine([x0, x1], [rm0, rm1], topk, 2, probs=probs)
+        assert np.all(y[0] == one) and np.all(y[1] == 0x3F81), (probs is None, y[:, 0])

@@ -142,6 +142,26 @@ def test_unpermute_weighted_sum_fp32_order(orc):
     assert np.array_equal(y, f32_to_bits(acc))
 
 
+def test_unpermute_k_order_half_ulp_tie(orc):
+    """R21: the terms are summed in fp32 in k order from +0, then rounded once to
+    BF16.  Hand-built terms where that order is visible in the BF16 result:
+        1, 2^-8, 2^-24, 2^-24  (all exact BF16)
+    k order: 1 + 2^-8 is exact; + 2^-24 is an fp32 tie (ulp 2^-23 at 1) -> even -> 1 + 2^-8,
+    twice; BF16(1 + 2^-8) is a BF16 tie (ulp 2^-7) -> even -> 1.0 = 0x3F80.
+    The reverse order (or pairwise sums, or an fp64 accumulator) keeps 2^-23 and ends at
+    1 + 2^-8 + 2^-23 -> rounds up to 1 + 2^-7 = 0x3F81.  A second token lists the same rows in
+    the opposite order, so its k-order result is 0x3F81.  Checked through the plain-add path
+    (probs NULL) and the fused multiply-add path (p = 1)."""
+    H = 128
+    vals = np.array([0x3F80, 0x3B80, 0x3380, 0x3380], np.uint16)         # 1, 2^-8, 2^-24, 2^-24
+    assert np.array_equal(bits_to_f64(vals), [1.0, 2.0 ** -8, 2.0 ** -24, 2.0 ** -24])
+    x = np.repeat(vals[:, None], H, axis=1)
+    row_map = np.array([[0, 1, 2, 3], [3, 2, 1, 0]], np.int32)
+    for probs in (None, np.ones((2, 4), np.float32)):
+        y = orc.unpermute(x, row_map, probs)
+        assert np.all(y[0] == 0x3F80) and np.all(y[1] == 0x3F81), (probs is None, y[:, 0])
+
+
 # ------------------------------------------------------------------------------ A5
 def test_swiglu_values_match_torch_float64(orc):
     h = synth.normal_bf16(256, 1024, 10, sigma=1.5)

@@ -243,6 +243,51 @@ def test_naive_constant_and_block_uniform_cases(orc):
     assert np.array_equal(va, vb)
 
 
+def test_naive_fresh_scale_per_column_block(orc):
+    """P:130 / P:224 (R29): the naive route dequantizes, transposes and re-quantizes column-wise,
+    with a FRESH pow2 scale for every (column, 128-row block of a segment).  Hand-built input
+    whose column maxima differ between the blocks of one segment and between columns, so any other
+    grouping of the amax (whole column, whole segment, blocks counted from the tensor's row 0,
+    the wrong source tile's row scale) changes scales and codes.
+
+    Value of local row l (segment e, block b = l // 128) at column j:
+        X = sgn * v(l) * 2^a,   a = (j + 3b + e) mod 8 - 4,   v(l) = [1, 0.75, 0.5, 0.625][l % 4]
+    (every block contains v = 1 rows, so the (column, block) amax is exactly 2^a).  Closed form of
+    the expected result, from Eq. 2 with the least-T pow2 rule (R3): amax 2^a <= 448 * 2^T  <=>
+    T = a - 8; the code is E4M3(X * 2^-T) = E4M3(sgn * 256 * v(l)), cast here by torch.
+    The row-wise input is built directly: codes = torch E4M3 of X * 2^-T_row with per-row,
+    per-tile T_row in {-2, -1, 0} (all values exact, no underflow)."""
+    m = [16, 256, 144]                                   # partial block, two full blocks, 128 + 16
+    seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
+    rows, cols = int(seg[-1]), 256
+    vtab = np.array([1.0, 0.75, 0.5, 0.625])
+    X = np.zeros((rows, cols))
+    A = np.zeros((rows, cols), np.int64)                 # the exponent a of each element
+    for e in range(3):
+        for l in range(m[e]):
+            i = int(seg[e]) + l
+            j = np.arange(cols)
+            A[i] = (j + 3 * (l // 128) + e) % 8 - 4
+            sgn = np.where((i * 7 + j) % 3 == 0, -1.0, 1.0)
+            X[i] = sgn * vtab[l % 4] * np.exp2(A[i])
+    Trow = (np.arange(rows)[None, :] + np.arange(cols // 128)[:, None]) % 3 - 2      # [tiles, rows]
+    s = (Trow + 127).astype(np.uint8)
+    q = lib_encode(X * np.exp2(-np.repeat(Trow.T, 128, axis=1)))
+    assert np.array_equal(tile_dequant(q, s), X)                                      # exact input
+
+    qT, sT = orc.naive_transpose(q, s, seg)
+    for e, (qe, se) in enumerate(seg_view(qT, sT, cols, seg)):
+        o = int(seg[e])
+        for b in range((m[e] + 127) // 128):
+            lo, hi = o + 128 * b, o + min(128 * (b + 1), m[e])
+            a_blk = A[lo, :]                                                          # [cols]
+            assert np.all(A[lo:hi] == a_blk)
+            assert np.array_equal(se[b], (a_blk - 8 + 127).astype(np.uint8)), (e, b)
+            want = lib_encode((X[lo:hi] * np.exp2(8 - a_blk)[None, :]).T)             # [cols, rows]
+            assert np.all(np.isin(np.abs(X[lo:hi] * np.exp2(8 - a_blk)), 256 * vtab))
+            assert np.array_equal(qe[:, lo - o: hi - o], want), (e, b)
+
+
 def test_double_quantization_error_eq1_real_scales(orc):
     """Eq. 1 / Eq. 9: with real-valued scales (Eq. 2 literal) the naive
     dequantize -> transpose -> column-wise requantize differs from single quantization Q_col(X)."""
