@@ -624,11 +624,11 @@ def ep_setup(device) -> dict:
                           s_out=torch.empty(HIDDEN // 128, mr, dtype=torch.uint8, device=device)))
     peers = ep.LocalPeers(ranks)
 
-    def receive(g, kernel_only=False):
+    def receive(g, kernel_only=False, kernel=F.DISPATCH_AUTO):
         p = plans[g]
         if kernel_only:
             F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), tpr, tpr, HIDDEN, p["row_map"],
-                                           p["src"], p["off"], p["q_out"], p["s_out"])
+                                           p["src"], p["off"], p["q_out"], p["s_out"], kernel=kernel)
         else:
             ep.dispatch_permute(peers, g, tpr, HIDDEN, TOP_K, E, tpr, p["topk_all"], p["row_map"], p["src"],
                                 p["off"], p["ws"], p["q_out"], p["s_out"])
@@ -681,13 +681,7 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
     nb_d = RL.dispatch_permute_bytes(uniq, R0, T_GLOBAL, TOP_K, HIDDEN)
     ms_k = med(lambda: receive(0, kernel_only=True))
     # the register-copy kernel the launcher takes when peers live on other GPUs, on the same data
-    prev = os.environ.get("FP8FLOW_EP_DISPATCH_LSU")
-    os.environ["FP8FLOW_EP_DISPATCH_LSU"] = "1"
-    ms_lsu = med(lambda: receive(0, kernel_only=True))
-    if prev is None:
-        del os.environ["FP8FLOW_EP_DISPATCH_LSU"]
-    else:
-        os.environ["FP8FLOW_EP_DISPATCH_LSU"] = prev
+    ms_lsu = med(lambda: receive(0, kernel_only=True, kernel=F.DISPATCH_REGISTER))
     ms_all = med(lambda: receive(0))
     nb_c = RL.combine_bytes(tpr, TOP_K, HIDDEN, True)
     ms_c = med(lambda: ep.combine(peers, 0, tpr, HIDDEN, E, ranks[0]["topk"], ranks[0]["probs"], y))

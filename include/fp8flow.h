@@ -81,9 +81,11 @@ FP8FLOW_API int fp8flow_device_check(void);
  *     point and its backward twin on dY ("from 12 to 2" P:28; R27).
  *   x_bf16  [rows][cols] BF16, row-major, 16-byte aligned             (read)
  *   q       [rows][cols] E4M3 codes, 16-byte aligned                  (written)
- *   s       [cols/128][ld_s] UE8M0 scale bytes, MN-major; ld_s >= rows, ld_s % 16 == 0 (written
- *           for rows [0, rows) of every tile column; bytes rows..ld_s-1 untouched)
- *   rows >= 0 (0 = no-op), cols > 0 and cols % 128 == 0.
+ *   s       [cols/128][ld_s] UE8M0 scale bytes, MN-major, 16-byte aligned; ld_s >= rows,
+ *           ld_s % 16 == 0 (written for rows [0, rows) of every tile column; bytes rows..ld_s-1
+ *           untouched; the kernel stores 4 rows' bytes as one 32-bit word)
+ *   rows >= 0 (0 = no-op), cols > 0 and cols % 128 == 0.  A misaligned pointer returns
+ *   FP8FLOW_ERR_ALIGN before anything is launched.
  *   Result: q[i][j] = E4M3_RNE(x[i][j] * 2^-T[i][j/128]) (the product is exact; |.| <= 448).
  * ========================================================================================== */
 FP8FLOW_API int fp8flow_quantize_rowwise(const void* x_bf16, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s, int64_t ld_s,
@@ -136,8 +138,12 @@ FP8FLOW_API int fp8flow_naive_transpose(const uint8_t* q, const uint8_t* s, int6
  *                   [offsets[e], offsets[e+1]), count_e real rows in ascending token order then
  *                   ceil(count_e/align)*align - count_e PAD rows (R16)
  *   max_rows        capacity; num_tokens*top_k + E_loc*(align-1) always suffices.  If the padded
- *                   total exceeds it, rows beyond are dropped (row_map = -1) and the workspace's
- *                   first int32 is set to 1 (else 0) -- readable by the caller after sync.
+ *                   total exceeds it, rows beyond are dropped (row_map = -1, src_of_row not
+ *                   written past max_rows), expert_offsets still hold the true padded offsets
+ *                   (so offsets[E_loc] > max_rows) and the workspace's first int32 is set to 1
+ *                   (else 0) -- readable by the caller after sync.  Every consumer of the plan
+ *                   (permute_pad, dispatch, SwiGLU via rows_dev) clamps the row count to its
+ *                   max_rows / rows_max, so an overflowed plan never writes out of bounds.
  *   ws              device workspace of fp8flow_permute_workspace_bytes() bytes
  *   1 <= top_k <= 16, 1 <= E_loc <= 1024, num_tokens >= 0.  Deterministic: the plan depends only
  *   on topk_idx (no atomics decide an order).
@@ -149,7 +155,7 @@ FP8FLOW_API int fp8flow_permute_plan(const int32_t* topk_idx, int64_t num_tokens
 
 /* fp8flow_permute_pad -- move row-wise FP8 tokens into the padded expert-major buffer in one pass:
  *   q_out[r] = q_tok[src_of_row[r]], s_out[j][r] = s_tok[j][src_of_row[r]] for r < R =
- *   expert_offsets[E_loc]; PAD rows get code 0x00 and scale byte 0x00 (R17, R11).
+ *   min(expert_offsets[E_loc], max_rows); PAD rows get code 0x00 and scale byte 0x00 (R17, R11).
  *   q_tok [num_tokens][hidden] + s_tok [hidden/128][ld_s_tok]  (row-wise FP8, as from A1)
  *   q_out [max_rows][hidden], s_out [hidden/128][max_rows]       (rows >= R untouched)
  *   hidden % 128 == 0; q_tok, q_out 16-byte aligned; max_rows % 16 == 0. */
@@ -177,7 +183,7 @@ FP8FLOW_API int fp8flow_unpermute_unpad(const void* x_bf16, int64_t hidden, cons
  *     acceptance: codes within 1 E4M3 ULP on <= 1e-4 of elements, scale bytes identical.
  *   h_bf16  [rows_max][2*ffn] BF16, 16-byte aligned
  *   rows_dev device int32 holding the actual row count (e.g. &expert_offsets[E_loc]), or NULL
- *           for rows_max rows; must be <= rows_max
+ *           for rows_max rows; a larger value (an overflowed plan's true total) is clamped to rows_max
  *   q       [rows_max][ffn] E4M3 codes; s [ffn/128][ld_s] MN-major, ld_s >= rows_max, % 16 == 0
  *   ffn % 128 == 0.
  * ========================================================================================== */
@@ -296,12 +302,17 @@ FP8FLOW_API int fp8flow_ipc_close(void* base);
 FP8FLOW_API int fp8flow_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int32_t* status,
                                      uint32_t timeout_ms, void* stream);
 
+/* Gating on the barrier's status (gather, dispatch, combine): `status` is a device int32 or NULL.
+ * When non-NULL and nonzero at the time the kernel runs (the preceding fp8flow_peer_barrier on the
+ * stream timed out, so a peer's buffers may be incomplete), the kernel writes NOTHING and returns;
+ * the caller must read status after the step and discard its outputs.  NULL = ungated. */
+
 /* fp8flow_peer_gather -- all-gather by pulls: dst[r*bytes_per_rank ...] = peer_src[r][0 .. bytes_per_rank)
  * (e.g. every rank's topk_idx for the dispatch plan).  bytes_per_rank % 4 == 0 (16-byte copies
  * when bytes_per_rank % 16 == 0, else 4-byte words), all pointers 16-byte aligned, dst device
- * [n*bytes_per_rank]. */
+ * [n*bytes_per_rank].  status: the barrier gate above. */
 FP8FLOW_API int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
-                                    void* stream);
+                                    const int32_t* status, void* stream);
 
 /* fp8flow_dispatch_permute_pad -- the receive side of the FP8 dispatch fused with A3's move: every
  *   token routed to one of this rank's experts is read ONCE from its owner (codes + scale bytes)
@@ -313,14 +324,23 @@ FP8FLOW_API int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int6
  *             [n*tokens_per_rank][top_k] with this rank's expert range (global token ids)
  *   q_out [max_rows][hidden], s_out [hidden/128][max_rows] (rows >= expert_offsets[E_loc] untouched)
  *   hidden % 128 == 0, q pointers 16-byte aligned, 1 <= top_k <= 16, ld_s_tok >= tokens_per_rank.
- *   Kernel choice (same result): when every peer_q lives on the calling device, a bulk-copy engine
- *   (cp.async.bulk token pulls into shared memory, bulk stores per row); when any lives on another
- *   device, register copies with plain 128-bit loads (valid on every peer mapping). */
+ *   kernel    which kernel (identical results): FP8FLOW_DISPATCH_ENGINE = bulk-copy engine
+ *             (cp.async.bulk token pulls into shared memory, bulk stores per row; verified for
+ *             peers on the calling device; FP8FLOW_ERR_CUDA if its shared-memory ring cannot hold
+ *             the shape, roughly hidden > 9K at DSv3 token counts), FP8FLOW_DISPATCH_REGISTER =
+ *             register copies with plain 128-bit loads (valid on every peer mapping and shape),
+ *             FP8FLOW_DISPATCH_AUTO = the engine when every peer_q lives on the calling device and
+ *             the ring fits, else register copies.  Other values: FP8FLOW_ERR_ARG.
+ *   status    the barrier gate above. */
+#define FP8FLOW_DISPATCH_AUTO 0
+#define FP8FLOW_DISPATCH_ENGINE 1
+#define FP8FLOW_DISPATCH_REGISTER 2
 FP8FLOW_API int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s,
                                              int64_t ld_s_tok, int32_t n, int64_t tokens_per_rank, int64_t hidden,
                                              const int32_t* row_map, int32_t top_k, const int32_t* src_of_row,
                                              const int32_t* expert_offsets, int32_t num_local_experts,
-                                             int64_t max_rows, uint8_t* q_out, uint8_t* s_out, void* stream);
+                                             int64_t max_rows, uint8_t* q_out, uint8_t* s_out, int32_t kernel,
+                                             const int32_t* status, void* stream);
 
 /* fp8flow_combine_unpermute -- the owner side of the BF16 combine fused with A4: for the caller's
  *   tokens t (global id token_begin + t),
@@ -332,11 +352,11 @@ FP8FLOW_API int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const
  *   peer_x       host array [n]: rank d's expert outputs, BF16 [rows_d][hidden], 16-byte aligned
  *   peer_row_map host array [n]: rank d's plan row_map [n*tokens_per_rank][top_k] (device int32)
  *   topk_idx [num_tokens][top_k], probs fp32 [num_tokens][top_k] or NULL, y BF16 [num_tokens][hidden].
- *   hidden % 8 == 0, 1 <= top_k <= 16. */
+ *   hidden % 8 == 0, 1 <= top_k <= 16.  status: the barrier gate above. */
 FP8FLOW_API int fp8flow_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
                                           int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank,
                                           const float* probs, int64_t token_begin, int64_t num_tokens, int32_t top_k,
-                                          void* y_bf16, void* stream);
+                                          void* y_bf16, const int32_t* status, void* stream);
 
 /* Verification checksum (DESIGN.md §4 C11): *out_dev = sum_i buf[i] * (i * 0x9E3779B97F4A7C15 + 1)
  * mod 2^64 over nbytes bytes.  buf 16-byte aligned; out_dev a device uint64. */

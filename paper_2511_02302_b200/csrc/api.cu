@@ -10,29 +10,34 @@
 
 using namespace fp8flow;
 
-int fp8flow::sched_for(const char* op, int tuned_default) {
-  char name[64] = "FP8FLOW_SCHED_";
-  strncat(name, op, sizeof(name) - strlen(name) - 1);
-  const char* v = getenv(name);
-  if (v && v[0] >= '0' && v[0] <= '2' && v[1] == 0) return v[0] - '0';
-  return tuned_default;
+PFN_encodeTiled fp8flow::tensor_map_encoder() {
+  static PFN_encodeTiled fn = nullptr;  // a process-wide driver entry point (not device state)
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
 }
 
-int fp8flow::tune_int(const char* name, int tuned_default) {
-  char env[64] = "FP8FLOW_";
-  strncat(env, name, sizeof(env) - strlen(env) - 1);
-  const char* v = getenv(env);
-  if (!v || !*v) return tuned_default;
-  char* end = nullptr;
-  const long x = strtol(v, &end, 10);
-  return (*end == 0 && x >= 0 && x < (1 << 20)) ? static_cast<int>(x) : tuned_default;
+bool fp8flow::encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t cols, uint64_t rows,
+                        uint64_t row_pitch_bytes, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swizzle) {
+  PFN_encodeTiled encode = tensor_map_encoder();
+  if (!encode) return false;
+  const cuuint64_t gdim[2] = {cols, rows};
+  const cuuint64_t gstride[1] = {row_pitch_bytes};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estride[2] = {1, 1};
+  return encode(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 namespace {
 
 thread_local int g_last_cuda_error = 0;
 
-constexpr int kMaxDevices = 64;
 int g_dev_ok[kMaxDevices];   // 0 = unknown, 1 = sm_100, 2 = other
 int g_dev_sms[kMaxDevices];
 
@@ -98,7 +103,7 @@ int fp8flow_quantize_rowwise(const void* x_bf16, int64_t rows, int64_t cols, uin
   if (ld_s < rows || ld_s % 16 != 0) return FP8FLOW_ERR_SHAPE;
   if (rows == 0) return FP8FLOW_OK;
   if (!x_bf16 || !q || !s) return FP8FLOW_ERR_NULL;
-  if (!aligned16(x_bf16) || !aligned16(q)) return FP8FLOW_ERR_ALIGN;
+  if (!aligned16(x_bf16) || !aligned16(q) || !aligned16(s)) return FP8FLOW_ERR_ALIGN;
   int sms = 0, st = device(&sms);
   if (st != FP8FLOW_OK) return st;
   return launched(launch_quantize_rowwise(x_bf16, rows, cols, q, s, ld_s, static_cast<cudaStream_t>(stream), sms));
@@ -353,7 +358,8 @@ int fp8flow_peer_barrier(void* const* peer_signal, int32_t rank, int32_t n, int3
   return launched(launch_peer_barrier(peer_signal, rank, n, status, timeout_ms, static_cast<cudaStream_t>(stream)));
 }
 
-int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst, void* stream) {
+int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
+                        const int32_t* status, void* stream) {
   if (n < 1 || n > FP8FLOW_MAX_RANKS) return FP8FLOW_ERR_ARG;
   if (bytes_per_rank < 0 || bytes_per_rank % 4 != 0) return FP8FLOW_ERR_SHAPE;
   if (bytes_per_rank == 0) return FP8FLOW_OK;
@@ -363,15 +369,17 @@ int fp8flow_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_pe
   if (!aligned16(dst)) return FP8FLOW_ERR_ALIGN;
   int sms = 0;
   if ((st = device(&sms)) != FP8FLOW_OK) return st;
-  return launched(launch_peer_gather(peer_src, n, bytes_per_rank, dst, static_cast<cudaStream_t>(stream), sms));
+  return launched(
+      launch_peer_gather(peer_src, n, bytes_per_rank, dst, status, static_cast<cudaStream_t>(stream), sms));
 }
 
 int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* const* peer_s, int64_t ld_s_tok,
                                  int32_t n, int64_t tokens_per_rank, int64_t hidden, const int32_t* row_map,
                                  int32_t top_k, const int32_t* src_of_row, const int32_t* expert_offsets,
                                  int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
-                                 void* stream) {
+                                 int32_t kernel, const int32_t* status, void* stream) {
   if (n < 1 || n > FP8FLOW_MAX_RANKS) return FP8FLOW_ERR_ARG;
+  if (kernel < FP8FLOW_DISPATCH_AUTO || kernel > FP8FLOW_DISPATCH_REGISTER) return FP8FLOW_ERR_ARG;
   if (top_k < 1 || top_k > 16 || num_local_experts < 1 || num_local_experts > 1024) return FP8FLOW_ERR_ARG;
   if (tokens_per_rank < 0 || hidden <= 0 || hidden % 128 != 0 || max_rows < 0) return FP8FLOW_ERR_SHAPE;
   if (ld_s_tok < tokens_per_rank) return FP8FLOW_ERR_SHAPE;
@@ -386,12 +394,13 @@ int fp8flow_dispatch_permute_pad(const uint8_t* const* peer_q, const uint8_t* co
   if ((st = device(&sms)) != FP8FLOW_OK) return st;
   return launched(launch_dispatch_permute_pad(peer_q, peer_s, ld_s_tok, n, tokens_per_rank, hidden, row_map, top_k,
                                               src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out,
-                                              static_cast<cudaStream_t>(stream), sms));
+                                              kernel, status, static_cast<cudaStream_t>(stream), sms));
 }
 
 int fp8flow_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
                               int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank, const float* probs,
-                              int64_t token_begin, int64_t num_tokens, int32_t top_k, void* y_bf16, void* stream) {
+                              int64_t token_begin, int64_t num_tokens, int32_t top_k, void* y_bf16,
+                              const int32_t* status, void* stream) {
   if (n < 1 || n > FP8FLOW_MAX_RANKS || experts_per_rank < 1) return FP8FLOW_ERR_ARG;
   if (top_k < 1 || top_k > 16) return FP8FLOW_ERR_ARG;
   if (num_tokens < 0 || token_begin < 0 || hidden <= 0 || hidden % 8 != 0) return FP8FLOW_ERR_SHAPE;
@@ -404,8 +413,8 @@ int fp8flow_combine_unpermute(const void* const* peer_x, const int32_t* const* p
   int sms = 0;
   if ((st = device(&sms)) != FP8FLOW_OK) return st;
   return launched(launch_combine_unpermute(peer_x, peer_row_map, n, hidden, topk_idx, experts_per_rank, probs,
-                                           token_begin, num_tokens, top_k, y_bf16, static_cast<cudaStream_t>(stream),
-                                           sms));
+                                           token_begin, num_tokens, top_k, y_bf16, status,
+                                           static_cast<cudaStream_t>(stream), sms));
 }
 
 }  // extern "C"

@@ -63,23 +63,6 @@ __device__ __forceinline__ float scale_from_byte(uint32_t byte) {
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
-// Warp-level work-item schedules (all items are independent):
-//   kSchedOnePerWarp  : one item per warp, grid = ceil(items / warps per CTA); the hardware CTA
-//                       scheduler balances (short-lived CTAs, no tail beyond one item)
-//   kSchedBlocked     : one wave of CTAs, warp g takes the contiguous range [g*n/W, (g+1)*n/W)
-//   kSchedInterleaved : one wave of CTAs, warp g takes items g, g+W, g+2W, ...
-enum Sched : int { kSchedOnePerWarp = 0, kSchedBlocked = 1, kSchedInterleaved = 2 };
-struct ItemIter {
-  int64_t cur, end, step;
-};
-__device__ __forceinline__ ItemIter warp_item_iter(int64_t n_items, int sched) {
-  const int64_t wpb = blockDim.x >> 5;
-  const int64_t W = static_cast<int64_t>(gridDim.x) * wpb;
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * wpb + (threadIdx.x >> 5);
-  if (sched == kSchedBlocked) return {g * n_items / W, (g + 1) * n_items / W, 1};
-  return {g, n_items, W};
-}
-
 // half-warp (16 lanes) max reduction; every lane of the half receives the result
 __device__ __forceinline__ uint32_t halfwarp_max_u32(uint32_t v) {
   v = max(v, __shfl_xor_sync(0xffffffffu, v, 8));
@@ -122,13 +105,27 @@ __device__ __forceinline__ uint32_t cvt_e4m3x4_from_f16x2_pairs(uint32_t p02, ui
       : "r"(p02), "r"(p13));
   return __byte_perm(r, 0u, 0x3120);  // [c0, c2, c1, c3] -> [c0, c1, c2, c3]
 }
-__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t m2) {
+// nan_acc accumulates the largest f16 magnitude half seen (u16x2 max): a code of magnitude 0x7F
+// (E4M3 NaN) is the only one that maps to 0x3F80, so has_nan_code() tells a caller to patch the
+// (rare) words holding NaN codes with keep_nan_codes() -- NaN propagates unchanged, as in the
+// oracle's shift (the f16 path alone would turn it into a finite code).
+__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t m2, uint32_t& nan_acc) {
   const uint32_t lo02 = (w & 0x007F007Fu) << 7;            // bytes 0, 2 -> f16 halves (value * 2^-8)
   const uint32_t hi13 = (w >> 1) & 0x3F803F80u;            // bytes 1, 3
+  nan_acc = __vmaxu2(nan_acc, __vmaxu2(lo02, hi13));
   __half2 p02 = __hmul2(*reinterpret_cast<const __half2*>(&lo02), *reinterpret_cast<const __half2*>(&m2));
   __half2 p13 = __hmul2(*reinterpret_cast<const __half2*>(&hi13), *reinterpret_cast<const __half2*>(&m2));
   return cvt_e4m3x4_from_f16x2_pairs(*reinterpret_cast<uint32_t*>(&p02), *reinterpret_cast<uint32_t*>(&p13)) |
          (w & 0x80808080u);
+}
+__device__ __forceinline__ bool has_nan_code(uint32_t nan_acc) {
+  return (nan_acc & 0xFFFFu) == 0x3F80u || (nan_acc >> 16) == 0x3F80u;
+}
+// bytes of w whose magnitude is 0x7F (NaN) replace the corresponding bytes of `shifted`
+__device__ __forceinline__ uint32_t keep_nan_codes(uint32_t shifted, uint32_t w) {
+  const uint32_t t = ((w & 0x7F7F7F7Fu) + 0x01010101u) & 0x80808080u;  // bit 7 of every NaN byte
+  const uint32_t m = (t >> 7) * 0xFFu;
+  return (shifted & ~m) | (w & m);
 }
 
 // ------------------------------------------------------------------------------------------

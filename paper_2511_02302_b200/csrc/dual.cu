@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
   Smem& sm = *reinterpret_cast<Smem*>(smem_dual);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
-  const int64_t rows = rows_dev != nullptr ? static_cast<int64_t>(*rows_dev) : rows_max;
+  const int64_t rows = rows_dev != nullptr ? min64(static_cast<int64_t>(*rows_dev), rows_max) : rows_max;  // clamped: an overflowed plan reports its true total
 
   if (tid == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -274,15 +274,26 @@ __global__ void __launch_bounds__(kDThreads, 1)
     const uint32_t sw = sm.sc[b][lane];  // scale bytes of rows 4a..4a+3
     const int pchunk = ((w ^ lane) & 7) << 2;  // physical word offset of chunk w in rows 4a..4a+3
     uint32_t R[4][4];
+    uint32_t nan_acc = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint4 v = *reinterpret_cast<const uint4*>(&sm.ctile[b][(4 * lane + r) * (kDT / 4) + pchunk]);
       const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // rows outside the segment: never stored
       const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v.x, m2);
-      R[r][1] = shift4(v.y, m2);
-      R[r][2] = shift4(v.z, m2);
-      R[r][3] = shift4(v.w, m2);
+      R[r][0] = shift4(v.x, m2, nan_acc);
+      R[r][1] = shift4(v.y, m2, nan_acc);
+      R[r][2] = shift4(v.z, m2, nan_acc);
+      R[r][3] = shift4(v.w, m2, nan_acc);
+    }
+    if (__any_sync(0xffffffffu, has_nan_code(nan_acc))) {  // rare: NaN codes keep their bytes
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint4 v = *reinterpret_cast<const uint4*>(&sm.ctile[b][(4 * lane + r) * (kDT / 4) + pchunk]);
+        R[r][0] = keep_nan_codes(R[r][0], v.x);
+        R[r][1] = keep_nan_codes(R[r][1], v.y);
+        R[r][2] = keep_nan_codes(R[r][2], v.z);
+        R[r][3] = keep_nan_codes(R[r][3], v.w);
+      }
     }
     mbar_arrive(&sm.cempty[b]);  // (per thread) its reads of code tile b, scales and maxima are done
     if (4 * lane < rows_valid) {
@@ -308,43 +319,17 @@ __global__ void __launch_bounds__(kDThreads, 1)
   }
 }
 
-typedef CUresult (*PFN_encodeTiled_d)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-PFN_encodeTiled_d encode_fn() {
-  static PFN_encodeTiled_d fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) == cudaSuccess &&
-        qres == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_d>(p);
-  }
-  return fn;
-}
-
 template <int OP, int STAGES>
 cudaError_t launch_dual(const void* in, int64_t in_cols, int64_t rows_max, const int32_t* rows_dev, int64_t cols,
                         const int32_t* seg_offsets, int32_t num_segs, uint8_t* q, uint8_t* s, int64_t ld_s,
                         uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
-  PFN_encodeTiled_d encode = encode_fn();
-  if (!encode) return cudaErrorNotSupported;
   using Smem = DualSmem<OP, STAGES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dual_kernel<OP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(Smem)));
-    attr = true;
-  }
+  static KernelSetup setup;
+  if (prepare_kernel(setup, dual_kernel<OP, STAGES>, kDThreads, sizeof(Smem), sizeof(Smem)) == 0)
+    return cudaErrorInvalidValue;
   CUtensorMap map;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(in_cols), static_cast<cuuint64_t>(rows_max)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(2 * in_cols)};
-  const cuuint32_t box[2] = {kDT, kDHalf};
-  const cuuint32_t estride[2] = {1, 1};
-  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(in), gdim, gstride, box, estride,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+  if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, static_cast<uint64_t>(in_cols),
+                 static_cast<uint64_t>(rows_max), static_cast<uint64_t>(2 * in_cols), kDT, kDHalf))
     return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows_max / kDT + (seg_offsets ? num_segs : 1)) * (cols / kDT);
   int64_t grid = ub_tiles < num_sms ? ub_tiles : num_sms;

@@ -45,7 +45,9 @@ struct PeerPtrs2 {
 // ---------------------------------------------------------------------------------------------
 template <typename V>
 __global__ void __launch_bounds__(kEpThreads) peer_gather_kernel(PeerPtrs src, int n, int64_t vec_per_rank,
-                                                                 V* __restrict__ out) {
+                                                                 V* __restrict__ out,
+                                                                 const int32_t* __restrict__ gate) {
+  if (gate != nullptr && *gate != 0) return;  // the barrier before it timed out: peers not ready
   const int64_t total = vec_per_rank * n;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(kEpThreads) peer_gather_kernel(PeerPtrs src, i
 }
 
 cudaError_t launch_peer_gather(const void* const* peer_src, int32_t n, int64_t bytes_per_rank, void* dst,
-                               cudaStream_t stream, int num_sms) {
+                               const int32_t* gate, cudaStream_t stream, int num_sms) {
   PeerPtrs pp{};
   for (int r = 0; r < n; ++r) pp.p[r] = peer_src[r];
   const bool v16 = bytes_per_rank % 16 == 0;  // else 4-byte words (the ABI requires bytes % 4 == 0)
@@ -69,10 +71,11 @@ cudaError_t launch_peer_gather(const void* const* peer_src, int32_t n, int64_t b
   if (grid > 4LL * num_sms) grid = 4LL * num_sms;
   if (grid < 1) grid = 1;
   if (v16)
-    peer_gather_kernel<uint4><<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec, static_cast<uint4*>(dst));
+    peer_gather_kernel<uint4><<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec, static_cast<uint4*>(dst),
+                                                                                     gate);
   else
     peer_gather_kernel<uint32_t><<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(pp, n, vec,
-                                                                                        static_cast<uint32_t*>(dst));
+                                                                                        static_cast<uint32_t*>(dst), gate);
   return cudaGetLastError();
 }
 
@@ -149,13 +152,14 @@ cudaError_t launch_peer_barrier(void* const* peer_signal, int32_t rank, int32_t 
 __global__ void __launch_bounds__(kEpThreads) dispatch_permute_lsu_kernel(
     PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
     const int32_t* __restrict__ src_of_row, const int32_t* __restrict__ offsets, int E_loc, int64_t max_rows,
-    uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out) {
+    uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out, const int32_t* __restrict__ gate) {
+  if (gate != nullptr && *gate != 0) return;  // the barrier before it timed out: peers not ready
   const int lane = threadIdx.x & 31;
   const int64_t W = static_cast<int64_t>(gridDim.x) * kEpWarps;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEpWarps + (threadIdx.x >> 5);
   const int64_t T = Tpr * n;
   const int64_t n_tiles = H / 128;
-  const int64_t R = offsets[E_loc];
+  const int64_t R = min64(offsets[E_loc], max_rows);  // an overflowed plan: only max_rows rows exist
 
   // warp roles: the first S warps gather the scale bytes (by 32-token batches, below), the other
   // Wc warps copy the codes -- so the scale batches' few serial link round trips overlap the
@@ -278,7 +282,9 @@ template <int SLACK>
 __global__ void __launch_bounds__(256) dispatch_engine_kernel(
     PeerPtrs2 peer, int64_t ld_s_tok, int64_t Tpr, int n, int64_t H, const int32_t* __restrict__ row_map, int K,
     const int32_t* __restrict__ src_of_row, const int32_t* __restrict__ offsets, int E_loc, int64_t max_rows,
-    uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out, int nslots, int list_cap) {
+    uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out, int nslots, int list_cap,
+    const int32_t* __restrict__ gate) {
+  if (gate != nullptr && *gate != 0) return;  // the barrier before it timed out: peers not ready
   extern __shared__ __align__(128) uint8_t smem_disp[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_disp);
   int32_t* list_n = reinterpret_cast<int32_t*>(full + kDispMaxSlots);
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(256) dispatch_engine_kernel(
     // scales, row-major like A3's move: the CTA's contiguous share of the output rows, (row, tile)
     // pairs with consecutive threads on consecutive rows (coalesced stores); a row's byte comes
     // from its source token's owner (src_of_row holds the global token id), PAD rows get 0x00
-    const int64_t R_all = offsets[E_loc];
+    const int64_t R_all = min64(offsets[E_loc], max_rows);
     const int64_t rb = cta * R_all / G;
     const int nr = static_cast<int>((cta + 1) * R_all / G - rb);
     const int tpr = static_cast<int>(Tpr);
@@ -372,7 +378,7 @@ __global__ void __launch_bounds__(256) dispatch_engine_kernel(
       s_out[static_cast<int64_t>(tl) * max_rows + r] = v;
     }
     // PAD rows: 32-row chunks over the grid's warps 1..7
-    const int64_t R = offsets[E_loc];
+    const int64_t R = min64(offsets[E_loc], max_rows);  // an overflowed plan: only max_rows rows exist
     for (int64_t c = cta * 7 + (warp - 1); c * 32 < R; c += G * 7) {
       const int64_t r0 = c * 32;
       const bool pad = r0 + lane < R && src_of_row[r0 + lane] < 0;
@@ -388,7 +394,7 @@ cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint
                                         int32_t n, int64_t tokens_per_rank, int64_t hidden, const int32_t* row_map,
                                         int32_t top_k, const int32_t* src_of_row, const int32_t* expert_offsets,
                                         int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
-                                        cudaStream_t stream, int num_sms) {
+                                        int32_t kernel, const int32_t* gate, cudaStream_t stream, int num_sms) {
   PeerPtrs2 pp{};
   for (int r = 0; r < n; ++r) {
     pp.a[r] = peer_q[r];
@@ -396,63 +402,57 @@ cudaError_t launch_dispatch_permute_pad(const uint8_t* const* peer_q, const uint
   }
   const int64_t T = tokens_per_rank * n;
   // The bulk-copy engine reads peers with cp.async.bulk; that is verified only for buffers on the
-  // calling device (virtual ranks, processes sharing a GPU).  When any peer's codes live on another
-  // device (NVLink), the register-copy kernel -- plain 128-bit loads, valid on every peer
-  // mapping -- is used instead.  FP8FLOW_EP_DISPATCH_LSU=1 forces it, =0 forces the engine.
-  const int force = tune_int("EP_DISPATCH_LSU", 2);
-  bool remote = false;
-  if (force == 2) {
+  // calling device (virtual ranks, processes sharing a GPU).  AUTO takes the register-copy kernel
+  // -- plain 128-bit loads, valid on every peer mapping -- when any peer's codes live on another
+  // device (NVLink), or when the engine's shared-memory ring does not fit the shape.
+  bool use_engine = kernel != 2;  // 0 auto, 1 engine, 2 register copies (fp8flow.h)
+  if (kernel == 0) {
     int dev = 0;
-    cudaGetDevice(&dev);
-    for (int r = 0; r < n && !remote; ++r) {
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    for (int r = 0; r < n && use_engine; ++r) {
       cudaPointerAttributes a;
       if (cudaPointerGetAttributes(&a, peer_q[r]) != cudaSuccess) {
         cudaGetLastError();
-        remote = true;  // unknown mapping: take the path that is valid everywhere
+        use_engine = false;  // unknown mapping: take the path that is valid everywhere
       } else if (a.device != dev) {
-        remote = true;
+        use_engine = false;
       }
     }
   }
-  if (force == 1 || (force == 2 && remote)) {
-    static const int occ = occupancy_of(dispatch_permute_lsu_kernel, kEpThreads, 0);
-    const int64_t need = (T + kEpWarps - 1) / kEpWarps;
-    const int64_t grid = one_wave_grid(occ, num_sms, need > num_local_experts ? need : num_local_experts);
-    dispatch_permute_lsu_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(
-        pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
-        max_rows, q_out, s_out);
-    return cudaGetLastError();
-  }
-  // CTAS_PER_SM_DISP co-resident CTAs per SM (smem budget split); more CTAs (queued) when a CTA
-  // would own more than 256 tokens
-  const int ctas = tune_int("CTAS_PER_SM_DISP", 4) > 0 ? tune_int("CTAS_PER_SM_DISP", 4) : 1;
-  const size_t budget = kDispSmemBudget / ctas;
-  int64_t grid = static_cast<int64_t>(num_sms) * ctas;
+  // engine geometry: 4 co-resident CTAs per SM share the shared-memory budget (1 CTA/SM 54 us,
+  // 2 34.7, 4 32.8 at DSv3 sizes); more CTAs (queued) when a CTA would own more than 256 tokens
+  constexpr int kCtasPerSm = 4;
+  const size_t budget = kDispSmemBudget / kCtasPerSm;
+  int64_t grid = static_cast<int64_t>(num_sms) * kCtasPerSm;
   if ((T + grid - 1) / grid > 256) grid = (T + 255) / 256;
   const int list_cap = static_cast<int>((T + grid - 1) / grid);
   const size_t head = ((8 * kDispMaxSlots + 16 + 4 * static_cast<size_t>(list_cap) * kDispListStride + 127) / 128) * 128;
-  if (head + static_cast<size_t>(hidden) * (kDispStoreSlack + 2) > budget) return cudaErrorInvalidValue;
-  int nslots = static_cast<int>((budget - head) / hidden);
+  int nslots = head + static_cast<size_t>(hidden) * (kDispStoreSlack + 2) <= budget
+                   ? static_cast<int>((budget - head) / hidden) : 0;
   if (nslots > kDispMaxSlots) nslots = kDispMaxSlots;
+  if (use_engine && nslots < kDispStoreSlack + 2) {
+    if (kernel == 1) return cudaErrorInvalidValue;  // explicitly requested, cannot run this shape
+    use_engine = false;
+  }
+  if (!use_engine) {
+    static KernelSetup lsu_setup;
+    const int occ = prepare_kernel(lsu_setup, dispatch_permute_lsu_kernel, kEpThreads, 0, 0);
+    if (occ == 0) return cudaErrorInvalidValue;
+    const int64_t need = (T + kEpWarps - 1) / kEpWarps;
+    const int64_t lgrid = one_wave_grid(occ, num_sms, need > num_local_experts ? need : num_local_experts);
+    dispatch_permute_lsu_kernel<<<static_cast<unsigned>(lgrid), kEpThreads, 0, stream>>>(
+        pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
+        max_rows, q_out, s_out, gate);
+    return cudaGetLastError();
+  }
   const size_t smem = head + static_cast<size_t>(hidden) * nslots;
-  const int slack = tune_int("DISP_SLACK", kDispStoreSlack);
-#define FP8FLOW_DISP_LAUNCH(SL)                                                                             \
-  do {                                                                                                      \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      cudaFuncSetAttribute(dispatch_engine_kernel<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                           static_cast<int>(kDispSmemBudget));                                              \
-      attr = true;                                                                                          \
-    }                                                                                                       \
-    if (nslots < SL + 2) return cudaErrorInvalidValue;                                                     \
-    dispatch_engine_kernel<SL><<<static_cast<unsigned>(grid), 256, smem, stream>>>(                         \
-        pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts, \
-        max_rows, q_out, s_out, nslots, list_cap);                                                          \
-  } while (0)
-  if (slack == 2) FP8FLOW_DISP_LAUNCH(2);
-  else if (slack == 8) FP8FLOW_DISP_LAUNCH(8);
-  else FP8FLOW_DISP_LAUNCH(4);
-#undef FP8FLOW_DISP_LAUNCH
+  static KernelSetup engine_setup;
+  if (prepare_kernel(engine_setup, dispatch_engine_kernel<kDispStoreSlack>, 256, kDispSmemBudget, smem) == 0)
+    return cudaErrorInvalidValue;
+  dispatch_engine_kernel<kDispStoreSlack><<<static_cast<unsigned>(grid), 256, smem, stream>>>(
+      pp, ld_s_tok, tokens_per_rank, n, hidden, row_map, top_k, src_of_row, expert_offsets, num_local_experts,
+      max_rows, q_out, s_out, nslots, list_cap, gate);
   return cudaGetLastError();
 }
 
@@ -467,7 +467,9 @@ constexpr int kCombKB = 8;  // rows loaded together
 __global__ void __launch_bounds__(kEpThreads) combine_kernel(PeerPtrs2 peer, int n, int64_t H,
                                                              const int32_t* __restrict__ topk_idx, int E_per,
                                                              const float* __restrict__ probs, int64_t token_begin,
-                                                             int64_t T, int K, __nv_bfloat16* __restrict__ y) {
+                                                             int64_t T, int K, __nv_bfloat16* __restrict__ y,
+                                                             const int32_t* __restrict__ gate) {
+  if (gate != nullptr && *gate != 0) return;  // the barrier before it timed out: peers not ready
   const int lane = threadIdx.x & 31;
   const int64_t W = static_cast<int64_t>(gridDim.x) * kEpWarps;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEpWarps + (threadIdx.x >> 5);
@@ -547,17 +549,19 @@ __global__ void __launch_bounds__(kEpThreads) combine_kernel(PeerPtrs2 peer, int
 cudaError_t launch_combine_unpermute(const void* const* peer_x, const int32_t* const* peer_row_map, int32_t n,
                                      int64_t hidden, const int32_t* topk_idx, int32_t experts_per_rank,
                                      const float* probs, int64_t token_begin, int64_t num_tokens, int32_t top_k,
-                                     void* y, cudaStream_t stream, int num_sms) {
+                                     void* y, const int32_t* gate, cudaStream_t stream, int num_sms) {
   PeerPtrs2 pp{};
   for (int r = 0; r < n; ++r) {
     pp.a[r] = peer_x[r];
     pp.b[r] = peer_row_map[r];
   }
-  static const int occ = occupancy_of(combine_kernel, kEpThreads, 0);
+  static KernelSetup setup;
+  const int occ = prepare_kernel(setup, combine_kernel, kEpThreads, 0, 0);
+  if (occ == 0) return cudaErrorInvalidValue;
   const int64_t grid = one_wave_grid(occ, num_sms, (num_tokens + kEpWarps - 1) / kEpWarps);
   combine_kernel<<<static_cast<unsigned>(grid), kEpThreads, 0, stream>>>(
       pp, n, hidden, topk_idx, experts_per_rank, probs, token_begin, num_tokens, top_k,
-      static_cast<__nv_bfloat16*>(y));
+      static_cast<__nv_bfloat16*>(y), gate);
   return cudaGetLastError();
 }
 

@@ -447,317 +447,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
 }
 
 // =============================================================================================
-// 2-SM variant (cta_group::2): a CTA pair computes a 256 x 256 output tile with M=256 MMAs issued by
-// the even CTA.  Each CTA holds its own 128 rows of A and its half (128 rows) of B, so per SM a
-// K step moves 32 KB into shared memory instead of 48 KB and the stage ring is 6 deep.  The pair
-// takes two consecutive 128-row blocks of one group (an odd last block is computed and masked);
-// both CTAs' TMA loads complete on the even CTA's stage barrier (peer bit cleared), its MMA
-// commits release the stages, scale slots and the accumulator in both CTAs (multicast), and the
-// odd CTA's scale warp and epilogue report to the even CTA's barriers through cluster addresses.
-// Each CTA stages the scales of its own 128 A rows and of all 256 B rows; tcgen05.cp.cta_group::2
-// copies them into both CTAs' tensor memory.
-// =============================================================================================
-constexpr int kG2Stages = 6;
-struct __align__(1024) Fp2Stage {
-  uint8_t a[kGM * kGK];        // this CTA's 128 rows of A
-  uint8_t b[(kGN / 2) * kGK];  // this CTA's 128 rows (half) of B
-};
-struct Gemm2Smem {
-  Fp2Stage st[kG2Stages];
-  alignas(1024) uint8_t stg[8][2048];
-  FpSf sf[2];
-  uint64_t full[kG2Stages];   // (even CTA) TMA bytes of both CTAs
-  uint64_t empty[kG2Stages];  // multicast MMA commit
-  uint64_t sffull[2];         // own scale loads
-  uint64_t sfready[2];        // (even CTA) 64 lanes: both CTAs' scale warps
-  uint64_t sfempty[2];        // multicast MMA commit
-  uint64_t tmem_full;         // multicast MMA commit
-  uint64_t tmem_empty;        // (even CTA) 512 epilogue threads of both CTAs
-  uint32_t tmem_base;
-  uint32_t red[kGThreads / 32];
-  int32_t seg_off[kGMaxGroups + 1];
-  int32_t blk_prefix[kGMaxGroups + 1];
-  int32_t pair_prefix[kGMaxGroups + 1];
-  int32_t total_rb;
-};
-
-__device__ __forceinline__ uint32_t cluster_addr_of(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1) {
-  // executed by both CTAs; the peer bit cleared, the bytes complete on the even CTA's barrier
-  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_mxf8_2sm(uint32_t d_taddr, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                                uint32_t accumulate, uint32_t sfa_taddr, uint32_t sfb_taddr) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_taddr),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_taddr), "r"(sfb_taddr));
-}
-__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(static_cast<uint16_t>(0x3))
-      : "memory");
-}
-__device__ __forceinline__ void tc_cp_2sm(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc));
-}
-__host__ __device__ constexpr uint32_t idesc_mxf8_m256(uint32_t sf_id) {
-  return (sf_id << 4) | (static_cast<uint32_t>(kGN >> 3) << 17) | (1u << 23) | (static_cast<uint32_t>(256 >> 4) << 24) |
-         (sf_id << 29);
-}
-
-struct Gemm2Tile {
-  int g, r0, rows, n0;
-};
-// tile t (over pairs of row blocks of every group x column tiles) -> this CTA's rows
-__device__ __forceinline__ Gemm2Tile gemm2_tile(const Gemm2Smem& sm, int ngroups, int n_nt, int t, int rank) {
-  const int pb = t / n_nt, nt = t - pb * n_nt;
-  int lo = 0, hi = ngroups;  // largest g with pair_prefix[g] <= pb
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (sm.pair_prefix[mid] <= pb) lo = mid;
-    else hi = mid;
-  }
-  const int g = lo;
-  const int r0 = sm.seg_off[g] + (2 * (pb - sm.pair_prefix[g]) + rank) * kGM;
-  return {g, r0, max(0, min(kGM, sm.seg_off[g + 1] - r0)), nt * kGN};
-}
-
-__global__ void __launch_bounds__(kGThreads, 1)
-    gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_d, const __grid_constant__ CUtensorMap tmap_sa,
-                    const __grid_constant__ CUtensorMap tmap_sb, int64_t M, int64_t N, int64_t K,
-                    const int32_t* __restrict__ seg_offsets, int32_t num_groups, void* __restrict__ D, int32_t d_f32) {
-  extern __shared__ __align__(1024) uint8_t smem_g2[];
-  Gemm2Smem& sm = *reinterpret_cast<Gemm2Smem*>((reinterpret_cast<uintptr_t>(smem_g2) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ngroups = seg_offsets == nullptr ? 1 : num_groups;
-  const uint32_t rank = cluster_ctarank();
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  if (tid == 32) {
-    for (int i = 0; i < kG2Stages; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.sffull[i], 1);
-      mbar_init(&sm.sfready[i], 64);
-      mbar_init(&sm.sfempty[i], 1);
-    }
-    mbar_init(&sm.tmem_full, 1);
-    mbar_init(&sm.tmem_empty, 2 * 8 * 32);
-    mbar_init_fence();
-  }
-  tc_fence_before();
-  load_segments<kGThreads>(sm, seg_offsets, ngroups, M);  // ends with a CTA barrier
-  if (warp == 0) {  // pair_prefix[g] = sum over g' < g of ceil(blocks_g' / 2)
-    int run = 0;
-    for (int g0 = 0; g0 <= ngroups; g0 += 32) {
-      const int g = g0 + lane;
-      const int nb = g < ngroups ? sm.blk_prefix[g + 1] - sm.blk_prefix[g] : 0;
-      const int v = (g < ngroups ? (nb + 1) / 2 : 0);
-      int incl = v;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int n = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += n;
-      }
-      if (g <= ngroups) sm.pair_prefix[g] = run + incl - v;
-      run += __shfl_sync(0xffffffffu, incl, 31);
-    }
-  }
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
-  const int n_nt = static_cast<int>(N / kGN);
-  const int nk = static_cast<int>(K / kGK);
-  const int total = sm.pair_prefix[ngroups] * n_nt;
-  const int cl = static_cast<int>(blockIdx.x) / 2, ncl = static_cast<int>(gridDim.x) / 2;
-
-  if (warp == 0) {  // --------------------------------------------------------- TMA producer
-    if (lane == 0) {
-      int st = 0, n = 0, ss = 0, ns = 0;
-      uint32_t parity = 0, sparity = 0;
-      const int kt = static_cast<int>(K / kGK);
-      for (int t = cl; t < total; t += ncl) {
-        const Gemm2Tile T = gemm2_tile(sm, ngroups, n_nt, t, static_cast<int>(rank));
-        for (int kb = 0; kb < nk; ++kb, ++n) {
-          if (kb % kSfGroup == 0) {  // own scales: this CTA's 128 A rows, all 256 B rows
-            if (ns >= 2) mbar_wait(&sm.sfempty[ss], sparity ^ 1u);
-            mbar_expect_tx(&sm.sffull[ss], kSfGroup * (kGM + kGN));
-            tma_load_2d(sm.sf[ss].sa, &tmap_sa, &sm.sffull[ss], T.r0, kb);
-            tma_load_2d(sm.sf[ss].sb, &tmap_sb, &sm.sffull[ss], T.n0, T.g * kt + kb);
-            ++ns;
-            if (++ss == 2) {
-              ss = 0;
-              sparity ^= 1u;
-            }
-          }
-          if (n >= kG2Stages) mbar_wait(&sm.empty[st], parity ^ 1u);
-          Fp2Stage& S = sm.st[st];
-          if (rank == 0) mbar_expect_tx(&sm.full[st], 2 * (kGM * kGK + (kGN / 2) * kGK));
-          tma_load_2d_2sm(S.a, &tmap_a, &sm.full[st], kb * kGK, T.r0);
-          tma_load_2d_2sm(S.b, &tmap_b, &sm.full[st], kb * kGK,
-                          static_cast<int32_t>(T.g * N + T.n0 + static_cast<int>(rank) * (kGN / 2)));
-          if (++st == kG2Stages) {
-            st = 0;
-            parity ^= 1u;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {  // ----------------------------------------- MMA issue (even CTA)
-    if (rank == 0) {
-      int st = 0, ss = 0, ng = 0;
-      uint32_t parity = 0, sparity = 0;
-      for (int t = cl, i = 0; t < total; t += ncl, ++i) {
-        if (i > 0) mbar_wait(&sm.tmem_empty, (i - 1) & 1);
-        tc_fence_after();
-        uint32_t sfa_t = 0, sfb_t = 0;
-        for (int kb = 0; kb < nk; ++kb) {
-          const int j = kb % kSfGroup;
-          if (j == 0) {
-            mbar_wait(&sm.sfready[ss], sparity);
-            tc_fence_after();
-            sfa_t = tmem + kSfCol + 16u * (ng & 1);
-            sfb_t = sfa_t + 4u;
-            if (lane == 0) {
-              tc_cp_2sm(sfa_t, desc_sf_chunk(sm.sf[ss].sfa));
-              tc_cp_2sm(sfb_t, desc_sf_chunk(sm.sf[ss].sfb[0]));
-              tc_cp_2sm(sfb_t + 4u, desc_sf_chunk(sm.sf[ss].sfb[1]));
-            }
-          }
-          mbar_wait(&sm.full[st], parity);
-          tc_fence_after();
-          if (lane == 0) {
-            Fp2Stage& S = sm.st[st];
-            const uint64_t adesc = desc_kmajor_sw128(S.a), bdesc = desc_kmajor_sw128(S.b);
-#pragma unroll
-            for (int k = 0; k < kGK / 32; ++k)
-              tc_mma_mxf8_2sm(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8_m256(static_cast<uint32_t>(j)),
-                              (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
-            tc_commit_2sm_mc(&sm.empty[st]);
-            if (j == kSfGroup - 1 || kb == nk - 1) tc_commit_2sm_mc(&sm.sfempty[ss]);
-          }
-          __syncwarp();
-          if (++st == kG2Stages) {
-            st = 0;
-            parity ^= 1u;
-          }
-          if (j == kSfGroup - 1 || kb == nk - 1) {
-            ++ng;
-            if (++ss == 2) {
-              ss = 0;
-              sparity ^= 1u;
-            }
-          }
-        }
-        if (lane == 0) tc_commit_2sm_mc(&sm.tmem_full);
-        __syncwarp();
-      }
-    }
-  } else if (warp == 2) {  // --------------------------------------------- scale expansion
-    int ss = 0;
-    uint32_t sparity = 0;
-    const uint32_t ready0 = cluster_addr_of(&sm.sfready[0], 0), ready1 = cluster_addr_of(&sm.sfready[1], 0);
-    for (int t = cl; t < total; t += ncl) {
-      for (int kb = 0; kb < nk; kb += kSfGroup) {
-        mbar_wait(&sm.sffull[ss], sparity);
-        FpSf& S = sm.sf[ss];
-        uint32_t w[4];
-#pragma unroll
-        for (int i2 = 0; i2 < 4; ++i2) {
-          const int r = lane + 32 * i2;
-          w[i2] = S.sa[0][r] | (S.sa[1][r] << 8) | (S.sa[2][r] << 16) | (static_cast<uint32_t>(S.sa[3][r]) << 24);
-        }
-        *reinterpret_cast<uint4*>(&S.sfa[lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-#pragma unroll
-          for (int i2 = 0; i2 < 4; ++i2) {
-            const int r = 128 * c + lane + 32 * i2;
-            w[i2] = S.sb[0][r] | (S.sb[1][r] << 8) | (S.sb[2][r] << 16) | (static_cast<uint32_t>(S.sb[3][r]) << 24);
-          }
-          *reinterpret_cast<uint4*>(&S.sfb[c][lane * 16]) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        mbar_arrive_cluster(ss == 0 ? ready0 : ready1);  // the even CTA's barrier
-        if (++ss == 2) {
-          ss = 0;
-          sparity ^= 1u;
-        }
-      }
-    }
-  } else {  // ------------------------------------------------------------------- epilogue
-    const int q = warp & 3;
-    const int half = (warp - 3) >> 2;
-    const uint32_t empty_addr = cluster_addr_of(&sm.tmem_empty, 0);
-    int pending = 0;
-    for (int t = cl, i = 0; t < total; t += ncl, ++i) {
-      const Gemm2Tile T = gemm2_tile(sm, ngroups, n_nt, t, static_cast<int>(rank));
-      mbar_wait(&sm.tmem_full, i & 1);
-      tc_fence_after();
-      uint32_t v[4][32];
-      tc_ld_128cols(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(128 * half), v);
-      tc_fence_before();
-      mbar_arrive_cluster(empty_addr);  // the even CTA's MMAs may reuse the accumulator
-      const int row = 32 * q + lane;
-      if (!d_f32 && 32 * q + 32 <= T.rows) {
-        epilogue_bf16_tma<1>(&tmap_d, sm.stg[warp - 3], v, T.n0 + 128 * half, T.r0 + 32 * q, lane, pending);
-      } else if (row < T.rows) {
-        const int64_t grow = static_cast<int64_t>(T.r0) + row;
-        const int col0 = T.n0 + 128 * half;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (d_f32) {
-            float* dp = static_cast<float*>(D) + grow * N + col0 + 32 * c;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[c][j], v[c][j + 1], v[c][j + 2], v[c][j + 3]));
-          } else {
-            __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(D) + grow * N + col0 + 32 * c;
-#pragma unroll
-            for (int j = 0; j < 32; j += 8)
-              st_v4(dp + j, make_uint4(pack_bf16x2(__uint_as_float(v[c][j]), __uint_as_float(v[c][j + 1])),
-                                       pack_bf16x2(__uint_as_float(v[c][j + 2]), __uint_as_float(v[c][j + 3])),
-                                       pack_bf16x2(__uint_as_float(v[c][j + 4]), __uint_as_float(v[c][j + 5])),
-                                       pack_bf16x2(__uint_as_float(v[c][j + 6]), __uint_as_float(v[c][j + 7]))));
-          }
-        }
-      }
-    }
-  }
-  if (warp >= 3 && lane == 0) bulk_wait_all();
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-  }
-}
-
-// =============================================================================================
 // Wgrad: groups split K (the tokens of each expert), e.g. dW1_e = dH_e^T X_e.  Both operands are
 // A2's column-wise outputs: per segment e a [rows][m_e] K-major matrix at byte offset rows * o_e,
 // scales sT rows P_e .. P_e + ceil(m_e/128) - 1 (A2's layout).  The row stride m_e changes per
@@ -991,43 +680,22 @@ __global__ void __launch_bounds__(kWThreads, 1)
   }
 }
 
-typedef CUresult (*PFN_encodeTiled_g)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 }  // namespace
-
-static PFN_encodeTiled_g encode_g() {
-  static PFN_encodeTiled_g fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) == cudaSuccess &&
-        qres == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled_g>(p);
-  }
-  return fn;
-}
 
 cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B,
                                     const uint8_t* sb, int64_t ld_sb, int64_t M, int64_t N, int64_t K,
                                     const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
                                     cudaStream_t stream, int num_sms) {
-  static PFN_encodeTiled_g encode = nullptr;
-  if (!encode) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) != cudaSuccess ||
-        qres != cudaDriverEntryPointSuccess)
-      return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_encodeTiled_g>(p);
-    cudaFuncSetAttribute(gemm_blockscaled_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(GemmSmem) + 1024));
-    cudaFuncSetAttribute(gemm_blockscaled_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(GemmSmem) + 1024));
-  }
+  PFN_encodeTiled encode = tensor_map_encoder();
+  if (!encode) return cudaErrorNotSupported;
+  static KernelSetup setup1, setup2;
+  if (prepare_kernel(setup1, gemm_blockscaled_kernel<1>, kGThreads, sizeof(GemmSmem) + 1024, sizeof(GemmSmem) + 1024) ==
+          0 ||
+      prepare_kernel(setup2, gemm_blockscaled_kernel<2>, kGThreads, sizeof(GemmSmem) + 1024, sizeof(GemmSmem) + 1024) ==
+          0)
+    return cudaErrorInvalidValue;
   // CTA pairs (clusters of 2) share the A tile of a row block when N has an even number of tiles
-  const int cl = (N / kGN) % 2 == 0 && tune_int("GEMM_CLUSTER", 2) == 2 ? 2 : 1;
+  const int cl = (N / kGN) % 2 == 0 ? 2 : 1;
   const int groups = seg_offsets == nullptr ? 1 : num_groups;
   CUtensorMap ma, mb, md;
   {  // BF16 output boxes of 32 rows x 32 columns (unused for fp32 output)
@@ -1072,42 +740,6 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  if (tune_int("GEMM_2SM", 0) == 1) {  // CTA pairs with M=256 MMAs (cta_group::2)
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sizeof(Gemm2Smem) + 1024));
-      attr2 = true;
-    }
-    CUtensorMap ma2, mb2;
-    const cuuint32_t box_a2[2] = {kGK, kGM};
-    const cuuint32_t box_b2[2] = {kGK, kGN / 2};
-    if (encode(&ma2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(A), gdim_a, gstr_a, box_a2, estride,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-        encode(&mb2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(B), gdim_b, gstr_b, box_b2, estride,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
-    const int64_t pairs_ub = ((M / kGM + groups) / 2 + groups) * (N / kGN);
-    int64_t g2 = num_sms / 2 * 2;
-    if (2 * pairs_ub < g2) g2 = 2 * pairs_ub;
-    if (g2 < 2) g2 = 2;
-    cudaLaunchConfig_t cfg2{};
-    cfg2.gridDim = dim3(static_cast<unsigned>(g2));
-    cfg2.blockDim = dim3(kGThreads);
-    cfg2.dynamicSmemBytes = sizeof(Gemm2Smem) + 1024;
-    cfg2.stream = stream;
-    cudaLaunchAttribute at2[1];
-    at2[0].id = cudaLaunchAttributeClusterDimension;
-    at2[0].val.clusterDim.x = 2;
-    at2[0].val.clusterDim.y = 1;
-    at2[0].val.clusterDim.z = 1;
-    cfg2.attrs = at2;
-    cfg2.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg2, gemm_2sm_kernel, ma2, mb2, md, msa, msb, M, N, K, seg_offsets, num_groups, D,
-                              d_f32);
-  }
   // persistent: at most one CTA per SM, tiles walked with a static stride (pairs of tiles for cl = 2)
   const int64_t tiles_ub = (M / kGM + groups) * (N / kGN);
   int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
@@ -1141,13 +773,10 @@ namespace fp8flow {
 cudaError_t launch_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT, const uint8_t* sbT,
                               int64_t Nb, const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
                               cudaStream_t stream, int num_sms) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(WgradSmem) + 1024));
-    attr = true;
-  }
-  PFN_encodeTiled_g encode = encode_g();
+  static KernelSetup setup;
+  if (prepare_kernel(setup, gemm_wgrad_kernel, kWThreads, sizeof(WgradSmem) + 1024, sizeof(WgradSmem) + 1024) == 0)
+    return cudaErrorInvalidValue;
+  PFN_encodeTiled encode = tensor_map_encoder();
   if (!encode) return cudaErrorNotSupported;
   CUtensorMap md;
   const cuuint64_t gdim_d[2] = {static_cast<cuuint64_t>(Nb), static_cast<cuuint64_t>(num_groups) * Ma};

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kChunk) plan_fused_kernel(const int32_t* __res
                                                             int32_t* __restrict__ expert_offsets,
                                                             int32_t* __restrict__ row_map,
                                                             int32_t* __restrict__ src_of_row, int64_t max_rows,
-                                                            int32_t* __restrict__ status, int stop) {
+                                                            int32_t* __restrict__ status) {
   extern __shared__ uint32_t smem_plan[];
   uint32_t* bits = smem_plan;                                            // [E_loc][kWords]
   int32_t* pre = reinterpret_cast<int32_t*>(bits + E_loc * kWords);      // [E_loc][kWords]
@@ -202,7 +202,6 @@ __global__ void __launch_bounds__(kChunk) plan_fused_kernel(const int32_t* __res
     if (le[k] >= 0) atomicOr(&bits[le[k] * kWords + (tid >> 5)], 1u << lane);
   }
   __syncthreads();
-  if (stop == 1) return;
   // prefix popcounts along each expert row; the row total is this chunk's count for the expert
   for (int r0 = warp * 2; r0 < E_loc; r0 += (kChunk / 32) * 2) {
     const int row = r0 + (lane >> 4), wi = lane & 15;
@@ -220,9 +219,7 @@ __global__ void __launch_bounds__(kChunk) plan_fused_kernel(const int32_t* __res
     }
   }
   __threadfence();
-  if (stop == 2) return;
   cooperative_groups::this_grid().sync();
-  if (stop == 3) return;
 
   // per-expert totals and this chunk's base (2 experts per thread: E_loc <= 1024)
   int cnt[2] = {0, 0}, pad[2] = {0, 0};
@@ -317,28 +314,22 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
   int32_t* status = static_cast<int32_t*>(ws);
   int32_t* chunk_counts = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + 256);
   const size_t smem = static_cast<size_t>(num_local_experts) * kWords * 8 + 4 * (2 * num_local_experts + 1);
-  // single cooperative launch when every chunk CTA can be resident at once
-  static int coop_occ = -1;
-  if (coop_occ < 0) {
-    int dev = 0, coop = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(plan_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-    int occ = 0;
-    if (coop && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plan_fused_kernel, kChunk, 64 * 1024) ==
-                    cudaSuccess)
-      coop_occ = occ * sms;  // conservative: occupancy at 64 KB of shared memory
-    else
-      coop_occ = 0;
-  }
-  if (top_k <= 16 && smem <= 64 * 1024 && grid <= coop_occ && tune_int("PLAN_FUSED", 1) == 1) {
+  // Single cooperative launch when every chunk CTA can be resident at once (up to ~150k tokens on
+  // 148 SMs); beyond that, or for shared-memory needs above 64 KB (E_loc > ~450), the two-kernel
+  // path (count, then place) -- same results, it re-reads the routing rows once more.
+  int dev = 0, coop = 0, sms = 0;
+  cudaError_t e0 = cudaGetDevice(&dev);
+  if (e0 == cudaSuccess) e0 = cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (e0 == cudaSuccess) e0 = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e0 != cudaSuccess) return e0;
+  static KernelSetup fused_setup;  // occupancy at 64 KB of shared memory (conservative)
+  const int occ = coop ? prepare_kernel(fused_setup, plan_fused_kernel, kChunk, 64 * 1024, 64 * 1024) : 0;
+  if (top_k <= 16 && smem <= 64 * 1024 && grid <= static_cast<int64_t>(occ) * sms) {
     int64_t n_chunks = grid;
-    int K = top_k, e0 = expert_begin, E = num_local_experts, al = align;
+    int K = top_k, e0i = expert_begin, E = num_local_experts, al = align;
     int64_t T = num_tokens, mr = max_rows;
-    int stop = tune_int("PLAN_STOP", 0);  // timing experiment only: end after stage 1/2/3
-    void* args[] = {const_cast<int32_t**>(&topk_idx), &T, &K, &e0, &E, &al, &n_chunks, &chunk_counts,
-                    &expert_offsets, &row_map, &src_of_row, &mr, &status, &stop};
+    void* args[] = {const_cast<int32_t**>(&topk_idx), &T, &K, &e0i, &E, &al, &n_chunks, &chunk_counts,
+                    &expert_offsets, &row_map, &src_of_row, &mr, &status};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_fused_kernel), dim3(static_cast<unsigned>(grid)),
                                        dim3(kChunk), args, smem, stream);
   }
@@ -349,8 +340,9 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
     plan_count_kernel<<<static_cast<unsigned>(chunks), kChunk, 4 * num_local_experts, stream>>>(
         topk_idx, num_tokens, top_k, expert_begin, num_local_experts, chunk_counts);
   }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(plan_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  static KernelSetup place_setup;  // opted in to the largest layout (E_loc = 1024)
+  if (prepare_kernel(place_setup, plan_place_kernel, kChunk, 1024 * kWords * 8 + 4 * (2 * 1024 + 1), smem) == 0)
+    return cudaErrorInvalidValue;
   plan_place_kernel<<<static_cast<unsigned>(grid), kChunk, smem, stream>>>(
       topk_idx, num_tokens, top_k, expert_begin, num_local_experts, align, chunks > 0 ? chunks : 1, chunk_counts,
       expert_offsets, row_map, src_of_row, max_rows, status);
@@ -385,7 +377,8 @@ __global__ void __launch_bounds__(256, 1) permute_pad_kernel(const uint8_t* __re
   uint8_t* zero = smem_move + 8 * kMaxMoveSlots;  // 256 B in: 128-byte aligned
   uint8_t* slots = zero + H;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t R = expert_offsets[E_loc];
+  // an overflowed plan (status 1) reports the true padded total here: only max_rows rows exist
+  const int64_t R = min64(expert_offsets[E_loc], max_rows);
   const int64_t G = gridDim.x, cta = blockIdx.x;
   const int64_t n_chunks = (R + kMoveChunk - 1) / kMoveChunk;
   const int64_t my_chunks = cta < n_chunks ? (n_chunks - cta + G - 1) / G : 0;
@@ -471,18 +464,15 @@ __global__ void __launch_bounds__(256, 1) permute_pad_kernel(const uint8_t* __re
 cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
                                const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_local_experts,
                                int64_t max_rows, uint8_t* q_out, uint8_t* s_out, cudaStream_t stream, int num_sms) {
-  const int ctas = tune_int("CTAS_PER_SM_A3", 2) > 0 ? tune_int("CTAS_PER_SM_A3", 2) : 1;  // co-resident CTAs per SM (smem budget split)
+  const int ctas = 2;  // co-resident CTAs per SM, sharing the shared-memory budget (r01_tune_ctas.txt)
   const size_t budget = kMoveSmemBudget / ctas;
   int nslots = static_cast<int>((budget - 8 * kMaxMoveSlots - hidden) / hidden);
   if (nslots > kMaxMoveSlots) nslots = kMaxMoveSlots;
   if (nslots < kMoveStoreSlack + 2) return cudaErrorInvalidValue;  // hidden too large for the ring
   const size_t smem = 8 * kMaxMoveSlots + static_cast<size_t>(hidden) * (1 + nslots);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(permute_pad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(8 * kMaxMoveSlots + kMoveSmemBudget));
-    attr = true;
-  }
+  static KernelSetup setup;
+  if (prepare_kernel(setup, permute_pad_kernel, 256, 8 * kMaxMoveSlots + kMoveSmemBudget, smem) == 0)
+    return cudaErrorInvalidValue;
   int64_t grid = (max_rows + kMoveChunk - 1) / kMoveChunk;
   if (grid > static_cast<int64_t>(num_sms) * ctas) grid = static_cast<int64_t>(num_sms) * ctas;
   if (grid < 1) grid = 1;
@@ -640,19 +630,16 @@ __global__ void __launch_bounds__(256, 1) unpermute_unpad_kernel(const __nv_bflo
 cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t* row_map, const float* probs,
                                    int64_t num_tokens, int32_t top_k, void* y, cudaStream_t stream, int num_sms) {
   const int64_t row_bytes = 2 * hidden;
-  const int ctas = tune_int("CTAS_PER_SM_A4", 2) > 0 ? tune_int("CTAS_PER_SM_A4", 2) : 1;  // co-resident CTAs per SM (smem budget split)
+  const int ctas = 2;  // co-resident CTAs per SM, sharing the shared-memory budget (r01_tune_ctas.txt)
   int nslots = static_cast<int>(kUnpermSmemBudget / ctas / row_bytes);
   if (nslots > kMaxUnpermSlots) nslots = kMaxUnpermSlots;
   // a token's rows must all fit the ring when the columns take more than one consumer pass
   const bool multi_pass = hidden / 8 > 224 * kUnpermChunksPerThread;
   if (nslots < 2 || (multi_pass && nslots < top_k)) return cudaErrorInvalidValue;
   const size_t smem = 16 * kMaxUnpermSlots + static_cast<size_t>(row_bytes) * nslots;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(unpermute_unpad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(16 * kMaxUnpermSlots + kUnpermSmemBudget));
-    attr = true;
-  }
+  static KernelSetup setup;
+  if (prepare_kernel(setup, unpermute_unpad_kernel, 256, 16 * kMaxUnpermSlots + kUnpermSmemBudget, smem) == 0)
+    return cudaErrorInvalidValue;
   const int64_t max_grid = static_cast<int64_t>(num_sms) * ctas;
   int64_t grid = num_tokens < max_grid ? num_tokens : max_grid;
   if (grid < 1) grid = 1;

@@ -32,46 +32,6 @@ __device__ __forceinline__ void a1_load(const __nv_bfloat16* __restrict__ x, int
   }
 }
 
-template <int ROWS>
-__device__ __forceinline__ void a1_process(int64_t rows, int64_t cols, int64_t col_pairs, int64_t item, int half,
-                                           int sub, const uint4 (&v)[ROWS], uint8_t* __restrict__ q,
-                                           uint8_t* __restrict__ s, int64_t ld_s) {
-  const int64_t rg = item / col_pairs;
-  const int64_t cp = item - rg * col_pairs;
-  const int64_t row0 = rg * ROWS;
-  const int64_t col = cp * 256 + half * 128 + sub * 8;
-  const bool col_ok = col < cols;  // odd number of tiles: upper half idles on the last pair
-  const int nrows = static_cast<int>(min64(ROWS, rows - row0));
-  uint32_t packed[ROWS / 4];  // scale bytes of rows row0.. for this half's tile, 4 per word
-#pragma unroll
-  for (int i = 0; i < ROWS / 4; ++i) packed[i] = 0;
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
-    uint32_t mag = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) mag = max(mag, max(w[j] & 0x7FFFu, (w[j] >> 16) & 0x7FFFu));
-    mag = halfwarp_max_u32(mag);
-    const uint32_t sb = scale_byte_from_bf16_mag(mag);
-    const float inv = inv_scale_from_byte(sb);
-    uint32_t c[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) c[j] = cvt_e4m3x2_f32(bf16lo_to_f32(w[j]) * inv, bf16hi_to_f32(w[j]) * inv);
-    if (r < nrows && col_ok) st_v2(q + (row0 + r) * cols + col, c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-    packed[r / 4] |= sb << (8 * (r % 4));
-  }
-  if (sub == 0 && col_ok) {
-    uint8_t* sp = s + (cp * 2 + half) * ld_s + row0;
-    if (nrows == ROWS) {
-#pragma unroll
-      for (int i = 0; i < ROWS / 4; ++i)
-        reinterpret_cast<uint32_t*>(sp)[i] = packed[i];  // row0 % 4 == 0 and ld_s % 16 == 0: aligned
-    } else {
-      for (int r = 0; r < nrows; ++r) sp[r] = static_cast<uint8_t>(packed[r / 4] >> (8 * (r % 4)));
-    }
-  }
-}
-
 // v2 of the per-item math (the default): the tile max of a half-warp by two
 // full-warp redux.sync (each half contributes to its own), magnitudes max'ed as packed 16-bit
 // pairs (__vmaxu2 on w & 0x7FFF7FFF), x * 2^-T as packed f32x2 multiplies (FMUL2).  Same results:
@@ -137,80 +97,13 @@ __global__ void __launch_bounds__(32 * WARPS) quantize_rowwise_v2_kernel(const _
   a1_process_v2<ROWS>(rows, cols, col_pairs, item, half, sub, v, q, s, ld_s);
 }
 
-// PIPE: the next item's loads are issued before the current item is processed, so a warp keeps
-// two items (2 x ROWS x 512 B) in flight -- for the short per-warp item lists of mid-size shapes.
-template <int ROWS, bool PIPE>
-__global__ void __launch_bounds__(256) quantize_rowwise_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
-                                                                int64_t cols, uint8_t* __restrict__ q,
-                                                                uint8_t* __restrict__ s, int64_t ld_s, int sched) {
-  const int lane = threadIdx.x & 31;
-  const int half = lane >> 4;
-  const int sub = lane & 15;
-  const int64_t col_pairs = (cols + 255) / 256;
-  const int64_t n_items = ((rows + ROWS - 1) / ROWS) * col_pairs;
-  ItemIter it = warp_item_iter(n_items, sched);
-  if (!PIPE) {
-    for (; it.cur < it.end; it.cur += it.step) {
-      uint4 v[ROWS];
-      a1_load<ROWS>(x, rows, cols, col_pairs, it.cur, half, sub, v);
-      a1_process<ROWS>(rows, cols, col_pairs, it.cur, half, sub, v, q, s, ld_s);
-    }
-  } else {
-    if (it.cur >= it.end) return;
-    uint4 v[ROWS];
-    a1_load<ROWS>(x, rows, cols, col_pairs, it.cur, half, sub, v);
-    for (; it.cur < it.end; it.cur += it.step) {
-      const int64_t nxt = it.cur + it.step;
-      uint4 nv[ROWS];
-      if (nxt < it.end) a1_load<ROWS>(x, rows, cols, col_pairs, nxt, half, sub, nv);
-      a1_process<ROWS>(rows, cols, col_pairs, it.cur, half, sub, v, q, s, ld_s);
-#pragma unroll
-      for (int r = 0; r < ROWS; ++r) v[r] = nv[r];
-    }
-  }
-}
-
-template <int ROWS, bool PIPE>
-static cudaError_t launch_a1(const void* x, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s, int64_t ld_s,
-                             cudaStream_t stream, int num_sms, int default_sched) {
-  const int64_t n_items = ((rows + ROWS - 1) / ROWS) * ((cols + 255) / 256);
-  static const int occ = occupancy_of(quantize_rowwise_kernel<ROWS, PIPE>, 256, 0);
-  const int sched = sched_for("A1", default_sched);
-  const int64_t grid = sched_grid(sched, n_items, 8, occ, num_sms);
-  quantize_rowwise_kernel<ROWS, PIPE><<<static_cast<unsigned>(grid), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s, sched);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_quantize_rowwise(const void* x, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s,
                                     int64_t ld_s, cudaStream_t stream, int num_sms) {
-  // Default: 8-row items, one per warp, 4 warps per CTA, v2 item math (tools/time_a1.py, DESIGN.md
-  // §6/§9; 4-warp CTAs: 2048x7168 14.3 -> 12.3-13.3 us, equal at larger shapes; 2 warps equal,
-  // 16 warps slower):
-  // 4096x7168 18.4 us, 16384x7168 56.2 us (0.945 of 6650 GB/s) vs 22.5 / 63.5 us for the
-  // shuffle-tree version (whose __shfl_xor_sync trees compiled to warp-collective fallbacks:
-  // 32 WARPSYNC/ENDCOLLECTIVE sequences per item, 1392 vs 944 SASS instructions).
-  // Experiments: FP8FLOW_A1_VARIANT 1 = that version, 2 = 4-row items, 3 = 4 rows pipelined,
-  // 4 = 8 rows pipelined, 5 = v2 with 8-warp CTAs, 6 = 16 rows (all slower or equal).
-  switch (tune_int("A1_VARIANT", 0)) {
-    case 1: return launch_a1<8, false>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedOnePerWarp);
-    case 2: return launch_a1<4, false>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedInterleaved);
-    case 3: return launch_a1<4, true>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedInterleaved);
-    case 4: return launch_a1<8, true>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedInterleaved);
-    case 6: return launch_a1<16, false>(x, rows, cols, q, s, ld_s, stream, num_sms, kSchedOnePerWarp);
-    case 5: {
-      const int64_t n_items = ((rows + 7) / 8) * ((cols + 255) / 256);
-      quantize_rowwise_v2_kernel<8, 8><<<static_cast<unsigned>((n_items + 7) / 8), 256, 0, stream>>>(
-          static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s);
-      return cudaGetLastError();
-    }
-    default: {
-      const int64_t n_items = ((rows + 7) / 8) * ((cols + 255) / 256);
-      quantize_rowwise_v2_kernel<8, 4><<<static_cast<unsigned>((n_items + 3) / 4), 128, 0, stream>>>(
-          static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s);
-      return cudaGetLastError();
-    }
-  }
+  // 8-row items, one per warp, 4 warps per CTA (DESIGN.md §6/§9)
+  const int64_t n_items = ((rows + 7) / 8) * ((cols + 255) / 256);
+  quantize_rowwise_v2_kernel<8, 4><<<static_cast<unsigned>((n_items + 3) / 4), 128, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s);
+  return cudaGetLastError();
 }
 
 }  // namespace fp8flow

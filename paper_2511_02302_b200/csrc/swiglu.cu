@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
   constexpr int kSwBox = Smem::kBox;
   Smem& sm = *reinterpret_cast<Smem*>(smem_sw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rows = rows_dev != nullptr ? static_cast<int64_t>(*rows_dev) : rows_max;
+  const int64_t rows = rows_dev != nullptr ? min64(static_cast<int64_t>(*rows_dev), rows_max) : rows_max;  // clamped: an overflowed plan reports its true total
   const int col_tiles = static_cast<int>((F + kSwCols - 1) / kSwCols);
   const int64_t n_rg = (rows + kSwRows - 1) / kSwRows;
   // tile t = (row group rg, column tile ct), strided by gridDim.x, walked incrementally
@@ -151,46 +151,25 @@ __global__ void __launch_bounds__(32 * (1 + CONS), 1)
   }
 }
 
-typedef CUresult (*PFN_encodeTiled_sw)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 cudaError_t launch_swiglu_quant(const void* h, int64_t rows_max, const int32_t* rows_dev, int64_t ffn, uint8_t* q,
                                 uint8_t* s, int64_t ld_s, cudaStream_t stream, int num_sms) {
-  static PFN_encodeTiled_sw encode = nullptr;
-  if (!encode) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) != cudaSuccess ||
-        qres != cudaDriverEntryPointSuccess)
-      return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_encodeTiled_sw>(p);
-    cudaFuncSetAttribute(swiglu_quant_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(SwigluSmem<16>)));
-    cudaFuncSetAttribute(swiglu_quant_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(SwigluSmem<8>)));
-  }
-  const int ctas = tune_int("CTAS_PER_SM_A5", 1) >= 2 ? 2 : 1;
-  const int rows_per_tile = ctas == 2 ? SwigluSmem<8>::kRows : SwigluSmem<16>::kRows;
-  CUtensorMap map;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(2 * ffn), static_cast<cuuint64_t>(rows_max)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(4 * ffn)};
-  const cuuint32_t box[2] = {kSwCols, static_cast<cuuint32_t>(rows_per_tile)};
-  const cuuint32_t estride[2] = {1, 1};
-  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(h), gdim, gstride, box, estride,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+  // one CTA per SM: 16 consumer warps + 1 TMA producer, 3-stage ring (2 CTAs/SM of 8 consumer
+  // warps measured slower); the producer polls the ring with a 128 ns sleep
+  constexpr int kCons = 16;
+  constexpr uint32_t kSleepNs = 128;
+  using Smem = SwigluSmem<kCons>;
+  static KernelSetup setup;
+  if (prepare_kernel(setup, swiglu_quant_kernel<kCons>, 32 * (kCons + 1), sizeof(Smem), sizeof(Smem)) == 0)
     return cudaErrorInvalidValue;
-  const int64_t tiles_ub = ((rows_max + rows_per_tile - 1) / rows_per_tile) * ((ffn + kSwCols - 1) / kSwCols);
-  const int64_t max_grid = static_cast<int64_t>(num_sms) * ctas;
-  int64_t grid = tiles_ub < max_grid ? tiles_ub : max_grid;
+  CUtensorMap map;
+  if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h, static_cast<uint64_t>(2 * ffn),
+                 static_cast<uint64_t>(rows_max), static_cast<uint64_t>(4 * ffn), kSwCols, Smem::kRows))
+    return cudaErrorInvalidValue;
+  const int64_t tiles_ub = ((rows_max + Smem::kRows - 1) / Smem::kRows) * ((ffn + kSwCols - 1) / kSwCols);
+  int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   if (grid < 1) grid = 1;
-  if (ctas == 2)
-    swiglu_quant_kernel<8><<<static_cast<unsigned>(grid), 32 * 9, sizeof(SwigluSmem<8>), stream>>>(
-        map, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<uint32_t>(tune_int("A5_SLEEP_NS", 128)));
-  else
-    swiglu_quant_kernel<16><<<static_cast<unsigned>(grid), 32 * 17, sizeof(SwigluSmem<16>), stream>>>(
-        map, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<uint32_t>(tune_int("A5_SLEEP_NS", 128)));
+  swiglu_quant_kernel<kCons><<<static_cast<unsigned>(grid), 32 * (kCons + 1), sizeof(Smem), stream>>>(
+      map, rows_max, rows_dev, ffn, q, s, ld_s, kSleepNs);
   return cudaGetLastError();
 }
 

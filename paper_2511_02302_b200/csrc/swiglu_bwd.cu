@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(32 * (1 + kBwCons), 1)
   extern __shared__ __align__(1024) uint8_t smem_bw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_bw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t rows = rows_dev != nullptr ? static_cast<int64_t>(*rows_dev) : rows_max;
+  const int64_t rows = rows_dev != nullptr ? min64(static_cast<int64_t>(*rows_dev), rows_max) : rows_max;  // clamped: an overflowed plan reports its true total
   const int col_tiles = static_cast<int>((F + kBwCols - 1) / kBwCols);
   const int64_t n_rg = (rows + kBwRows - 1) / kBwRows;
   // tile t = (row group rg, column tile ct), t = rg * col_tiles + ct, strided by gridDim.x; the
@@ -283,45 +283,26 @@ __global__ void __launch_bounds__(32 * (1 + kBwCons), 1)
   }
 }
 
-typedef CUresult (*PFN_encodeTiled_bw)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 }  // namespace
 
 cudaError_t launch_swiglu_bwd_quant(const void* h, const void* dA, int64_t rows_max, const int32_t* rows_dev,
                                     int64_t ffn, uint8_t* q, uint8_t* s, int64_t ld_s, cudaStream_t stream,
                                     int num_sms) {
-  static PFN_encodeTiled_bw encode = nullptr;
-  if (!encode) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) != cudaSuccess ||
-        qres != cudaDriverEntryPointSuccess)
-      return cudaErrorNotSupported;
-    encode = reinterpret_cast<PFN_encodeTiled_bw>(p);
-    cudaFuncSetAttribute(swiglu_bwd_quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(BwdSmem)));
-  }
+  constexpr uint32_t kSleepNs = 128;  // producer's ring poll interval
+  static KernelSetup setup;
+  if (prepare_kernel(setup, swiglu_bwd_quant_kernel, 32 * (1 + kBwCons), sizeof(BwdSmem), sizeof(BwdSmem)) == 0)
+    return cudaErrorInvalidValue;
   CUtensorMap mh, md;
-  const cuuint32_t box[2] = {kBwCols, kBwRows};
-  const cuuint32_t estride[2] = {1, 1};
-  const cuuint64_t gdim_h[2] = {static_cast<cuuint64_t>(2 * ffn), static_cast<cuuint64_t>(rows_max)};
-  const cuuint64_t gstr_h[1] = {static_cast<cuuint64_t>(4 * ffn)};
-  const cuuint64_t gdim_d[2] = {static_cast<cuuint64_t>(ffn), static_cast<cuuint64_t>(rows_max)};
-  const cuuint64_t gstr_d[1] = {static_cast<cuuint64_t>(2 * ffn)};
-  if (encode(&mh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(h), gdim_h, gstr_h, box, estride,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-      encode(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(dA), gdim_d, gstr_d, box, estride,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+  if (!encode_2d(&mh, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h, static_cast<uint64_t>(2 * ffn),
+                 static_cast<uint64_t>(rows_max), static_cast<uint64_t>(4 * ffn), kBwCols, kBwRows) ||
+      !encode_2d(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dA, static_cast<uint64_t>(ffn),
+                 static_cast<uint64_t>(rows_max), static_cast<uint64_t>(2 * ffn), kBwCols, kBwRows))
     return cudaErrorInvalidValue;
   const int64_t tiles_ub = ((rows_max + kBwRows - 1) / kBwRows) * ((ffn + kBwCols - 1) / kBwCols);
   int64_t grid = tiles_ub < num_sms ? tiles_ub : num_sms;
   if (grid < 1) grid = 1;
   swiglu_bwd_quant_kernel<<<static_cast<unsigned>(grid), 32 * (1 + kBwCons), sizeof(BwdSmem), stream>>>(
-      mh, md, rows_max, rows_dev, ffn, q, s, ld_s, static_cast<uint32_t>(tune_int("BWD_SLEEP_NS", 128)));
+      mh, md, rows_max, rows_dev, ffn, q, s, ld_s, kSleepNs);
   return cudaGetLastError();
 }
 

@@ -129,15 +129,26 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 
     // ---- shift rows, transpose 4x4 byte blocks ----------------------------------------------
     uint32_t R[4][4];
+    uint32_t nan_acc = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
       const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
       const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v.x, m2);
-      R[r][1] = shift4(v.y, m2);
-      R[r][2] = shift4(v.z, m2);
-      R[r][3] = shift4(v.w, m2);
+      R[r][0] = shift4(v.x, m2, nan_acc);
+      R[r][1] = shift4(v.y, m2, nan_acc);
+      R[r][2] = shift4(v.z, m2, nan_acc);
+      R[r][3] = shift4(v.w, m2, nan_acc);
+    }
+    if (__any_sync(0xffffffffu, has_nan_code(nan_acc))) {  // rare: NaN codes keep their bytes
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
+        R[r][0] = keep_nan_codes(R[r][0], v.x);
+        R[r][1] = keep_nan_codes(R[r][1], v.y);
+        R[r][2] = keep_nan_codes(R[r][2], v.z);
+        R[r][3] = keep_nan_codes(R[r][3], v.w);
+      }
     }
     if (++st == kTStages) {
       st = 0;
@@ -183,65 +194,24 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 // ---------------------------------------------------------------------------------------------
 // host side: tensor map + launch
 // ---------------------------------------------------------------------------------------------
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static PFN_encodeTiled get_encode_fn() {
-  static PFN_encodeTiled fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qres) == cudaSuccess &&
-        qres == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_encodeTiled>(p);
-  }
-  return fn;
-}
-
-template <int S, int O, int B>
-static void launch_transpose_variant(const CUtensorMap& map, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
-                                     const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
-                                     cudaStream_t stream, int num_sms, int64_t ub_tiles) {
-  static int occ = 0;
-  if (occ == 0) {
-    cudaFuncSetAttribute(scaling_aware_transpose_kernel<S, O, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(TransposeSmem<S, O>)));
-    occ = occupancy_of(scaling_aware_transpose_kernel<S, O, B>, kTThreads, sizeof(TransposeSmem<S, O>));
-  }
-  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
-  scaling_aware_transpose_kernel<S, O, B><<<static_cast<unsigned>(grid), kTThreads, sizeof(TransposeSmem<S, O>),
-                                             stream>>>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
-}
+constexpr int kTStagesA2 = 3, kTOutBufA2 = 1, kTMinBlocksA2 = 3;  // 3 CTAs/SM (r01 sweep of 2-4 stages)
+using A2Smem = TransposeSmem<kTStagesA2, kTOutBufA2>;
 
 cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows,
                                            int64_t cols, const int32_t* seg_offsets, int32_t num_segs,
                                            uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
-  PFN_encodeTiled encode = get_encode_fn();
-  if (!encode) return cudaErrorNotSupported;
   CUtensorMap map;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(cols)};
-  const cuuint32_t box[2] = {kTile, kTile};
-  const cuuint32_t estride[2] = {1, 1};
-  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(q), gdim, gstride, box, estride,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
+                 static_cast<uint64_t>(cols), kTile, kTile))
+    return cudaErrorInvalidValue;
+  static KernelSetup setup;
+  auto kernel = scaling_aware_transpose_kernel<kTStagesA2, kTOutBufA2, kTMinBlocksA2>;
+  const int occ = prepare_kernel(setup, kernel, kTThreads, sizeof(A2Smem), sizeof(A2Smem));
+  if (occ == 0) return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  switch (tune_int("A2_VARIANT", 0)) {
-    case 1:  // 2 stages, double staging buffer: 3 CTAs/SM, one barrier per tile
-      launch_transpose_variant<2, 2, 3>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
-      break;
-    case 2:  // 2 stages, single staging buffer: 4 CTAs/SM
-      launch_transpose_variant<2, 1, 4>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
-      break;
-    case 3:  // 4 stages, double staging buffer: 2 CTAs/SM
-      launch_transpose_variant<4, 2, 2>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
-      break;
-    default:  // 3 stages, single staging buffer: 3 CTAs/SM
-      launch_transpose_variant<3, 1, 3>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms, ub_tiles);
-  }
+  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
+  kernel<<<static_cast<unsigned>(grid), kTThreads, sizeof(A2Smem), stream>>>(map, s, ld_s, rows, cols, seg_offsets,
+                                                                             num_segs, qT, sT);
   return cudaGetLastError();
 }
 

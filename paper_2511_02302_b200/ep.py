@@ -107,22 +107,25 @@ def signal_buffer(world: int, device) -> torch.Tensor:
 def dispatch_permute(peers, rank: int, tokens_per_rank: int, hidden: int, top_k: int, num_experts: int,
                      ld_s_tok: int, topk_all: torch.Tensor, row_map: torch.Tensor, src_of_row: torch.Tensor,
                      expert_offsets: torch.Tensor, ws: torch.Tensor, q_out: torch.Tensor, s_out: torch.Tensor,
-                     align: int = 16, stream=None) -> None:
+                     align: int = 16, kernel: int = F.DISPATCH_AUTO, status: torch.Tensor | None = None,
+                     stream=None) -> None:
     """Rank `rank`'s receive side: gather every rank's routing (peers table "topk"), plan its own
     experts over the global tokens, then pull + permute + pad the routed FP8 tokens (tables "q",
-    "s").  Outputs as fp8flow_permute_pad on the rank-order concatenation."""
+    "s").  Outputs as fp8flow_permute_pad on the rank-order concatenation.  status: the preceding
+    barrier's device flag (gather and dispatch write nothing if it is nonzero) or None."""
     world = peers.world
     e0, per = expert_range(rank, world, num_experts)
-    F.fp8flow_peer_gather(peers.table("topk"), tokens_per_rank * top_k * 4, topk_all, stream=stream)
+    F.fp8flow_peer_gather(peers.table("topk"), tokens_per_rank * top_k * 4, topk_all, status=status, stream=stream)
     F.fp8flow_permute_plan(topk_all, e0, per, align, row_map, src_of_row, expert_offsets, ws, stream=stream)
     F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), ld_s_tok, tokens_per_rank, hidden, row_map,
-                                   src_of_row, expert_offsets, q_out, s_out, stream=stream)
+                                   src_of_row, expert_offsets, q_out, s_out, kernel=kernel, status=status,
+                                   stream=stream)
 
 
 def combine(peers, rank: int, tokens_per_rank: int, hidden: int, num_experts: int, topk_idx: torch.Tensor,
-            probs: torch.Tensor | None, y: torch.Tensor, stream=None) -> None:
+            probs: torch.Tensor | None, y: torch.Tensor, status: torch.Tensor | None = None, stream=None) -> None:
     """Owner side: y = sum_k p * (expert output row) pulled from the ranks' "x" buffers located by
     their "row_map" plans."""
     _, per = expert_range(rank, peers.world, num_experts)
     F.fp8flow_combine_unpermute(peers.table("x"), peers.table("row_map"), hidden, topk_idx, per, probs,
-                                token_range(rank, tokens_per_rank)[0], y, stream=stream)
+                                token_range(rank, tokens_per_rank)[0], y, status=status, stream=stream)

@@ -51,10 +51,10 @@ SIGNATURES = {
     "fp8flow_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "fp8flow_ipc_close": (ctypes.c_int, [_P]),
     "fp8flow_peer_barrier": (ctypes.c_int, [_P, _I32, _I32, _P, ctypes.c_uint32, _P]),
-    "fp8flow_peer_gather": (ctypes.c_int, [_P, _I32, _I64, _P, _P]),
+    "fp8flow_peer_gather": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P]),
     "fp8flow_dispatch_permute_pad": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P, _I32, _P, _P, _I32, _I64,
-                                                    _P, _P, _P]),
-    "fp8flow_combine_unpermute": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _I32, _P, _I64, _I64, _I32, _P, _P]),
+                                                    _P, _P, _I32, _P, _P]),
+    "fp8flow_combine_unpermute": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _I32, _P, _I64, _I64, _I32, _P, _P, _P]),
 }
 
 IPC_HANDLE_BYTES = 64
@@ -298,35 +298,44 @@ def fp8flow_peer_barrier(peer_signal, rank: int, status: torch.Tensor | None = N
            "fp8flow_peer_barrier")
 
 
-def fp8flow_peer_gather(peer_src, bytes_per_rank: int, dst: torch.Tensor, stream=None) -> None:
+def fp8flow_peer_gather(peer_src, bytes_per_rank: int, dst: torch.Tensor, status: torch.Tensor | None = None,
+                        stream=None) -> None:
+    """status: the barrier's device int32 (the kernel writes nothing if it is nonzero) or None."""
     n = len(peer_src)
-    _check(lib().fp8flow_peer_gather(_table(peer_src), n, bytes_per_rank, _ptr(dst), _stream(stream)),
+    _check(lib().fp8flow_peer_gather(_table(peer_src), n, bytes_per_rank, _ptr(dst), _ptr(status), _stream(stream)),
            "fp8flow_peer_gather")
+
+
+DISPATCH_AUTO, DISPATCH_ENGINE, DISPATCH_REGISTER = 0, 1, 2
 
 
 def fp8flow_dispatch_permute_pad(peer_q, peer_s, ld_s_tok: int, tokens_per_rank: int, hidden: int,
                                  row_map: torch.Tensor, src_of_row: torch.Tensor, expert_offsets: torch.Tensor,
-                                 q_out: torch.Tensor, s_out: torch.Tensor, stream=None) -> None:
+                                 q_out: torch.Tensor, s_out: torch.Tensor, kernel: int = DISPATCH_AUTO,
+                                 status: torch.Tensor | None = None, stream=None) -> None:
     """peer_q / peer_s: n device pointers (or tensors) of the ranks' A1 outputs; row_map etc. from
-    fp8flow_permute_plan over the gathered topk_idx [n*tokens_per_rank, K]."""
+    fp8flow_permute_plan over the gathered topk_idx [n*tokens_per_rank, K].  kernel: DISPATCH_*
+    (identical results); status: the barrier gate or None."""
     n = len(peer_q)
     assert len(peer_s) == n
     _check(lib().fp8flow_dispatch_permute_pad(_table(peer_q), _table(peer_s), ld_s_tok, n, tokens_per_rank, hidden,
                                               _ptr(row_map), row_map.shape[1], _ptr(src_of_row),
                                               _ptr(expert_offsets), expert_offsets.numel() - 1, q_out.shape[0],
-                                              _ptr(_u8(q_out)), _ptr(_u8(s_out)), _stream(stream)),
+                                              _ptr(_u8(q_out)), _ptr(_u8(s_out)), kernel, _ptr(status),
+                                              _stream(stream)),
            "fp8flow_dispatch_permute_pad")
 
 
 def fp8flow_combine_unpermute(peer_x, peer_row_map, hidden: int, topk_idx: torch.Tensor, experts_per_rank: int,
-                              probs: torch.Tensor | None, token_begin: int, y: torch.Tensor, stream=None) -> None:
+                              probs: torch.Tensor | None, token_begin: int, y: torch.Tensor,
+                              status: torch.Tensor | None = None, stream=None) -> None:
     """peer_x: n device pointers to BF16 expert outputs; peer_row_map: n device pointers to the
     ranks' plan row_maps; topk_idx/probs [T, K] of the caller's tokens; y bf16 [T, hidden]."""
     n = len(peer_x)
     assert y.dtype == torch.bfloat16
     T, K = topk_idx.shape
     _check(lib().fp8flow_combine_unpermute(_table(peer_x), _table(peer_row_map), n, hidden, _ptr(topk_idx),
-                                           experts_per_rank, _ptr(probs), token_begin, T, K, _ptr(y),
+                                           experts_per_rank, _ptr(probs), token_begin, T, K, _ptr(y), _ptr(status),
                                            _stream(stream)), "fp8flow_combine_unpermute")
 
 # ----------------------------------------------------------------------------------- sizes

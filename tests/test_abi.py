@@ -132,23 +132,26 @@ def test_validation_of_next3_entry_points(L):
     assert L.fp8flow_peer_barrier(None, 0, 2, None, 100, None) == 1
     assert L.fp8flow_peer_barrier(tab_null, 0, 2, None, 100, None) == 1
     # gather: bytes % 4, empty no-op, misaligned peer
-    assert L.fp8flow_peer_gather(tab2, 2, 22, a16, None) == 2
-    assert L.fp8flow_peer_gather(tab2, 2, 0, None, None) == 0
-    assert L.fp8flow_peer_gather(tab_mis, 2, 32, a16, None) == 3
-    # dispatch: top_k, hidden % 128, ld_s < tokens, NULL plan
+    assert L.fp8flow_peer_gather(tab2, 2, 22, a16, None, None) == 2
+    assert L.fp8flow_peer_gather(tab2, 2, 0, None, None, None) == 0
+    assert L.fp8flow_peer_gather(tab_mis, 2, 32, a16, None, None) == 3
+    # dispatch: top_k, hidden % 128, ld_s < tokens, NULL plan, unknown kernel choice
     assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 7168, a16, 17, a16, a16, 32, 1024, a16, a16,
-                                          None) == 4
+                                          0, None, None) == 4
     assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 100, a16, 8, a16, a16, 32, 1024, a16, a16,
-                                          None) == 2
+                                          0, None, None) == 2
     assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 32, 2, 64, 7168, a16, 8, a16, a16, 32, 1024, a16, a16,
-                                          None) == 2
+                                          0, None, None) == 2
     assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 7168, None, 8, a16, a16, 32, 1024, a16, a16,
-                                          None) == 1
+                                          0, None, None) == 1
+    assert L.fp8flow_dispatch_permute_pad(tab2, tab2, 64, 2, 64, 7168, a16, 8, a16, a16, 32, 1024, a16, a16,
+                                          3, None, None) == 4
     # combine: experts_per_rank, hidden % 8, empty no-op, NULL peer entry
-    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7168, a16, 0, None, 0, 4, 8, a16, None) == 4
-    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7164, a16, 32, None, 0, 4, 8, a16, None) == 2
-    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7168, a16, 32, None, 0, 0, 8, a16, None) == 0
-    assert L.fp8flow_combine_unpermute(tab_null, tab2, 2, 7168, a16, 32, None, 0, 4, 8, a16, None) == 1
+    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7168, a16, 0, None, 0, 4, 8, a16, None, None) == 4
+    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7164, a16, 32, None, 0, 4, 8, a16, None, None) == 2
+    assert L.fp8flow_combine_unpermute(tab2, tab2, 2, 7168, a16, 32, None, 0, 0, 8, a16, None, None) == 0
+    assert L.fp8flow_combine_unpermute(tab_null, tab2, 2, 7168, a16, 32, None, 0, 4, 8, a16, None, None) == 1
+
 
 def test_no_device_means_error_not_fallback(L):
     import torch
@@ -196,3 +199,15 @@ def test_oracle_loaded_only_by_tests_smoke_and_bench_cpu_leg():
         owners.append(re.findall(r"^def (\w+)", head, re.M)[-1])
     assert sorted(owners) == ["cpu_baseline_leg", "run_reference"], owners
 
+
+
+def test_product_library_has_no_environment_knobs():
+    """The library reads no environment variables (no tuning or results-changing switches): every
+    launch configuration is a constant of the source; kernel choices that a caller may need are
+    explicit arguments (fp8flow_dispatch_permute_pad's `kernel`)."""
+    csrc = os.path.join(ROOT, "paper_2511_02302_b200", "csrc")
+    for f in os.listdir(csrc):
+        txt = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in txt and "FP8FLOW_" not in txt.replace("FP8FLOW_OK", "").replace(
+            "FP8FLOW_ERR_", "").replace("FP8FLOW_DISPATCH_", "").replace("FP8FLOW_MAX_RANKS", "").replace(
+            "FP8FLOW_IPC_HANDLE_BYTES", "").replace("FP8FLOW_UNKNOWN_STATUS", ""), f

@@ -43,22 +43,10 @@ def test_step_outputs_repeat_bit_for_bit(step):
     assert step.checksums() == first
 
 
-def test_step_outputs_independent_of_launch_knobs(step, monkeypatch):
-    step.launch_ops(record=False)
-    torch.cuda.synchronize()
-    ref = step.checksums()
-    for knob, val in (("FP8FLOW_CTAS_PER_SM_A3", "1"), ("FP8FLOW_CTAS_PER_SM_A4", "1"), ("FP8FLOW_PLAN_FUSED", "0"),
-                      ("FP8FLOW_A2_VARIANT", "3"), ("FP8FLOW_A1_VARIANT", "2")):
-        monkeypatch.setenv(knob, val)
-        step.launch_ops(record=False)
-        torch.cuda.synchronize()
-        assert step.checksums() == ref, knob
-        monkeypatch.delenv(knob)
-
-
-def test_next3_dispatch_independent_of_grid_shape(monkeypatch):
-    """The dispatch engine's per-CTA token lists are filled through shared atomics: any CTA count
-    (hence any list order) and the register-copy kernel give the same bytes."""
+def test_next3_dispatch_independent_of_kernel():
+    """The dispatch engine's per-CTA token lists are filled through shared atomics (list order is
+    not deterministic): repeated engine launches, the register-copy kernel and AUTO give the same
+    bytes."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from test_gpu_ep import make_ranks, run_dispatch
@@ -67,13 +55,8 @@ def test_next3_dispatch_independent_of_grid_shape(monkeypatch):
     n, tpr, H, E, K = 4, 512, 2048, 64, 8
     ranks, ld = make_ranks(F, n, tpr, H, E, K, 9090)
     outs = []
-    for knobs in ({}, {"FP8FLOW_CTAS_PER_SM_DISP": "1"}, {"FP8FLOW_CTAS_PER_SM_DISP": "3"},
-                  {"FP8FLOW_EP_DISPATCH_LSU": "1"}):
-        for k, v in knobs.items():
-            monkeypatch.setenv(k, v)
-        o = run_dispatch(F, ranks, ld, 1, tpr, H, E, K)
+    for kernel in (F.DISPATCH_ENGINE, F.DISPATCH_ENGINE, F.DISPATCH_REGISTER, F.DISPATCH_AUTO):
+        o = run_dispatch(F, ranks, ld, 1, tpr, H, E, K, kernel=kernel)
         outs.append((o["q_out"].clone(), o["s_out"].clone(), o["row_map"].clone()))
-        for k in knobs:
-            monkeypatch.delenv(k)
     for q, s, rm in outs[1:]:
         assert torch.equal(q, outs[0][0]) and torch.equal(s, outs[0][1]) and torch.equal(rm, outs[0][2])

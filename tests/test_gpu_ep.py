@@ -50,7 +50,7 @@ def make_ranks(F, n, tpr, H, E, K, seed, gain_sigma=1.0):
     return ranks, ld
 
 
-def run_dispatch(F, ranks, ld, rank, tpr, H, E, K, align=16):
+def run_dispatch(F, ranks, ld, rank, tpr, H, E, K, align=16, kernel=0):
     from paper_2511_02302_b200 import ep
 
     n = len(ranks)
@@ -64,7 +64,8 @@ def run_dispatch(F, ranks, ld, rank, tpr, H, E, K, align=16):
     ws = torch.empty(F.fp8flow_permute_workspace_bytes(n * tpr, K, per), dtype=torch.uint8, device="cuda")
     q_out = torch.full((max_rows, H), 0xEE, dtype=torch.uint8, device="cuda")
     s_out = torch.full((H // 128, max_rows), 0xEE, dtype=torch.uint8, device="cuda")
-    ep.dispatch_permute(peers, rank, tpr, H, K, E, ld, topk_all, row_map, src, off, ws, q_out, s_out, align=align)
+    ep.dispatch_permute(peers, rank, tpr, H, K, E, ld, topk_all, row_map, src, off, ws, q_out, s_out, align=align,
+                        kernel=kernel)
     torch.cuda.synchronize()
     return dict(topk_all=topk_all, row_map=row_map, src=src, off=off, q_out=q_out, s_out=s_out, max_rows=max_rows)
 
@@ -72,16 +73,16 @@ def run_dispatch(F, ranks, ld, rank, tpr, H, E, K, align=16):
 @pytest.mark.parametrize("kernel", ["engine", "lsu"])
 @pytest.mark.parametrize("n,tpr,H,E,K", [(1, 300, 1024, 16, 4), (2, 256, 7168, 32, 8), (4, 100, 1152, 64, 8),
                                          (8, 64, 7168, 256, 8), (2, 0, 256, 8, 2)])
-def test_dispatch_permute_parity(F, orc, n, tpr, H, E, K, kernel, monkeypatch):
+def test_dispatch_permute_parity(F, orc, n, tpr, H, E, K, kernel):
     """Both dispatch kernels: the bulk-copy engine (peers on this device) and the register-copy
     kernel the launcher takes when a peer lives on another GPU (NVLink)."""
-    monkeypatch.setenv("FP8FLOW_EP_DISPATCH_LSU", "1" if kernel == "lsu" else "0")
+    kern = F.DISPATCH_REGISTER if kernel == "lsu" else F.DISPATCH_ENGINE
     ranks, ld = make_ranks(F, n, tpr, H, E, K, 1000 + n * tpr)
     qs = [host(r["q"]) for r in ranks]
     ss = [host(r["s"]) for r in ranks]
     ts = [host(r["topk"]) for r in ranks]
     for g in range(n):
-        out = run_dispatch(F, ranks, ld, g, tpr, H, E, K)
+        out = run_dispatch(F, ranks, ld, g, tpr, H, E, K, kernel=kern)
         qo_ref, so_ref, rm_ref, src_ref, off_ref = orc.dispatch_permute_pad(qs, ss, ts, g, E,
                                                                             max_rows=out["max_rows"])
         off = host(out["off"])
@@ -205,9 +206,9 @@ def _free_port():
     return p
 
 
-def _ipc_worker(rank, world, port, q, lsu="2"):
+def _ipc_worker(rank, world, port, q, kernel=0):
     try:
-        os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port), "FP8FLOW_EP_DISPATCH_LSU": lsu})
+        os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
         import torch.distributed as dist
 
         import oracle
@@ -237,7 +238,8 @@ def _ipc_worker(rank, world, port, q, lsu="2"):
         ws = torch.empty(F.fp8flow_permute_workspace_bytes(world * tpr, K, per), dtype=torch.uint8, device="cuda")
         q_out = torch.zeros(max_rows, H, dtype=torch.uint8, device="cuda")
         s_out = torch.zeros(H // 128, max_rows, dtype=torch.uint8, device="cuda")
-        ep.dispatch_permute(peers, rank, tpr, H, K, E, ld, topk_all, bufs["row_map"], src, off, ws, q_out, s_out)
+        ep.dispatch_permute(peers, rank, tpr, H, K, E, ld, topk_all, bufs["row_map"], src, off, ws, q_out, s_out,
+                            kernel=kernel)
         torch.cuda.synchronize()
         dist.barrier()                       # every rank's row_map is complete before the combine
         y = torch.empty(tpr, H, dtype=torch.bfloat16, device="cuda")
@@ -266,16 +268,16 @@ def _ipc_worker(rank, world, port, q, lsu="2"):
         del e
 
 
-@pytest.mark.parametrize("lsu", ["2", "1"])
-def test_two_processes_over_cuda_ipc(F, lsu):
-    """lsu "2": the launcher's own choice (same device -> bulk-copy engine); "1": the register-copy
-    kernel used across GPUs."""
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_two_processes_over_cuda_ipc(F, kernel):
+    """kernel 0 (AUTO): the launcher's own choice (same device -> bulk-copy engine); 2 (REGISTER): the
+    register-copy kernel used across GPUs."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, lsu)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, kernel)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
@@ -287,13 +289,13 @@ def test_two_processes_over_cuda_ipc(F, lsu):
 
 
 @pytest.mark.parametrize("kernel", ["engine", "lsu"])
-def test_dispatch_combine_edge_cases(F, orc, kernel, monkeypatch):
+def test_dispatch_combine_edge_cases(F, orc, kernel):
     """A rank that receives nothing (every token routed to the other rank's experts), top_k = 1 and
     top_k = 16, an odd token count (routing bytes not a multiple of 16): both dispatch kernels and
     the combine stay bit-exact against the oracle."""
     from paper_2511_02302_b200 import ep
 
-    monkeypatch.setenv("FP8FLOW_EP_DISPATCH_LSU", "1" if kernel == "lsu" else "0")
+    kern = F.DISPATCH_REGISTER if kernel == "lsu" else F.DISPATCH_ENGINE
     H = 512
     # (37 tokens x top-1 = 148 routing bytes per rank: the routing gather's 4-byte-word path)
     for n, tpr, E, K, force in [(2, 64, 8, 2, "low"), (2, 48, 32, 1, None), (2, 40, 64, 16, None),
@@ -307,7 +309,7 @@ def test_dispatch_combine_edge_cases(F, orc, kernel, monkeypatch):
         ts = [host(r["topk"]) for r in ranks]
         outs = []
         for g in range(n):
-            out = run_dispatch(F, ranks, ld, g, tpr, H, E, K)
+            out = run_dispatch(F, ranks, ld, g, tpr, H, E, K, kernel=kern)
             qo_ref, so_ref, rm_ref, _, off_ref = orc.dispatch_permute_pad(qs, ss, ts, g, E, max_rows=out["max_rows"])
             R = int(off_ref[-1])
             if force == "low" and g == 1:
@@ -398,3 +400,43 @@ def test_next3_sequence_captures_into_a_cuda_graph(F):
         assert bufs[g]["st"].item() == 0
         for k, v in eager[g].items():
             assert torch.equal(bufs[g][k], v), (g, k)
+
+
+def test_timed_out_barrier_gates_gather_dispatch_and_combine(F):
+    """with the barrier's status nonzero (a peer did not arrive), the gather, both
+    dispatch kernels and the combine write nothing; with status 0 they run."""
+    n, tpr, H, E, K = 2, 64, 512, 16, 4
+    ranks, ld = make_ranks(F, n, tpr, H, E, K, 31337)
+    from paper_2511_02302_b200 import ep
+
+    peers = ep.LocalPeers(ranks)
+    per = E // n
+    mr = F.permute_max_rows(n * tpr, K, per)
+    bad = torch.ones(1, dtype=torch.int32, device="cuda")
+    topk_all = torch.full((n * tpr, K), -5, dtype=torch.int32, device="cuda")
+    F.fp8flow_peer_gather(peers.table("topk"), tpr * K * 4, topk_all, status=bad)
+    torch.cuda.synchronize()
+    assert torch.all(topk_all == -5)
+    good = run_dispatch(F, ranks, ld, 0, tpr, H, E, K)                    # a valid plan for rank 0
+    for kernel in (F.DISPATCH_ENGINE, F.DISPATCH_REGISTER):
+        q_out = torch.full((mr, H), 0xEE, dtype=torch.uint8, device="cuda")
+        s_out = torch.full((H // 128, mr), 0xEE, dtype=torch.uint8, device="cuda")
+        F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), ld, tpr, H, good["row_map"], good["src"],
+                                       good["off"], q_out, s_out, kernel=kernel, status=bad)
+        torch.cuda.synchronize()
+        assert torch.all(q_out == 0xEE) and torch.all(s_out == 0xEE), kernel
+        F.fp8flow_dispatch_permute_pad(peers.table("q"), peers.table("s"), ld, tpr, H, good["row_map"], good["src"],
+                                       good["off"], q_out, s_out, kernel=kernel, status=bad.zero_() + 0)
+        torch.cuda.synchronize()
+        R = int(good["off"][-1])
+        assert torch.equal(q_out[:R], good["q_out"][:R]), kernel
+        bad.fill_(1)
+    for r in range(n):
+        ranks[r]["x"] = synth.normal_bf16(mr, H, 90 + r).cuda()
+        ranks[r]["row_map"] = good["row_map"]
+    peers = ep.LocalPeers(ranks)
+    y = torch.full((tpr, H), 7.0, dtype=torch.bfloat16, device="cuda")
+    F.fp8flow_combine_unpermute(peers.table("x"), peers.table("row_map"), H, ranks[0]["topk"], per, None, 0, y,
+                                status=bad)
+    torch.cuda.synchronize()
+    assert torch.all(y == 7.0)

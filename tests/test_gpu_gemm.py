@@ -55,10 +55,10 @@ def check(D, ref, mag, rows, bf16=False, what=""):
     assert np.all(err <= bound), (np.argwhere(err > bound)[:5], rel)
 
 
-@pytest.mark.parametrize("mode", ["1sm", "2sm"])  # CTA-pair A multicast (default) / cta_group::2 M=256 MMAs
-@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 512, 512), (384, 256, 1024)])
-def test_gemm_single_group(F, orc, M, N, K, mode, monkeypatch):
-    monkeypatch.setenv("FP8FLOW_GEMM_2SM", "1" if mode == "2sm" else "0")
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 512, 512), (384, 256, 1024), (256, 768, 256)])
+def test_gemm_single_group(F, orc, M, N, K):
+    """N = 256 or 768 (odd number of 256-column tiles): one CTA per tile; N = 512: CTA pairs that
+    share the A tile by TMA multicast."""
     rng = np.random.default_rng(M + N + K)
     A, sa = rand_operand(rng, M, K, M)
     B, sb = rand_operand(rng, N, K, N)
@@ -95,12 +95,9 @@ def test_gemm_scale_layout(F, orc):
     np.testing.assert_array_equal(D, orc.gemm_blockscaled(A, sa, B, sb))
 
 
-@pytest.mark.parametrize("mode", ["1sm", "2sm"])
-def test_gemm_groups_and_bf16(F, orc, mode, monkeypatch):
-    """Expert groups over M (multiples of 16, an empty group, partial 128-row blocks, odd block
-    counts for the 2-SM pairs) with per-group weights; rows outside every group untouched; BF16
-    output."""
-    monkeypatch.setenv("FP8FLOW_GEMM_2SM", "1" if mode == "2sm" else "0")
+def test_gemm_groups_and_bf16(F, orc):
+    """Expert groups over M (multiples of 16, an empty group, partial 128-row blocks) with
+    per-group weights; rows outside every group untouched; BF16 output."""
     rng = np.random.default_rng(7)
     seg = np.array([0, 48, 48, 208, 400], np.int32)
     M, N, K, G = 416, 256, 256, 4

@@ -121,13 +121,14 @@ def check_transpose(F, orc, q, s, seg=None, naive=False):
     assert np.array_equal(sT[:sT_ref.shape[0]], sT_ref)
 
 
-def constructed_rowwise(rows, cols, seed, k_max=40):
-    """Row-wise FP8 built directly: all 254 non-NaN codes appear in every row block and the block's
-    row scales span k = 0..k_max (the adversarial all-codes x all-k suite)."""
+def constructed_rowwise(rows, cols, seed, k_max=40, nan=False):
+    """Row-wise FP8 built directly: all 254 non-NaN codes (all 256 codes with nan=True) appear in
+    every row block and the block's row scales span k = 0..k_max (the adversarial all-codes x
+    all-k suite)."""
     rng = np.random.default_rng(seed)
-    codes = np.array([c for c in range(256) if c not in (0x7F, 0xFF)], np.uint8)
+    codes = np.array([c for c in range(256) if nan or c not in (0x7F, 0xFF)], np.uint8)
     q = codes[rng.integers(0, codes.size, (rows, cols))]
-    q[:, :254] = codes[None, :]
+    q[:, :codes.size] = codes[None, :]
     T = 100 - (np.arange(rows) % (k_max + 1))                            # block max 100 -> k = 0..k_max
     s = np.tile(T.astype(np.uint8), (cols // 128, 1))
     s = np.ascontiguousarray(np.roll(s, 3, axis=1))
@@ -144,6 +145,15 @@ def test_transpose_parity_quantized(F, orc, rows, cols):
 def test_transpose_all_codes_all_k(F, orc):
     q, s = constructed_rowwise(512, 384, 1)
     check_transpose(F, orc, q, s)
+
+
+def test_transpose_nan_codes_propagate(F, orc):
+    """E4M3 NaN codes (0x7F, 0xFF; A1 emits them for NaN input) keep their bytes through the
+    exponent shift for every k, as the oracle's shift does; the rest is unchanged."""
+    q, s = constructed_rowwise(256, 384, 11, nan=True)
+    check_transpose(F, orc, q, s)
+    qT, _ = run_transpose(F, q, s)
+    assert np.array_equal(qT.reshape(384, 256) == 0x7F, q.T == 0x7F)
 
 
 def test_transpose_ragged_segments(F, orc):
@@ -190,12 +200,14 @@ def run_plan(F, topk_idx, e0, E_loc, align=16, max_rows=None):
     return host(row_map), host(src), host(off), int(host(ws[:4].view(torch.int32))[0])
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])  # single cooperative launch / 2-kernel fallback
 @pytest.mark.parametrize("T,E,K,group,ngroups,align", [
-    (16384, 256, 8, 0, 8, 16), (16384, 256, 8, 5, 8, 16), (3000, 64, 6, 0, 1, 16), (777, 32, 4, 1, 4, 128),
-    (5, 8, 2, 0, 2, 16)])
-def test_permute_plan_parity(F, orc, T, E, K, group, ngroups, align, fused, monkeypatch):
-    monkeypatch.setenv("FP8FLOW_PLAN_FUSED", fused)
+    (16384, 256, 8, 0, 8, 16), (16384, 256, 8, 5, 8, 16), (16384, 256, 8, 0, 1, 16), (3000, 64, 6, 0, 1, 16),
+    (777, 32, 4, 1, 4, 128), (5, 8, 2, 0, 2, 16), (200000, 64, 8, 3, 8, 16)])
+def test_permute_plan_parity(F, orc, T, E, K, group, ngroups, align):
+    """The single cooperative launch for token counts whose 512-token chunks fit on the GPU at once
+    (<= 148 x its occupancy, ~75k tokens), and the two-kernel path (count, then place) beyond:
+    200,000 tokens = 391 chunks.  (16384, 256 local experts) is the whole DeepSeek-V3 layer on one
+    GPU."""
     idx, _ = synth.routing(T, 400 + T, num_experts=E, top_k=K, num_groups=min(8, E // 4), topk_groups=2)
     per = E // ngroups
     e0 = group * per
@@ -225,6 +237,32 @@ def test_permute_plan_overflow_status(F):
     idx = np.zeros((64, 1), np.int32)
     rm, src, off, status = run_plan(F, idx, 0, 1, 16, max_rows=32)
     assert status == 1 and off[-1] == 64 and np.all(rm[32:] == -1) and np.all(rm[:32, 0] == np.arange(32))
+
+
+def test_overflowed_plan_consumers_stay_in_bounds(F):
+    """a plan whose padded total (64) exceeds max_rows (32) reports the true total in
+    expert_offsets[E_loc] and status 1; the move and SwiGLU+quant that consume it clamp to their
+    capacity.  Guard bytes right after every output buffer must stay untouched."""
+    T, H, FF, mr = 64, 256, 128, 32
+    idx = np.zeros((T, 1), np.int32)
+    rm, src, off, status = run_plan(F, idx, 0, 1, 16, max_rows=mr)
+    assert status == 1 and off[-1] == 64
+    q_tok = torch.randint(0, 0x7E, (T, H), dtype=torch.uint8, device="cuda")
+    s_tok = torch.randint(100, 140, (H // 128, T), dtype=torch.uint8, device="cuda")
+    guard = 4096
+    qbuf = torch.full((mr * H + guard,), 0xEE, dtype=torch.uint8, device="cuda")
+    sbuf = torch.full(((H // 128) * mr + guard,), 0xEE, dtype=torch.uint8, device="cuda")
+    q_out, s_out = qbuf[: mr * H].view(mr, H), sbuf[: (H // 128) * mr].view(H // 128, mr)
+    F.fp8flow_permute_pad(q_tok, s_tok, dev(src), dev(off), q_out, s_out)
+    h = synth.normal_bf16(mr, 2 * FF, 77).cuda()
+    abuf = torch.full((mr * FF + guard,), 0xEE, dtype=torch.uint8, device="cuda")
+    sab = torch.full(((FF // 128) * mr + guard,), 0xEE, dtype=torch.uint8, device="cuda")
+    F.fp8flow_swiglu_quant(h, abuf[: mr * FF].view(mr, FF), sab[: (FF // 128) * mr].view(FF // 128, mr),
+                           rows_dev=dev(off)[1:])
+    torch.cuda.synchronize()
+    for buf, n in ((qbuf, mr * H), (sbuf, (H // 128) * mr), (abuf, mr * FF), (sab, (FF // 128) * mr)):
+        assert torch.all(buf[n:] == 0xEE), "write past the capacity"
+    assert torch.equal(q_out, q_tok[:mr]) and torch.equal(s_out, s_tok[:, :mr])   # rows 0..31 = tokens 0..31
 
 
 def run_move(F, q_tok, s_tok, src, off, max_rows):
