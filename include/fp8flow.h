@@ -83,7 +83,7 @@ FP8FLOW_API int fp8flow_device_check(void);
  *   q       [rows][cols] E4M3 codes, 16-byte aligned                  (written)
  *   s       [cols/128][ld_s] UE8M0 scale bytes, MN-major, 16-byte aligned; ld_s >= rows,
  *           ld_s % 16 == 0 (written for rows [0, rows) of every tile column; bytes rows..ld_s-1
- *           untouched; the kernel stores 4 rows' bytes as one 32-bit word)
+ *           untouched)
  *   rows >= 0 (0 = no-op), cols > 0 and cols % 128 == 0.  A misaligned pointer returns
  *   FP8FLOW_ERR_ALIGN before anything is launched.
  *   Result: q[i][j] = E4M3_RNE(x[i][j] * 2^-T[i][j/128]) (the product is exact; |.| <= 448).

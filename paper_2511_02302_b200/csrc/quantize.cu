@@ -3,105 +3,108 @@
 // Paper: Eq. 2 (tile scale), Eq. 3 (code = round(x / s)), power-of-two scales
 // s = 2^T, "no explicit casting except at the entry point".
 //
-// Work decomposition (HBM-bound streaming op, 3.008 B/element):
-//   warp item = 8 consecutive rows x 256 columns (two 1x128 tiles), one item per warp; the warp
-//   issues its 8 row loads (8 x 16 B per lane) before using any.  A half-warp owns one tile row:
-//   in-thread max over 8 BF16 magnitudes as packed 16-bit pairs, the tile amax by two full-warp
-//   redux.sync (one per half), the scale byte from the amax bit pattern (exact integer rule),
-//   x * 2^-T exact in fp32 (packed f32x2 multiplies), cvt.rn.satfinite packs the codes.  The 8
-//   scale bytes of a warp's rows are contiguous in the MN-major layout s[tile][row] and leave as
-//   two 32-bit stores per tile.
+// HBM-bound streaming op (3.008 B/element).  The r01 kernel spent 707 warp-instructions per 2048
+// elements (issue slots 72 % busy at 4096 x 7168); this one ~0.2 per element:
+//   * a 1x128 tile row is held by 8 lanes, 16 consecutive BF16 per lane (two 128-bit loads), so
+//     every scale decision is amortised over 16 elements per lane;
+//   * warp item = 8 rows x 256 columns (lanes 8r..8r+7: rows r and r + 4 of two adjacent tiles),
+//     all 8 loads (4 KB per warp) issued before any use; one item per warp, 4-warp CTAs, so the
+//     hardware CTA scheduler sweeps the tensor in address order with ~128 KB in flight per SM
+//     (r02 marginal cold-L2 times, tools/probe/marginal_a1.py: 4096 x 7168 16.2 -> 14.1 us,
+//     16384 x 7168 53.4 -> 48.7 us, 65536 x 7168 209 -> 200 us; a persistent blocked or
+//     interleaved schedule was 5-20 % slower at the large shapes);
+//   * in-lane |max| by 7 packed bf16x2 `max.xorsign.abs` (HMNMX2), the 8-lane max by 3 butterfly
+//     shuffles on the 15-bit magnitude;
+//   * the scale byte and 2^-T straight from the amax bit pattern: T + 127 = max(((mag + 0x1F) >> 7)
+//     - 8, 0) (the +0x1F carries into the exponent exactly when the 7-bit mantissa exceeds 0x60,
+//     i.e. amax > 1.75 * 2^e = 448 * 2^(e-8)); zero / subnormal amax -> byte 0 (R11, R13);
+//   * x * 2^-T exact in fp32 (packed f32x2 multiplies), cvt.rn.satfinite.e4m3x2 (the single RNE),
+//     16 codes per lane leave as one 128-bit store, the row's scale byte from its first lane.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace fp8flow {
 
-template <int ROWS>
-__device__ __forceinline__ void a1_load(const __nv_bfloat16* __restrict__ x, int64_t rows, int64_t cols,
-                                        int64_t col_pairs, int64_t item, int half, int sub, uint4 (&v)[ROWS]) {
-  const int64_t rg = item / col_pairs;
-  const int64_t cp = item - rg * col_pairs;
-  const int64_t row0 = rg * ROWS;
-  const int64_t col = cp * 256 + half * 128 + sub * 8;
-  const bool col_ok = col < cols;
-  const int nrows = static_cast<int>(min64(ROWS, rows - row0));
+namespace {
+
+constexpr int kA1Warps = 4;  // 128-thread CTAs (8-warp CTAs measured equal)
+
+__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;  // per half: max(|a|, |b|) with the xor of the signs
+}
+
+// one 1x128 tile row held by 8 lanes (16 BF16 each): amax, scale byte, 16 codes, stores
+__device__ __forceinline__ void a1_tile_row(const uint4 (&v)[2], int lane, bool ok, uint8_t* pq, uint8_t* ps) {
+  const uint32_t w[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
+  const uint32_t m = absmax_bf16x2(absmax_bf16x2(absmax_bf16x2(w[0], w[1]), absmax_bf16x2(w[2], w[3])),
+                                   absmax_bf16x2(absmax_bf16x2(w[4], w[5]), absmax_bf16x2(w[6], w[7])));
+  uint32_t mag = max(m & 0x7FFFu, (m >> 16) & 0x7FFFu);
+  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 1));
+  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 2));
+  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 4));
+  const int sb = max(static_cast<int>((mag + 0x1Fu) >> 7) - 8, 0);
+  const float inv = __uint_as_float(static_cast<uint32_t>(254 - sb) << 23);
+  const float2 iv = make_float2(inv, inv);
+  uint32_t c[8];
 #pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    v[r] = make_uint4(0, 0, 0, 0);
-    if (r < nrows && col_ok) v[r] = ld_nc_v4(x + (row0 + r) * cols + col);
+  for (int j = 0; j < 8; ++j) {
+    const float2 p = __fmul2_rn(make_float2(bf16lo_to_f32(w[j]), bf16hi_to_f32(w[j])), iv);
+    c[j] = cvt_e4m3x2_f32(p.x, p.y);
+  }
+  if (ok) {
+    st_v4(pq, make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16), c[6] | (c[7] << 16)));
+    if ((lane & 7) == 0) *ps = static_cast<uint8_t>(sb);
   }
 }
 
-// v2 of the per-item math (the default): the tile max of a half-warp by two
-// full-warp redux.sync (each half contributes to its own), magnitudes max'ed as packed 16-bit
-// pairs (__vmaxu2 on w & 0x7FFF7FFF), x * 2^-T as packed f32x2 multiplies (FMUL2).  Same results:
-// max over |bf16| bit patterns, exact power-of-two scaling, one RNE per element.
-template <int ROWS>
-__device__ __forceinline__ void a1_process_v2(int64_t rows, int64_t cols, int64_t col_pairs, int64_t item, int half,
-                                              int sub, const uint4 (&v)[ROWS], uint8_t* __restrict__ q,
-                                              uint8_t* __restrict__ s, int64_t ld_s) {
-  const int64_t rg = item / col_pairs;
-  const int64_t cp = item - rg * col_pairs;
-  const int64_t row0 = rg * ROWS;
-  const int64_t col = cp * 256 + half * 128 + sub * 8;
-  const bool col_ok = col < cols;
-  const int nrows = static_cast<int>(min64(ROWS, rows - row0));
-  uint32_t packed[ROWS / 4];
-#pragma unroll
-  for (int i = 0; i < ROWS / 4; ++i) packed[i] = 0;
-  uint8_t* qrow = q + row0 * cols + col;
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
-    uint32_t m2 = __vmaxu2(__vmaxu2(w[0] & 0x7FFF7FFFu, w[1] & 0x7FFF7FFFu),
-                           __vmaxu2(w[2] & 0x7FFF7FFFu, w[3] & 0x7FFF7FFFu));
-    const uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
-    const uint32_t lo = __reduce_max_sync(0xffffffffu, half ? 0u : m);
-    const uint32_t hi = __reduce_max_sync(0xffffffffu, half ? m : 0u);
-    const uint32_t sb = scale_byte_from_bf16_mag(half ? hi : lo);
-    const float inv = inv_scale_from_byte(sb);
-    const float2 iv = make_float2(inv, inv);
-    uint32_t c[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 p = __fmul2_rn(make_float2(bf16lo_to_f32(w[j]), bf16hi_to_f32(w[j])), iv);
-      c[j] = cvt_e4m3x2_f32(p.x, p.y);
-    }
-    if (r < nrows && col_ok) st_v2(qrow + r * cols, c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-    packed[r / 4] |= sb << (8 * (r % 4));
-  }
-  if (sub == 0 && col_ok) {
-    uint8_t* sp = s + (cp * 2 + half) * ld_s + row0;
-    if (nrows == ROWS) {
-#pragma unroll
-      for (int i = 0; i < ROWS / 4; ++i) reinterpret_cast<uint32_t*>(sp)[i] = packed[i];
-    } else {
-      for (int r = 0; r < nrows; ++r) sp[r] = static_cast<uint8_t>(packed[r / 4] >> (8 * (r % 4)));
-    }
-  }
-}
-
-template <int ROWS, int WARPS = 8>
-__global__ void __launch_bounds__(32 * WARPS) quantize_rowwise_v2_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
-                                                                   int64_t cols, uint8_t* __restrict__ q,
-                                                                   uint8_t* __restrict__ s, int64_t ld_s) {
+// one warp = 8 rows x 256 columns: lanes 8r..8r+7 take rows r and r + 4 of two adjacent tiles
+template <int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) quantize_rowwise_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
+                                                                 int64_t cols, uint8_t* __restrict__ q,
+                                                                 uint8_t* __restrict__ s, int64_t ld_s) {
   const int lane = threadIdx.x & 31;
-  const int half = lane >> 4;
-  const int sub = lane & 15;
-  const int64_t col_pairs = (cols + 255) / 256;
-  const int64_t n_items = ((rows + ROWS - 1) / ROWS) * col_pairs;
-  const int64_t item = static_cast<int64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);  // one item per warp
-  if (item >= n_items) return;
-  uint4 v[ROWS];
-  a1_load<ROWS>(x, rows, cols, col_pairs, item, half, sub, v);
-  a1_process_v2<ROWS>(rows, cols, col_pairs, item, half, sub, v, q, s, ld_s);
+  const int r_in = lane >> 3, c16 = (lane & 7) * 16;
+  const int64_t n_tiles = cols / kTile;
+  const int64_t n_pairs = (n_tiles + 1) / 2;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+  const int64_t rg = item / n_pairs;                 // 8-row group
+  const int64_t tp = item - rg * n_pairs;
+  const int64_t row0 = rg * 8 + r_in;
+  if (rg * 8 >= rows) return;
+  uint4 v[2][2][2];                                  // [row half][tile][2 loads]
+  bool ok[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int64_t row = row0 + 4 * h, tj = tp * 2 + t;
+      ok[h][t] = row < rows && tj < n_tiles;
+      const __nv_bfloat16* p = x + row * cols + tj * kTile + c16;
+      if (ok[h][t]) {
+        v[h][t][0] = ld_nc_v4(p);
+        v[h][t][1] = ld_nc_v4(p + 8);
+      }
+    }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int64_t row = row0 + 4 * h, tj = tp * 2 + t;
+      a1_tile_row(v[h][t], lane, ok[h][t], q + row * cols + tj * kTile + c16, s + tj * ld_s + row);
+    }
 }
+
+}  // namespace
 
 cudaError_t launch_quantize_rowwise(const void* x, int64_t rows, int64_t cols, uint8_t* q, uint8_t* s,
                                     int64_t ld_s, cudaStream_t stream, int num_sms) {
-  // 8-row items, one per warp, 4 warps per CTA (DESIGN.md §6/§9)
-  const int64_t n_items = ((rows + 7) / 8) * ((cols + 255) / 256);
-  quantize_rowwise_v2_kernel<8, 4><<<static_cast<unsigned>((n_items + 3) / 4), 128, 0, stream>>>(
+  (void)num_sms;  // one warp item per warp; the hardware CTA scheduler balances and sweeps in order
+  const int64_t n_items = ((rows + 7) / 8) * ((cols / kTile + 1) / 2);
+  const int64_t grid = (n_items + kA1Warps - 1) / kA1Warps;
+  if (grid > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
+  quantize_rowwise_kernel<kA1Warps><<<static_cast<unsigned>(grid), 32 * kA1Warps, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(x), rows, cols, q, s, ld_s);
   return cudaGetLastError();
 }
