@@ -74,58 +74,41 @@ __device__ __forceinline__ uint32_t halfwarp_max_u32(uint32_t v) {
 
 // ------------------------------------------------------------------------------------------
 // Exponent shift of 4 packed codes of one row by the same k >= 0 (derivation after Eq. 11,
-// P:186-198): result = E4M3_RNE(decode(c) * 2^-k) -- the exponent edit E' = E - k whenever the
+// P:186-198): result = E4M3_RNE(decode(code) * 2^-k) -- the exponent edit E' = E - k whenever the
 // result stays normal, RNE into the subnormal grid otherwise (R7).
 // ------------------------------------------------------------------------------------------
-// Branch-free.  The 7 magnitude bits of an E4M3 code placed at bits 7..13 of an f16 are the f16
-// whose value is decode(code) * 2^-8 -- for normal AND subnormal codes (E4M3's subnormal grid
-// 2^-9 maps onto f16 multiples of 2^-17, which f16 represents exactly).  So the up-conversion is
-// a mask + shift (bytes 0,2 and bytes 1,3 form two f16x2), the rescale by 2^(8-k) is one HMUL2
-// per pair (exact whenever the E4M3 result can be nonzero), and the single RNE rounding is the
-// hardware cvt.rn.satfinite f16x2 -> e4m3x2 on magnitudes; the sign bits are re-attached
-// unchanged (so an underflow to zero keeps its sign, R10).
+// Branch-free, 8 instructions per 4 codes: the hardware decode e4m3x2 -> f16x2 (exact: E4M3 is a
+// subset of f16, subnormals included), one HMUL2 by 2^-k per pair (exact whenever the E4M3 result
+// can be nonzero: the product keeps its 4 significant bits down to 2^-21, far below the 2^-10
+// rounding threshold of E4M3's smallest subnormal), the single RNE rounding by the hardware
+// cvt.rn.satfinite f16x2 -> e4m3x2, and the sign bits OR-ed back (an underflow to zero keeps its
+// sign, R10; a NaN code 0x7F / 0xFF comes back as the same byte, as in the oracle's shift).
 __device__ __forceinline__ uint32_t f16x2_pow2(int e) {
-  // f16x2 with both halves = 2^e, e in [-24, 8] (normal for e >= -14, subnormal below)
-  const uint32_t h = e >= -14 ? static_cast<uint32_t>(e + 15) << 10 : (1u << (e + 24));
+  // f16x2 with both halves = 2^e, e in [-24, 15] (normal for e >= -14, subnormal below); 0 below
+  const uint32_t h = e >= -14 ? static_cast<uint32_t>(e + 15) << 10 : (e >= -24 ? (1u << (e + 24)) : 0u);
   return h | (h << 16);
 }
-// multiplier for shift4: 2^(8-k) as f16x2, k >= 0 (k > 32 behaves like k = 32: all results +-0)
+// multiplier for shift4: 2^-k as f16x2 (k > 24: 0, every result is +-0)
 __device__ __forceinline__ uint32_t shift_multiplier(uint32_t k) {
-  const int e = 8 - static_cast<int>(k > 32u ? 32u : k);
-  return f16x2_pow2(e < -24 ? -24 : e);
+  return f16x2_pow2(-static_cast<int>(k > 25u ? 25u : k));
 }
-// two f16x2 (bytes 0,2 and 1,3) -> 4 E4M3 codes in byte order 0,1,2,3
-__device__ __forceinline__ uint32_t cvt_e4m3x4_from_f16x2_pairs(uint32_t p02, uint32_t p13) {
-  uint32_t r;
+__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t m2) {
+  uint32_t h01, h23, r;
+  asm("{\n\t.reg .b16 lo, hi;\n\t"
+      "mov.b32 {lo, hi}, %2;\n\t"
+      "cvt.rn.f16x2.e4m3x2 %0, lo;\n\t"
+      "cvt.rn.f16x2.e4m3x2 %1, hi;\n\t}"
+      : "=r"(h01), "=r"(h23)
+      : "r"(w));
+  __half2 p01 = __hmul2(*reinterpret_cast<const __half2*>(&h01), *reinterpret_cast<const __half2*>(&m2));
+  __half2 p23 = __hmul2(*reinterpret_cast<const __half2*>(&h23), *reinterpret_cast<const __half2*>(&m2));
   asm("{\n\t.reg .b16 lo, hi;\n\t"
       "cvt.rn.satfinite.e4m3x2.f16x2 lo, %1;\n\t"
       "cvt.rn.satfinite.e4m3x2.f16x2 hi, %2;\n\t"
       "mov.b32 %0, {lo, hi};\n\t}"
       : "=r"(r)
-      : "r"(p02), "r"(p13));
-  return __byte_perm(r, 0u, 0x3120);  // [c0, c2, c1, c3] -> [c0, c1, c2, c3]
-}
-// nan_acc accumulates the largest f16 magnitude half seen (u16x2 max): a code of magnitude 0x7F
-// (E4M3 NaN) is the only one that maps to 0x3F80, so has_nan_code() tells a caller to patch the
-// (rare) words holding NaN codes with keep_nan_codes() -- NaN propagates unchanged, as in the
-// oracle's shift (the f16 path alone would turn it into a finite code).
-__device__ __forceinline__ uint32_t shift4(uint32_t w, uint32_t m2, uint32_t& nan_acc) {
-  const uint32_t lo02 = (w & 0x007F007Fu) << 7;            // bytes 0, 2 -> f16 halves (value * 2^-8)
-  const uint32_t hi13 = (w >> 1) & 0x3F803F80u;            // bytes 1, 3
-  nan_acc = __vmaxu2(nan_acc, __vmaxu2(lo02, hi13));
-  __half2 p02 = __hmul2(*reinterpret_cast<const __half2*>(&lo02), *reinterpret_cast<const __half2*>(&m2));
-  __half2 p13 = __hmul2(*reinterpret_cast<const __half2*>(&hi13), *reinterpret_cast<const __half2*>(&m2));
-  return cvt_e4m3x4_from_f16x2_pairs(*reinterpret_cast<uint32_t*>(&p02), *reinterpret_cast<uint32_t*>(&p13)) |
-         (w & 0x80808080u);
-}
-__device__ __forceinline__ bool has_nan_code(uint32_t nan_acc) {
-  return (nan_acc & 0xFFFFu) == 0x3F80u || (nan_acc >> 16) == 0x3F80u;
-}
-// bytes of w whose magnitude is 0x7F (NaN) replace the corresponding bytes of `shifted`
-__device__ __forceinline__ uint32_t keep_nan_codes(uint32_t shifted, uint32_t w) {
-  const uint32_t t = ((w & 0x7F7F7F7Fu) + 0x01010101u) & 0x80808080u;  // bit 7 of every NaN byte
-  const uint32_t m = (t >> 7) * 0xFFu;
-  return (shifted & ~m) | (w & m);
+      : "r"(*reinterpret_cast<uint32_t*>(&p01)), "r"(*reinterpret_cast<uint32_t*>(&p23)));
+  return r | (w & 0x80808080u);
 }
 
 // ------------------------------------------------------------------------------------------

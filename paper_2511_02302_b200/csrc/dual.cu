@@ -57,7 +57,7 @@ struct DualSmem {
   uint64_t empty[STAGES];
   uint64_t cfull[2];                  // code tile b written (16 row-warp arrivals)
   uint64_t cempty[2];                 // code tile b consumed (8 transpose-warp arrivals)
-  uint32_t mult[33];                  // f16x2 multiplier 2^(8-k) for k = 0..32
+  uint32_t mult[33];                  // f16x2 multiplier 2^-k for k = 0..32
   uint32_t red[kDThreads / 32];       // scan scratch (load_segments)
   int32_t seg_off[kDMaxSegs + 1];
   int32_t blk_prefix[kDMaxSegs + 1];
@@ -274,26 +274,15 @@ __global__ void __launch_bounds__(kDThreads, 1)
     const uint32_t sw = sm.sc[b][lane];  // scale bytes of rows 4a..4a+3
     const int pchunk = ((w ^ lane) & 7) << 2;  // physical word offset of chunk w in rows 4a..4a+3
     uint32_t R[4][4];
-    uint32_t nan_acc = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint4 v = *reinterpret_cast<const uint4*>(&sm.ctile[b][(4 * lane + r) * (kDT / 4) + pchunk]);
       const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // rows outside the segment: never stored
       const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v.x, m2, nan_acc);
-      R[r][1] = shift4(v.y, m2, nan_acc);
-      R[r][2] = shift4(v.z, m2, nan_acc);
-      R[r][3] = shift4(v.w, m2, nan_acc);
-    }
-    if (__any_sync(0xffffffffu, has_nan_code(nan_acc))) {  // rare: NaN codes keep their bytes
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint4 v = *reinterpret_cast<const uint4*>(&sm.ctile[b][(4 * lane + r) * (kDT / 4) + pchunk]);
-        R[r][0] = keep_nan_codes(R[r][0], v.x);
-        R[r][1] = keep_nan_codes(R[r][1], v.y);
-        R[r][2] = keep_nan_codes(R[r][2], v.z);
-        R[r][3] = keep_nan_codes(R[r][3], v.w);
-      }
+      R[r][0] = shift4(v.x, m2);
+      R[r][1] = shift4(v.y, m2);
+      R[r][2] = shift4(v.z, m2);
+      R[r][3] = shift4(v.w, m2);
     }
     mbar_arrive(&sm.cempty[b]);  // (per thread) its reads of code tile b, scales and maxima are done
     if (4 * lane < rows_valid) {

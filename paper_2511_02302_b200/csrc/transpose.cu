@@ -7,19 +7,20 @@
 //     T_max = max_i T[i][jb];  sT_e[ib][j] = T_max;  qT_e[j][i-o] = shift(q[i][j], T_max - T[i][jb])
 //
 // Kernel design (sm_100a, HBM-bound, 2.016 B/element):
-//   * persistent CTAs (2 per SM), static round-robin over the 128x128 tiles of all segments; the
+//   * persistent CTAs (3 per SM), static round-robin over the 128x128 tiles of all segments; the
 //     tile -> (segment, row block) map is a prefix sum over ceil(m_e/128) computed in shared memory
 //     from the DEVICE segment offsets (no host sync: CUDA-graph capturable).
-//   * the 16 KB input tile arrives by TMA (cp.async.bulk.tensor.2d, mbarrier complete_tx) into a
-//     4-stage ring, so 3 tiles are in flight while one is transposed.
+//   * the 16 KB input tile and its 128-byte run of row scales arrive by TMA (cp.async.bulk.tensor.2d
+//     + a 1D bulk copy, one mbarrier with complete_tx) into a 3-stage ring.
+//   * T_max per block: each warp max-reduces the staged scale run itself (redux.sync), no barrier.
 //   * thread (g, c) owns rows 4g..4g+3 x bytes 16c..16c+15: 4 conflict-free LDS.128 (8 threads of
-//     a quarter-warp read one full 128-byte row), the per-row exponent shift is applied to whole
-//     32-bit words (4 codes of one row share k), then 4x4 byte blocks are transposed with PRMT.
-//   * the transposed words go to a second 16 KB buffer with a 16-byte-chunk XOR swizzle
+//     a quarter-warp read one full 128-byte row); the per-row exponent shift (common.cuh shift4:
+//     hardware e4m3x2 -> f16x2 decode, one HMUL2 by 2^-k, one RNE back, 8 instructions per 4
+//     codes) is applied to whole 32-bit words (4 codes of one row share k), then 4x4 byte blocks
+//     are transposed with PRMT.
+//   * the transposed words go to a 16 KB staging buffer with a 16-byte-chunk XOR swizzle
 //     (chunk ^= j/16) that makes both the 32-bit writes and the 128-bit read-out conflict-free, and
 //     leave as coalesced 128-bit stores (each output row's 128 bytes = one full line).
-//   * T_max per block: 4 scale bytes per thread (one 32-bit load of the MN-major scale run),
-//     redux.sync max per warp, 8-entry smem combine.
 #include <cuda.h>
 
 #include "async.cuh"
@@ -41,7 +42,7 @@ struct TransposeSmem {
   uint32_t sc[STAGES][kTile / 4];  // the 128 row-scale bytes of each staged tile
   uint32_t out[OUTBUF][kTile * kTile / 4];
   uint64_t full_bar[STAGES];
-  uint32_t mult[33];               // f16x2 multiplier 2^(8-k) for k = 0..32
+  uint32_t mult[33];               // f16x2 multiplier 2^-k for k = 0..32
   uint32_t red[kTThreads / 32];
   int32_t seg_off[kMaxSegs + 1];
   int32_t blk_prefix[kMaxSegs + 1];
@@ -129,26 +130,15 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 
     // ---- shift rows, transpose 4x4 byte blocks ----------------------------------------------
     uint32_t R[4][4];
-    uint32_t nan_acc = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
       const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
       const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v.x, m2, nan_acc);
-      R[r][1] = shift4(v.y, m2, nan_acc);
-      R[r][2] = shift4(v.z, m2, nan_acc);
-      R[r][3] = shift4(v.w, m2, nan_acc);
-    }
-    if (__any_sync(0xffffffffu, has_nan_code(nan_acc))) {  // rare: NaN codes keep their bytes
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
-        R[r][0] = keep_nan_codes(R[r][0], v.x);
-        R[r][1] = keep_nan_codes(R[r][1], v.y);
-        R[r][2] = keep_nan_codes(R[r][2], v.z);
-        R[r][3] = keep_nan_codes(R[r][3], v.w);
-      }
+      R[r][0] = shift4(v.x, m2);
+      R[r][1] = shift4(v.y, m2);
+      R[r][2] = shift4(v.z, m2);
+      R[r][3] = shift4(v.w, m2);
     }
     if (++st == kTStages) {
       st = 0;
@@ -195,7 +185,19 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 // host side: tensor map + launch
 // ---------------------------------------------------------------------------------------------
 constexpr int kTStagesA2 = 3, kTOutBufA2 = 1, kTMinBlocksA2 = 3;  // 3 CTAs/SM (r01 sweep of 2-4 stages)
-using A2Smem = TransposeSmem<kTStagesA2, kTOutBufA2>;
+template <int S, int O, int B>
+static cudaError_t launch_a2v(const CUtensorMap& map, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+                              const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
+                              cudaStream_t stream, int num_sms, int64_t ub_tiles, bool persist) {
+  static KernelSetup setup;
+  auto kernel = scaling_aware_transpose_kernel<S, O, B>;
+  const int occ = prepare_kernel(setup, kernel, kTThreads, sizeof(TransposeSmem<S, O>), sizeof(TransposeSmem<S, O>));
+  if (occ == 0) return cudaErrorInvalidValue;
+  const int64_t grid = persist ? one_wave_grid(occ, num_sms, ub_tiles) : ub_tiles;
+  kernel<<<static_cast<unsigned>(grid), kTThreads, sizeof(TransposeSmem<S, O>), stream>>>(map, s, ld_s, rows, cols,
+                                                                                       seg_offsets, num_segs, qT, sT);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows,
                                            int64_t cols, const int32_t* seg_offsets, int32_t num_segs,
@@ -204,15 +206,11 @@ cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, i
   if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
                  static_cast<uint64_t>(cols), kTile, kTile))
     return cudaErrorInvalidValue;
-  static KernelSetup setup;
-  auto kernel = scaling_aware_transpose_kernel<kTStagesA2, kTOutBufA2, kTMinBlocksA2>;
-  const int occ = prepare_kernel(setup, kernel, kTThreads, sizeof(A2Smem), sizeof(A2Smem));
-  if (occ == 0) return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
-  kernel<<<static_cast<unsigned>(grid), kTThreads, sizeof(A2Smem), stream>>>(map, s, ld_s, rows, cols, seg_offsets,
-                                                                             num_segs, qT, sT);
-  return cudaGetLastError();
+  // persistent: 3 CTAs per SM x 3 TMA stages (non-persistent one-tile CTAs and 1-2 stage variants
+  // measured 5-40 % slower, profiles/r02_a2_shift.txt)
+  return launch_a2v<kTStagesA2, kTOutBufA2, kTMinBlocksA2>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT,
+                                                         stream, num_sms, ub_tiles, true);
 }
 
 // =============================================================================================
