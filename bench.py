@@ -1,25 +1,32 @@
 #!/usr/bin/env python
 """bench.py -- FP8-Flow-MoE hot path on B200: scaling-aware transpose + quantize GB/s.
 
-One STEP = one pass of the whole hot path for one expert-parallel
-rank of a DeepSeek-V3 MoE layer (16384 tokens, top-8 of 256 experts, hidden 7168, expert FFN
-2x2048; the rank owns expert group g = rank mod 8, i.e. 32 experts, the EP8 partition):
+One STEP = one pass of the whole hot path over one DeepSeek-V3 MoE
+layer (16384 tokens, top-8 of 256 experts, hidden 7168, expert FFN 2x2048), partitioned over the
+job's GPUs (paper_2511_02302_b200/dist.py):
 
-    A1  quantize the rank's 2048-token BF16 shard (forward entry cast)
-    A3  permute plan (3 kernels) + fused permute/pad move of the received FP8 tokens
+  --partition strong (default)  GPU g of n owns experts [g*256/n, (g+1)*256/n) and tokens
+                                [g*T/n, (g+1)*T/n) of the entry casts; n = 1 is the WHOLE layer
+                                (256 experts, ~133k padded rows) on one GPU; total work fixed.
+  --partition weak              every GPU owns one EP8 expert group (32 experts, 1/8 of tokens).
+
+Per GPU and step:
+    A1  quantize the rank's BF16 token shard (forward entry cast)
+    A3  permute plan + fused permute/pad move of the received FP8 tokens
     A5  fused SwiGLU + quant of the fc1 output [R, 4096]
     A4  fused unpermute + unpad of the fc2 output [R, 7168] with gate probs
-    A1  quantize the rank's 2048-token BF16 output gradient dY (backward entry cast)
+    A1  quantize the rank's BF16 output gradient dY shard (backward entry cast)
     A2  scaling-aware transpose of X_perm [R, 7168] and of A [R, 2048], segments = experts (Alg. 1)
+The received tokens are what the dispatch would deliver (constructed: the rank's routed tokens,
+quantized by A1 at setup; the NEXT-3 lines measure the fused dispatch itself).
 
-Inputs are synthetic (synth/, seeded) and resident in HBM; the L2 is flushed (256 MiB write + 256 MiB
-read) before every step, outside the timed events.  The step's dependency DAG runs on four streams
-(plan -> move -> A2(X_perm) | A1(x), A1(dY) | A5 -> A2(A) | A4), all enqueued while the streams
-are held by a short spin kernel, so the events measure GPU execution only; a serial pass of the
-same steps gives the per-op breakdown and the roofline of the dominant kernel.
-value = algorithmic bytes of all ranks' steps / max-over-ranks time (GB/s); weak scaling (every
-rank owns one expert group).  N > 1: launch under torchrun (one process per GPU, NCCL used only
-after timing).  `--impl reference` times the CPU oracle on a bounded sample of the same workload.
+Inputs are synthetic (synth/, seeded, drawn on the device) and resident in HBM; the L2 is flushed
+(256 MiB write + 256 MiB read) before every step, outside the timed events.  The step's dependency
+DAG runs on four streams, captured once into a CUDA graph and replayed behind a spin kernel.
+value = algorithmic bytes of all ranks' steps / max-over-ranks time (GB/s).  N > 1: launch under
+torchrun (one process per GPU; NCCL only after timing).  After timing, every rank runs the CPU
+oracle over its WHOLE step (the cpu_baseline timing) and compares every output element by element
+and by C11 checksum.  `--impl reference` times the CPU oracle on a bounded sample.
 """
 from __future__ import annotations
 
@@ -47,7 +54,7 @@ NVTX = os.environ.get("FP8FLOW_NVTX", "0") == "1"   # profiling runs only (e.g. 
 # only (tests/test_gpu_bench_multirank.py); the line's config always reports the token count used.
 T_GLOBAL = int(os.environ.get("FP8FLOW_BENCH_TOKENS", "16384"))
 HIDDEN, FFN, N_EXPERTS, TOP_K, ALIGN = synth.HIDDEN, synth.FFN, synth.NUM_EXPERTS, synth.TOP_K, 16
-KERNELS_PER_STEP = 9    # A1, plan x2 (count, place), move, A5, A4, A1(dY), A2 x2
+KERNELS_PER_STEP = 8    # A1, plan (one cooperative launch), move, A5, A4, A1(dY), A2 x2
 OPS = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
        "A2_transpose_xperm", "A2_transpose_a"]
 
@@ -57,54 +64,89 @@ def log(*a):
 
 
 # =============================================================================================
-# workload (host side, seeded)
+# workload (seeded; drawn on the device, host copies kept for the e2e leg and the oracle)
 # =============================================================================================
-class HostWorkload:
-    """Everything one rank's step consumes, on the host (numpy / CPU torch)."""
+class Workload:
+    """Everything one rank's step consumes.  Device tensors are the resident inputs; `host` holds
+    pinned host copies of the same bytes (the e2e leg copies them in each step; the oracle reads
+    them)."""
 
-    def __init__(self, group: int):
+    def __init__(self, rank: int, world: int, mode: str, device: torch.device, seed_offset: int = 0):
+        from paper_2511_02302_b200 import fp8flow as F
+
         t0 = time.time()
-        self.group = group
+        self.F, self.dev, self.mode = F, device, mode
+        sh = D.shard(rank, world, mode, N_EXPERTS, T_GLOBAL)
+        self.shard = sh
+        self.e0, self.E_loc = sh["expert_begin"], sh["num_local_experts"]
+        self.t0, self.t1 = sh["token_begin"], sh["token_end"]
         idx, probs = synth.routing(T_GLOBAL, synth.BASE_SEED)
-        sh = synth.expert_shard(idx, probs, group, D.NUM_GROUPS)
-        self.e0, self.E_loc = sh.expert_begin, sh.num_local_experts
-        self.recv = sh.recv_tokens
-        self.topk_idx = sh.topk_idx                      # [T_recv, 8] int32
-        self.probs = sh.probs                            # [T_recv, 8] fp32
+        rs = synth.expert_range_shard(idx, probs, self.e0, self.E_loc)
+        self.recv = rs.recv_tokens
+        self.topk_idx, self.probs = rs.topk_idx, rs.probs     # [T_recv, 8] int32 / fp32
         self.T_recv = len(self.recv)
-        # the layer's input activations; the received tokens are what dispatch would deliver
-        x_full = synth.activations_bf16(T_GLOBAL, HIDDEN, synth.BASE_SEED + 1)
-        tok0 = (T_GLOBAL // D.NUM_GROUPS) * group
-        self.x_shard = x_full[tok0: tok0 + T_GLOBAL // D.NUM_GROUPS].contiguous()
-        self.x_recv = x_full[torch.from_numpy(self.recv)].contiguous()
-        del x_full
-        self.dy_shard = synth.activations_bf16(T_GLOBAL // D.NUM_GROUPS, HIDDEN, synth.BASE_SEED + 2 + group)
         counts = np.array([np.sum(self.topk_idx == self.e0 + e) for e in range(self.E_loc)])
         self.counts = counts
         self.padded = (counts + ALIGN - 1) // ALIGN * ALIGN
-        self.R = int(self.padded.sum())                  # padded rows of this rank
+        self.R = int(self.padded.sum())                   # padded rows of this rank
         self.valid_rows = int(counts.sum())
-        self.h = synth.normal_bf16(self.R, 2 * FFN, synth.BASE_SEED + 3 + group, sigma=1.5)
-        self.y = synth.normal_bf16(self.R, HIDDEN, synth.BASE_SEED + 4 + group)
-        log(f"[bench] group {group}: T_recv={self.T_recv} R={self.R} valid={self.valid_rows} "
-            f"(host inputs in {time.time() - t0:.1f}s)")
-
-    def zero_pad_rows(self, src_of_row: np.ndarray) -> None:
-        """fc1/fc2 outputs of PAD rows are GEMM outputs of zero rows: zero them."""
-        pad = torch.from_numpy(src_of_row[: self.R] < 0)
+        self.n_tiles_T = int(np.sum((self.padded + 127) // 128))   # row blocks of the transposed outputs
+        self.n_shard = self.t1 - self.t0
+        # device inputs: the layer's activations (A1's token shard, and the received tokens that the
+        # dispatch would deliver, quantized once here), dY, fc1 output h, fc2 output y
+        x_full = synth.activations_bf16_device(T_GLOBAL, HIDDEN, synth.BASE_SEED + 1, device)
+        self.x_shard = x_full[self.t0:self.t1].contiguous()
+        x_recv = x_full[torch.from_numpy(self.recv).to(device)].contiguous()
+        del x_full
+        self.q_recv = torch.empty(self.T_recv, HIDDEN, dtype=torch.uint8, device=device)
+        self.s_recv = torch.empty(HIDDEN // 128, (self.T_recv + 15) // 16 * 16, dtype=torch.uint8, device=device)
+        F.fp8flow_quantize_rowwise(x_recv, self.q_recv, self.s_recv)
+        del x_recv
+        self.dy_shard = synth.activations_bf16_device(self.n_shard, HIDDEN, synth.BASE_SEED + 2 + rank + seed_offset,
+                                                      device)
+        self.topk = torch.from_numpy(self.topk_idx).to(device)
+        self.probs_dev = torch.from_numpy(self.probs).to(device)
+        self.h = synth.normal_bf16_device(self.R, 2 * FFN, synth.BASE_SEED + 3 + rank + seed_offset, device,
+                                          sigma=1.5)
+        self.y = synth.normal_bf16_device(self.R, HIDDEN, synth.BASE_SEED + 4 + rank + seed_offset, device)
+        # fc1/fc2 outputs of PAD rows are GEMM outputs of zero rows: zero them (the plan's PAD rows)
+        i32 = torch.int32
+        row_map = torch.empty(self.T_recv, TOP_K, dtype=i32, device=device)
+        src = torch.empty(self.R, dtype=i32, device=device)
+        off = torch.empty(self.E_loc + 1, dtype=i32, device=device)
+        ws = torch.empty(F.fp8flow_permute_workspace_bytes(self.T_recv, TOP_K, self.E_loc), dtype=torch.uint8,
+                         device=device)
+        F.fp8flow_permute_plan(self.topk, self.e0, self.E_loc, ALIGN, row_map, src, off, ws)
+        torch.cuda.synchronize(device)
+        assert int(off[-1].item()) == self.R and int(ws[:4].view(torch.int32).item()) == 0
+        pad = src < 0
         self.h[pad] = 0
         self.y[pad] = 0
+        del row_map, src, off, ws
+        torch.cuda.synchronize(device)
+        self.host = None
+        log(f"[bench] rank {rank}/{world} {mode}: experts [{self.e0}, {self.e0 + self.E_loc}) T_recv={self.T_recv} "
+            f"R={self.R} valid={self.valid_rows} (inputs in {time.time() - t0:.1f}s)")
+
+    def inputs(self) -> dict:
+        return {"x_shard": self.x_shard, "dy_shard": self.dy_shard, "topk": self.topk, "probs": self.probs_dev,
+                "q_recv": self.q_recv, "s_recv": self.s_recv, "h": self.h, "y": self.y}
+
+    def make_host_copies(self) -> dict:
+        """Pinned host copies of every input (once; used by the e2e leg and by the oracle)."""
+        if self.host is None:
+            self.host = {k: v.cpu().pin_memory() for k, v in self.inputs().items()}
+        return self.host
 
     def op_bytes(self) -> dict:
         seg = [int(x) for x in self.padded]
-        n_shard = T_GLOBAL // D.NUM_GROUPS
         return {
-            "A1_quantize_x": RL.quantize_bytes(n_shard, HIDDEN),
+            "A1_quantize_x": RL.quantize_bytes(self.n_shard, HIDDEN),
             "A3_plan": RL.permute_plan_bytes(self.T_recv, TOP_K, self.R),
             "A3_move": RL.permute_move_bytes(self.T_recv, self.R, HIDDEN),
             "A5_swiglu_quant": RL.swiglu_quant_bytes(self.R, FFN),
             "A4_unpermute": RL.unpermute_bytes(self.valid_rows, self.T_recv, TOP_K, HIDDEN, True),
-            "A1_quantize_dy": RL.quantize_bytes(n_shard, HIDDEN),
+            "A1_quantize_dy": RL.quantize_bytes(self.n_shard, HIDDEN),
             "A2_transpose_xperm": RL.transpose_bytes(seg, HIDDEN),
             "A2_transpose_a": RL.transpose_bytes(seg, FFN),
         }
@@ -113,29 +155,43 @@ class HostWorkload:
 # =============================================================================================
 # device side
 # =============================================================================================
-class DeviceStep:
-    def __init__(self, hw: HostWorkload, device: torch.device):
-        from paper_2511_02302_b200 import fp8flow as F
+def marginal_us(fn, flush, K: int = 10, reps: int = 3) -> float:
+    """Marginal cold-L2 cost of one launch of fn: K x [L2 flush, fn] against K x [L2 flush], both
+    enqueued behind a long spin so the host never limits, CUDA events around each sequence;
+    (T_with - T_without) / K, median of reps.  A single flushed launch timed alone also carries
+    ~6 us of fixed launch cost on this box (a 4-byte add measures 5.6-6.2 us that way,
+    profiles/r02_a1_redesign.txt); the marginal cost is the op's time inside a stream of work."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    fn()
+    res = []
+    for _ in range(reps):
+        tt = []
+        for with_op in (True, False):
+            torch.cuda.synchronize()
+            torch.cuda._sleep(20_000_000)
+            ev[0].record()
+            for _ in range(K):
+                flush()
+                if with_op:
+                    fn()
+            ev[1].record()
+            ev[1].synchronize()
+            tt.append(ev[0].elapsed_time(ev[1]))
+        res.append((tt[0] - tt[1]) / K)
+    return statistics.median(res) * 1e3
 
-        self.F, self.hw, self.dev = F, hw, device
+
+class DeviceStep:
+    def __init__(self, wl: Workload):
+        F, device = wl.F, wl.dev
+        self.F, self.wl, self.dev = F, wl, device
         F.fp8flow_device_check()
-        T, R, E = hw.T_recv, hw.R, hw.E_loc
-        n_shard = T_GLOBAL // D.NUM_GROUPS
+        T, R, E = wl.T_recv, wl.R, wl.E_loc
         u8, i32 = torch.uint8, torch.int32
         z = lambda *s, dt=u8: torch.empty(*s, dtype=dt, device=device)  # noqa: E731
-        # inputs (resident)
-        self.x_shard = hw.x_shard.to(device)
-        self.dy_shard = hw.dy_shard.to(device)
-        self.topk = torch.from_numpy(hw.topk_idx).to(device)
-        self.probs = torch.from_numpy(hw.probs).to(device)
-        x_recv = hw.x_recv.to(device)
-        self.q_recv = z(T, HIDDEN)
-        self.s_recv = z(HIDDEN // 128, (T + 15) // 16 * 16)
-        F.fp8flow_quantize_rowwise(x_recv, self.q_recv, self.s_recv)   # setup: dispatch payload
-        del x_recv
-        # outputs
-        self.q_x, self.s_x = z(n_shard, HIDDEN), z(HIDDEN // 128, n_shard)
-        self.q_dy, self.s_dy = z(n_shard, HIDDEN), z(HIDDEN // 128, n_shard)
+        n = wl.n_shard
+        self.q_x, self.s_x = z(n, HIDDEN), z(HIDDEN // 128, (n + 15) // 16 * 16)
+        self.q_dy, self.s_dy = z(n, HIDDEN), z(HIDDEN // 128, (n + 15) // 16 * 16)
         self.row_map, self.src, self.off = z(T, TOP_K, dt=i32), z(R, dt=i32), z(E + 1, dt=i32)
         self.ws = z(F.fp8flow_permute_workspace_bytes(T, TOP_K, E))
         self.x_perm, self.s_perm = z(R, HIDDEN), z(HIDDEN // 128, R)
@@ -143,13 +199,6 @@ class DeviceStep:
         self.y_tok = z(T, HIDDEN, dt=torch.bfloat16)
         self.xT, self.sxT = z(R * HIDDEN), z(R // 128 + E, HIDDEN)
         self.aT, self.saT = z(R * FFN), z(R // 128 + E, FFN)
-        # plan once at setup to zero the PAD rows of the synthetic GEMM outputs
-        F.fp8flow_permute_plan(self.topk, hw.e0, E, ALIGN, self.row_map, self.src, self.off, self.ws)
-        torch.cuda.synchronize(device)
-        assert int(self.off[-1].item()) == R and int(self.ws[:4].view(torch.int32).item()) == 0
-        hw.zero_pad_rows(self.src.cpu().numpy())
-        self.h = hw.h.to(device)
-        self.y = hw.y.to(device)
         self.l2_flush = torch.empty(256 << 20, dtype=u8, device=device)
         self.l2_clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(len(OPS) + 1)]
@@ -160,82 +209,45 @@ class DeviceStep:
         self.ev_end = torch.cuda.Event(enable_timing=True)
         self.ev_plan = torch.cuda.Event()
         self.ev_side = [torch.cuda.Event() for _ in range(3)]
-
-    def launch_ops(self, record: bool) -> None:
-        if NVTX:  # opt-in NVTX ranges per op for profiler filtering (host calls; off when timing)
-            if record:
-                self.events[0].record()
-            for i, (op, fn) in enumerate(self.op_fns().items()):
-                torch.cuda.nvtx.range_push(op)
-                fn()
-                torch.cuda.nvtx.range_pop()
-                if record:
-                    self.events[i + 1].record()
-            return
-        F, hw, ev = self.F, self.hw, self.events
-        if record:
-            ev[0].record()
-        F.fp8flow_quantize_rowwise(self.x_shard, self.q_x, self.s_x)
-        if record:
-            ev[1].record()
-        F.fp8flow_permute_plan(self.topk, hw.e0, hw.E_loc, ALIGN, self.row_map, self.src, self.off, self.ws)
-        if record:
-            ev[2].record()
-        F.fp8flow_permute_pad(self.q_recv, self.s_recv, self.src, self.off, self.x_perm, self.s_perm)
-        if record:
-            ev[3].record()
-        F.fp8flow_swiglu_quant(self.h, self.q_a, self.s_a, rows_dev=self.off[hw.E_loc:])
-        if record:
-            ev[4].record()
-        F.fp8flow_unpermute_unpad(self.y, self.row_map, self.probs, self.y_tok)
-        if record:
-            ev[5].record()
-        F.fp8flow_quantize_rowwise(self.dy_shard, self.q_dy, self.s_dy)
-        if record:
-            ev[6].record()
-        F.fp8flow_scaling_aware_transpose(self.x_perm, self.s_perm, self.xT, self.sxT, seg_offsets=self.off)
-        if record:
-            ev[7].record()
-        F.fp8flow_scaling_aware_transpose(self.q_a, self.s_a, self.aT, self.saT, seg_offsets=self.off)
-        if record:
-            ev[8].record()
+        self.graph = None
 
     def op_fns(self) -> dict:
-        """The step's ops as separate launches (same arguments as launch_ops), keyed like OPS."""
-        F, hw = self.F, self.hw
+        """The step's ops as separate launches, keyed like OPS (serial order)."""
+        F, wl = self.F, self.wl
         return {
-            "A1_quantize_x": lambda: F.fp8flow_quantize_rowwise(self.x_shard, self.q_x, self.s_x),
-            "A3_plan": lambda: F.fp8flow_permute_plan(self.topk, hw.e0, hw.E_loc, ALIGN, self.row_map, self.src,
+            "A1_quantize_x": lambda: F.fp8flow_quantize_rowwise(wl.x_shard, self.q_x, self.s_x),
+            "A3_plan": lambda: F.fp8flow_permute_plan(wl.topk, wl.e0, wl.E_loc, ALIGN, self.row_map, self.src,
                                                       self.off, self.ws),
-            "A3_move": lambda: F.fp8flow_permute_pad(self.q_recv, self.s_recv, self.src, self.off, self.x_perm,
+            "A3_move": lambda: F.fp8flow_permute_pad(wl.q_recv, wl.s_recv, self.src, self.off, self.x_perm,
                                                      self.s_perm),
-            "A5_swiglu_quant": lambda: F.fp8flow_swiglu_quant(self.h, self.q_a, self.s_a,
-                                                              rows_dev=self.off[hw.E_loc:]),
-            "A4_unpermute": lambda: F.fp8flow_unpermute_unpad(self.y, self.row_map, self.probs, self.y_tok),
-            "A1_quantize_dy": lambda: F.fp8flow_quantize_rowwise(self.dy_shard, self.q_dy, self.s_dy),
+            "A5_swiglu_quant": lambda: F.fp8flow_swiglu_quant(wl.h, self.q_a, self.s_a,
+                                                              rows_dev=self.off[wl.E_loc:]),
+            "A4_unpermute": lambda: F.fp8flow_unpermute_unpad(wl.y, self.row_map, wl.probs_dev, self.y_tok),
+            "A1_quantize_dy": lambda: F.fp8flow_quantize_rowwise(wl.dy_shard, self.q_dy, self.s_dy),
             "A2_transpose_xperm": lambda: F.fp8flow_scaling_aware_transpose(self.x_perm, self.s_perm, self.xT,
                                                                             self.sxT, seg_offsets=self.off),
             "A2_transpose_a": lambda: F.fp8flow_scaling_aware_transpose(self.q_a, self.s_a, self.aT, self.saT,
                                                                         seg_offsets=self.off),
         }
 
-    def isolated_us(self, reps: int = 10) -> dict:
-        """Each op alone after a clean L2 flush (median of reps): the kernel's own speed, without
-        the write-back of the previous kernels' dirty lines that the serial pass includes."""
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        out = {}
-        for op, fn in self.op_fns().items():
-            ts = []
-            for _ in range(reps):
-                self.flush_l2()
-                torch.cuda._sleep(1_000_000)
-                ev[0].record()
-                fn()
-                ev[1].record()
-                ev[1].synchronize()
-                ts.append(ev[0].elapsed_time(ev[1]))
-            out[op] = statistics.median(ts) * 1e3
-        return out
+    def launch_ops(self, record: bool) -> None:
+        """The step serially on the current stream (events between the kernels when record)."""
+        ev = self.events
+        if record:
+            ev[0].record()
+        for i, (op, fn) in enumerate(self.op_fns().items()):
+            if NVTX:  # opt-in NVTX ranges per op for profiler filtering (host calls; off when timing)
+                torch.cuda.nvtx.range_push(op)
+            fn()
+            if NVTX:
+                torch.cuda.nvtx.range_pop()
+            if record:
+                ev[i + 1].record()
+
+    def isolated_us(self) -> dict:
+        """Each op's marginal cold-L2 cost (marginal_us): its own speed without the write-back of the
+        previous kernels' dirty lines that the serial pass includes."""
+        return {op: marginal_us(fn, self.flush_l2) for op, fn in self.op_fns().items()}
 
     def flush_l2(self) -> None:
         """Write a 256 MiB buffer (evicts everything), then read another 256 MiB buffer so the L2 is
@@ -247,27 +259,27 @@ class DeviceStep:
     def launch_ops_concurrent(self, fork=None, join=None) -> None:
         """The step's DAG on 4 streams; `fork`/`join` are the events that open and close it
         (the timing events by default, plain events when the DAG is captured into a graph)."""
-        F, hw = self.F, self.hw
+        F, wl = self.F, self.wl
         main = torch.cuda.current_stream()
         s1, s2, s3 = self.side
         fork = self.ev_start if fork is None else fork
         join = self.ev_end if join is None else join
         fork.record(main)
         s1.wait_event(fork)
-        F.fp8flow_quantize_rowwise(self.x_shard, self.q_x, self.s_x, stream=s1)
-        F.fp8flow_quantize_rowwise(self.dy_shard, self.q_dy, self.s_dy, stream=s1)
+        F.fp8flow_quantize_rowwise(wl.x_shard, self.q_x, self.s_x, stream=s1)
+        F.fp8flow_quantize_rowwise(wl.dy_shard, self.q_dy, self.s_dy, stream=s1)
         self.ev_side[0].record(s1)
-        F.fp8flow_permute_plan(self.topk, hw.e0, hw.E_loc, ALIGN, self.row_map, self.src, self.off, self.ws,
+        F.fp8flow_permute_plan(wl.topk, wl.e0, wl.E_loc, ALIGN, self.row_map, self.src, self.off, self.ws,
                                stream=main)
         self.ev_plan.record(main)
         s2.wait_event(self.ev_plan)
         s3.wait_event(self.ev_plan)
-        F.fp8flow_swiglu_quant(self.h, self.q_a, self.s_a, rows_dev=self.off[hw.E_loc:], stream=s2)
+        F.fp8flow_swiglu_quant(wl.h, self.q_a, self.s_a, rows_dev=self.off[wl.E_loc:], stream=s2)
         F.fp8flow_scaling_aware_transpose(self.q_a, self.s_a, self.aT, self.saT, seg_offsets=self.off, stream=s2)
         self.ev_side[1].record(s2)
-        F.fp8flow_unpermute_unpad(self.y, self.row_map, self.probs, self.y_tok, stream=s3)
+        F.fp8flow_unpermute_unpad(wl.y, self.row_map, wl.probs_dev, self.y_tok, stream=s3)
         self.ev_side[2].record(s3)
-        F.fp8flow_permute_pad(self.q_recv, self.s_recv, self.src, self.off, self.x_perm, self.s_perm, stream=main)
+        F.fp8flow_permute_pad(wl.q_recv, wl.s_recv, self.src, self.off, self.x_perm, self.s_perm, stream=main)
         F.fp8flow_scaling_aware_transpose(self.x_perm, self.s_perm, self.xT, self.sxT, seg_offsets=self.off,
                                           stream=main)
         for e in self.ev_side:
@@ -311,141 +323,60 @@ class DeviceStep:
         return [self.events[i].elapsed_time(self.events[i + 1]) for i in range(len(OPS))]
 
     def outputs(self) -> dict:
-        return {"q_x": self.q_x, "s_x": self.s_x, "x_perm": self.x_perm, "s_perm": self.s_perm, "q_a": self.q_a,
-                "s_a": self.s_a, "y_tok": self.y_tok, "q_dy": self.q_dy, "s_dy": self.s_dy, "xT": self.xT,
-                "sxT": self.sxT, "aT": self.aT, "saT": self.saT}
+        n, nt = self.wl.n_shard, self.wl.n_tiles_T
+        return {"q_x": self.q_x, "s_x": self.s_x[:, :n], "x_perm": self.x_perm, "s_perm": self.s_perm,
+                "q_a": self.q_a, "s_a": self.s_a, "y_tok": self.y_tok, "q_dy": self.q_dy, "s_dy": self.s_dy[:, :n],
+                "xT": self.xT, "sxT": self.sxT[:nt], "aT": self.aT, "saT": self.saT[:nt]}
 
-    def checksums(self) -> list[int]:
-        out = torch.zeros(len(self.outputs()), dtype=torch.int64, device=self.dev)
-        for i, t in enumerate(self.outputs().values()):
-            self.F.fp8flow_checksum64(t, out[i:i + 1])
-        return [int(v) & ((1 << 64) - 1) for v in out.cpu().tolist()]
+    def checksums(self) -> dict:
+        """C11 checksum of every output (fp8flow_checksum64 on the device), name -> uint64."""
+        outs = {k: v.contiguous() for k, v in self.outputs().items()}
+        res = torch.zeros(len(outs), dtype=torch.int64, device=self.dev)
+        for i, t in enumerate(outs.values()):
+            self.F.fp8flow_checksum64(t, res[i:i + 1])
+        return {k: int(v) & ((1 << 64) - 1) for k, v in zip(outs, res.cpu().tolist())}
 
 
 # =============================================================================================
 # end to end through the C ABI with host buffers
 # =============================================================================================
 def run_e2e(ds: DeviceStep, steps: int) -> dict:
-    """Per step: H2D of every input from pinned host memory, the step, output checksums, D2H of
-    the checksums (the step's verification result).  Timed with CUDA events on the stream."""
-    hw = ds.hw
-    host_in = {
-        "x_shard": hw.x_shard, "dy_shard": hw.dy_shard, "topk": torch.from_numpy(hw.topk_idx),
-        "probs": torch.from_numpy(hw.probs), "q_recv": ds.q_recv.cpu(), "s_recv": ds.s_recv.cpu(),
-        "h": hw.h, "y": hw.y,
-    }
-    pinned = {k: v.contiguous().pin_memory() for k, v in host_in.items()}
-    dev_in = {"x_shard": ds.x_shard, "dy_shard": ds.dy_shard, "topk": ds.topk, "probs": ds.probs,
-              "q_recv": ds.q_recv, "s_recv": ds.s_recv, "h": ds.h, "y": ds.y}
-    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
-    n_out = len(ds.outputs())
-    res_dev = torch.zeros(n_out, dtype=torch.int64, device=ds.dev)
-    res_host = torch.zeros(n_out, dtype=torch.int64).pin_memory()
+    """Per step, inside the timed events: H2D of every input from pinned host memory, the step
+    (graph replay), and D2H of EVERY output (codes, scales, BF16 combine output, transposes) into
+    pinned host memory.  Returns the mean ms and the bytes copied each way."""
+    wl = ds.wl
+    host_in = wl.make_host_copies()
+    dev_in = wl.inputs()
+    outs = ds.outputs()
+    host_out = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in outs.items()}
+    h2d = sum(t.numel() * t.element_size() for t in host_in.values())
+    d2h = sum(t.numel() * t.element_size() for t in host_out.values())
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     for it in range(steps + 1):
         ds.flush_l2()
         torch.cuda.synchronize(ds.dev)
         s.record()
-        for k, t in pinned.items():
+        for k, t in host_in.items():
             dev_in[k].copy_(t, non_blocking=True)
-        if getattr(ds, "graph", None) is not None:
-            ds.graph.replay()
-        else:
-            ds.launch_ops_concurrent()
-        for i, t in enumerate(ds.outputs().values()):
-            ds.F.fp8flow_checksum64(t, res_dev[i:i + 1])
-        res_host.copy_(res_dev, non_blocking=True)
+        ds.graph.replay()
+        for k, t in outs.items():
+            host_out[k].copy_(t, non_blocking=True)
         e.record()
         e.synchronize()
         if it > 0:
             times.append(s.elapsed_time(e))
-    ms = statistics.mean(times)
-    return {"ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": n_out * 8}
+    ds.host_out = host_out          # the last step's outputs, on the host (the verification reads them)
+    return {"ms_per_step": statistics.mean(times), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
 
 # =============================================================================================
-# parity of the timed outputs against the oracle (sampled; after timing)
+# the CPU-oracle leg: whole-step verification + the cpu_baseline timing (after the GPU timing)
 # =============================================================================================
-def _oracle_parity(O, ds: DeviceStep) -> dict:
-    """Sampled parity of the timed outputs against the oracle module O (passed in by
-    cpu_baseline_leg, the only code in bench.py that loads the oracle)."""
-    hw, res = ds.hw, {}
-    host = lambda t: t.cpu().numpy()  # noqa: E731
-    bits = synth.bf16_bits
-    rows = np.r_[0:64, len(hw.x_shard) - 64:len(hw.x_shard)]
-    for name, x, q, s in (("A1_quantize_x", hw.x_shard, ds.q_x, ds.s_x), ("A1_quantize_dy", hw.dy_shard, ds.q_dy, ds.s_dy)):
-        qr, sr = O.quantize_rowwise_bf16(bits(x)[rows])
-        res[name] = bool(np.array_equal(host(q)[rows], qr) and np.array_equal(host(s)[:, rows], sr))
-    rm, src, off = O.permute_plan(hw.topk_idx, hw.e0, hw.E_loc, max_rows=hw.R)
-    res["A3_plan"] = bool(np.array_equal(host(ds.row_map), rm) and np.array_equal(host(ds.off), off)
-                          and np.array_equal(host(ds.src), src))
-    q_recv, s_recv = host(ds.q_recv), host(ds.s_recv)
-    qo, so = O.permute_pad(q_recv, s_recv, src, off, max_rows=hw.R)
-    res["A3_move"] = bool(np.array_equal(host(ds.x_perm), qo) and np.array_equal(host(ds.s_perm), so))
-    sample = np.r_[0:256, hw.R - 256:hw.R]
-    qa, sa = O.swiglu_quant(bits(hw.h)[sample])
-    q_a, s_a = host(ds.q_a)[sample], host(ds.s_a)[:, sample]
-    ulp = lambda c: np.where(c < 0x80, c & 0x7F, -(c.astype(np.int32) & 0x7F))  # noqa: E731
-    d = np.abs(ulp(q_a.astype(np.int32)) - ulp(qa.astype(np.int32)))
-    res["A5_swiglu_quant"] = bool(np.array_equal(s_a, sa) and d.max() <= 1 and np.mean(d > 0) <= 1e-4)
-    toks = np.r_[0:128, hw.T_recv - 128:hw.T_recv]
-    y_ref = O.unpermute(bits(hw.y), rm[toks], hw.probs[toks])
-    res["A4_unpermute"] = bool(np.array_equal(host(ds.y_tok.view(torch.int16))[toks].view(np.uint16), y_ref))
-    # A2 on three experts (first, middle, last), each checked as its own segment
-    for name, qsrc, ssrc, qT, sT, cols in (("A2_transpose_xperm", qo, so, ds.xT, ds.sxT, HIDDEN),
-                                           ("A2_transpose_a", host(ds.q_a), host(ds.s_a), ds.aT, ds.saT, FFN)):
-        ok = True
-        qT_h, sT_h = host(qT), host(sT)
-        tiles = np.concatenate([[0], np.cumsum((np.diff(off) + 127) // 128)])
-        for e in (0, hw.E_loc // 2, hw.E_loc - 1):
-            o, m = int(off[e]), int(off[e + 1] - off[e])
-            if m == 0:
-                continue
-            qr, sr = O.scaling_aware_transpose(np.ascontiguousarray(qsrc[o:o + m]), np.ascontiguousarray(ssrc[:, o:o + m]))
-            ok &= np.array_equal(qT_h[cols * o: cols * (o + m)], qr)
-            ok &= np.array_equal(sT_h[tiles[e]: tiles[e + 1]], sr)
-        res[name] = bool(ok)
-    return res
-
-
-# =============================================================================================
-# CPU oracle timing (cpu_baseline and the reference arm)
-# =============================================================================================
-def oracle_sample(O, hw: HostWorkload, frac: float, threads: int | None) -> tuple[float, float, str]:
-    """Runs the oracle module O on a bounded sample (fraction `frac` of every op's rows) of this
-    rank's step.  Returns (algorithmic bytes of the sample, seconds, description)."""
-    bits = synth.bf16_bits
-    n_sh = max(16, int(len(hw.x_shard) * frac) // 16 * 16)
-    n_tok = max(16, int(hw.T_recv * frac))
-    n_rows = max(128, int(hw.R * frac) // 16 * 16)
-    xs, dys = bits(hw.x_shard[:n_sh]), bits(hw.dy_shard[:n_sh])
-    hs, ys = bits(hw.h[:n_rows]), bits(hw.y)
-    x_recv_bits = bits(hw.x_recv[:n_tok])
-    q_tok, s_tok = O.quantize_rowwise_bf16(x_recv_bits)                     # setup (untimed)
-    idx_s = hw.topk_idx[:n_tok]
-    counts = np.array([np.sum(idx_s == hw.e0 + e) for e in range(hw.E_loc)])
-    padded = (counts + ALIGN - 1) // ALIGN * ALIGN
-    R_s = int(padded.sum())
-    t0 = time.perf_counter()
-    O.quantize_rowwise_bf16(xs, threads=threads)
-    rm, src, off = O.permute_plan(idx_s, hw.e0, hw.E_loc, max_rows=R_s)
-    qo, so = O.permute_pad(q_tok, s_tok, src, off, max_rows=R_s, threads=threads)
-    qa, sa = O.swiglu_quant(hs, threads=threads)
-    O.unpermute(ys, rm, hw.probs[:n_tok], threads=threads)
-    O.quantize_rowwise_bf16(dys, threads=threads)
-    O.scaling_aware_transpose(qo, so, off, threads=threads)
-    seg_a = np.array([0, n_rows], np.int32)
-    O.scaling_aware_transpose(qa, sa, seg_a, threads=threads)
-    dt = time.perf_counter() - t0
-    nbytes = (2 * RL.quantize_bytes(n_sh, HIDDEN) + RL.permute_plan_bytes(n_tok, TOP_K, R_s)
-              + RL.permute_move_bytes(n_tok, R_s, HIDDEN) + RL.swiglu_quant_bytes(n_rows, FFN)
-              + RL.unpermute_bytes(int(counts.sum()), n_tok, TOP_K, HIDDEN, True)
-              + RL.transpose_bytes([int(p) for p in padded], HIDDEN) + RL.transpose_bytes([n_rows], FFN))
-    desc = (f"oracle (plain C, fp64) on {frac:.4g} of rank-0's step: A1 {n_sh}x{HIDDEN} x2, A3 plan+move "
-            f"{n_tok} tokens -> {R_s} rows, A5 {n_rows}x{2 * FFN}, A4 {n_tok} tokens, A2 {R_s}x{HIDDEN} + "
-            f"{n_rows}x{FFN}")
-    return nbytes, dt, desc
+def _ulp_dist(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Distance in E4M3 code order (codes of one sign are monotone in magnitude)."""
+    o = lambda c: np.where(c < 0x80, c & 0x7F, -(c & 0x7F))  # noqa: E731
+    return np.abs(o(a.astype(np.int32)) - o(b.astype(np.int32)))
 
 
 def _gemm_rows_check(O, entry: dict, samples, what: str) -> None:
@@ -458,29 +389,82 @@ def _gemm_rows_check(O, entry: dict, samples, what: str) -> None:
     entry.update({"parity_rows": what, "parity_worst": worst, "parity_ok": worst <= 2.0 ** -14})
 
 
-def cpu_baseline_leg(hw: "HostWorkload", ds: "DeviceStep", time_it: bool, verify: bool, checks: list) -> tuple:
-    """The CPU-oracle leg of bench.py -- the only code here that loads oracle/ (test
-    infrastructure): (1) on rank 0 at N = 1, the oracle as it stands timed on a bounded sample of the
-    step (all host cores, and one core on 1/16 of it); (2) the sampled parity of the timed GPU
-    outputs (step ops and the queued NEXT-2 GEMM rows) against the oracle, after timing.  Returns
-    (cpu_baseline dict or None, parity dict or None)."""
+def cpu_baseline_leg(wl: Workload, ds: DeviceStep, time_it: bool, verify: bool, checks: list,
+                     threads: int | None) -> dict:
+    """The CPU-oracle leg of bench.py -- with run_reference, the only code here that loads oracle/
+    (test infrastructure).  The oracle, as it stands, runs the rank's WHOLE step on the same input
+    bytes as the GPU (host copies): that run is timed (the cpu_baseline, `threads` host threads)
+    and its outputs are compared with the timed GPU outputs element by element (codes, scales,
+    plan, BF16: identical; A5 codes within 1 E4M3 ULP on <= 1e-4 of elements, scales identical)
+    and by the C11 checksum of every output.  The queued NEXT-2 GEMM rows are checked too."""
     if not (time_it or verify):
-        return None, None
+        return {}
     import oracle as O
 
-    cpu = parity = None
-    if verify:
-        parity = _oracle_parity(O, ds)
-        for entry, samples, what in checks:
-            _gemm_rows_check(O, entry, samples, what)
+    host = wl.make_host_copies()
+    bits = synth.bf16_bits
+    x, dy = bits(host["x_shard"]), bits(host["dy_shard"])
+    h, y = bits(host["h"]), bits(host["y"])
+    q_recv = host["q_recv"].numpy()[: wl.T_recv]
+    s_recv = np.ascontiguousarray(host["s_recv"].numpy()[:, : wl.T_recv])
+    topk, probs = host["topk"].numpy(), host["probs"].numpy()
+    t0 = time.perf_counter()
+    ref = {}
+    ref["q_x"], ref["s_x"] = O.quantize_rowwise_bf16(x, threads=threads)
+    rm, src, off = O.permute_plan(topk, wl.e0, wl.E_loc, max_rows=wl.R)
+    ref["x_perm"], ref["s_perm"] = O.permute_pad(q_recv, s_recv, src, off, max_rows=wl.R, threads=threads)
+    ref["q_a"], ref["s_a"] = O.swiglu_quant(h, threads=threads)
+    ref["y_tok"] = O.unpermute(y, rm, probs, threads=threads)
+    ref["q_dy"], ref["s_dy"] = O.quantize_rowwise_bf16(dy, threads=threads)
+    ref["xT"], ref["sxT"] = O.scaling_aware_transpose(ref["x_perm"], ref["s_perm"], off, threads=threads)
+    ref["aT"], ref["saT"] = O.scaling_aware_transpose(ref["q_a"], ref["s_a"], off, threads=threads)
+    secs = time.perf_counter() - t0
+    nbytes = sum(wl.op_bytes().values())
+    out = {}
     if time_it:
-        nbytes, secs, desc = oracle_sample(O, hw, 1.0, None)
-        nb1, secs1, desc1 = oracle_sample(O, hw, 1.0 / 16, 1)  # the same oracle on one core, 1/16 of the sample
-        cpu = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": desc, "seconds": round(secs, 2), "cpu_model": cpu_model(),
-               "single_thread": {"value": round(nb1 / secs1 / 1e9, 4), "unit": "GB/s", "sample": desc1,
-                                 "seconds": round(secs1, 2)}}
-    return cpu, parity
+        out["cpu"] = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": threads or cpu_cores(),
+                      "kind": "oracle", "seconds": round(secs, 2), "bytes": nbytes, "cpu_model": cpu_model(),
+                      "sample": f"the rank's whole step (plain C, fp64 where the paper does not fix the "
+                                f"precision): A1 {wl.n_shard}x{HIDDEN} x2, A3 plan+move {wl.T_recv} tokens -> "
+                                f"{wl.R} rows over {wl.E_loc} experts, A5 {wl.R}x{2 * FFN}, A4 {wl.T_recv} "
+                                f"tokens, A2 {wl.R}x{HIDDEN} + {wl.R}x{FFN}"}
+    if not verify:
+        return out
+    gpu = getattr(ds, "host_out", None)
+    if gpu is None:
+        gpu = {k: v.cpu() for k, v in ds.outputs().items()}
+    g = {k: (v.view(torch.int16).numpy().view(np.uint16) if v.dtype == torch.bfloat16 else v.numpy())
+         for k, v in gpu.items()}
+    eq = np.array_equal
+    par = {}
+    par["A1_quantize_x"] = bool(eq(g["q_x"], ref["q_x"]) and eq(g["s_x"], ref["s_x"]))
+    par["A3_plan"] = bool(eq(ds.row_map.cpu().numpy(), rm) and eq(ds.off.cpu().numpy(), off)
+                          and eq(ds.src.cpu().numpy(), src))
+    par["A3_move"] = bool(eq(g["x_perm"], ref["x_perm"]) and eq(g["s_perm"], ref["s_perm"]))
+    d = _ulp_dist(g["q_a"], ref["q_a"])
+    a5_mism = int(np.count_nonzero(d))
+    par["A5_swiglu_quant"] = bool(eq(g["s_a"], ref["s_a"]) and d.max() <= 1 and a5_mism <= 1e-4 * d.size)
+    par["A4_unpermute"] = bool(eq(g["y_tok"], ref["y_tok"]))
+    par["A1_quantize_dy"] = bool(eq(g["q_dy"], ref["q_dy"]) and eq(g["s_dy"], ref["s_dy"]))
+    par["A2_transpose_xperm"] = bool(eq(g["xT"], ref["xT"]) and eq(g["sxT"], ref["sxT"]))
+    if a5_mism:   # A2's own input is the GPU's A: transpose exactly that (untimed)
+        aT_ref, saT_ref = O.scaling_aware_transpose(g["q_a"], g["s_a"], off, threads=threads)
+    else:
+        aT_ref, saT_ref = ref["aT"], ref["saT"]
+    par["A2_transpose_a"] = bool(eq(g["aT"], aT_ref) and eq(g["saT"], saT_ref))
+    # C11: the GPU's device checksums against the oracle's checksum of its own outputs
+    gsum = ds.checksums()
+    osum = {k: O.checksum64(np.ascontiguousarray(v).view(np.uint8)) for k, v in ref.items()}
+    match = {k: gsum[k] == osum[k] for k in gsum}
+    exact = [k for k in match if k not in ("q_a", "aT")]   # A5 codes: <= 1 ULP allowed (R20)
+    out.update({"parity": par, "checksums_match": all(match[k] for k in exact),
+                "a5_codes_checksums_match": bool(match["q_a"] and match["aT"]), "a5_code_mismatches": a5_mism,
+                "checksums": {k: f"{v:016x}" for k, v in gsum.items()},
+                "verified": "every output element of the rank's step vs the oracle on the same inputs"})
+    for entry, samples, what in checks:
+        _gemm_rows_check(O, entry, samples, what)
+    return out
+
 
 def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
@@ -495,6 +479,7 @@ def cpu_model() -> str:
     except OSError:
         pass
     return "unknown"
+
 
 
 # =============================================================================================
@@ -544,49 +529,117 @@ class ClockSampler:
 # =============================================================================================
 # config-2 sub-measurement (4096 x 7168, one expert): A1, A2 and the naive comparator
 # =============================================================================================
-def next_ops_measure(ds: "DeviceStep", peak: float, reps: int = 20, checks: list | None = None) -> dict:
-    """NEXT rows measured on the same workload (not part of the headline step): NEXT-1 fused
-    SwiGLU backward + quant of dA [R, 2048] with the saved fc1 output h [R, 4096], and the
-    dual-output SwiGLU + quant emitting A row-wise and column-wise (per expert) in one pass, against
-    the two launches (A5 then A2) it replaces."""
-    F = ds.F
-    hw = ds.hw
-    dA = synth.normal_bf16(hw.R, FFN, synth.BASE_SEED + 5, sigma=0.5).to(ds.dev)
-    q = torch.empty(hw.R, 2 * FFN, dtype=torch.uint8, device=ds.dev)
-    s = torch.empty(2 * FFN // 128, hw.R, dtype=torch.uint8, device=ds.dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    rows_dev = ds.off[hw.E_loc:]
+def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
+    """Config 2: one expert's activations 4096 x 7168.  Per op: the marginal cold-L2 cost
+    (marginal_us, the reported `us`/`frac`) and the single flushed launch timed alone
+    (`single_launch_us`, which also carries the ~6 us fixed launch cost), plus hot-L2 numbers."""
+    from paper_2511_02302_b200 import fp8flow as F
 
-    def med(fn):
+    rows, cols = 4096, HIDDEN
+    x = synth.activations_bf16_device(rows, cols, synth.BASE_SEED + 9, device)
+    q = torch.empty(rows, cols, dtype=torch.uint8, device=device)
+    s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=device)
+    qT = torch.empty(rows * cols, dtype=torch.uint8, device=device)
+    sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
+    ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, 1), dtype=torch.uint8, device=device)
+    flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
+    flush = lambda: (flush_w.zero_(), clean.sum())  # noqa: E731
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    naive_actual = RL.naive_transpose_actual_bytes([rows], cols)
+    ops = {"A1_quantize": (lambda: F.fp8flow_quantize_rowwise(x, q, s), RL.quantize_bytes(rows, cols)),
+           "A2_transpose": (lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT), RL.transpose_bytes([rows], cols)),
+           "naive_dequant_transpose_requant": (lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws),
+                                               RL.transpose_bytes([rows], cols)),
+           "A1_then_A2_two_launches": (lambda: (F.fp8flow_quantize_rowwise(x, q, s),
+                                                F.fp8flow_scaling_aware_transpose(q, s, qT, sT)),
+                                       RL.quantize_dual_bytes([rows], cols)),
+           "NEXT1_quantize_dual": (lambda: F.fp8flow_quantize_dual(x, q, s, qT, sT), RL.quantize_dual_bytes([rows], cols))}
+    out = {"shape": [rows, cols], "l2": "flushed before each launch (256 MiB write + 256 MiB read)",
+           "timing": "us = marginal cold-L2 cost (K x [flush, op] - K x [flush], K=10, median of 3); "
+                     "single_launch_us = one flushed launch alone between events (mean of reps)"}
+    for name, (fn, nbytes) in ops.items():
+        us = marginal_us(fn, flush)
         fn()
         ts = []
         for _ in range(reps):
-            ds.flush_l2()
+            flush()
             torch.cuda._sleep(1_000_000)
             ev[0].record()
             fn()
             ev[1].record()
             ev[1].synchronize()
             ts.append(ev[0].elapsed_time(ev[1]))
-        return statistics.median(ts)
+        single = statistics.mean(ts) * 1e3
+        out[name] = {"us": round(us, 2), "gbs": round(nbytes / us / 1e3, 1), "frac": round(nbytes / us / 1e3 / peak, 3),
+                     "single_launch_us": round(single, 2), "single_launch_frac": round(nbytes / single / 1e3 / peak, 3)}
+    nv = out["naive_dequant_transpose_requant"]
+    nv["actual_bytes"] = naive_actual
+    nv["actual_gbs"] = round(naive_actual / nv["us"] / 1e3, 1)
+    nv["actual_frac"] = round(naive_actual / nv["us"] / 1e3 / peak, 3)
+    out["naive_over_direct_latency"] = round(nv["us"] / out["A2_transpose"]["us"], 2)
+    out["naive_over_direct_bytes"] = round(naive_actual / RL.transpose_bytes([rows], cols), 2)
+    # hot-L2 numbers (labelled as such, SURVEY §8(d)): the working set (58.7 MB in + 29.4 MB out)
+    # fits the 126 MB L2, so back-to-back launches without a flush, 20 per CUDA graph replay
+    hot = {}
+    for name in ("A1_quantize", "A2_transpose"):
+        fn, nbytes = ops[name]
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            ev[0].record()
+            g.replay()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]) / 20)
+        ms = statistics.median(ts)
+        hot[name] = {"us": round(ms * 1e3, 2), "gbs": round(nbytes / ms / 1e6, 1)}
+    out["hot_l2_graph"] = hot
+    return out
+
+
+def next_ops_measure(device, peak: float, reps: int = 20, checks: list | None = None) -> dict:
+    """NEXT rows on one EP8 expert group of the layer (group 0, 32 experts; not part of the
+    headline step): NEXT-1 fused SwiGLU backward + quant and the dual-output SwiGLU + quant,
+    NEXT-2 GEMMs on the step's outputs, NEXT-3 dispatch/combine over 8 virtual ranks."""
+    wl = Workload(0, 1, "weak", device, seed_offset=0)
+    ds = DeviceStep(wl)
+    ds.launch_ops(record=False)
+    torch.cuda.synchronize(device)
+    F = ds.F
+    R, E = wl.R, wl.E_loc
+    dA = synth.normal_bf16_device(R, FFN, synth.BASE_SEED + 5, device, sigma=0.5)
+    q = torch.empty(R, 2 * FFN, dtype=torch.uint8, device=device)
+    s = torch.empty(2 * FFN // 128, R, dtype=torch.uint8, device=device)
+    rows_dev = ds.off[E:]
+
+    def med(fn):
+        return marginal_us(fn, ds.flush_l2) / 1e3
 
     def line(ms, nb, **kw):
         return {"us": round(ms * 1e3, 2), "bytes": nb, "gbs": round(nb / ms / 1e6, 1),
                 "frac": round(nb / ms / 1e6 / peak, 3), **kw}
 
-    out = {}
-    ms = med(lambda: F.fp8flow_swiglu_bwd_quant(ds.h, dA, q, s, rows_dev=rows_dev))
-    out["NEXT1_swiglu_bwd_quant"] = line(ms, RL.swiglu_bwd_quant_bytes(hw.R, FFN),
-                                         shape={"h": [hw.R, 2 * FFN], "dA": [hw.R, FFN]})
-    segs = [int(v) for v in hw.padded]
+    out = {"workload": f"EP8 expert group 0: {wl.T_recv} received tokens, {R} padded rows, {E} experts; "
+                       "times are marginal cold-L2 costs"}
+    ms = med(lambda: F.fp8flow_swiglu_bwd_quant(wl.h, dA, q, s, rows_dev=rows_dev))
+    out["NEXT1_swiglu_bwd_quant"] = line(ms, RL.swiglu_bwd_quant_bytes(R, FFN),
+                                         shape={"h": [R, 2 * FFN], "dA": [R, FFN]})
+    segs = [int(v) for v in wl.padded]
     nb = RL.swiglu_quant_dual_bytes(segs, FFN)
-    ms_two = med(lambda: (F.fp8flow_swiglu_quant(ds.h, ds.q_a, ds.s_a, rows_dev=rows_dev),
+    ms_two = med(lambda: (F.fp8flow_swiglu_quant(wl.h, ds.q_a, ds.s_a, rows_dev=rows_dev),
                           F.fp8flow_scaling_aware_transpose(ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off)))
-    ms = med(lambda: F.fp8flow_swiglu_quant_dual(ds.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off))
-    out["NEXT1_swiglu_quant_dual"] = line(ms, nb, segments=len(segs),
-                                          vs_A5_then_A2_us=round(ms_two * 1e3, 2))
-    out.update(gemm_measure(ds, reps, checks))
-    out.update(ep_measure(ds.dev, peak, reps))
+    ms = med(lambda: F.fp8flow_swiglu_quant_dual(wl.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off))
+    out["NEXT1_swiglu_quant_dual"] = line(ms, nb, segments=len(segs), vs_A5_then_A2_us=round(ms_two * 1e3, 2))
+    out.update(gemm_measure(ds, reps=10, checks=checks))
+    out.update(ep_measure(device, peak, reps))
     return out
 
 
@@ -895,7 +948,7 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10, checks: list | None = None) -
     with synthetic FP8 expert weights; TFLOP/s against the FP8 dense peak (2 x measured bf16, the
     profiling guide's nominal ratio).  Sampled output rows are queued in `checks` for the oracle
     comparison in cpu_baseline_leg."""
-    F, hw, dev = ds.F, ds.hw, ds.dev
+    F, hw, dev = ds.F, ds.wl, ds.dev
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     bf16 = json.load(open(peaks_path))["bf16_tflops"] if os.path.exists(peaks_path) else 1673.3
     fp8_peak = 2.0 * bf16
@@ -946,10 +999,10 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10, checks: list | None = None) -
 
     # Wgrad of fc1, all FP8: dH from NEXT-1 (SwiGLU backward + quant) -> A2 per expert -> grouped-K
     # GEMM with A2(X_perm) from the step: dW1_e = dH_e^T X_e, BF16 [32][4096][7168]
-    dA = synth.normal_bf16(hw.R, FFN, synth.BASE_SEED + 5, sigma=0.5).to(dev)
+    dA = synth.normal_bf16_device(hw.R, FFN, synth.BASE_SEED + 5, dev, sigma=0.5)
     qh = torch.empty(hw.R, 2 * FFN, dtype=torch.uint8, device=dev)
     sh = torch.empty(2 * FFN // 128, hw.R, dtype=torch.uint8, device=dev)
-    F.fp8flow_swiglu_bwd_quant(ds.h, dA, qh, sh, rows_dev=ds.off[E:])
+    F.fp8flow_swiglu_bwd_quant(hw.h, dA, qh, sh, rows_dev=ds.off[E:])
     hT = torch.empty(hw.R * 2 * FFN, dtype=torch.uint8, device=dev)
     shT = torch.empty(hw.R // 128 + E, 2 * FFN, dtype=torch.uint8, device=dev)
     F.fp8flow_scaling_aware_transpose(qh, sh, hT, shT, seg_offsets=ds.off)
@@ -975,70 +1028,6 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10, checks: list | None = None) -
     return out
 
 
-def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
-    from paper_2511_02302_b200 import fp8flow as F
-
-    rows, cols = 4096, HIDDEN
-    x = synth.activations_bf16(rows, cols, synth.BASE_SEED + 9).to(device)
-    q = torch.empty(rows, cols, dtype=torch.uint8, device=device)
-    s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=device)
-    qT = torch.empty(rows * cols, dtype=torch.uint8, device=device)
-    sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
-    ws = torch.empty(F.fp8flow_naive_workspace_bytes(rows, cols, 1), dtype=torch.uint8, device=device)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
-    clean = torch.ones(64 << 20, dtype=torch.float32, device=device)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    ops = {"A1_quantize": (lambda: F.fp8flow_quantize_rowwise(x, q, s), RL.quantize_bytes(rows, cols)),
-           "A2_transpose": (lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT), RL.transpose_bytes([rows], cols)),
-           "naive_dequant_transpose_requant": (lambda: F.fp8flow_naive_transpose(q, s, qT, sT, ws),
-                                               RL.transpose_bytes([rows], cols)),
-           "A1_then_A2_two_launches": (lambda: (F.fp8flow_quantize_rowwise(x, q, s),
-                                                F.fp8flow_scaling_aware_transpose(q, s, qT, sT)),
-                                       RL.quantize_dual_bytes([rows], cols)),
-           "NEXT1_quantize_dual": (lambda: F.fp8flow_quantize_dual(x, q, s, qT, sT), RL.quantize_dual_bytes([rows], cols))}
-    out = {"shape": [rows, cols], "l2": "flushed before each launch (256 MiB write + 256 MiB read)"}
-    for name, (fn, nbytes) in ops.items():
-        fn()
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            clean.sum()
-            torch.cuda._sleep(1_000_000)
-            ev[0].record()
-            fn()
-            ev[1].record()
-            ev[1].synchronize()
-            ts.append(ev[0].elapsed_time(ev[1]))
-        ms = statistics.median(ts)
-        out[name] = {"us": round(ms * 1e3, 2), "gbs": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / peak, 3)}
-    out["naive_over_direct_latency"] = round(out["naive_dequant_transpose_requant"]["us"] / out["A2_transpose"]["us"], 2)
-    # hot-L2 numbers (labelled as such): the working set (58.7 MB in + 29.4 MB out)
-    # fits the 126 MB L2, so back-to-back launches without a flush, 20 per CUDA graph replay
-    # (launch overhead separated), per launch
-    hot = {}
-    for name in ("A1_quantize", "A2_transpose"):
-        fn, nbytes = ops[name]
-        fn()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for _ in range(20):
-                fn()
-        g.replay()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(reps):
-            ev[0].record()
-            g.replay()
-            ev[1].record()
-            ev[1].synchronize()
-            ts.append(ev[0].elapsed_time(ev[1]) / 20)
-        ms = statistics.median(ts)
-        hot[name] = {"us": round(ms * 1e3, 2), "gbs": round(nbytes / ms / 1e6, 1)}
-    out["hot_l2_graph"] = hot
-    return out
-
-
 # =============================================================================================
 def main():
     ap = argparse.ArgumentParser()
@@ -1046,9 +1035,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--partition", choices=["strong", "weak"], default="strong",
+                    help="strong: the layer's 256 experts split over the GPUs (N=1: whole layer); "
+                         "weak: one EP8 expert group (32 experts) per GPU")
+    ap.add_argument("--no-verify", action="store_true", help="skip the whole-step oracle comparison")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the cfg-2 and NEXT-row sub-measurements")
     ap.add_argument("--no-ep", action="store_true", help="skip the N>1 NEXT-3 dispatch/combine measurement")
     ap.add_argument("--sweep", action="store_true", help="config 5: transpose vs naive bandwidth sweep (one JSON line)")
     args = ap.parse_args()
@@ -1059,15 +1052,18 @@ def main():
         log(f"[bench] WORLD_SIZE={world} but --gpus {args.gpus}; launch N>1 under torchrun")
         if args.gpus > 1 and world == 1:
             sys.exit(2)
-    group = D.expert_group(rank)
-    cfg = {"workload": "DeepSeek-V3 MoE layer hot path, one EP8 expert-group shard per GPU (32 of 256 experts), "
+    sh = D.shard(rank, world, args.partition, N_EXPERTS, T_GLOBAL)
+    scope = ("whole layer, 256 experts" if world == 1 else f"{N_EXPERTS // world} of 256 experts per GPU") \
+        if args.partition == "strong" else "one EP8 expert group (32 of 256 experts) per GPU"
+    cfg = {"workload": f"DeepSeek-V3 MoE layer hot path, {scope} ({args.partition} partition), "
                        f"{T_GLOBAL} tokens top-8, hidden 7168, expert FFN 2x2048: A1 x2, A3 plan+move, A5, A4, A2 x2",
-           "tokens": T_GLOBAL, "hidden": HIDDEN, "ffn": FFN, "experts": N_EXPERTS, "top_k": TOP_K,
-           "local_experts": N_EXPERTS // D.NUM_GROUPS, "align": ALIGN, "routing": "DSv3 group-limited top-8, "
-           "skewed expert bias N(0,1) + Gumbel, seed 2511023020", "parallelism": f"ep-group shard x{world} (weak)"}
+           "partition": args.partition, "tokens": T_GLOBAL, "hidden": HIDDEN, "ffn": FFN, "experts": N_EXPERTS,
+           "top_k": TOP_K, "local_experts": sh["num_local_experts"], "align": ALIGN,
+           "routing": "DSv3 group-limited top-8, skewed expert bias N(0,1) + Gumbel, seed 2511023020",
+           "parallelism": f"ep{world} ({'strong: experts split' if args.partition == 'strong' else 'weak: one expert group per GPU'})"}
 
     if args.impl == "reference":
-        run_reference(args, rank, world, group, cfg)
+        run_reference(args, rank, world, cfg)
         return
 
     D.init(D.backend())
@@ -1082,9 +1078,9 @@ def main():
                               "peak_source": peaks["source"], "l2": "flushed before each launch", "rows": rows}))
         D.barrier(device)
         return
-    hw = HostWorkload(group)
-    ds = DeviceStep(hw, device)
-    op_bytes = hw.op_bytes()
+    wl = Workload(rank, world, args.partition, device)
+    ds = DeviceStep(wl)
+    op_bytes = wl.op_bytes()
     step_bytes = sum(op_bytes.values())
     peaks = RL.measured_peaks(ROOT)
     peak = peaks["hbm_gbs"]
@@ -1111,7 +1107,7 @@ def main():
     max_total_ms = D.max_over_ranks(total_ms, device)
     all_bytes = D.sum_over_ranks(step_bytes * args.steps, device)
     value = all_bytes / (max_total_ms / 1e3) / 1e9
-    # EP load imbalance: the heaviest expert group's bytes over the mean (routing skew)
+    # EP load imbalance: the heaviest rank's bytes over the mean (routing skew)
     imbalance = D.max_over_ranks(float(step_bytes), device) / (all_bytes / args.steps / world)
     op_ms = {op: statistics.mean(p[i] for p in per_step) for i, op in enumerate(OPS)}
     ops = {op: {"us": round(op_ms[op] * 1e3, 2), "bytes": op_bytes[op],
@@ -1120,30 +1116,32 @@ def main():
                 "share": round(op_ms[op] / statistics.mean(serial_ms), 3)} for op in OPS}
     iso = ds.isolated_us()
     for op in OPS:
-        ops[op]["isolated_us"] = round(iso[op], 2)
-        ops[op]["isolated_frac"] = round(op_bytes[op] / iso[op] / 1e3 / peak, 3)
+        ops[op]["marginal_us"] = round(iso[op], 2)
+        ops[op]["marginal_frac"] = round(op_bytes[op] / iso[op] / 1e3 / peak, 3)
     dom = max(OPS, key=lambda o: op_ms[o])
     traffic = ncu_traffic(dom)
-    cfg.update({"expert_group": group, "recv_tokens": hw.T_recv, "padded_rows": hw.R, "valid_rows": hw.valid_rows,
+    cfg.update({"expert_begin": wl.e0, "recv_tokens": wl.T_recv, "padded_rows": wl.R, "valid_rows": wl.valid_rows,
+                "token_shard": [wl.t0, wl.t1],
                 "l2": "flushed before every step outside the timed events: 256 MiB write, then a 256 MiB "
-                      "read so the L2 holds clean unrelated lines",
+                      "read so the L2 holds clean unrelated lines (inputs of the step: "
+                      f"{sum(t.numel() * t.element_size() for t in wl.inputs().values()) / 1e9:.2f} GB)",
                 "timing": "CUDA events; the step's dependency DAG on 4 streams (plan->move->A2(X) | A1,A1 | "
                           "A5->A2(A) | A4) captured once into a CUDA graph and replayed behind a spin kernel each "
                           "step; per-op breakdown from the same steps launched serially on one stream "
-                          "(ops.*.us), and each op alone after a clean L2 flush (ops.*.isolated_us)",
+                          "(ops.*.us), and each op's marginal cold-L2 cost (ops.*.marginal_us: K x [flush, op] "
+                          "minus K x [flush])",
                 "serial_ms_per_step": round(statistics.mean(serial_ms), 4)})
 
     e2e = None
     if not args.no_e2e:
-        r = run_e2e(ds, min(args.steps, 5))
+        r = run_e2e(ds, 3)
         e_ms = D.max_over_ranks(r["ms_per_step"], device)
         e2e = {"value": round(D.sum_over_ranks(step_bytes, device) / (e_ms / 1e3) / 1e9, 2), "unit": "GB/s",
                "ms_per_step": round(e_ms, 3), "h2d_bytes_per_step": r["h2d_bytes_per_step"],
                "d2h_bytes_per_step": r["d2h_bytes_per_step"],
-               "note": "H2D of all step inputs from pinned host memory + the step + checksum kernels + D2H of "
-                       "the output checksums, per step, CUDA events"}
+               "note": "per step: H2D of every step input from pinned host memory, the step (graph replay), "
+                       "D2H of every step output into pinned host memory; CUDA events, max over ranks"}
 
-    sums = D.gather_checksums(ds.checksums(), device)
     next3_dist = None
     if world > 1 and not args.no_ep:
         try:
@@ -1152,19 +1150,22 @@ def main():
             next3_dist = {"error": f"{type(e).__name__}: {e}"[:300]}
     checks: list = []
     extra = {}
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_next:
         extra["cfg2"] = cfg2_measure(device, peak)
-        extra["next_ops"] = next_ops_measure(ds, peak, checks=checks)
-    cpu, parity = cpu_baseline_leg(hw, ds, time_it=rank == 0 and world == 1 and not args.no_cpu_baseline,
-                                   verify=not args.no_verify, checks=checks)
+        extra["next_ops"] = next_ops_measure(device, peak, checks=checks)
+    threads = max(1, cpu_cores() // world)
+    rep = cpu_baseline_leg(wl, ds, time_it=not args.no_cpu_baseline, verify=not args.no_verify, checks=checks,
+                           threads=threads)
+    reports = D.gather_objects({k: rep.get(k) for k in ("parity", "checksums_match", "cpu")}, device)
+    merged = D.merge_rank_reports(reports)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_total_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "e4m3",
+            "scaling": "strong" if args.partition == "strong" else "weak", "vs_baseline": None, "dtype": "e4m3",
             "dtypes": {"codes": "e4m3 (u8)", "scales": "ue8m0 (u8)", "bf16_io": "bf16", "math": "fp32 (fp64 refine)"},
-            "data": "synthetic (seeded; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
+            "data": "synthetic (seeded, drawn on the device; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
             "frac_of_hbm_peak": round(value / world / peak, 3),
             "per_gpu_gbs": round(value / world, 1),
             "load_imbalance": round(imbalance, 3),
@@ -1173,10 +1174,14 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ops[dom]["gbs"], "peak": peak, "unit": "GB/s",
                          "frac": ops[dom]["frac"], "traffic": traffic, "peak_source": peaks["source"],
                          "algorithmic_bytes_per_launch": op_bytes[dom]},
-            "ops": ops, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": KERNELS_PER_STEP * args.steps,
-            "clocks": clk, "parity": parity,
-            "checksums": {f"rank{r}": f"{(sum(c) & ((1 << 64) - 1)):016x}" for r, c in enumerate(sums)},
+            "ops": ops, "cpu_baseline": merged.get("cpu_baseline"), "e2e": e2e,
+            "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+            "parity": merged["parity"] if world > 1 else merged["parity"]["rank0"],
+            "parity_all_ranks": merged["parity_all_ranks"], "checksums_match": merged["checksums_match"],
         }
+        if rep:
+            line.update({"a5_code_mismatches": rep.get("a5_code_mismatches"), "checksums": rep.get("checksums"),
+                         "verified": rep.get("verified")})
         line.update(extra)
         if next3_dist is not None:
             line["next3_multi_rank"] = next3_dist
@@ -1281,25 +1286,66 @@ def ncu_traffic(kernel_op: str):
     return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
 
 
-def run_reference(args, rank, world, group, cfg):
-    """The reference arm: the CPU oracle as it stands, on host cores, each step a bounded sample."""
+
+def oracle_sample(O, frac: float, threads: int | None, rank: int = 0, world: int = 1, mode: str = "strong"):
+    """Runs the oracle module O on a bounded, host-generated sample (fraction `frac` of the rank's
+    rows, same recipe and shapes as the step) of one rank's step.  Returns (algorithmic bytes,
+    seconds, description).  Used by the reference arm, which must not need a GPU."""
+    sh = D.shard(rank, world, mode, N_EXPERTS, T_GLOBAL)
+    e0, E_loc = sh["expert_begin"], sh["num_local_experts"]
+    idx, probs = synth.routing(T_GLOBAL, synth.BASE_SEED)
+    rs = synth.expert_range_shard(idx, probs, e0, E_loc)
+    n_tok = max(16, int(len(rs.recv_tokens) * frac))
+    topk, pr = rs.topk_idx[:n_tok], rs.probs[:n_tok]
+    counts = np.array([np.sum(topk == e0 + e) for e in range(E_loc)])
+    padded = (counts + ALIGN - 1) // ALIGN * ALIGN
+    R_s = int(padded.sum())
+    n_sh = max(16, int((sh["token_end"] - sh["token_begin"]) * frac) // 16 * 16)
+    bits = synth.bf16_bits
+    xs = bits(synth.activations_bf16(n_sh, HIDDEN, synth.BASE_SEED + 1))
+    dys = bits(synth.activations_bf16(n_sh, HIDDEN, synth.BASE_SEED + 2))
+    hs = bits(synth.normal_bf16(R_s, 2 * FFN, synth.BASE_SEED + 3, sigma=1.5))
+    ys = bits(synth.normal_bf16(R_s, HIDDEN, synth.BASE_SEED + 4))
+    q_tok, s_tok = O.quantize_rowwise_bf16(bits(synth.activations_bf16(n_tok, HIDDEN, synth.BASE_SEED + 5)))
+    t0 = time.perf_counter()
+    O.quantize_rowwise_bf16(xs, threads=threads)
+    rm, src, off = O.permute_plan(topk, e0, E_loc, max_rows=R_s)
+    qo, so = O.permute_pad(q_tok, s_tok, src, off, max_rows=R_s, threads=threads)
+    qa, sa = O.swiglu_quant(hs, threads=threads)
+    O.unpermute(ys, rm, pr, threads=threads)
+    O.quantize_rowwise_bf16(dys, threads=threads)
+    O.scaling_aware_transpose(qo, so, off, threads=threads)
+    O.scaling_aware_transpose(qa, sa, off, threads=threads)
+    dt = time.perf_counter() - t0
+    nbytes = (2 * RL.quantize_bytes(n_sh, HIDDEN) + RL.permute_plan_bytes(n_tok, TOP_K, R_s)
+              + RL.permute_move_bytes(n_tok, R_s, HIDDEN) + RL.swiglu_quant_bytes(R_s, FFN)
+              + RL.unpermute_bytes(int(counts.sum()), n_tok, TOP_K, HIDDEN, True)
+              + RL.transpose_bytes([int(p) for p in padded], HIDDEN) + RL.transpose_bytes([int(p) for p in padded], FFN))
+    desc = (f"oracle (plain C) on {frac:.4g} of rank {rank}'s step ({mode} partition, {world} rank(s)): A1 "
+            f"{n_sh}x{HIDDEN} x2, A3 plan+move {n_tok} tokens -> {R_s} rows, A5 {R_s}x{2 * FFN}, A4 {n_tok} "
+            f"tokens, A2 {R_s}x{HIDDEN} + {R_s}x{FFN}")
+    return nbytes, dt, desc
+
+
+def run_reference(args, rank, world, cfg):
+    """The reference arm: the CPU oracle as it stands, on host cores, each step a bounded sample of
+    rank 0's workload (rank 0 alone runs it; the other ranks exit without work)."""
     if rank != 0:
         return
     import oracle as O  # the reference arm IS the oracle (tier framing)
 
-    hw = HostWorkload(group)
-    frac = 1.0 / 8
+    frac = 1.0 / 64 if args.partition == "strong" and world == 1 else 1.0 / 8
     for _ in range(args.warmup):
-        oracle_sample(O, hw, frac, None)
+        oracle_sample(O, frac, None, 0, world, args.partition)
     nb, ts, desc = 0.0, 0.0, ""
     for _ in range(args.steps):
-        b, t, desc = oracle_sample(O, hw, frac, None)
+        b, t, desc = oracle_sample(O, frac, None, 0, world, args.partition)
         nb, ts = nb + b, ts + t
     v = nb / ts / 1e9
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ts / args.steps * 1e3, 2), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-            "impl": "reference",
+            "scaling": "strong" if args.partition == "strong" else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg, "impl": "reference",
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

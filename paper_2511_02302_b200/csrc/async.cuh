@@ -92,6 +92,10 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 // wait until all committed bulk groups are complete (writes performed)
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// barrier among `count` threads (a multiple of 32) on hardware barrier `id` (1..15; 0 = __syncthreads)
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 // order generic-proxy shared-memory writes before subsequent async-proxy reads
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

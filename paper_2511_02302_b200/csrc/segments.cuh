@@ -33,41 +33,47 @@ __device__ __forceinline__ int block_exclusive_scan(int v, uint32_t* warp_tmp, i
   return base + incl - v;
 }
 
-// Loads the segment offsets and builds blk_prefix[e] = sum_{e'<e} ceil(m_e'/128) in smem.
-template <int NT, typename Smem>
-__device__ __forceinline__ void load_segments(Smem& sm, const int32_t* seg_offsets, int32_t num_segs,
-                                              int64_t rows) {
+// Loads the segment offsets into seg_off[0..num_segs] and builds blk_prefix[e] = sum_{e'<e}
+// ceil(m_e'/128) in shared memory; *total_rb = blk_prefix[num_segs].  NT * 4 > num_segs.
+template <int NT>
+__device__ __forceinline__ void load_segments(int32_t* seg_off, int32_t* blk_prefix, uint32_t* red, int32_t* total_rb,
+                                              const int32_t* seg_offsets, int32_t num_segs, int64_t rows) {
   const int tid = threadIdx.x;
   if (seg_offsets == nullptr) {  // one segment: no scan, one barrier
     if (tid == 0) {
       const int32_t nb = static_cast<int32_t>((rows + kTile - 1) / kTile);
-      sm.seg_off[0] = 0;
-      sm.seg_off[1] = static_cast<int32_t>(rows);
-      sm.blk_prefix[0] = 0;
-      sm.blk_prefix[1] = nb;
-      sm.total_rb = nb;
+      seg_off[0] = 0;
+      seg_off[1] = static_cast<int32_t>(rows);
+      blk_prefix[0] = 0;
+      blk_prefix[1] = nb;
+      *total_rb = nb;
     }
     __syncthreads();
     return;
   }
-  for (int i = tid; i <= num_segs; i += NT) sm.seg_off[i] = seg_offsets[i];
+  for (int i = tid; i <= num_segs; i += NT) seg_off[i] = seg_offsets[i];
   __syncthreads();
   // 4 consecutive segments per thread (num_segs <= 1024)
   int nb[4], tsum = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int e = tid * 4 + i;
-    nb[i] = e < num_segs ? (sm.seg_off[e + 1] - sm.seg_off[e] + kTile - 1) / kTile : 0;
+    nb[i] = e < num_segs ? (seg_off[e + 1] - seg_off[e] + kTile - 1) / kTile : 0;
     tsum += nb[i];
   }
-  int run = block_exclusive_scan<NT>(tsum, sm.red, &sm.total_rb);
+  int run = block_exclusive_scan<NT>(tsum, red, total_rb);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int e = tid * 4 + i;
-    if (e <= num_segs) sm.blk_prefix[e] = run;
+    if (e <= num_segs) blk_prefix[e] = run;
     run += nb[i];
   }
   __syncthreads();
+}
+template <int NT, typename Smem>
+__device__ __forceinline__ void load_segments(Smem& sm, const int32_t* seg_offsets, int32_t num_segs,
+                                              int64_t rows) {
+  load_segments<NT>(sm.seg_off, sm.blk_prefix, sm.red, &sm.total_rb, seg_offsets, num_segs, rows);
 }
 
 // warp-cooperative: the segment owning row block rb = #{e in [1, num_segs) : blk_prefix[e] <= rb}

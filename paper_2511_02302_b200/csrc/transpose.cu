@@ -7,11 +7,14 @@
 //     T_max = max_i T[i][jb];  sT_e[ib][j] = T_max;  qT_e[j][i-o] = shift(q[i][j], T_max - T[i][jb])
 //
 // Kernel design (sm_100a, HBM-bound, 2.016 B/element):
-//   * persistent CTAs (3 per SM), static round-robin over the 128x128 tiles of all segments; the
-//     tile -> (segment, row block) map is a prefix sum over ceil(m_e/128) computed in shared memory
-//     from the DEVICE segment offsets (no host sync: CUDA-graph capturable).
-//   * the 16 KB input tile and its 128-byte run of row scales arrive by TMA (cp.async.bulk.tensor.2d
-//     + a 1D bulk copy, one mbarrier with complete_tx) into a 3-stage ring.
+//   * persistent CTAs (3 per SM; 2 when there are >= 64 tiles per SM) of 8 consumer warps and one
+//     producer warp, static round-robin over the 128x128 tiles of all segments in segment-major
+//     order (tile_coord below); the segment tables are built in shared memory from the DEVICE
+//     segment offsets (no host sync: CUDA-graph capturable).
+//   * producer (one lane): per tile its coordinates, the 16 KB code tile by TMA (one 128x128 box,
+//     or 16-row boxes for a segment's partial last block, so no bytes of the next segment are
+//     read) and the block's run of row scales by a 1D bulk copy, all on one mbarrier of a 3-stage
+//     ring; it refills a stage as soon as every consumer warp has copied it to registers.
 //   * T_max per block: each warp max-reduces the staged scale run itself (redux.sync), no barrier.
 //   * thread (g, c) owns rows 4g..4g+3 x bytes 16c..16c+15: 4 conflict-free LDS.128 (8 threads of
 //     a quarter-warp read one full 128-byte row); the per-row exponent shift (common.cuh shift4:
@@ -30,46 +33,103 @@
 
 namespace fp8flow {
 
-// kernel variants <STAGES, OUTBUF>: TMA stages of the input ring, and 1 or 2 staging buffers for
-// the transposed tile (2 removes one CTA barrier per tile at the cost of 16 KB of shared memory)
-constexpr int kTThreads = 256;
+// <STAGES, OUTBUF>: TMA stages of the input ring and staging buffers for the transposed tile
+// (r02 sweep, profiles/r02_a2_order_window.txt: 3 stages x 1 buffer)
+constexpr int kTConsumers = 256;              // 8 consumer warps
+constexpr int kTThreads = kTConsumers + 32;   // + 1 producer warp
 constexpr int kMaxSegs = 1024;
 constexpr int kTileBytes = kTile * kTile;
+constexpr int kRowGroup = 8;                  // row blocks of a segment walked together (tile order)
+
+struct TileCoord {
+  int32_t o, m;     // segment row offset and length
+  int32_t ib, jb;   // row block inside the segment, column block
+  int32_t rb;       // global row-block index of the output scales
+  int32_t rows_valid;
+  int32_t pad[2];
+};
 
 template <int STAGES, int OUTBUF>
 struct TransposeSmem {
   uint8_t in[STAGES][kTileBytes];
   uint32_t sc[STAGES][kTile / 4];  // the 128 row-scale bytes of each staged tile
   uint32_t out[OUTBUF][kTile * kTile / 4];
+  TileCoord tc[STAGES];            // coordinates of the staged tile (written by the producer)
   uint64_t full_bar[STAGES];
+  uint64_t empty_bar[STAGES];
   uint32_t mult[33];               // f16x2 multiplier 2^-k for k = 0..32
   uint32_t red[kTThreads / 32];
-  int32_t seg_off[kMaxSegs + 1];
-  int32_t blk_prefix[kMaxSegs + 1];
   int32_t total_rb;
+  // followed in dynamic shared memory by seg_off[num_segs + 1] and blk_prefix[num_segs + 1]
 };
+template <typename Smem>
+__host__ __device__ constexpr size_t a2_smem_bytes(int nsegs) {
+  return (sizeof(Smem) + 15) / 16 * 16 + 8 * static_cast<size_t>(nsegs + 1);
+}
+struct SegTables {
+  const int32_t* seg_off;
+  const int32_t* blk_prefix;
+};
+
+// Tile order (segment-major): for each segment e, its row blocks in groups of kRowGroup, and inside
+// a group column block jb, then row block ib fastest.  Consecutive tiles -- the ones the persistent
+// CTAs hold at the same time -- therefore read whole input rows of up to 1024 rows (contiguous) and
+// write, for each output row j, up to 1024 contiguous bytes: at the whole-layer size (256 experts,
+// output rows of ~520 bytes spread over 1 GB) a row-block-major order left the L2 evicting 128-byte
+// pieces of ~60 MB of scattered output (r02: 0.54 of peak).  Tile t -> (e, ib, jb):
+//   e = segment of virtual row block t / n_jb (segment tiles = n_jb * blocks, contiguous in t),
+//   t' = t - n_jb * blk_prefix[e], group g = t' / (n_jb * RG), gsz = min(RG, nblk - g * RG),
+//   u = t' - g * n_jb * RG, jb = u / gsz, ib = g * RG + u % gsz.
+__device__ __forceinline__ TileCoord tile_coord(const SegTables& sm, int nsegs, int n_jb, int t) {
+  const int rbv = t / n_jb;
+  const int e = find_segment(sm.blk_prefix, nsegs, rbv);
+  const int b0 = sm.blk_prefix[e];
+  const int nblk = sm.blk_prefix[e + 1] - b0;
+  const int tp = t - b0 * n_jb;
+  const int g = tp / (n_jb * kRowGroup);
+  const int gsz = min(kRowGroup, nblk - g * kRowGroup);
+  const int u = tp - g * n_jb * kRowGroup;
+  const int jb = u / gsz;
+  const int ib = g * kRowGroup + (u - jb * gsz);
+  TileCoord c;
+  c.o = sm.seg_off[e];
+  c.m = sm.seg_off[e + 1] - c.o;
+  c.ib = ib;
+  c.jb = jb;
+  c.rb = b0 + ib;
+  c.rows_valid = min(kTile, c.m - ib * kTile);
+  return c;
+}
 
 template <int STAGES, int OUTBUF, int MINB>
 __global__ void __launch_bounds__(kTThreads, MINB)
-    scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q, const uint8_t* __restrict__ s,
+    scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                                   const __grid_constant__ CUtensorMap tmap_q16, const uint8_t* __restrict__ s,
                                    int64_t ld_s, int64_t rows, int64_t cols, const int32_t* __restrict__ seg_offsets,
                                    int32_t num_segs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using Smem = TransposeSmem<STAGES, OUTBUF>;
-  constexpr int kTStages = STAGES;
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  const int warp = tid >> 5;
   const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
+  int32_t* seg_off = reinterpret_cast<int32_t*>(smem_raw + (sizeof(Smem) + 15) / 16 * 16);
+  int32_t* blk_prefix = seg_off + nsegs + 1;
+  const SegTables segt{seg_off, blk_prefix};
 
   if (tid == 0) {
-    for (int i = 0; i < kTStages; ++i) mbar_init(&sm.full_bar[i], 1);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&sm.full_bar[i], 1);
+      mbar_init(&sm.empty_bar[i], kTConsumers / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q16)) : "memory");
   }
   if (tid <= 32) sm.mult[tid] = shift_multiplier(static_cast<uint32_t>(tid));
-  load_segments<kTThreads>(sm, seg_offsets, nsegs, rows);  // (ends with a CTA barrier)
+  load_segments<kTThreads>(seg_off, blk_prefix, sm.red, &sm.total_rb, seg_offsets, nsegs, rows);  // (+ barrier)
 
   const int n_jb = static_cast<int>(cols / kTile);
   const int total_tiles = sm.total_rb * n_jb;  // < 2^31 (rows < 2^31, checked by the ABI)
@@ -77,76 +137,75 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   const int stride = gridDim.x;
   const int n_local = first < total_tiles ? (total_tiles - first + stride - 1) / stride : 0;
 
-  // producer: tile i of this CTA is t = first + i * stride; the 16 KB code tile (TMA 2D) and its
-  // 128-byte run of row scales (1D bulk copy, rows_valid bytes) land on the same mbarrier
-  auto issue = [&](int i) {
-    const int t = first + i * stride;
-    const int rb = t / n_jb;
-    const int jb = t - rb * n_jb;
-    const int e = find_segment(sm.blk_prefix, nsegs, rb);
-    const int ib = rb - sm.blk_prefix[e];
-    const int r0 = sm.seg_off[e] + ib * kTile;
-    const int rows_valid = min(kTile, sm.seg_off[e + 1] - r0);
-    const int st = i % kTStages;
-    mbar_expect_tx(&sm.full_bar[st], kTileBytes + rows_valid);
-    tma_load_2d(sm.in[st], &tmap_q, &sm.full_bar[st], jb * kTile, r0);
-    bulk_load_1d(sm.sc[st], s + static_cast<int64_t>(jb) * ld_s + r0, rows_valid, &sm.full_bar[st]);
-  };
-
-  if (tid == 0) {
-    for (int i = 0; i < n_local && i < kTStages; ++i) issue(i);
+  if (warp == kTConsumers / 32) {
+    // ---- producer warp (lane 0): tile i of this CTA is t = first + i * stride.  The code tile
+    // arrives by TMA -- one 128x128 box, or rows_valid/16 boxes of 16 rows for the partial last
+    // block of a segment (no bytes of the next segment are read) -- and its run of row scales by
+    // a 1D bulk copy, all on the stage's full barrier; the coordinates go with it.
+    if (lane == 0) {
+      int st = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_local; ++i) {
+        if (i >= STAGES) mbar_wait_sleep(&sm.empty_bar[st], phase ^ 1u, 32);
+        const TileCoord c = tile_coord(segt, nsegs, n_jb, first + i * stride);
+        sm.tc[st] = c;
+        const int r0 = c.o + c.ib * kTile;
+        mbar_expect_tx(&sm.full_bar[st], static_cast<uint32_t>(c.rows_valid * (kTile + 1)));
+        if (c.rows_valid == kTile) {
+          tma_load_2d(sm.in[st], &tmap_q, &sm.full_bar[st], c.jb * kTile, r0);
+        } else {
+          for (int r = 0; r < c.rows_valid; r += 16)
+            tma_load_2d(sm.in[st] + r * kTile, &tmap_q16, &sm.full_bar[st], c.jb * kTile, r0 + r);
+        }
+        bulk_load_1d(sm.sc[st], s + static_cast<int64_t>(c.jb) * ld_s + r0, c.rows_valid, &sm.full_bar[st]);
+        if (++st == STAGES) {
+          st = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
   }
 
+  // ---- consumer warps (256 threads) ----------------------------------------------------------
   const int g = tid >> 3;  // row quad 0..31
   const int c = tid & 7;   // 16-byte column chunk 0..7
-
-  // (rb, jb) of tile i advance incrementally (no division in the loop)
-  const int stride_rb = stride / n_jb, stride_jb = stride % n_jb;
-  int rb = first / n_jb, jb = first % n_jb;
   int st = 0;
   uint32_t phase = 0;
   for (int i = 0; i < n_local; ++i) {
-    if (i > 0) {
-      jb += stride_jb;
-      rb += stride_rb;
-      if (jb >= n_jb) {
-        jb -= n_jb;
-        ++rb;
-      }
-    }
-    const int e = find_segment_warp(sm.blk_prefix, nsegs, rb);
-    const int o = sm.seg_off[e];
-    const int m = sm.seg_off[e + 1] - o;
-    const int ib = rb - sm.blk_prefix[e];
-    const int rows_valid = min(kTile, m - ib * kTile);  // multiple of 16
-
     mbar_wait(&sm.full_bar[st], phase);
+    const TileCoord tc = sm.tc[st];
     // ---- block scale max (Algorithm 1: S_max = max_i S_i^row), per warp, no CTA barrier:
     // lane l reads the staged scale bytes of rows 4l..4l+3; rows beyond the segment count as 0
-    const uint32_t sw_l = (4 * lane < rows_valid) ? sm.sc[st][lane] : 0u;
+    const uint32_t sw_l = (4 * lane < tc.rows_valid) ? sm.sc[st][lane] : 0u;
     const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
     const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
     const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);  // this thread's rows 4g..4g+3
 
-    // ---- shift rows, transpose 4x4 byte blocks ----------------------------------------------
+    // ---- shift rows (rows past rows_valid hold stale bytes: shifted, never stored) -----------
+    uint4 v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty_bar[st]);  // this warp is done with the stage
     uint32_t R[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const uint4 v = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
       const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
       const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v.x, m2);
-      R[r][1] = shift4(v.y, m2);
-      R[r][2] = shift4(v.z, m2);
-      R[r][3] = shift4(v.w, m2);
+      R[r][0] = shift4(v[r].x, m2);
+      R[r][1] = shift4(v[r].y, m2);
+      R[r][2] = shift4(v[r].z, m2);
+      R[r][3] = shift4(v[r].w, m2);
     }
-    if (++st == kTStages) {
+    if (++st == STAGES) {
       st = 0;
       phase ^= 1u;
     }
+    // ---- 4x4 byte transposes into the swizzled staging buffer ----------------------------------
     const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
     uint32_t* out = sm.out[OUTBUF == 2 ? (i & 1) : 0];
-    if (OUTBUF == 1 && i > 0) __syncthreads();  // previous tile's read-out of the buffer is complete
+    if (OUTBUF == 1 && i > 0) named_barrier_sync(1, kTConsumers);  // previous read-out complete
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
@@ -159,24 +218,22 @@ __global__ void __launch_bounds__(kTThreads, MINB)
       out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
       out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
     }
-    __syncthreads();  // tile consumed (stage free), out buffer complete
-
-    if (tid == 0 && i + kTStages < n_local) issue(i + kTStages);
+    named_barrier_sync(1, kTConsumers);  // staging buffer complete
 
     // ---- coalesced 128-bit read-out: 8 threads per output row --------------------------------
-    uint8_t* qTe = qT + cols * static_cast<int64_t>(o);
+    uint8_t* qTe = qT + cols * static_cast<int64_t>(tc.o);
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int j = (tid >> 3) + 32 * it;
-      if (16 * c < rows_valid) {
+      if (16 * c < tc.rows_valid) {
         const int phys = c ^ ((j >> 4) & 7);
-        const uint4 v = *reinterpret_cast<const uint4*>(&out[j * 32 + 4 * phys]);
-        st_v4(qTe + (static_cast<int64_t>(jb) * kTile + j) * m + ib * kTile + 16 * c, v);
+        const uint4 o4 = *reinterpret_cast<const uint4*>(&out[j * 32 + 4 * phys]);
+        st_v4(qTe + (static_cast<int64_t>(tc.jb) * kTile + j) * tc.m + tc.ib * kTile + 16 * c, o4);
       }
     }
     if (tid < 8) {
       const uint32_t b4 = tmax * 0x01010101u;
-      st_v4(sT + static_cast<int64_t>(rb) * cols + jb * kTile + 16 * tid, make_uint4(b4, b4, b4, b4));
+      st_v4(sT + static_cast<int64_t>(tc.rb) * cols + tc.jb * kTile + 16 * tid, make_uint4(b4, b4, b4, b4));
     }
   }
 }
@@ -186,31 +243,39 @@ __global__ void __launch_bounds__(kTThreads, MINB)
 // ---------------------------------------------------------------------------------------------
 constexpr int kTStagesA2 = 3, kTOutBufA2 = 1, kTMinBlocksA2 = 3;  // 3 CTAs/SM (r01 sweep of 2-4 stages)
 template <int S, int O, int B>
-static cudaError_t launch_a2v(const CUtensorMap& map, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
+static cudaError_t launch_a2v(const CUtensorMap& map, const CUtensorMap& map16, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
                               const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
-                              cudaStream_t stream, int num_sms, int64_t ub_tiles, bool persist) {
+                              cudaStream_t stream, int num_sms, int64_t ub_tiles) {
   static KernelSetup setup;
   auto kernel = scaling_aware_transpose_kernel<S, O, B>;
-  const int occ = prepare_kernel(setup, kernel, kTThreads, sizeof(TransposeSmem<S, O>), sizeof(TransposeSmem<S, O>));
-  if (occ == 0) return cudaErrorInvalidValue;
-  const int64_t grid = persist ? one_wave_grid(occ, num_sms, ub_tiles) : ub_tiles;
-  kernel<<<static_cast<unsigned>(grid), kTThreads, sizeof(TransposeSmem<S, O>), stream>>>(map, s, ld_s, rows, cols,
-                                                                                       seg_offsets, num_segs, qT, sT);
+  const size_t smem = a2_smem_bytes<TransposeSmem<S, O>>(seg_offsets ? num_segs : 1);
+  if (prepare_kernel(setup, kernel, kTThreads, a2_smem_bytes<TransposeSmem<S, O>>(kMaxSegs), smem) == 0)
+    return cudaErrorInvalidValue;
+  int occ = 0;  // occupancy at this launch's shared memory (the segment tables vary with num_segs)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  // Tiles held at once = SMs x CTAs x stages.  Launches with many tiles per SM stream better with a
+  // smaller window (fewer DRAM pages open at once): whole-layer X_perm 462 -> 364 us with 2 CTAs
+  // per SM instead of 3; mid-size launches (~12 tiles per SM) need the deeper window to ramp up
+  // (profiles/r02_a2_order_window.txt).
+  if (ub_tiles >= 64LL * num_sms && occ > 2) occ = 2;
+  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
+  kernel<<<static_cast<unsigned>(grid), kTThreads, smem, stream>>>(
+      map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows,
                                            int64_t cols, const int32_t* seg_offsets, int32_t num_segs,
                                            uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
-  CUtensorMap map;
+  CUtensorMap map, map16;  // 128x128 boxes; 128x16 boxes for the partial last block of a segment
   if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
-                 static_cast<uint64_t>(cols), kTile, kTile))
+                 static_cast<uint64_t>(cols), kTile, kTile) ||
+      !encode_2d(&map16, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
+                 static_cast<uint64_t>(cols), kTile, 16))
     return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  // persistent: 3 CTAs per SM x 3 TMA stages (non-persistent one-tile CTAs and 1-2 stage variants
-  // measured 5-40 % slower, profiles/r02_a2_shift.txt)
-  return launch_a2v<kTStagesA2, kTOutBufA2, kTMinBlocksA2>(map, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT,
-                                                         stream, num_sms, ub_tiles, true);
+  return launch_a2v<kTStagesA2, kTOutBufA2, kTMinBlocksA2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT,
+                                                         stream, num_sms, ub_tiles);
 }
 
 // =============================================================================================

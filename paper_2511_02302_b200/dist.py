@@ -1,10 +1,17 @@
-"""Expert-group sharding and the post-timing collectives.
+"""Expert-parallel sharding and the post-timing collectives.
 
-The hot path shards with no exchange step: rank r of N owns DeepSeek-V3 expert group r mod 8
-(32 of the 256 experts, the EP8 partition) and runs the whole hot path on what that group
-receives.  torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests) is used
-only OUTSIDE the timed region: barriers around it, the max over ranks of the measured time, the
-sum of bytes, and the gather of per-rank output checksums.
+The hot path shards with no exchange step.  Two partitions of the DeepSeek-V3
+layer (256 experts, 16384 tokens):
+
+* strong (the default): rank g of n owns experts [g*256/n, (g+1)*256/n) and the token shard
+  [g*T/n, (g+1)*T/n) of the two entry casts; n = 1 is the whole layer on one GPU.  Total work is
+  fixed; the per-rank load follows the routing skew (reported as load_imbalance).
+* weak: rank r owns DeepSeek-V3 expert group r mod 8 (32 experts, the EP8 partition) and 1/8 of
+  the tokens, so per-GPU work is one expert group at every n.
+
+torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests) is used only OUTSIDE
+the timed region: barriers around it, the max over ranks of the measured time, the sum of bytes,
+the gather of per-rank output checksums and verification reports.
 """
 from __future__ import annotations
 
@@ -36,6 +43,57 @@ def init(backend: str) -> bool:
 def expert_group(rank: int, num_groups: int = NUM_GROUPS) -> int:
     """Expert group owned by a rank (weak scaling: every rank owns one full group)."""
     return rank % num_groups
+
+
+def shard(rank: int, world: int, mode: str, num_experts: int = 256, num_tokens: int = 16384,
+          num_groups: int = NUM_GROUPS) -> dict:
+    """The rank's part of the layer: experts [expert_begin, expert_begin + num_local_experts) and
+    entry-cast tokens [token_begin, token_end).  mode 'strong' splits the whole layer over the
+    world (world must divide the expert count); 'weak' gives every rank one expert group."""
+    if mode == "strong":
+        if world < 1 or num_experts % world:
+            raise ValueError(f"{num_experts} experts do not split over {world} ranks")
+        per = num_experts // world
+        t0, t1 = rank * num_tokens // world, (rank + 1) * num_tokens // world
+        return {"mode": mode, "expert_begin": rank * per, "num_local_experts": per, "token_begin": t0,
+                "token_end": t1}
+    if mode == "weak":
+        g = expert_group(rank, num_groups)
+        per = num_experts // num_groups
+        t0, t1 = g * num_tokens // num_groups, (g + 1) * num_tokens // num_groups
+        return {"mode": mode, "expert_begin": g * per, "num_local_experts": per, "token_begin": t0,
+                "token_end": t1, "group": g}
+    raise ValueError(f"unknown partition {mode!r}")
+
+
+def gather_objects(obj, device=torch.device("cpu")) -> list:
+    """All-gather a picklable object from every rank (verification reports; outside timing)."""
+    if not dist.is_initialized():
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def merge_rank_reports(reports: list[dict]) -> dict:
+    """Rank 0's view of the per-rank verification reports: every rank's parity flags, whether
+    every rank's GPU checksums equal the oracle's C11 checksums of its shard, and the CPU-oracle
+    baseline as one job (bytes of all ranks / the slowest rank's seconds, cores of all ranks)."""
+    out = {"parity": {f"rank{i}": r.get("parity") for i, r in enumerate(reports)}}
+    flags = [v for r in reports for v in (r.get("parity") or {}).values()]
+    out["parity_all_ranks"] = bool(flags) and all(flags)
+    cs = [r.get("checksums_match") for r in reports]
+    out["checksums_match"] = all(c is True for c in cs) if cs else None
+    cpu = [r.get("cpu") for r in reports if r.get("cpu")]
+    if cpu and len(cpu) == len(reports):
+        secs = max(c["seconds"] for c in cpu)
+        nbytes = sum(c["bytes"] for c in cpu)
+        out["cpu_baseline"] = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s",
+                               "cores": sum(c["cores"] for c in cpu), "kind": "oracle",
+                               "sample": cpu[0]["sample"] + (f" (x{len(cpu)} ranks, each on its own shard, "
+                                                            "concurrently)" if len(cpu) > 1 else ""),
+                               "seconds": round(secs, 2)}
+    return out
 
 
 def backend() -> str:

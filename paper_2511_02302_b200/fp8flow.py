@@ -99,6 +99,15 @@ def _ptr(t: torch.Tensor | None):
     return t.data_ptr()
 
 
+def _ptr_rows(t: torch.Tensor):
+    """A 2-D matrix whose rows are contiguous (its row pitch is passed separately)."""
+    if not t.is_cuda:
+        raise Fp8FlowError("libfp8flow takes device tensors only (no CPU fallback)")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise Fp8FlowError("matrix rows must be contiguous")
+    return t.data_ptr()
+
+
 def _stream(stream) -> int | None:
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -125,10 +134,11 @@ def fp8flow_build_target() -> str:
 
 # ----------------------------------------------------------------------------------- A1
 def fp8flow_quantize_rowwise(x: torch.Tensor, q: torch.Tensor, s: torch.Tensor, stream=None) -> None:
-    """x bf16 [rows, cols] -> q uint8 [rows, cols], s uint8 [cols/128, ld_s]."""
-    assert x.dtype == torch.bfloat16 and x.dim() == 2
+    """x bf16 [rows, cols] -> q uint8 [rows, cols], s uint8 [cols/128, ld_s] (ld_s = s.stride(0): a
+    column slice of a wider scale matrix is accepted)."""
+    assert x.dtype == torch.bfloat16 and x.dim() == 2 and s.stride(1) == 1
     rows, cols = x.shape
-    _check(lib().fp8flow_quantize_rowwise(_ptr(x), rows, cols, _ptr(_u8(q)), _ptr(_u8(s)), s.shape[1],
+    _check(lib().fp8flow_quantize_rowwise(_ptr(x), rows, cols, _ptr(_u8(q)), _ptr_rows(_u8(s)), s.stride(0),
                                           _stream(stream)), "fp8flow_quantize_rowwise")
 
 

@@ -119,7 +119,11 @@ class ExpertShard:
 def expert_shard(topk_idx: torch.Tensor, probs: torch.Tensor, group: int, num_groups: int,
                  num_experts: int = NUM_EXPERTS) -> ExpertShard:
     per = num_experts // num_groups
-    e0 = group * per
+    return expert_range_shard(topk_idx, probs, group * per, per, group)
+
+
+def expert_range_shard(topk_idx: torch.Tensor, probs: torch.Tensor, e0: int, per: int, group: int = -1) -> ExpertShard:
+    """The tokens routed to >= 1 expert of [e0, e0 + per) and their routing rows (a selection)."""
     idx = topk_idx.numpy()
     local = (idx >= e0) & (idx < e0 + per)
     recv = np.nonzero(local.any(axis=1))[0]

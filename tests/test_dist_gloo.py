@@ -191,3 +191,76 @@ def test_ipc_export_failure_raises_on_every_rank():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(msg is not None and "rank(s) [1]" in msg for _, msg in out), out
+
+
+# ------------------------------------------------------------------ strong partition + N>1 reports
+def _strong_worker(rank, world, port, q):
+    """bench.py's N>1 host logic on gloo: the strong split of the layer (experts and entry-cast
+    tokens), the per-rank verification reports gathered to every rank and merged (parity of every
+    rank, checksum agreement, the CPU-oracle baseline as one job)."""
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import numpy as np
+
+    import synth
+    from paper_2511_02302_b200 import dist as D
+
+    assert D.init("gloo")
+    sh = D.shard(rank, world, "strong")
+    idx, probs = synth.routing(16384, synth.BASE_SEED)
+    rs = synth.expert_range_shard(idx, probs, sh["expert_begin"], sh["num_local_experts"])
+    counts = np.bincount(idx.numpy().ravel(), minlength=256)
+    per = counts[sh["expert_begin"]: sh["expert_begin"] + sh["num_local_experts"]]
+    rows = int(np.sum((per + 15) // 16 * 16))
+    rep = {"parity": {"A1_quantize_x": True, "A2_transpose_xperm": rank == 0 or world == 1},
+           "checksums_match": True,
+           "cpu": {"seconds": 2.0 + rank, "bytes": 1e9 * (rank + 1), "cores": 4, "sample": "shard"}}
+    reports = D.gather_objects(rep)
+    merged = D.merge_rank_reports(reports)
+    D.barrier()
+    q.put((rank, sh, len(rs.recv_tokens), rows, merged))
+    D.dist.destroy_process_group()
+
+
+def test_two_rank_gloo_strong_partition_and_reports():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strong_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, s0, n0, r0, m0), (_, s1, n1, r1, m1) = out
+    # GPU g of n owns experts [g*256/n, (g+1)*256/n) and tokens [g*T/n, (g+1)*T/n) (SURVEY 8(e))
+    assert (s0["expert_begin"], s0["num_local_experts"], s0["token_begin"], s0["token_end"]) == (0, 128, 0, 8192)
+    assert (s1["expert_begin"], s1["num_local_experts"], s1["token_begin"], s1["token_end"]) == (128, 128, 8192, 16384)
+    # the two halves cover the whole layer: ~133k padded rows, every token received by >= 1 rank
+    import synth
+    import numpy as np
+    idx, _ = synth.routing(16384, synth.BASE_SEED)
+    counts = np.bincount(idx.numpy().ravel(), minlength=256)
+    assert r0 + r1 == int(np.sum((counts + 15) // 16 * 16)) and r0 != r1       # skewed: imbalance
+    assert n0 <= 16384 and n1 <= 16384 and n0 + n1 >= 16384
+    # merged reports: every rank's parity, a failing rank flips the overall flag, baseline as one job
+    assert m0 == m1
+    assert m0["parity"] == {"rank0": {"A1_quantize_x": True, "A2_transpose_xperm": True},
+                            "rank1": {"A1_quantize_x": True, "A2_transpose_xperm": False}}
+    assert m0["parity_all_ranks"] is False and m0["checksums_match"] is True
+    assert m0["cpu_baseline"]["value"] == round(3e9 / 3.0 / 1e9, 4) and m0["cpu_baseline"]["cores"] == 8
+
+
+def test_partition_modes_single_process():
+    from paper_2511_02302_b200 import dist as D
+
+    whole = D.shard(0, 1, "strong")
+    assert (whole["expert_begin"], whole["num_local_experts"], whole["token_begin"], whole["token_end"]) == \
+        (0, 256, 0, 16384)
+    assert [D.shard(r, 8, "strong")["expert_begin"] for r in range(8)] == [32 * r for r in range(8)]
+    assert D.shard(3, 4, "weak")["expert_begin"] == 96 and D.shard(9, 16, "weak")["group"] == 1
+    with pytest.raises(ValueError):
+        D.shard(0, 3, "strong")
+    with pytest.raises(ValueError):
+        D.shard(0, 1, "sideways")

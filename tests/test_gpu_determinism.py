@@ -22,8 +22,8 @@ def step():
     import bench
 
     dev = torch.device("cuda", 0)
-    hw = bench.HostWorkload(1)            # expert group 1 (the bench times group 0)
-    return bench.DeviceStep(hw, dev)
+    wl = bench.Workload(1, 8, "weak", dev)     # expert group 1 of the layer
+    return bench.DeviceStep(wl)
 
 
 def test_step_outputs_repeat_bit_for_bit(step):

@@ -30,13 +30,25 @@ rng = np.random.default_rng(1)
 def segs(rows, n):
     w = rng.gamma(1.0, 1.0, n); m = np.floor(w / w.sum() * rows / 16).astype(int) * 16
     m[-1] += rows - m.sum(); return np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
-for rows, cols, nseg in [(2048, 7168, 1), (4096, 7168, 1), (16384, 7168, 1), (15872, 2048, 32), (15872, 7168, 32), (65536, 7168, 1)]:
-    x = synth.activations_bf16_device(rows, cols, 7, dev)
+idx, _ = synth.routing(16384, synth.BASE_SEED)
+cnt = np.bincount(idx.numpy().ravel(), minlength=256)
+layer = np.concatenate([[0], np.cumsum((cnt + 15) // 16 * 16)]).astype(np.int32)   # whole-layer experts
+g0 = np.concatenate([[0], np.cumsum(((cnt + 15) // 16 * 16)[:32])]).astype(np.int32)
+shapes = [(2048, 7168, 1), (4096, 7168, 1), (16384, 7168, 1), (int(g0[-1]), 2048, g0), (int(g0[-1]), 7168, g0),
+          (65536, 7168, 1), (int(layer[-1]), 2048, layer), (int(layer[-1]), 7168, layer)]
+if len(sys.argv) > 1 and sys.argv[1] == "big":
+    shapes = shapes[-3:]
+    sys.argv.pop(1)
+for rows, cols, nseg in shapes:
     q = torch.empty(rows, cols, dtype=torch.uint8, device=dev)
     s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=dev)
-    F.fp8flow_quantize_rowwise(x, q, s)
-    del x
-    seg = segs(rows, nseg) if nseg > 1 else None
+    for r0 in range(0, rows, 16384):
+        r1 = min(rows, r0 + 16384)
+        x = synth.activations_bf16_device(r1 - r0, cols, 7 + r0, dev)
+        F.fp8flow_quantize_rowwise(x, q[r0:r1], s[:, r0:r1])
+        del x
+    seg = nseg if isinstance(nseg, np.ndarray) else (segs(rows, nseg) if nseg > 1 else None)
+    nseg = 1 if seg is None else len(seg) - 1
     seg_t = torch.from_numpy(seg).to(dev) if seg is not None else None
     qT = torch.empty(rows * cols, dtype=torch.uint8, device=dev)
     sT = torch.empty(rows // 128 + nseg, cols, dtype=torch.uint8, device=dev)
@@ -44,7 +56,7 @@ for rows, cols, nseg in [(2048, 7168, 1), (4096, 7168, 1), (16384, 7168, 1), (15
     line = []
     ref = None
     for v in sys.argv[1:]:
-        os.environ["A2X"] = v
+        os.environ["A2X"], os.environ["A2C"] = (v.split(":") + ["0"])[:2]
         fn = lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT, seg_offsets=seg_t)
         t = marginal(fn, K=20 if rows < 60000 else 6)
         fn(); torch.cuda.synchronize()

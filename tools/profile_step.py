@@ -1,8 +1,10 @@
 """Profiling driver (not product): warms up bench.py's step, then runs ONE serial pass of the
-step's 9 launches plus the NEXT-row kernels (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM,
-NEXT-3 dispatch and combine of rank 0 of 8 virtual EP ranks) between cudaProfilerStart/Stop, so that
-    ncu --set full --profile-from-start off ... python tools/profile_step.py
+step's 8 launches (whole DeepSeek-V3 layer on one GPU, bench.py's default strong partition) plus
+the NEXT-row kernels on expert group 0 (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM,
+NEXT-3 dispatch and combine of rank 0 of 8 virtual EP ranks) between cudaProfilerStart/Stop, so
+    ncu --set full --profile-from-start off ... python tools/profile_step.py [--partition weak]
 captures exactly one launch of each kernel, in this order."""
+import argparse
 import os
 import sys
 
@@ -19,42 +21,50 @@ ORDER = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--partition", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--no-next", action="store_true")
+    args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    hw = bench.HostWorkload(0)
-    ds = bench.DeviceStep(hw, dev)
-    F = ds.F
-    dA = synth.normal_bf16(hw.R, bench.FFN, synth.BASE_SEED + 5, sigma=0.5).to(dev)
-    qb = torch.empty(hw.R, 2 * bench.FFN, dtype=torch.uint8, device=dev)
-    sbw = torch.empty(2 * bench.FFN // 128, hw.R, dtype=torch.uint8, device=dev)
-    E = hw.E_loc
-    W = torch.randint(0, 0x7E, (E, 2 * bench.FFN, bench.HIDDEN), dtype=torch.uint8, device=dev)
-    sW = torch.full((E, bench.HIDDEN // 128, 2 * bench.FFN), 115, dtype=torch.uint8, device=dev)
-    Dg = torch.empty(hw.R, 2 * bench.FFN, dtype=torch.bfloat16, device=dev)
-    rows_dev = ds.off[E:]
+    ds = bench.DeviceStep(bench.Workload(0, 1, args.partition, dev))
+    extra = None
+    if not args.no_next:
+        g0 = bench.DeviceStep(bench.Workload(0, 1, "weak", dev))
+        wl, F = g0.wl, g0.F
+        dA = synth.normal_bf16_device(wl.R, bench.FFN, synth.BASE_SEED + 5, dev, sigma=0.5)
+        qb = torch.empty(wl.R, 2 * bench.FFN, dtype=torch.uint8, device=dev)
+        sbw = torch.empty(2 * bench.FFN // 128, wl.R, dtype=torch.uint8, device=dev)
+        E = wl.E_loc
+        W = torch.randint(0, 0x7E, (E, 2 * bench.FFN, bench.HIDDEN), dtype=torch.uint8, device=dev)
+        sW = torch.full((E, bench.HIDDEN // 128, 2 * bench.FFN), 115, dtype=torch.uint8, device=dev)
+        Dg = torch.empty(wl.R, 2 * bench.FFN, dtype=torch.bfloat16, device=dev)
+        rows_dev = g0.off[E:]
+        g0.launch_ops(record=False)
+        st = bench.ep_setup(dev)  # NEXT-3: 8 virtual EP ranks on this device
 
-    st = bench.ep_setup(dev)  # NEXT-3: 8 virtual EP ranks on this device
-
-    def extra():
-        F.fp8flow_swiglu_bwd_quant(ds.h, dA, qb, sbw, rows_dev=rows_dev)
-        F.fp8flow_swiglu_quant_dual(ds.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off)
-        F.fp8flow_gemm_blockscaled(ds.x_perm, ds.s_perm, W, sW, Dg, seg_offsets=ds.off)
-        st["receive"](0, kernel_only=True)
-        st["ep"].combine(st["peers"], 0, st["tpr"], bench.HIDDEN, st["E"], st["ranks"][0]["topk"],
-                         st["ranks"][0]["probs"], st["y"])
+        def extra():
+            F.fp8flow_swiglu_bwd_quant(wl.h, dA, qb, sbw, rows_dev=rows_dev)
+            F.fp8flow_swiglu_quant_dual(wl.h, g0.q_a, g0.s_a, g0.aT, g0.saT, seg_offsets=g0.off)
+            F.fp8flow_gemm_blockscaled(g0.x_perm, g0.s_perm, W, sW, Dg, seg_offsets=g0.off)
+            st["receive"](0, kernel_only=True)
+            st["ep"].combine(st["peers"], 0, st["tpr"], bench.HIDDEN, st["E"], st["ranks"][0]["topk"],
+                             st["ranks"][0]["probs"], st["y"])
 
     for _ in range(3):
         ds.launch_ops(record=False)
-        extra()
+        if extra:
+            extra()
     torch.cuda.synchronize()
     ds.flush_l2()
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     ds.launch_ops(record=False)
-    extra()
+    if extra:
+        extra()
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
-    print("profiled:", ", ".join(ORDER))
+    print("profiled:", ", ".join(ORDER if extra else ORDER[:8]))
 
 
 if __name__ == "__main__":
