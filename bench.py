@@ -218,7 +218,7 @@ class DeviceStep:
             "A1_quantize_x": lambda: F.fp8flow_quantize_rowwise(wl.x_shard, self.q_x, self.s_x),
             "A3_plan": lambda: F.fp8flow_permute_plan(wl.topk, wl.e0, wl.E_loc, ALIGN, self.row_map, self.src,
                                                       self.off, self.ws),
-            "A3_move": lambda: F.fp8flow_permute_pad(wl.q_recv, wl.s_recv, self.src, self.off, self.x_perm,
+            "A3_move": lambda: F.fp8flow_permute_pad(wl.q_recv, wl.s_recv, self.row_map, self.src, self.off, self.x_perm,
                                                      self.s_perm),
             "A5_swiglu_quant": lambda: F.fp8flow_swiglu_quant(wl.h, self.q_a, self.s_a,
                                                               rows_dev=self.off[wl.E_loc:]),
@@ -279,7 +279,7 @@ class DeviceStep:
         self.ev_side[1].record(s2)
         F.fp8flow_unpermute_unpad(wl.y, self.row_map, wl.probs_dev, self.y_tok, stream=s3)
         self.ev_side[2].record(s3)
-        F.fp8flow_permute_pad(wl.q_recv, wl.s_recv, self.src, self.off, self.x_perm, self.s_perm, stream=main)
+        F.fp8flow_permute_pad(wl.q_recv, wl.s_recv, self.row_map, self.src, self.off, self.x_perm, self.s_perm, stream=main)
         F.fp8flow_scaling_aware_transpose(self.x_perm, self.s_perm, self.xT, self.sxT, seg_offsets=self.off,
                                           stream=main)
         for e in self.ev_side:
@@ -742,7 +742,7 @@ def ep_measure(device, peak: float, reps: int = 20) -> dict:
     q_cat = torch.cat([r["q"] for r in ranks])
     s_cat = torch.cat([r["s"] for r in ranks], dim=1).contiguous()
     ref_q, ref_s = torch.empty_like(p0["q_out"]), torch.empty_like(p0["s_out"])
-    F.fp8flow_permute_pad(q_cat, s_cat, p0["src"], p0["off"], ref_q, ref_s)
+    F.fp8flow_permute_pad(q_cat, s_cat, p0["row_map"], p0["src"], p0["off"], ref_q, ref_s)
     ok_d = bool(torch.equal(ref_q[:R0], p0["q_out"][:R0]) and torch.equal(ref_s[:, :R0], p0["s_out"][:, :R0]))
     base = [0]
     for g in range(n):
@@ -808,7 +808,7 @@ def nccl_dispatch_baseline(F, rank, world, tpr, E, q, s_, topk, device, out):
     ld = (nr + 15) // 16 * 16
     rs_mn = torch.zeros(HIDDEN // 128, max(ld, 16), dtype=torch.uint8, device=device)
     rs_mn[:, :nr] = rs.t()
-    F.fp8flow_permute_pad(rq, rs_mn, src, out["off"], out["q_out"], out["s_out"])
+    F.fp8flow_permute_pad(rq, rs_mn, row_map, src, out["off"], out["q_out"], out["s_out"])
 
 
 def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) -> dict:
@@ -905,7 +905,7 @@ def ep_measure_dist(device, peak: float, rank: int, world: int, reps: int = 10) 
             lst[i].copy_(buf[i])
     R = int(off[-1].item())
     ref_q, ref_s = torch.empty_like(q_out), torch.empty_like(s_out)
-    F.fp8flow_permute_pad(torch.cat(gq), torch.cat(gs, dim=1).contiguous(), src, off, ref_q, ref_s)
+    F.fp8flow_permute_pad(torch.cat(gq), torch.cat(gs, dim=1).contiguous(), row_map, src, off, ref_q, ref_s)
     rm_glob = torch.full((tpr, TOP_K), -1, dtype=i32, device=device)
     for g in range(world):
         rmg = gr[g][rank * tpr:(rank + 1) * tpr]

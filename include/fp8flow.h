@@ -156,12 +156,17 @@ FP8FLOW_API int fp8flow_permute_plan(const int32_t* topk_idx, int64_t num_tokens
 /* fp8flow_permute_pad -- move row-wise FP8 tokens into the padded expert-major buffer in one pass:
  *   q_out[r] = q_tok[src_of_row[r]], s_out[j][r] = s_tok[j][src_of_row[r]] for r < R =
  *   min(expert_offsets[E_loc], max_rows); PAD rows get code 0x00 and scale byte 0x00 (R17, R11).
+ *   Each token is read once and written to all of its local rows (row_map from the plan gives a
+ *   token's rows), i.e. the one-rank case of fp8flow_dispatch_permute_pad.
  *   q_tok [num_tokens][hidden] + s_tok [hidden/128][ld_s_tok]  (row-wise FP8, as from A1)
+ *   row_map [num_tokens][top_k], src_of_row [max_rows], expert_offsets [E_loc + 1]: the plan's
  *   q_out [max_rows][hidden], s_out [hidden/128][max_rows]       (rows >= R untouched)
- *   hidden % 128 == 0; q_tok, q_out 16-byte aligned; max_rows % 16 == 0. */
+ *   hidden % 128 == 0; q_tok, q_out 16-byte aligned; max_rows % 16 == 0; 1 <= top_k <= 16;
+ *   num_tokens == 0 is a no-op (every expert is empty). */
 FP8FLOW_API int fp8flow_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t num_tokens,
-                        int64_t hidden, const int32_t* src_of_row, const int32_t* expert_offsets,
-                        int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out, void* stream);
+                        int64_t hidden, const int32_t* row_map, int32_t top_k, const int32_t* src_of_row,
+                        const int32_t* expert_offsets, int32_t num_local_experts, int64_t max_rows, uint8_t* q_out,
+                        uint8_t* s_out, void* stream);
 
 /* ==========================================================================================
  * A4  Fused unpermute + unpadding, BF16 at the second boundary (R22):

@@ -177,20 +177,23 @@ int fp8flow_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int32_t to
 }
 
 int fp8flow_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t num_tokens,
-                        int64_t hidden, const int32_t* src_of_row, const int32_t* expert_offsets,
-                        int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out, void* stream) {
+                        int64_t hidden, const int32_t* row_map, int32_t top_k, const int32_t* src_of_row,
+                        const int32_t* expert_offsets, int32_t num_local_experts, int64_t max_rows, uint8_t* q_out,
+                        uint8_t* s_out, void* stream) {
   if (num_tokens < 0 || hidden <= 0 || hidden % 128 != 0 || max_rows < 0 || max_rows % 16 != 0)
     return FP8FLOW_ERR_SHAPE;
-  if (ld_s_tok < num_tokens) return FP8FLOW_ERR_SHAPE;
-  if (num_local_experts < 1 || num_local_experts > 1024) return FP8FLOW_ERR_ARG;
-  if (max_rows == 0) return FP8FLOW_OK;
-  if (!src_of_row || !expert_offsets || !q_out || !s_out || (num_tokens > 0 && (!q_tok || !s_tok)))
-    return FP8FLOW_ERR_NULL;
-  if ((q_tok && !aligned16(q_tok)) || !aligned16(q_out)) return FP8FLOW_ERR_ALIGN;
+  if (ld_s_tok < num_tokens || num_tokens > INT32_MAX) return FP8FLOW_ERR_SHAPE;
+  if (num_local_experts < 1 || num_local_experts > 1024 || top_k < 1 || top_k > 16) return FP8FLOW_ERR_ARG;
+  if (max_rows == 0 || num_tokens == 0) return FP8FLOW_OK;  // no tokens: every expert is empty
+  if (!row_map || !src_of_row || !expert_offsets || !q_out || !s_out || !q_tok || !s_tok) return FP8FLOW_ERR_NULL;
+  if (!aligned16(q_tok) || !aligned16(q_out)) return FP8FLOW_ERR_ALIGN;
   int sms = 0, st = device(&sms);
   if (st != FP8FLOW_OK) return st;
-  return launched(launch_permute_pad(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts,
-                                     max_rows, q_out, s_out, static_cast<cudaStream_t>(stream), sms));
+  // the move is the one-rank case of the fused dispatch: each token is read once and written to all
+  // of its local expert rows (bulk-copy engine; register copies when the engine's ring cannot fit)
+  return launched(launch_dispatch_permute_pad(&q_tok, &s_tok, ld_s_tok, 1, num_tokens, hidden, row_map, top_k,
+                                              src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out,
+                                              FP8FLOW_DISPATCH_AUTO, nullptr, static_cast<cudaStream_t>(stream), sms));
 }
 
 int fp8flow_unpermute_unpad(const void* x_bf16, int64_t hidden, const int32_t* row_map, const float* probs,

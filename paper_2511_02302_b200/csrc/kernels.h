@@ -77,9 +77,6 @@ size_t permute_workspace_bytes(int64_t num_tokens, int32_t num_local_experts);
 cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int32_t top_k, int32_t expert_begin,
                                 int32_t num_local_experts, int32_t align, int32_t* row_map, int32_t* src_of_row,
                                 int64_t max_rows, int32_t* expert_offsets, void* ws, cudaStream_t stream);
-cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
-                               const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_local_experts,
-                               int64_t max_rows, uint8_t* q_out, uint8_t* s_out, cudaStream_t stream, int num_sms);
 cudaError_t launch_unpermute_unpad(const void* x, int64_t hidden, const int32_t* row_map, const float* probs,
                                    int64_t num_tokens, int32_t top_k, void* y, cudaStream_t stream, int num_sms);
 

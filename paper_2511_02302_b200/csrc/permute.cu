@@ -349,137 +349,9 @@ cudaError_t launch_permute_plan(const int32_t* topk_idx, int64_t num_tokens, int
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------------------------
-// A3 move
-// ---------------------------------------------------------------------------------------------
-// Move on the bulk-copy engine: one CTA per SM; warp 0, lane 0 streams whole rows global ->
-// shared -> global with 1D bulk copies (cp.async.bulk, mbarrier-completed loads, bulk-group stores)
-// through a ring of row slots, keeping kMoveLead rows in flight per SM with no register staging.
-// PAD rows are stored from a zeroed row.  Warps 1-7 gather the rows' scale bytes meanwhile.
-// Rows are dealt to CTAs in chunks of kMoveChunk, interleaved.
-constexpr int kMoveChunk = 4;
-constexpr int kMoveStoreSlack = 4;  // slots whose bulk stores may still be reading shared memory
-constexpr int kMaxMoveSlots = 32;
-constexpr size_t kMoveSmemBudget = 220 * 1024;
-
-__device__ __forceinline__ int64_t move_row(int64_t n, int64_t cta, int64_t G) {
-  return (cta + (n / kMoveChunk) * G) * kMoveChunk + (n % kMoveChunk);
-}
-
-__global__ void __launch_bounds__(256, 1) permute_pad_kernel(const uint8_t* __restrict__ q_tok,
-                                                             const uint8_t* __restrict__ s_tok, int64_t ld_s_tok,
-                                                             int64_t H, const int32_t* __restrict__ src_of_row,
-                                                             const int32_t* __restrict__ expert_offsets, int E_loc,
-                                                             int64_t max_rows, uint8_t* __restrict__ q_out,
-                                                             uint8_t* __restrict__ s_out, int nslots) {
-  extern __shared__ __align__(128) uint8_t smem_move[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_move);
-  uint8_t* zero = smem_move + 8 * kMaxMoveSlots;  // 256 B in: 128-byte aligned
-  uint8_t* slots = zero + H;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // an overflowed plan (status 1) reports the true padded total here: only max_rows rows exist
-  const int64_t R = min64(expert_offsets[E_loc], max_rows);
-  const int64_t G = gridDim.x, cta = blockIdx.x;
-  const int64_t n_chunks = (R + kMoveChunk - 1) / kMoveChunk;
-  const int64_t my_chunks = cta < n_chunks ? (n_chunks - cta + G - 1) / G : 0;
-  int64_t n_rows = my_chunks * kMoveChunk;  // rows of this CTA (the last chunk of all may be partial)
-  if (my_chunks > 0 && move_row(n_rows - 1, cta, G) >= R) n_rows -= move_row(n_rows - 1, cta, G) - R + 1;
-
-  if (tid == 0) {
-    for (int i = 0; i < nslots; ++i) mbar_init(&full[i], 1);
-    mbar_init_fence();
-  }
-  for (int64_t i = tid * 16; i < H; i += 256 * 16) *reinterpret_cast<uint4*>(zero + i) = make_uint4(0, 0, 0, 0);
-  fence_proxy_async_smem();  // zero row (generic writes) is read by bulk stores (async proxy)
-  __syncthreads();
-
-  if (warp == 0) {
-    // the whole warp walks the rows (lane l holds the source of row batch+l); lane 0 issues.
-    // Ring positions and global row indices advance incrementally (no division in the loop).
-    const int lead = nslots - kMoveStoreSlack;  // rows whose loads are in flight ahead of the stores
-    const int nr = static_cast<int>(n_rows);
-    uint32_t phase_bits = 0;
-    int32_t src_prev = -1, src_cur = -1;
-    int slot_ld = 0, slot_st = 0, k_st = 0;  // k_st: position of the store row inside its chunk
-    int64_t row_st = cta * kMoveChunk;       // global row of the store stage
-    const int64_t chunk_jump = (G - 1) * kMoveChunk + 1;
-    for (int n = 0; n < nr + lead; ++n) {
-      if ((n & 31) == 0) {  // next batch of 32 row sources, one per lane
-        src_prev = src_cur;
-        const int ln = n + lane;
-        src_cur = ln < nr ? __ldg(src_of_row + move_row(ln, cta, G)) : -1;
-      }
-      const int m = n - lead;  // store stage
-      if (m >= 0) {
-        const int ml = m - (n & ~31);  // < 0: the row is in the previous batch
-        const int32_t sm_src = __shfl_sync(0xffffffffu, ml >= 0 ? src_cur : src_prev, ml & 31);
-        if (lane == 0) {
-          const uint8_t* from = zero;
-          if (sm_src >= 0) {
-            mbar_wait(&full[slot_st], (phase_bits >> slot_st) & 1u);
-            phase_bits ^= 1u << slot_st;
-            from = slots + static_cast<int64_t>(slot_st) * H;
-          }
-          bulk_store_1d(q_out + row_st * H, from, static_cast<uint32_t>(H));
-          bulk_commit();
-        }
-        if (++slot_st == nslots) slot_st = 0;
-        if (++k_st == kMoveChunk) {
-          k_st = 0;
-          row_st += chunk_jump;
-        } else {
-          ++row_st;
-        }
-      }
-      if (n < nr) {  // load stage
-        const int32_t sn = __shfl_sync(0xffffffffu, src_cur, n & 31);
-        if (lane == 0) {
-          if (n >= nslots) bulk_wait_read<kMoveStoreSlack>();  // row n - nslots's store has read the slot
-          if (sn >= 0) {
-            mbar_expect_tx(&full[slot_ld], static_cast<uint32_t>(H));
-            bulk_load_1d(slots + static_cast<int64_t>(slot_ld) * H, q_tok + static_cast<int64_t>(sn) * H,
-                         static_cast<uint32_t>(H), &full[slot_ld]);
-          }
-        }
-        if (++slot_ld == nslots) slot_ld = 0;
-      }
-    }
-    if (lane == 0) bulk_wait_all();
-  } else {
-    // scale bytes: (local row, tile) pairs over warps 1..7; PAD rows -> 0x00
-    const int n_tiles = static_cast<int>(H / kTile);
-    const int pairs = static_cast<int>(n_rows) * n_tiles;
-    const int nr = static_cast<int>(n_rows);
-    for (int p = tid - 32; p < pairs; p += 224) {
-      const int tl = p / nr;
-      const int n = p - tl * nr;
-      const int64_t r = move_row(n, cta, G);
-      const int32_t src = __ldg(src_of_row + r);
-      s_out[static_cast<int64_t>(tl) * max_rows + r] =
-          src >= 0 ? __ldg(s_tok + static_cast<int64_t>(tl) * ld_s_tok + src) : static_cast<uint8_t>(0);
-    }
-  }
-}
-
-cudaError_t launch_permute_pad(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
-                               const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_local_experts,
-                               int64_t max_rows, uint8_t* q_out, uint8_t* s_out, cudaStream_t stream, int num_sms) {
-  const int ctas = 2;  // co-resident CTAs per SM, sharing the shared-memory budget (r01_tune_ctas.txt)
-  const size_t budget = kMoveSmemBudget / ctas;
-  int nslots = static_cast<int>((budget - 8 * kMaxMoveSlots - hidden) / hidden);
-  if (nslots > kMaxMoveSlots) nslots = kMaxMoveSlots;
-  if (nslots < kMoveStoreSlack + 2) return cudaErrorInvalidValue;  // hidden too large for the ring
-  const size_t smem = 8 * kMaxMoveSlots + static_cast<size_t>(hidden) * (1 + nslots);
-  static KernelSetup setup;
-  if (prepare_kernel(setup, permute_pad_kernel, 256, 8 * kMaxMoveSlots + kMoveSmemBudget, smem) == 0)
-    return cudaErrorInvalidValue;
-  int64_t grid = (max_rows + kMoveChunk - 1) / kMoveChunk;
-  if (grid > static_cast<int64_t>(num_sms) * ctas) grid = static_cast<int64_t>(num_sms) * ctas;
-  if (grid < 1) grid = 1;
-  permute_pad_kernel<<<static_cast<unsigned>(grid), 256, smem, stream>>>(
-      q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts, max_rows, q_out, s_out, nslots);
-  return cudaGetLastError();
-}
+// A3 move: fp8flow_permute_pad runs the one-rank case of the fused dispatch (ep.cu): every routed
+// token is read ONCE and fanned out to all of its local expert rows (r01's per-row move read a
+// token once per row -- 8x at top-8 with all experts local, 1.27x at EP8).
 
 // ---------------------------------------------------------------------------------------------
 // A4 unpermute + unpad on the bulk-copy engine.  One CTA per SM; tokens dealt round-robin.

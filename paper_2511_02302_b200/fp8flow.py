@@ -38,7 +38,7 @@ SIGNATURES = {
     "fp8flow_naive_transpose": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P, _SZ, _P]),
     "fp8flow_permute_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
     "fp8flow_permute_plan": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _I64, _P, _P, _SZ, _P]),
-    "fp8flow_permute_pad": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _P, _I32, _I64, _P, _P, _P]),
+    "fp8flow_permute_pad": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _I32, _I64, _P, _P, _P]),
     "fp8flow_unpermute_unpad": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _I32, _P, _P]),
     "fp8flow_swiglu_quant": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _P]),
     "fp8flow_checksum64": (ctypes.c_int, [_P, _I64, _P, _P]),
@@ -182,11 +182,13 @@ def fp8flow_permute_plan(topk_idx: torch.Tensor, expert_begin: int, num_local_ex
                                       ws.numel() * ws.element_size(), _stream(stream)), "fp8flow_permute_plan")
 
 
-def fp8flow_permute_pad(q_tok, s_tok, src_of_row, expert_offsets, q_out, s_out, stream=None) -> None:
+def fp8flow_permute_pad(q_tok, s_tok, row_map, src_of_row, expert_offsets, q_out, s_out, stream=None) -> None:
+    """A3 move with the plan's (row_map, src_of_row, expert_offsets): q_tok [T, H] + s_tok [H/128, ld]."""
     T, H = q_tok.shape
-    _check(lib().fp8flow_permute_pad(_ptr(_u8(q_tok)), _ptr(_u8(s_tok)), s_tok.shape[1], T, H, _ptr(src_of_row),
-                                     _ptr(expert_offsets), expert_offsets.numel() - 1, q_out.shape[0],
-                                     _ptr(_u8(q_out)), _ptr(_u8(s_out)), _stream(stream)), "fp8flow_permute_pad")
+    _check(lib().fp8flow_permute_pad(_ptr(_u8(q_tok)), _ptr(_u8(s_tok)), s_tok.shape[1], T, H, _ptr(row_map),
+                                     row_map.shape[1], _ptr(src_of_row), _ptr(expert_offsets),
+                                     expert_offsets.numel() - 1, q_out.shape[0], _ptr(_u8(q_out)), _ptr(_u8(s_out)),
+                                     _stream(stream)), "fp8flow_permute_pad")
 
 
 # ----------------------------------------------------------------------------------- A4

@@ -107,7 +107,7 @@ def test_dispatch_equals_device_permute_of_concatenation_full_size(F):
         out = run_dispatch(F, ranks, ld, g, tpr, H, E, K)
         ref_q = torch.full_like(out["q_out"], 0xEE)
         ref_s = torch.full_like(out["s_out"], 0xEE)
-        F.fp8flow_permute_pad(q_cat, s_cat, out["src"], out["off"], ref_q, ref_s)
+        F.fp8flow_permute_pad(q_cat, s_cat, out["row_map"], out["src"], out["off"], ref_q, ref_s)
         torch.cuda.synchronize()
         assert torch.equal(out["q_out"], ref_q) and torch.equal(out["s_out"], ref_s)
         src, R = host(out["src"]), int(host(out["off"])[-1])

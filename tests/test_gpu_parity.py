@@ -253,7 +253,7 @@ def test_overflowed_plan_consumers_stay_in_bounds(F):
     qbuf = torch.full((mr * H + guard,), 0xEE, dtype=torch.uint8, device="cuda")
     sbuf = torch.full(((H // 128) * mr + guard,), 0xEE, dtype=torch.uint8, device="cuda")
     q_out, s_out = qbuf[: mr * H].view(mr, H), sbuf[: (H // 128) * mr].view(H // 128, mr)
-    F.fp8flow_permute_pad(q_tok, s_tok, dev(src), dev(off), q_out, s_out)
+    F.fp8flow_permute_pad(q_tok, s_tok, dev(rm), dev(src), dev(off), q_out, s_out)
     h = synth.normal_bf16(mr, 2 * FF, 77).cuda()
     abuf = torch.full((mr * FF + guard,), 0xEE, dtype=torch.uint8, device="cuda")
     sab = torch.full(((FF // 128) * mr + guard,), 0xEE, dtype=torch.uint8, device="cuda")
@@ -265,28 +265,30 @@ def test_overflowed_plan_consumers_stay_in_bounds(F):
     assert torch.equal(q_out, q_tok[:mr]) and torch.equal(s_out, s_tok[:, :mr])   # rows 0..31 = tokens 0..31
 
 
-def run_move(F, q_tok, s_tok, src, off, max_rows):
+def run_move(F, q_tok, s_tok, rm, src, off, max_rows):
     T, H = q_tok.shape
     q_out = torch.full((max_rows, H), 0xEE, dtype=torch.uint8, device="cuda")
     s_out = torch.full((H // 128, max_rows), 0xEE, dtype=torch.uint8, device="cuda")
-    F.fp8flow_permute_pad(dev(q_tok), dev(s_tok), dev(src), dev(off), q_out, s_out)
+    F.fp8flow_permute_pad(dev(q_tok), dev(s_tok), dev(rm), dev(src), dev(off), q_out, s_out)
     torch.cuda.synchronize()
     return host(q_out), host(s_out)
 
 
-@pytest.mark.parametrize("T,H,group", [(16384, 7168, 3), (1000, 1024, 0)])
-def test_permute_pad_parity(F, orc, T, H, group):
+@pytest.mark.parametrize("T,H,group,ngroups", [(16384, 7168, 3, 8), (1000, 1024, 0, 8), (16384, 7168, 0, 1)])
+def test_permute_pad_parity(F, orc, T, H, group, ngroups):
+    """EP8 shards and the whole DeepSeek-V3 layer on one GPU (ngroups 1: 256 local experts, every
+    token fanned out to its 8 rows, ~133k padded rows)."""
     x = synth.activations_bf16(T, H, 500 + T)
     q_tok, s_tok = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
     idx, _ = synth.routing(T, 501 + T)
-    sh = synth.expert_shard(idx, torch.zeros(idx.shape), group, 8)
+    sh = synth.expert_shard(idx, torch.zeros(idx.shape), group, ngroups)
     q_recv = np.ascontiguousarray(q_tok[sh.recv_tokens])
     s_recv = np.ascontiguousarray(s_tok[:, sh.recv_tokens])
     rm, src, off = orc.permute_plan(sh.topk_idx, sh.expert_begin, sh.num_local_experts)
     max_rows = (len(src) + 15) // 16 * 16
     src_p = np.full(max_rows, -1, np.int32)
     src_p[: len(src)] = src
-    qo, so = run_move(F, q_recv, s_recv, src_p, off, max_rows)
+    qo, so = run_move(F, q_recv, s_recv, rm, src_p, off, max_rows)
     qo_ref, so_ref = orc.permute_pad(q_recv, s_recv, src_p, off, max_rows=max_rows)
     R = int(off[-1])
     assert np.array_equal(qo[:R], qo_ref[:R]) and np.array_equal(so[:, :R], so_ref[:, :R])
@@ -554,7 +556,7 @@ def test_all_ops_capture_into_a_cuda_graph(F, orc):
         b = bufs
         F.fp8flow_quantize_rowwise(x, b["q"], b["s"])
         F.fp8flow_permute_plan(idx, 0, E_loc, 16, b["row_map"], b["src"], b["off"], ws)
-        F.fp8flow_permute_pad(b["q"], b["s"], b["src"], b["off"], b["q_out"], b["s_out"])
+        F.fp8flow_permute_pad(b["q"], b["s"], b["row_map"], b["src"], b["off"], b["q_out"], b["s_out"])
         F.fp8flow_swiglu_quant(h, b["qa"], b["sa"], rows_dev=b["off"][E_loc:])
         F.fp8flow_unpermute_unpad(y_in, b["row_map"], probs, b["y"])
         F.fp8flow_scaling_aware_transpose(b["q_out"], b["s_out"], b["qT"], b["sT"], seg_offsets=b["off"])
