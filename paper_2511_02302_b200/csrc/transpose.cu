@@ -317,96 +317,162 @@ __global__ void seg_prefix_kernel(const int32_t* __restrict__ seg_offsets, int32
   }
 }
 
-__global__ void naive_dequant_kernel(const uint8_t* __restrict__ q, const uint8_t* __restrict__ s, int64_t ld_s,
-                                     int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ xd) {
-  const int64_t n16 = rows * cols / 16;
-  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n16;
-       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t e0 = v * 16, r = e0 / cols, cc = e0 - r * cols;
-    const uint4 w = ld_nc_v4(q + e0);
-    const float sc = scale_from_byte(s[(cc / kTile) * ld_s + r]);
-    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+// K1 dequantize: thread per 2 x 16 codes (two 128-bit loads in flight), the row's 1x128 scale
+// byte from the MN-major run; decode exactly (e4m3x2 -> f16x2 -> f32), x 2^T in fp32 (exact), one
+// RNE to BF16 (R29); two 128-bit stores per 16 codes.
+constexpr int kNaiveU = 2;
+__global__ void __launch_bounds__(256) naive_dequant_kernel(const uint8_t* __restrict__ q, const uint8_t* __restrict__ s,
+                                                            int64_t ld_s, int64_t rows, int64_t cols,
+                                                            __nv_bfloat16* __restrict__ xd) {
+  const int64_t cpr = cols / 16;                   // 16-code chunks per row
+  const int64_t n16 = rows * cpr;
+  const int64_t k0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x) * kNaiveU + threadIdx.x;
+  uint4 w[kNaiveU];
+  float sc[kNaiveU];
+#pragma unroll
+  for (int u = 0; u < kNaiveU; ++u) {
+    const int64_t k = k0 + u * blockDim.x;
+    if (k < n16) {
+      const int64_t r = k / cpr, cc = k - r * cpr;
+      w[u] = ld_nc_v4(q + k * 16);
+      sc[u] = scale_from_byte(__ldg(s + (cc >> 3) * ld_s + r));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kNaiveU; ++u) {
+    const int64_t k = k0 + u * blockDim.x;
+    if (k >= n16) continue;
+    const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
     uint32_t o[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t lo = cvt_f16x2_from_e4m3x2(ws[k] & 0xFFFFu), hi = cvt_f16x2_from_e4m3x2(ws[k] >> 16);
-      float2 a = __half22float2(*reinterpret_cast<__half2*>(&lo));
-      float2 b = __half22float2(*reinterpret_cast<__half2*>(&hi));
-      __nv_bfloat162 pa = __floats2bfloat162_rn(a.x * sc, a.y * sc);
-      __nv_bfloat162 pb = __floats2bfloat162_rn(b.x * sc, b.y * sc);
-      o[2 * k] = *reinterpret_cast<uint32_t*>(&pa);
-      o[2 * k + 1] = *reinterpret_cast<uint32_t*>(&pb);
+    for (int t = 0; t < 4; ++t) {
+      uint32_t lo = cvt_f16x2_from_e4m3x2(ws[t] & 0xFFFFu), hi = cvt_f16x2_from_e4m3x2(ws[t] >> 16);
+      const float2 a = __half22float2(*reinterpret_cast<__half2*>(&lo));
+      const float2 b = __half22float2(*reinterpret_cast<__half2*>(&hi));
+      __nv_bfloat162 pa = __floats2bfloat162_rn(a.x * sc[u], a.y * sc[u]);
+      __nv_bfloat162 pb = __floats2bfloat162_rn(b.x * sc[u], b.y * sc[u]);
+      o[2 * t] = *reinterpret_cast<uint32_t*>(&pa);
+      o[2 * t + 1] = *reinterpret_cast<uint32_t*>(&pb);
     }
-    st_v4(xd + e0, make_uint4(o[0], o[1], o[2], o[3]));
-    st_v4(xd + e0 + 8, make_uint4(o[4], o[5], o[6], o[7]));
+    st_v4(xd + k * 16, make_uint4(o[0], o[1], o[2], o[3]));
+    st_v4(xd + k * 16 + 8, make_uint4(o[4], o[5], o[6], o[7]));
   }
 }
 
-// per segment: xT_e[j][i] = xd[o + i][j]; block = 16 rows (never straddles a segment) x 128 cols
-__global__ void naive_transpose_bf16_kernel(const __nv_bfloat16* __restrict__ xd, int64_t cols,
-                                            const int32_t* __restrict__ seg_off, int32_t nsegs,
-                                            __nv_bfloat16* __restrict__ xT) {
-  __shared__ uint16_t tile[16][128 + 2];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 16;
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 128;
-  if (r0 >= seg_off[nsegs]) return;
-  int lo = 0, hi = nsegs;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (seg_off[mid] <= r0) lo = mid;
-    else hi = mid;
-  }
-  const int64_t o = seg_off[lo], m = seg_off[lo + 1] - o;
-  const uint16_t* src = reinterpret_cast<const uint16_t*>(xd);
-  for (int idx = threadIdx.x; idx < 16 * 128; idx += blockDim.x) {
-    const int r = idx / 128, cc = idx % 128;
-    tile[r][cc] = src[(r0 + r) * cols + c0 + cc];
+// K2 BF16 transpose per segment, xT_e[j][i] = xd[o + i][j]: CTA tile = one 128-row block of a
+// segment x 64 columns (16 KB).  Loads: 128-bit, 8 threads per 128-byte row piece, into shared
+// memory with the 16-byte chunks XOR-swizzled by (row / 8) & 7.  Read-out: a thread takes 8 rows x
+// one 32-bit word (2 columns), i.e. 8 i-elements of output rows j and j + 1, packs them with PRMT
+// and stores one 16-byte chunk to each row.  Lane l of a warp: i-chunk l & 7 (+ 8 * half), word
+// 4 * chunk + (l >> 3): the 32 lanes read 32 distinct banks, and 8 lanes write 128 contiguous
+// bytes of each of the warp's 8 output rows.
+__global__ void __launch_bounds__(256) naive_transpose_bf16_kernel(const __nv_bfloat16* __restrict__ xd, int64_t cols,
+                                                                   const int32_t* __restrict__ seg_off,
+                                                                   const int32_t* __restrict__ blk_prefix,
+                                                                   int32_t nsegs, __nv_bfloat16* __restrict__ xT) {
+  __shared__ __align__(16) uint32_t tile[128][32];
+  __shared__ int32_t seg_s[3];
+  const int tid = threadIdx.x;
+  const int n_jt = static_cast<int>(cols / 64);
+  const int rb = blockIdx.x / n_jt;
+  const int jt = blockIdx.x - rb * n_jt;
+  if (rb >= __ldg(blk_prefix + nsegs)) return;  // (the grid is an upper bound)
+  if (tid == 0) {
+    const int e = find_segment(blk_prefix, nsegs, rb);
+    seg_s[0] = seg_off[e];
+    seg_s[1] = seg_off[e + 1] - seg_off[e];
+    seg_s[2] = rb - blk_prefix[e];
   }
   __syncthreads();
-  uint16_t* dst = reinterpret_cast<uint16_t*>(xT) + cols * o;
-  for (int idx = threadIdx.x; idx < 16 * 128; idx += blockDim.x) {
-    const int j = idx / 16, r = idx % 16;
-    dst[(c0 + j) * m + (r0 - o) + r] = tile[r][j];
+  const int o = seg_s[0], m = seg_s[1], ib = seg_s[2];
+  const int valid = min(kTile, m - ib * kTile);
+  const uint16_t* src = reinterpret_cast<const uint16_t*>(xd) + (static_cast<int64_t>(o) + ib * kTile) * cols + jt * 64;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int id = tid + 256 * k, i = id >> 3, c = id & 7;
+    if (i < valid) {
+      const uint4 v = ld_nc_v4(src + static_cast<int64_t>(i) * cols + c * 8);
+      *reinterpret_cast<uint4*>(&tile[i][4 * (c ^ ((i >> 3) & 7))]) = v;
+    }
+  }
+  __syncthreads();
+  uint16_t* dst = reinterpret_cast<uint16_t*>(xT) + static_cast<int64_t>(cols) * o;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int p = tid + 256 * k, l = p & 31, w = p >> 5;   // w: 0..15
+    const int ic = (l & 7) + 8 * (w >> 3);                  // 8-row chunk of the block
+    const int jp = 4 * (w & 7) + (l >> 3);                  // 32-bit word = column pair 2jp, 2jp+1
+    if (ic * 8 >= valid) continue;
+    uint32_t wv[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = ic * 8 + r;
+      wv[r] = tile[i][4 * ((jp >> 2) ^ ((i >> 3) & 7)) + (jp & 3)];
+    }
+    uint32_t a[4], b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      a[t] = __byte_perm(wv[2 * t], wv[2 * t + 1], 0x5410);  // column 2 jp, rows i, i + 1
+      b[t] = __byte_perm(wv[2 * t], wv[2 * t + 1], 0x7632);  // column 2 jp + 1
+    }
+    const int64_t j = static_cast<int64_t>(jt) * 64 + 2 * jp;
+    st_v4(dst + j * m + ib * kTile + ic * 8, make_uint4(a[0], a[1], a[2], a[3]));
+    st_v4(dst + (j + 1) * m + ib * kTile + ic * 8, make_uint4(b[0], b[1], b[2], b[3]));
   }
 }
 
-// column-wise requantization: rows j of xT_e (length m_e), 1x128 tiles along i (ragged last tile)
-__global__ void naive_colquant_kernel(const __nv_bfloat16* __restrict__ xT, int64_t cols,
-                                      const int32_t* __restrict__ seg_off, const int32_t* __restrict__ blk_prefix,
-                                      int32_t nsegs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
-  const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+// K3 column-wise requantization: rows j of xT_e (length m_e), 1x128 tiles along i with a fresh
+// scale each (ragged last tile).  A1's structure: 8 lanes per tile row, 16 BF16 per lane; a warp
+// takes 8 output rows (lanes 8r..8r+7: rows 8w + r and 8w + r + 4) of one 128-column tile.
+__device__ __forceinline__ uint32_t absmax2_bf16(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__global__ void __launch_bounds__(256) naive_colquant_kernel(const __nv_bfloat16* __restrict__ xT, int64_t cols,
+                                                             const int32_t* __restrict__ seg_off,
+                                                             const int32_t* __restrict__ blk_prefix, int32_t nsegs,
+                                                             uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
+  const int lane = threadIdx.x & 31;
+  const int64_t jg8 = cols / 8;                                  // 8-row groups per block
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t jgroups = cols / 32;
-  const int64_t total = static_cast<int64_t>(blk_prefix[nsegs]) * jgroups;
+  const int64_t total = static_cast<int64_t>(__ldg(blk_prefix + nsegs)) * jg8;
   if (warp >= total) return;
-  const int rb = static_cast<int>(warp / jgroups);
-  const int64_t j0 = (warp - static_cast<int64_t>(rb) * jgroups) * 32;
+  const int rb = static_cast<int>(warp / jg8);
+  const int64_t j0 = (warp - static_cast<int64_t>(rb) * jg8) * 8 + (lane >> 3);
   const int e = find_segment(blk_prefix, nsegs, rb);
-  const int64_t o = seg_off[e], m = seg_off[e + 1] - o;
-  const int ib = rb - blk_prefix[e];
+  const int64_t o = __ldg(seg_off + e), m = __ldg(seg_off + e + 1) - o;
+  const int ib = rb - __ldg(blk_prefix + e);
   const int valid = static_cast<int>(min64(kTile, m - ib * kTile));
-  uint32_t keep = 0;
-  for (int jj = 0; jj < 32; jj += 2) {
-    const int64_t j = j0 + jj + half;
-    const int i0 = ib * kTile + sub * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (sub * 8 < valid) v = ld_nc_v4(xT + cols * o + j * m + i0);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t mag = 0;
+  const int c16 = (lane & 7) * 16;
+  const bool ok = c16 < valid;
+  uint4 v[2][2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) mag = max(mag, max(w[k] & 0x7FFFu, (w[k] >> 16) & 0x7FFFu));
-    mag = halfwarp_max_u32(mag);
-    const uint32_t sb = scale_byte_from_bf16_mag(mag);
-    const float inv = inv_scale_from_byte(sb);
-    uint32_t cc[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = cvt_e4m3x2_f32(bf16lo_to_f32(w[k]) * inv, bf16hi_to_f32(w[k]) * inv);
-    if (sub * 8 < valid) st_v2(qT + cols * o + j * m + i0, cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
-    const uint32_t a = __shfl_sync(0xffffffffu, sb, 0), b = __shfl_sync(0xffffffffu, sb, 16);
-    if (lane == jj) keep = a;
-    if (lane == jj + 1) keep = b;
+  for (int h = 0; h < 2; ++h) {
+    const __nv_bfloat16* p = xT + cols * o + (j0 + 4 * h) * m + ib * kTile + c16;
+    v[h][0] = ok ? ld_nc_v4(p) : make_uint4(0, 0, 0, 0);
+    v[h][1] = ok ? ld_nc_v4(p + 8) : make_uint4(0, 0, 0, 0);
   }
-  sT[static_cast<int64_t>(rb) * cols + j0 + lane] = static_cast<uint8_t>(keep);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t w[8] = {v[h][0].x, v[h][0].y, v[h][0].z, v[h][0].w, v[h][1].x, v[h][1].y, v[h][1].z, v[h][1].w};
+    const uint32_t mm = absmax2_bf16(absmax2_bf16(absmax2_bf16(w[0], w[1]), absmax2_bf16(w[2], w[3])),
+                                     absmax2_bf16(absmax2_bf16(w[4], w[5]), absmax2_bf16(w[6], w[7])));
+    uint32_t mag = max(mm & 0x7FFFu, (mm >> 16) & 0x7FFFu);
+    mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 1));
+    mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 2));
+    mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 4));
+    const int sb = max(static_cast<int>((mag + 0x1Fu) >> 7) - 8, 0);  // the A1 scale rule (R3)
+    const float inv = __uint_as_float(static_cast<uint32_t>(254 - sb) << 23);
+    uint32_t c[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t] = cvt_e4m3x2_f32(bf16lo_to_f32(w[t]) * inv, bf16hi_to_f32(w[t]) * inv);
+    const int64_t j = j0 + 4 * h;
+    if (ok)
+      st_v4(qT + cols * o + j * m + ib * kTile + c16,
+            make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16), c[6] | (c[7] << 16)));
+    if ((lane & 7) == 0) sT[static_cast<int64_t>(rb) * cols + j] = static_cast<uint8_t>(sb);
+  }
 }
 
 size_t naive_workspace_bytes(int64_t rows, int64_t cols, int32_t num_segs) {
@@ -425,12 +491,13 @@ cudaError_t launch_naive_transpose(const uint8_t* q, const uint8_t* s, int64_t l
   __nv_bfloat16* xT = xd + rows * cols;
   seg_prefix_kernel<<<1, kTThreads, 0, stream>>>(seg_offsets, num_segs, rows, seg_out, blk_prefix);
   const int64_t n16 = rows * cols / 16;
-  int64_t g1 = (n16 + 255) / 256;
-  if (g1 > static_cast<int64_t>(num_sms) * 16) g1 = static_cast<int64_t>(num_sms) * 16;
-  naive_dequant_kernel<<<static_cast<unsigned>(g1 < 1 ? 1 : g1), 256, 0, stream>>>(q, s, ld_s, rows, cols, xd);
-  dim3 g2(static_cast<unsigned>(cols / 128), static_cast<unsigned>((rows + 15) / 16));
-  naive_transpose_bf16_kernel<<<g2, 256, 0, stream>>>(xd, cols, seg_out, nsegs, xT);
-  const int64_t warps = (rows / kTile + nsegs) * (cols / 32);
+  const int64_t g1 = (n16 + 256 * kNaiveU - 1) / (256 * kNaiveU);
+  if (g1 > 0)
+    naive_dequant_kernel<<<static_cast<unsigned>(g1), 256, 0, stream>>>(q, s, ld_s, rows, cols, xd);
+  const int64_t blocks_ub = rows / kTile + nsegs;  // 128-row blocks (upper bound; extra CTAs exit)
+  naive_transpose_bf16_kernel<<<static_cast<unsigned>(blocks_ub * (cols / 64)), 256, 0, stream>>>(
+      xd, cols, seg_out, blk_prefix, nsegs, xT);
+  const int64_t warps = blocks_ub * (cols / 8);
   naive_colquant_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, stream>>>(xT, cols, seg_out, blk_prefix,
                                                                                       nsegs, qT, sT);
   return cudaGetLastError();

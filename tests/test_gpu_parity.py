@@ -177,13 +177,23 @@ def test_transpose_involution_on_gpu(F, orc):
     assert np.array_equal(q3, q1) and np.array_equal(s3, s1)
 
 
-@pytest.mark.parametrize("rows,cols", [(256, 256), (1024, 1024)])
+@pytest.mark.parametrize("rows,cols", [(256, 256), (1024, 1024), (4096, 7168)])
 def test_naive_transpose_parity(F, orc, rows, cols):
     x = synth.activations_bf16(rows, cols, 300 + rows)
     q, s = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
     check_transpose(F, orc, q, s, naive=True)
     m = [16, 128, 0, rows - 144]
     seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
+    check_transpose(F, orc, q, s, seg, naive=True)
+
+
+def test_naive_transpose_ragged_segments(F, orc):
+    """The comparator over expert segments {0, 16, ..., 272} rows (partial 128-row blocks, empty
+    segments): fresh scales per (column, 128-row block of a segment), as the oracle (R29)."""
+    m = [0, 16, 16, 16, 32, 128, 128, 144, 0, 256, 272, 16]
+    seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
+    x = synth.activations_bf16(int(seg[-1]), 512, 31)
+    q, s = orc.quantize_rowwise_bf16(synth.bf16_bits(x))
     check_transpose(F, orc, q, s, seg, naive=True)
 
 
