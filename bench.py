@@ -1220,9 +1220,10 @@ SWEEP_SHAPES = [(128, 128), (256, 256), (512, 512), (1024, 1024), (2048, 2048), 
 
 def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
     """Config 5: scaling-aware transpose vs the naive dequant -> transpose -> requant comparator,
-    128^2 .. 65536x7168, the same shape on every GPU (weak scaling).  Latency per launch (L2
-    flushed before each), GB/s on A2's algorithmic bytes, naive/direct latency ratio; plus
-    A1 alone and the one-pass quantize + transpose (NEXT-1 dual) on the same shape."""
+    128^2 .. 65536x7168, the same shape on every GPU (weak scaling).  Marginal cold-L2 time per
+    launch (marginal_us), GB/s on A2's algorithmic bytes, the naive route on its own bytes, the
+    naive/direct latency ratio; plus A1 alone and the one-pass quantize + transpose (NEXT-1
+    dual) on the same shape."""
     from paper_2511_02302_b200 import fp8flow as F
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -1230,19 +1231,8 @@ def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     out = []
 
-    def timed(fn):
-        fn()
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            clean.sum()
-            torch.cuda._sleep(200_000)
-            ev[0].record()
-            fn()
-            ev[1].record()
-            ev[1].synchronize()
-            ts.append(ev[0].elapsed_time(ev[1]))
-        return statistics.median(ts)
+    def timed(fn):  # marginal cold-L2 cost per launch, ms (marginal_us)
+        return marginal_us(fn, lambda: (flush.zero_(), clean.sum()), K=10 if rows * cols < (1 << 28) else 4) / 1e3
 
     for rows, cols in SWEEP_SHAPES:
         x = synth.activations_bf16_device(rows, cols, synth.BASE_SEED + rows + cols, device)
@@ -1289,6 +1279,7 @@ def run_sweep(device, peak: float, world: int, reps: int = 10) -> list[dict]:
                     "direct_gbs_per_gpu": round(nb / t_d / 1e6, 1), "direct_frac": round(nb / t_d / 1e6 / peak, 3),
                     "naive_effective_gbs_per_gpu": round(nb / t_n / 1e6, 1),
                     "naive_actual_gbs_per_gpu": round(RL.naive_transpose_actual_bytes([rows], cols) / t_n / 1e6, 1),
+                    "naive_actual_frac": round(RL.naive_transpose_actual_bytes([rows], cols) / t_n / 1e6 / peak, 3),
                     "direct_gbs_all_gpus": round(world * nb / t_d / 1e6, 1),
                     "quantize_us": round(t_q * 1e3, 2),
                     "quantize_frac": round(RL.quantize_bytes(rows, cols) / t_q / 1e6 / peak, 3),
