@@ -27,7 +27,7 @@ def main(path):
     f = lambda r, m: float(r[idx[m]].replace(",", "") or 0) * SCALE.get(units[idx[m]], 1)  # noqa: E731
     res = {"_about": "DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from one `ncu --set full "
                      "--clock-control none` capture of one serial pass of bench.py's step kernels plus the NEXT-row "
-                     "kernels (tools/profile_step.py; summary profiles/r01_ncu_summary.md). ncu flushes caches "
+                     "kernels (tools/profile_step.py; summary profiles/r02_ncu_summary.md). ncu flushes caches "
                      "before each kernel; writes still resident in L2 when the kernel ends are not counted, so "
                      "traffic can be below the algorithmic bytes."}
     for op, r in zip(ORDER, launches):
