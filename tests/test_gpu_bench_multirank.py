@@ -1,7 +1,9 @@
 """The N > 1 path of bench.py on one GPU: two ranks (gloo for the host collectives, CUDA IPC between
 the two processes for NEXT-3), a reduced token count.  Guards what the driver's multi-GPU run
-executes: the per-rank step, max-over-ranks timing, the NEXT-3 dispatch/combine across ranks and
-the NCCL-style all-to-all baseline, each checked bit-exact."""
+executes: the strong split of the layer, the per-rank step, max-over-ranks timing, every rank's
+whole-step verification against the oracle (elementwise + C11 checksums) merged on rank 0 with
+the CPU-oracle baseline of all ranks, the NEXT-3 dispatch/combine across ranks and the NCCL-style
+all-to-all baseline, each checked bit-exact."""
 import json
 import os
 import socket
@@ -29,12 +31,18 @@ def test_bench_two_ranks_one_gpu():
     env = dict(os.environ, FP8FLOW_DIST_BACKEND="gloo", FP8FLOW_BENCH_TOKENS="2048")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+           "--steps", "3", "--warmup", "3", "--no-e2e"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["tokens"] == 2048
-    assert all(line["parity"].values()), line["parity"]
+    # the strong split: each rank owns 128 of the 256 experts; every rank verified its whole step
+    assert line["scaling"] == "strong" and line["config"]["local_experts"] == 128
+    assert set(line["parity"]) == {"rank0", "rank1"}, line["parity"]
+    assert all(all(p.values()) for p in line["parity"].values()), line["parity"]
+    assert line["parity_all_ranks"] is True and line["checksums_match"] is True
+    cb = line["cpu_baseline"]
+    assert cb is not None and cb["kind"] == "oracle" and cb["value"] > 0 and "x2 ranks" in cb["sample"], cb
     ep = line["next3_multi_rank"]
     assert ep.get("parity") is True, ep
     assert ep["baseline_all_to_all_then_permute"].get("same_output") is True, ep
