@@ -365,17 +365,35 @@ __global__ void __launch_bounds__(256) dispatch_engine_kernel(
     const int64_t R_all = min64(offsets[E_loc], max_rows);
     const int64_t rb = cta * R_all / G;
     const int nr = static_cast<int>((cta + 1) * R_all / G - rb);
+    // 8 (row, tile) pairs per thread in flight: the source-row loads, then the byte gathers, then
+    // the stores (a dependent load -> load -> store chain per pair otherwise bounds the kernel's tail)
     const int tpr = static_cast<int>(Tpr);
-    for (int p = tid - 32; p < nr * static_cast<int>(n_tiles); p += 224) {
-      const int tl = p / nr;
-      const int64_t r = rb + (p - tl * nr);
-      const int32_t src = __ldg(src_of_row + r);
-      uint8_t v = 0;
-      if (src >= 0) {
-        const int src_rank = src / tpr;
-        v = __ldg(static_cast<const uint8_t*>(peer.b[src_rank]) + static_cast<int64_t>(tl) * ld_s_tok + (src - src_rank * tpr));
+    constexpr int kSU = 8;
+    const int total = nr * static_cast<int>(n_tiles);
+    for (int p0 = tid - 32; p0 < total; p0 += 224 * kSU) {
+      int32_t src[kSU];
+      int64_t r[kSU];
+      int tl[kSU];
+#pragma unroll
+      for (int u = 0; u < kSU; ++u) {
+        const int p = p0 + 224 * u;
+        tl[u] = p < total ? p / nr : 0;
+        r[u] = rb + (p - tl[u] * nr);
+        src[u] = p < total ? __ldg(src_of_row + r[u]) : -2;
       }
-      s_out[static_cast<int64_t>(tl) * max_rows + r] = v;
+      uint8_t v[kSU];
+#pragma unroll
+      for (int u = 0; u < kSU; ++u) {
+        v[u] = 0;
+        if (src[u] >= 0) {
+          const int src_rank = src[u] / tpr;
+          v[u] = __ldg(static_cast<const uint8_t*>(peer.b[src_rank]) + static_cast<int64_t>(tl[u]) * ld_s_tok +
+                       (src[u] - src_rank * tpr));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kSU; ++u)
+        if (src[u] != -2) s_out[static_cast<int64_t>(tl[u]) * max_rows + r[u]] = v[u];
     }
     // PAD rows: 32-row chunks over the grid's warps 1..7
     const int64_t R = min64(offsets[E_loc], max_rows);  // an overflowed plan: only max_rows rows exist
