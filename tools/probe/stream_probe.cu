@@ -62,3 +62,23 @@ extern "C" int probe_touch(const void* p, int64_t bytes, int64_t stride, void* o
   touch_kernel<<<64, 256, 0, (cudaStream_t)stream>>>((const uint8_t*)p, bytes, stride, (uint32_t*)out);
   return (int)cudaGetLastError();
 }
+
+// 1:1 copy (A2's read:write mix), U 16-byte loads in flight per thread
+template <int U>
+__global__ void __launch_bounds__(256) copy_kernel(const uint4* __restrict__ p, int64_t n16, uint4* __restrict__ o) {
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * T < n16; i += U * T) {
+    uint4 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(a[u].x), "=r"(a[u].y), "=r"(a[u].z), "=r"(a[u].w) : "l"(p + i + u * T));
+#pragma unroll
+    for (int u = 0; u < U; ++u) o[i + u * T] = a[u];
+  }
+  for (; i < n16; i += T) o[i] = p[i];
+}
+extern "C" int probe_copy(const void* p, int64_t bytes, void* o, int grid, void* stream) {
+  copy_kernel<4><<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)p, bytes / 16, (uint4*)o);
+  return (int)cudaGetLastError();
+}
