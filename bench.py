@@ -286,31 +286,39 @@ class DeviceStep:
             main.wait_event(e)
         join.record(main)
 
+    # serial orders: OPS order, and one that runs each A2 right after the op that writes its input
+    # (the tail of X_perm / A still in the 126 MB L2 when the transpose starts)
+    SERIAL_ORDERS = {"serial": OPS,
+                     "serial_reuse": ["A1_quantize_x", "A3_plan", "A3_move", "A2_transpose_xperm", "A5_swiglu_quant",
+                                      "A2_transpose_a", "A4_unpermute", "A1_quantize_dy"]}
+
     def capture_graph(self, schedule: str = "dag") -> None:
         """Capture the step once into a CUDA graph (every launch is graph-capturable: no host
         synchronisation, data-dependent sizes stay on the device).  schedule "dag": the dependency
-        DAG on 4 streams; "serial": the 8 launches in OPS order on one stream."""
+        DAG on 4 streams; "serial" / "serial_reuse": the 8 launches on one stream (SERIAL_ORDERS)."""
         g = torch.cuda.CUDAGraph()
         fork, join = torch.cuda.Event(), torch.cuda.Event()
         torch.cuda.synchronize()
+        fns = self.op_fns()
         with torch.cuda.graph(g):
             if schedule == "dag":
                 self.launch_ops_concurrent(fork, join)
             else:
-                for fn in self.op_fns().values():
-                    fn()
+                for op in self.SERIAL_ORDERS[schedule]:
+                    fns[op]()
         torch.cuda.synchronize()
         self.graphs = getattr(self, "graphs", {})
         self.graphs[schedule] = g
         self.graph, self.schedule = g, schedule
 
     def choose_schedule(self, trials: int = 5) -> dict:
-        """Times both captured schedules (L2 flushed, median of `trials`) and keeps the faster for
+        """Times the captured schedules (L2 flushed, median of `trials`) and keeps the fastest for
         the timed region: the 4-stream DAG overlaps the small launches of an expert-group shard,
         while at the whole-layer size every launch already fills the GPU and running them side by
-        side only makes them contend."""
+        side only makes them contend (there, a serial order that transposes each tensor right after
+        it is written also reads its tail from L2)."""
         med = {}
-        for name in ("dag", "serial"):
+        for name in ("dag", "serial", "serial_reuse"):
             self.capture_graph(name)
             med[name] = statistics.median(self.timed_step_graph() for _ in range(trials))
         best = min(med, key=med.get)
@@ -1149,7 +1157,7 @@ def main():
                 "timing": "CUDA events; the step captured once into a CUDA graph and replayed behind a spin "
                           "kernel each step, as the faster of two schedules timed in warm-up (schedule_trial_ms): "
                           "the dependency DAG on 4 streams (plan->move->A2(X) | A1,A1 | A5->A2(A) | A4) or the 8 "
-                          "launches serially on one stream; per-op breakdown from the same steps launched serially "
+                          "launches serially on one stream in two orders; per-op breakdown from the same steps launched serially "
                           "with events between the kernels (ops.*.us), and each op's marginal cold-L2 cost "
                           "(ops.*.marginal_us: K x [flush, op] minus K x [flush])",
                 "schedule": ds.schedule, "schedule_trial_ms": trial_ms,

@@ -7,13 +7,14 @@
 //     T_max = max_i T[i][jb];  sT_e[ib][j] = T_max;  qT_e[j][i-o] = shift(q[i][j], T_max - T[i][jb])
 //
 // Kernel design (sm_100a, HBM-bound, 2.016 B/element):
-//   * persistent CTAs (3 per SM; 2 when there are >= 64 tiles per SM) of 8 consumer warps and one
-//     producer warp, static round-robin over the 128x128 tiles of all segments in segment-major
-//     order (tile_coord below); the segment tables are built in shared memory from the DEVICE
-//     segment offsets (no host sync: CUDA-graph capturable).
+//   * persistent CTAs, warp-specialised: 8 consumer warps (shift + transpose), 2-4 store warps
+//     (read-out + global stores) and one producer warp; below 64 tiles per SM 3 CTAs per SM with
+//     2 TMA stages and 2 store warps, above 2 CTAs per SM with 3 stages and 4 store warps.  Tiles
+//     are walked in segment-major order (tile_coord below); the segment tables are built in shared
+//     memory from the DEVICE segment offsets (no host sync: CUDA-graph capturable).
 //   * producer (one lane): per tile its coordinates, the 16 KB code tile by TMA (one 128x128 box,
 //     or 16-row boxes for a segment's partial last block, so no bytes of the next segment are
-//     read) and the block's run of row scales by a 1D bulk copy, all on one mbarrier of a 3-stage
+//     read) and the block's run of row scales by a 1D bulk copy, all on one mbarrier of the stage
 //     ring; it refills a stage as soon as every consumer warp has copied it to registers.
 //   * T_max per block: each warp max-reduces the staged scale run itself (redux.sync), no barrier.
 //   * thread (g, c) owns rows 4g..4g+3 x bytes 16c..16c+15: 4 conflict-free LDS.128 (8 threads of
@@ -21,9 +22,10 @@
 //     hardware e4m3x2 -> f16x2 decode, one HMUL2 by 2^-k, one RNE back, 8 instructions per 4
 //     codes) is applied to whole 32-bit words (4 codes of one row share k), then 4x4 byte blocks
 //     are transposed with PRMT.
-//   * the transposed words go to a 16 KB staging buffer with a 16-byte-chunk XOR swizzle
-//     (chunk ^= j/16) that makes both the 32-bit writes and the 128-bit read-out conflict-free, and
-//     leave as coalesced 128-bit stores (each output row's 128 bytes = one full line).
+//   * the transposed words go to one of two 16 KB staging buffers with a 16-byte-chunk XOR swizzle
+//     (chunk ^= j/16) that makes both the 32-bit writes and the 128-bit read-out conflict-free; the
+//     store warps drain a buffer (coalesced 128-bit stores, each output row's 128 bytes one full
+//     line) while the consumers fill the other -- handed over on mbarriers, no CTA-wide barrier.
 #include <cuda.h>
 
 #include "async.cuh"
@@ -34,9 +36,11 @@
 namespace fp8flow {
 
 // <STAGES, OUTBUF>: TMA stages of the input ring and staging buffers for the transposed tile
-// (r02 sweep, profiles/r02_a2_order_window.txt: 3 stages x 1 buffer)
-constexpr int kTConsumers = 256;              // 8 consumer warps
-constexpr int kTThreads = kTConsumers + 32;   // + 1 producer warp
+constexpr int kTConsumers = 256;              // 8 consumer (shift + transpose) warps
+constexpr int kMaxThreadsA2 = kTConsumers + 32 * 4 + 32;
+constexpr int kPrefixThreads = 288;             // 4 segments per thread: covers offsets[0..1024]
+template <int WS>
+__host__ __device__ constexpr int a2_threads() { return kTConsumers + 32 * WS + 32; }  // + WS store warps + 1 producer
 constexpr int kMaxSegs = 1024;
 constexpr int kTileBytes = kTile * kTile;
 constexpr int kRowGroup = 8;                  // row blocks of a segment walked together (tile order)
@@ -55,10 +59,13 @@ struct TransposeSmem {
   uint32_t sc[STAGES][kTile / 4];  // the 128 row-scale bytes of each staged tile
   uint32_t out[OUTBUF][kTile * kTile / 4];
   TileCoord tc[STAGES];            // coordinates of the staged tile (written by the producer)
+  TileCoord out_tc[OUTBUF];        // coordinates (pad[0] = T_max) of the tile in each staging buffer
   uint64_t full_bar[STAGES];
   uint64_t empty_bar[STAGES];
+  uint64_t out_full[OUTBUF];       // store-warp mode: staging buffer written / drained
+  uint64_t out_empty[OUTBUF];
   uint32_t mult[33];               // f16x2 multiplier 2^-k for k = 0..32
-  uint32_t red[kTThreads / 32];
+  uint32_t red[kMaxThreadsA2 / 32];
   int32_t total_rb;
   // followed in dynamic shared memory by seg_off[num_segs + 1] and blk_prefix[num_segs + 1]
 };
@@ -101,8 +108,11 @@ __device__ __forceinline__ TileCoord tile_coord(const SegTables& sm, int nsegs, 
   return c;
 }
 
-template <int STAGES, int OUTBUF, int MINB>
-__global__ void __launch_bounds__(kTThreads, MINB)
+// WS > 0 (store-warp mode, OUTBUF == 2): WS extra warps drain the staging buffers (read-out and
+// global stores) while the 8 consumer warps shift and transpose the next tile; buffers are handed
+// over on out_full / out_empty mbarriers instead of consumer-wide barriers.
+template <int STAGES, int OUTBUF, int MINB, int WS>
+__global__ void __launch_bounds__(a2_threads<WS>(), MINB)
     scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q,
                                    const __grid_constant__ CUtensorMap tmap_q16, const uint8_t* __restrict__ s,
                                    int64_t ld_s, int64_t rows, int64_t cols, const int32_t* __restrict__ seg_offsets,
@@ -118,10 +128,17 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   int32_t* blk_prefix = seg_off + nsegs + 1;
   const SegTables segt{seg_off, blk_prefix};
 
+  static_assert(WS > 0 && OUTBUF == 2, "store warps drain a double staging buffer");
+  constexpr int kThreads = a2_threads<WS>();
+  constexpr int kProducerWarp = kTConsumers / 32 + WS;
   if (tid == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&sm.full_bar[i], 1);
       mbar_init(&sm.empty_bar[i], kTConsumers / 32);
+    }
+    for (int i = 0; i < OUTBUF; ++i) {
+      mbar_init(&sm.out_full[i], kTConsumers / 32);
+      mbar_init(&sm.out_empty[i], WS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -129,7 +146,7 @@ __global__ void __launch_bounds__(kTThreads, MINB)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_q16)) : "memory");
   }
   if (tid <= 32) sm.mult[tid] = shift_multiplier(static_cast<uint32_t>(tid));
-  load_segments<kTThreads>(seg_off, blk_prefix, sm.red, &sm.total_rb, seg_offsets, nsegs, rows);  // (+ barrier)
+  load_segments<kThreads>(seg_off, blk_prefix, sm.red, &sm.total_rb, seg_offsets, nsegs, rows);  // (+ barrier)
 
   const int n_jb = static_cast<int>(cols / kTile);
   const int total_tiles = sm.total_rb * n_jb;  // < 2^31 (rows < 2^31, checked by the ABI)
@@ -137,7 +154,35 @@ __global__ void __launch_bounds__(kTThreads, MINB)
   const int stride = gridDim.x;
   const int n_local = first < total_tiles ? (total_tiles - first + stride - 1) / stride : 0;
 
-  if (warp == kTConsumers / 32) {
+  if (warp >= kTConsumers / 32 && warp < kProducerWarp) {
+    // ---- store warps: drain staging buffer b of tile i (coalesced 128-bit stores, 16 bytes per
+    // thread per output-row chunk), then hand it back
+    const int st_tid = tid - kTConsumers;
+    const int c8 = st_tid & 7;
+    for (int i = 0; i < n_local; ++i) {
+      const int b = i & 1;
+      mbar_wait(&sm.out_full[b], (i >> 1) & 1);
+      const TileCoord tc = sm.out_tc[b];
+      const uint32_t* out = sm.out[b];
+      uint8_t* qTe = qT + cols * static_cast<int64_t>(tc.o);
+      if (16 * c8 < tc.rows_valid) {
+#pragma unroll 4
+        for (int j = st_tid >> 3; j < kTile; j += 4 * WS) {
+          const int phys = c8 ^ ((j >> 4) & 7);
+          const uint4 o4 = *reinterpret_cast<const uint4*>(&out[j * 32 + 4 * phys]);
+          st_v4(qTe + (static_cast<int64_t>(tc.jb) * kTile + j) * tc.m + tc.ib * kTile + 16 * c8, o4);
+        }
+      }
+      if (st_tid < 8) {
+        const uint32_t b4 = static_cast<uint32_t>(tc.pad[0]) * 0x01010101u;
+        st_v4(sT + static_cast<int64_t>(tc.rb) * cols + tc.jb * kTile + 16 * st_tid, make_uint4(b4, b4, b4, b4));
+      }
+      __syncwarp();
+      if ((st_tid & 31) == 0) mbar_arrive(&sm.out_empty[b]);
+    }
+    return;
+  }
+  if (warp == kProducerWarp) {
     // ---- producer warp (lane 0): tile i of this CTA is t = first + i * stride.  The code tile
     // arrives by TMA -- one 128x128 box, or rows_valid/16 boxes of 16 rows for the partial last
     // block of a segment (no bytes of the next segment are read) -- and its run of row scales by
@@ -204,8 +249,8 @@ __global__ void __launch_bounds__(kTThreads, MINB)
     }
     // ---- 4x4 byte transposes into the swizzled staging buffer ----------------------------------
     const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
-    uint32_t* out = sm.out[OUTBUF == 2 ? (i & 1) : 0];
-    if (OUTBUF == 1 && i > 0) named_barrier_sync(1, kTConsumers);  // previous read-out complete
+    uint32_t* out = sm.out[i & 1];
+    if (i >= 2) mbar_wait(&sm.out_empty[i & 1], ((i >> 1) - 1) & 1);  // drained by the store warps
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
@@ -218,48 +263,34 @@ __global__ void __launch_bounds__(kTThreads, MINB)
       out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
       out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
     }
-    named_barrier_sync(1, kTConsumers);  // staging buffer complete
-
-    // ---- coalesced 128-bit read-out: 8 threads per output row --------------------------------
-    uint8_t* qTe = qT + cols * static_cast<int64_t>(tc.o);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int j = (tid >> 3) + 32 * it;
-      if (16 * c < tc.rows_valid) {
-        const int phys = c ^ ((j >> 4) & 7);
-        const uint4 o4 = *reinterpret_cast<const uint4*>(&out[j * 32 + 4 * phys]);
-        st_v4(qTe + (static_cast<int64_t>(tc.jb) * kTile + j) * tc.m + tc.ib * kTile + 16 * c, o4);
-      }
+    // hand the buffer (and the tile's coordinates) to the store warps
+    if (tid == 0) {
+      TileCoord o = tc;
+      o.pad[0] = static_cast<int32_t>(tmax);
+      sm.out_tc[i & 1] = o;
     }
-    if (tid < 8) {
-      const uint32_t b4 = tmax * 0x01010101u;
-      st_v4(sT + static_cast<int64_t>(tc.rb) * cols + tc.jb * kTile + 16 * tid, make_uint4(b4, b4, b4, b4));
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.out_full[i & 1]);
   }
 }
 
 // ---------------------------------------------------------------------------------------------
 // host side: tensor map + launch
 // ---------------------------------------------------------------------------------------------
-constexpr int kTStagesA2 = 3, kTOutBufA2 = 1, kTMinBlocksA2 = 3;  // 3 CTAs/SM (r01 sweep of 2-4 stages)
-template <int S, int O, int B>
+template <int S, int O, int B, int WS>
 static cudaError_t launch_a2v(const CUtensorMap& map, const CUtensorMap& map16, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
                               const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
                               cudaStream_t stream, int num_sms, int64_t ub_tiles) {
   static KernelSetup setup;
-  auto kernel = scaling_aware_transpose_kernel<S, O, B>;
+  auto kernel = scaling_aware_transpose_kernel<S, O, B, WS>;
+  constexpr int kThreads = a2_threads<WS>();
   const size_t smem = a2_smem_bytes<TransposeSmem<S, O>>(seg_offsets ? num_segs : 1);
-  if (prepare_kernel(setup, kernel, kTThreads, a2_smem_bytes<TransposeSmem<S, O>>(kMaxSegs), smem) == 0)
+  if (prepare_kernel(setup, kernel, kThreads, a2_smem_bytes<TransposeSmem<S, O>>(kMaxSegs), smem) == 0)
     return cudaErrorInvalidValue;
   int occ = 0;  // occupancy at this launch's shared memory (the segment tables vary with num_segs)
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kTThreads, smem) != cudaSuccess || occ < 1) occ = 1;
-  // Tiles held at once = SMs x CTAs x stages.  Launches with many tiles per SM stream better with a
-  // smaller window (fewer DRAM pages open at once): whole-layer X_perm 462 -> 364 us with 2 CTAs
-  // per SM instead of 3; mid-size launches (~12 tiles per SM) need the deeper window to ramp up
-  // (profiles/r02_a2_order_window.txt).
-  if (ub_tiles >= 64LL * num_sms && occ > 2) occ = 2;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
   const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
-  kernel<<<static_cast<unsigned>(grid), kTThreads, smem, stream>>>(
+  kernel<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
       map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
   return cudaGetLastError();
 }
@@ -274,8 +305,14 @@ cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, i
                  static_cast<uint64_t>(cols), kTile, 16))
     return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  return launch_a2v<kTStagesA2, kTOutBufA2, kTMinBlocksA2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT,
-                                                         stream, num_sms, ub_tiles);
+  // Tiles held at once = SMs x CTAs x stages.  Launches with many tiles per SM stream better with a
+  // small window (fewer DRAM pages open at once) and more store warps; mid-size launches (~12 tiles
+  // per SM) need 3 CTAs per SM to ramp up (profiles/r02_a2_order_window.txt).
+  if (ub_tiles >= 64LL * num_sms)
+    return launch_a2v<3, 2, 2, 4>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                  ub_tiles);
+  return launch_a2v<2, 2, 3, 2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                ub_tiles);
 }
 
 // =============================================================================================
@@ -285,7 +322,7 @@ cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, i
 __global__ void seg_prefix_kernel(const int32_t* __restrict__ seg_offsets, int32_t num_segs, int64_t rows,
                                   int32_t* __restrict__ seg_out, int32_t* __restrict__ blk_prefix) {
   __shared__ int32_t so[kMaxSegs + 1];
-  __shared__ uint32_t red[kTThreads / 32];
+  __shared__ uint32_t red[kPrefixThreads / 32];
   __shared__ int total;
   const int tid = threadIdx.x;
   const int nsegs = seg_offsets == nullptr ? 1 : num_segs;
@@ -295,7 +332,7 @@ __global__ void seg_prefix_kernel(const int32_t* __restrict__ seg_offsets, int32
       so[1] = static_cast<int32_t>(rows);
     }
   } else {
-    for (int i = tid; i <= nsegs; i += kTThreads) so[i] = seg_offsets[i];
+    for (int i = tid; i <= nsegs; i += kPrefixThreads) so[i] = seg_offsets[i];
   }
   __syncthreads();
   int nb[4], tsum = 0;
@@ -305,7 +342,7 @@ __global__ void seg_prefix_kernel(const int32_t* __restrict__ seg_offsets, int32
     nb[i] = e < nsegs ? (so[e + 1] - so[e] + kTile - 1) / kTile : 0;
     tsum += nb[i];
   }
-  int run = block_exclusive_scan<kTThreads>(tsum, red, &total);
+  int run = block_exclusive_scan<kPrefixThreads>(tsum, red, &total);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int e = tid * 4 + i;
@@ -489,7 +526,7 @@ cudaError_t launch_naive_transpose(const uint8_t* q, const uint8_t* s, int64_t l
   size_t off = (2 * 4 * static_cast<size_t>(nsegs + 1) + 255) / 256 * 256;
   __nv_bfloat16* xd = reinterpret_cast<__nv_bfloat16*>(base + off);
   __nv_bfloat16* xT = xd + rows * cols;
-  seg_prefix_kernel<<<1, kTThreads, 0, stream>>>(seg_offsets, num_segs, rows, seg_out, blk_prefix);
+  seg_prefix_kernel<<<1, kPrefixThreads, 0, stream>>>(seg_offsets, num_segs, rows, seg_out, blk_prefix);
   const int64_t n16 = rows * cols / 16;
   const int64_t g1 = (n16 + 256 * kNaiveU - 1) / (256 * kNaiveU);
   if (g1 > 0)
