@@ -303,6 +303,18 @@ class DeviceStep:
         with torch.cuda.graph(g):
             if schedule == "dag":
                 self.launch_ops_concurrent(fork, join)
+            elif schedule == "serial_plan_overlap":
+                # the plan (one small cooperative launch, latency-bound) beside A1(x); the rest serial
+                main, side = torch.cuda.current_stream(), self.side[0]
+                fork.record(main)
+                side.wait_event(fork)
+                with torch.cuda.stream(side):
+                    fns["A1_quantize_x"]()
+                join.record(side)
+                fns["A3_plan"]()
+                main.wait_event(join)
+                for op in OPS[2:]:
+                    fns[op]()
             else:
                 for op in self.SERIAL_ORDERS[schedule]:
                     fns[op]()
@@ -318,7 +330,7 @@ class DeviceStep:
         side only makes them contend (there, a serial order that transposes each tensor right after
         it is written also reads its tail from L2)."""
         med = {}
-        for name in ("dag", "serial", "serial_reuse"):
+        for name in ("dag", "serial", "serial_reuse", "serial_plan_overlap"):
             self.capture_graph(name)
             med[name] = statistics.median(self.timed_step_graph() for _ in range(trials))
         best = min(med, key=med.get)
@@ -1157,7 +1169,7 @@ def main():
                 "timing": "CUDA events; the step captured once into a CUDA graph and replayed behind a spin "
                           "kernel each step, as the faster of two schedules timed in warm-up (schedule_trial_ms): "
                           "the dependency DAG on 4 streams (plan->move->A2(X) | A1,A1 | A5->A2(A) | A4) or the 8 "
-                          "launches serially on one stream in two orders; per-op breakdown from the same steps launched serially "
+                          "launches serially on one stream in two orders, or serially with the plan beside A1(x); per-op breakdown from the same steps launched serially "
                           "with events between the kernels (ops.*.us), and each op's marginal cold-L2 cost "
                           "(ops.*.marginal_us: K x [flush, op] minus K x [flush])",
                 "schedule": ds.schedule, "schedule_trial_ms": trial_ms,
