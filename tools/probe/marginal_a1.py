@@ -32,7 +32,7 @@ for rows, cols in [(2048, 7168), (4096, 7168), (16384, 7168), (65536, 7168)]:
     nb = RL.quantize_bytes(rows, cols)
     line = []
     for v in sys.argv[1:]:
-        os.environ["A1X"] = v
+        os.environ["A1H"] = v
         t = marginal(lambda: F.fp8flow_quantize_rowwise(x, q, s), K=20 if rows < 60000 else 6)
         line.append(f"v{v} {t:.2f}us {nb/t*1e-3/peak:.3f}")
     print(rows, cols, " | ".join(line), flush=True)
