@@ -1322,15 +1322,18 @@ def ncu_traffic(kernel_op: str):
 
 
 def oracle_sample(O, frac: float, threads: int | None, rank: int = 0, world: int = 1, mode: str = "strong"):
-    """Runs the oracle module O on a bounded, host-generated sample (fraction `frac` of the rank's
-    rows, same recipe and shapes as the step) of one rank's step.  Returns (algorithmic bytes,
-    seconds, description).  Used by the reference arm, which must not need a GPU."""
+    """Runs the oracle module O on a bounded, host-generated sample of one rank's step: the first
+    `frac` of its experts with ALL of their routed tokens (so per-expert row counts and padding are
+    the workload's), and `frac` of its entry-cast token shard; same recipe and shapes as the step.
+    Returns (algorithmic bytes, seconds, description).  Used by the reference arm, which must not
+    need a GPU."""
     sh = D.shard(rank, world, mode, N_EXPERTS, T_GLOBAL)
-    e0, E_loc = sh["expert_begin"], sh["num_local_experts"]
+    e0, E_all = sh["expert_begin"], sh["num_local_experts"]
+    E_loc = max(1, int(round(E_all * frac)))
     idx, probs = synth.routing(T_GLOBAL, synth.BASE_SEED)
     rs = synth.expert_range_shard(idx, probs, e0, E_loc)
-    n_tok = max(16, int(len(rs.recv_tokens) * frac))
-    topk, pr = rs.topk_idx[:n_tok], rs.probs[:n_tok]
+    n_tok = len(rs.recv_tokens)
+    topk, pr = rs.topk_idx, rs.probs
     counts = np.array([np.sum(topk == e0 + e) for e in range(E_loc)])
     padded = (counts + ALIGN - 1) // ALIGN * ALIGN
     R_s = int(padded.sum())
@@ -1355,9 +1358,9 @@ def oracle_sample(O, frac: float, threads: int | None, rank: int = 0, world: int
               + RL.permute_move_bytes(n_tok, R_s, HIDDEN) + RL.swiglu_quant_bytes(R_s, FFN)
               + RL.unpermute_bytes(int(counts.sum()), n_tok, TOP_K, HIDDEN, True)
               + RL.transpose_bytes([int(p) for p in padded], HIDDEN) + RL.transpose_bytes([int(p) for p in padded], FFN))
-    desc = (f"oracle (plain C) on {frac:.4g} of rank {rank}'s step ({mode} partition, {world} rank(s)): A1 "
-            f"{n_sh}x{HIDDEN} x2, A3 plan+move {n_tok} tokens -> {R_s} rows, A5 {R_s}x{2 * FFN}, A4 {n_tok} "
-            f"tokens, A2 {R_s}x{HIDDEN} + {R_s}x{FFN}")
+    desc = (f"oracle (plain C) on {E_loc} of rank {rank}'s {E_all} experts with all their tokens and {frac:.4g} of its "
+            f"token shard ({mode} partition, {world} rank(s)): A1 {n_sh}x{HIDDEN} x2, A3 plan+move {n_tok} tokens "
+            f"-> {R_s} rows, A5 {R_s}x{2 * FFN}, A4 {n_tok} tokens, A2 {R_s}x{HIDDEN} + {R_s}x{FFN}")
     return nbytes, dt, desc
 
 
@@ -1368,7 +1371,7 @@ def run_reference(args, rank, world, cfg):
         return
     import oracle as O  # the reference arm IS the oracle (tier framing)
 
-    frac = 1.0 / 64 if args.partition == "strong" and world == 1 else 1.0 / 8
+    frac = 1.0 / 32 if args.partition == "strong" and world == 1 else 1.0 / 8
     for _ in range(args.warmup):
         oracle_sample(O, frac, None, 0, world, args.partition)
     nb, ts, desc = 0.0, 0.0, ""
