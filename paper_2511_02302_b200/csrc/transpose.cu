@@ -134,11 +134,11 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
   if (tid == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&sm.full_bar[i], 1);
-      mbar_init(&sm.empty_bar[i], kTConsumers / 32);
+      mbar_init(&sm.empty_bar[i], kTConsumers);
     }
-    for (int i = 0; i < OUTBUF; ++i) {
-      mbar_init(&sm.out_full[i], kTConsumers / 32);
-      mbar_init(&sm.out_empty[i], WS);
+    for (int i = 0; i < OUTBUF; ++i) {  // every thread arrives: each releases its own accesses
+      mbar_init(&sm.out_full[i], kTConsumers);
+      mbar_init(&sm.out_empty[i], 32 * WS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -177,8 +177,7 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
         const uint32_t b4 = static_cast<uint32_t>(tc.pad[0]) * 0x01010101u;
         st_v4(sT + static_cast<int64_t>(tc.rb) * cols + tc.jb * kTile + 16 * st_tid, make_uint4(b4, b4, b4, b4));
       }
-      __syncwarp();
-      if ((st_tid & 31) == 0) mbar_arrive(&sm.out_empty[b]);
+      mbar_arrive(&sm.out_empty[b]);
     }
     return;
   }
@@ -231,8 +230,7 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
     uint4 v[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty_bar[st]);  // this warp is done with the stage
+    mbar_arrive(&sm.empty_bar[st]);  // this thread is done with the stage (scales, coordinates, codes)
     uint32_t R[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -269,8 +267,8 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
       o.pad[0] = static_cast<int32_t>(tmax);
       sm.out_tc[i & 1] = o;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.out_full[i & 1]);
+    __syncwarp();  // (tid 0's out_tc write above, before warp 0's arrivals)
+    mbar_arrive(&sm.out_full[i & 1]);
   }
 }
 
