@@ -56,7 +56,7 @@ for rows, cols, nseg in shapes:
     line = []
     ref = None
     for v in sys.argv[1:]:
-        os.environ["A2X"], os.environ["A2C"] = (v.split(":") + ["0"])[:2]
+        os.environ["A2R"] = v
         fn = lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT, seg_offsets=seg_t)
         t = marginal(fn, K=20 if rows < 60000 else 6)
         fn(); torch.cuda.synchronize()
