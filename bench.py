@@ -1219,6 +1219,8 @@ def main():
                          "algorithmic_bytes_per_launch": op_bytes[dom]},
             "ops": ops, "cpu_baseline": merged.get("cpu_baseline"), "e2e": e2e,
             "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+            "build": {"library": "paper_2511_02302_b200/libfp8flow.so", "target": ds.F.fp8flow_build_target(),
+                      "source_hash": ds.F.fp8flow_source_hash()},
             "parity": merged["parity"] if world > 1 else merged["parity"]["rank0"],
             "parity_all_ranks": merged["parity_all_ranks"], "checksums_match": merged["checksums_match"],
         }

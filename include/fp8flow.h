@@ -72,6 +72,9 @@ FP8FLOW_API int fp8flow_last_cuda_error(void);
 /* Library version (major*10000 + minor*100 + patch) and the compiled target ("sm_100a"). */
 FP8FLOW_API int fp8flow_version(void);
 FP8FLOW_API const char* fp8flow_build_target(void);
+/* sha256 prefix (16 hex digits) of the sources the library was compiled from (build.py); the Python
+ * binding refuses a library whose hash differs from the sources next to it (a stale binary). */
+FP8FLOW_API const char* fp8flow_source_hash(void);
 /* FP8FLOW_OK if the current CUDA device is sm_100, else FP8FLOW_ERR_ARCH / FP8FLOW_ERR_CUDA. */
 FP8FLOW_API int fp8flow_device_check(void);
 

@@ -23,13 +23,30 @@ def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def source_files() -> list[str]:
+    """Every file the library is built from (kernels, headers, the C ABI header)."""
+    return sorted(sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                  + [os.path.join(os.path.dirname(PKG), "include", "fp8flow.h")])
+
+
+def source_hash() -> str:
+    """sha256 (first 16 hex digits) over the library's source files' names and bytes: compiled into
+    the library (fp8flow_source_hash) so a stale binary is detected at load time."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in source_files():
+        h.update(os.path.relpath(f, os.path.dirname(PKG)).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
-    deps.append(os.path.join(os.path.dirname(PKG), "include", "fp8flow.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+    return any(os.path.getmtime(d) > t for d in source_files())
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
@@ -39,9 +56,10 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    hash_flag = f"-DFP8FLOW_SOURCE_HASH=\"{source_hash()}\""
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *NVCC_FLAGS, hash_flag, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))

@@ -91,6 +91,10 @@ const char* fp8flow_status_string(int status) {
 int fp8flow_last_cuda_error(void) { return g_last_cuda_error; }
 int fp8flow_version(void) { return 100; }  // 0.1.0
 const char* fp8flow_build_target(void) { return "sm_100a"; }
+#ifndef FP8FLOW_SOURCE_HASH
+#define FP8FLOW_SOURCE_HASH "unknown"
+#endif
+const char* fp8flow_source_hash(void) { return FP8FLOW_SOURCE_HASH; }
 
 int fp8flow_device_check(void) {
   int sms = 0;

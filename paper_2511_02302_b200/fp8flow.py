@@ -31,6 +31,7 @@ SIGNATURES = {
     "fp8flow_last_cuda_error": (ctypes.c_int, []),
     "fp8flow_version": (ctypes.c_int, []),
     "fp8flow_build_target": (ctypes.c_char_p, []),
+    "fp8flow_source_hash": (ctypes.c_char_p, []),
     "fp8flow_device_check": (ctypes.c_int, []),
     "fp8flow_quantize_rowwise": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _I64, _P]),
     "fp8flow_scaling_aware_transpose": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I32, _P, _P, _P]),
@@ -77,6 +78,12 @@ def lib() -> ctypes.CDLL:
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        from . import build as _build
+
+        built, current = L.fp8flow_source_hash().decode(), _build.source_hash()
+        if built != current:
+            raise Fp8FlowError(f"{LIB_PATH} was built from other sources (hash {built}, sources {current}): "
+                               "rebuild with `python -c 'import __graft_entry__ as g; g.build()'`")
         _lib = L
     return _lib
 
@@ -130,6 +137,10 @@ def fp8flow_version() -> int:
 
 def fp8flow_build_target() -> str:
     return lib().fp8flow_build_target().decode()
+
+
+def fp8flow_source_hash() -> str:
+    return lib().fp8flow_source_hash().decode()
 
 
 # ----------------------------------------------------------------------------------- A1

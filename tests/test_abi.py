@@ -210,4 +210,18 @@ def test_product_library_has_no_environment_knobs():
         txt = open(os.path.join(csrc, f)).read()
         assert "getenv" not in txt and "FP8FLOW_" not in txt.replace("FP8FLOW_OK", "").replace(
             "FP8FLOW_ERR_", "").replace("FP8FLOW_DISPATCH_", "").replace("FP8FLOW_MAX_RANKS", "").replace(
-            "FP8FLOW_IPC_HANDLE_BYTES", "").replace("FP8FLOW_UNKNOWN_STATUS", ""), f
+            "FP8FLOW_IPC_HANDLE_BYTES", "").replace("FP8FLOW_UNKNOWN_STATUS", "").replace(
+            "FP8FLOW_SOURCE_HASH", ""), f
+
+
+def test_stale_library_is_refused(monkeypatch):
+    """Build provenance: the library carries the hash of the sources it was compiled from; the
+    binding refuses to load a library whose hash differs from the sources next to it."""
+    from paper_2511_02302_b200 import build as B
+    from paper_2511_02302_b200 import fp8flow
+
+    assert fp8flow.lib().fp8flow_source_hash().decode() == B.source_hash()
+    monkeypatch.setattr(fp8flow, "_lib", None)
+    monkeypatch.setattr(B, "source_hash", lambda: "0000000000000000")
+    with pytest.raises(fp8flow.Fp8FlowError, match="built from other sources"):
+        fp8flow.lib()
