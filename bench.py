@@ -81,6 +81,10 @@ class Workload:
         self.e0, self.E_loc = sh["expert_begin"], sh["num_local_experts"]
         self.t0, self.t1 = sh["token_begin"], sh["token_end"]
         idx, probs = synth.routing(T_GLOBAL, synth.BASE_SEED)
+        if mode == "balanced":   # expert placement by load (relabelled ids, D.balanced_relabel)
+            counts = np.bincount(idx.numpy().ravel(), minlength=N_EXPERTS)
+            new_id = torch.tensor(D.balanced_relabel(counts, world), dtype=torch.int32)
+            idx = new_id[idx.long()].contiguous()
         rs = synth.expert_range_shard(idx, probs, self.e0, self.E_loc)
         self.recv = rs.recv_tokens
         self.topk_idx, self.probs = rs.topk_idx, rs.probs     # [T_recv, 8] int32 / fp32
@@ -1076,8 +1080,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--partition", choices=["strong", "weak"], default="strong",
-                    help="strong: the layer's 256 experts split over the GPUs (N=1: whole layer); "
+    ap.add_argument("--partition", choices=["strong", "balanced", "weak"], default="strong",
+                    help="strong: the layer's 256 experts split over the GPUs in id ranges (N=1: whole layer); "
+                         "balanced: 256/N experts per GPU placed by load (LPT); "
                          "weak: one EP8 expert group (32 experts) per GPU")
     ap.add_argument("--no-verify", action="store_true", help="skip the whole-step oracle comparison")
     ap.add_argument("--no-e2e", action="store_true")
@@ -1085,6 +1090,9 @@ def main():
     ap.add_argument("--no-next", action="store_true", help="skip the cfg-2 and NEXT-row sub-measurements")
     ap.add_argument("--no-ep", action="store_true", help="skip the N>1 NEXT-3 dispatch/combine measurement")
     ap.add_argument("--sweep", action="store_true", help="config 5: transpose vs naive bandwidth sweep (one JSON line)")
+    ap.add_argument("--emulate-scaling", action="store_true",
+                    help="time every rank's workload of N = 1, 2, 4, 8 on this one GPU, one rank after the other "
+                         "(valid because the step has no exchange): the N-GPU step time is the max over ranks")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
 
@@ -1094,14 +1102,15 @@ def main():
         if args.gpus > 1 and world == 1:
             sys.exit(2)
     sh = D.shard(rank, world, args.partition, N_EXPERTS, T_GLOBAL)
-    scope = ("whole layer, 256 experts" if world == 1 else f"{N_EXPERTS // world} of 256 experts per GPU") \
-        if args.partition == "strong" else "one EP8 expert group (32 of 256 experts) per GPU"
+    scope = ("whole layer, 256 experts" if world == 1 else f"{N_EXPERTS // world} of 256 experts per GPU"
+             + (" placed by load" if args.partition == "balanced" else "")) \
+        if args.partition in ("strong", "balanced") else "one EP8 expert group (32 of 256 experts) per GPU"
     cfg = {"workload": f"DeepSeek-V3 MoE layer hot path, {scope} ({args.partition} partition), "
                        f"{T_GLOBAL} tokens top-8, hidden 7168, expert FFN 2x2048: A1 x2, A3 plan+move, A5, A4, A2 x2",
            "partition": args.partition, "tokens": T_GLOBAL, "hidden": HIDDEN, "ffn": FFN, "experts": N_EXPERTS,
            "top_k": TOP_K, "local_experts": sh["num_local_experts"], "align": ALIGN,
            "routing": "DSv3 group-limited top-8, skewed expert bias N(0,1) + Gumbel, seed 2511023020",
-           "parallelism": f"ep{world} ({'strong: experts split' if args.partition == 'strong' else 'weak: one expert group per GPU'})"}
+           "parallelism": f"ep{world} ({dict(strong='strong: experts split in id ranges', balanced='strong: experts placed by load (LPT)', weak='weak: one expert group per GPU')[args.partition]})"}
 
     if args.impl == "reference":
         run_reference(args, rank, world, cfg)
@@ -1117,6 +1126,11 @@ def main():
             print(json.dumps({"sweep": "config 5: scaling-aware transpose vs naive dequant->transpose->requant",
                               "n_gpus": world, "scaling": "weak (same shape per GPU)", "peak_gbs": peaks["hbm_gbs"],
                               "peak_source": peaks["source"], "l2": "flushed before each launch", "rows": rows}))
+        D.barrier(device)
+        return
+    if args.emulate_scaling:
+        if rank == 0:
+            print(json.dumps(emulate_scaling(device, args)), flush=True)
         D.barrier(device)
         return
     wl = Workload(rank, world, args.partition, device)
@@ -1206,7 +1220,7 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_total_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong" if args.partition == "strong" else "weak", "vs_baseline": None, "dtype": "e4m3",
+            "scaling": "weak" if args.partition == "weak" else "strong", "vs_baseline": None, "dtype": "e4m3",
             "dtypes": {"codes": "e4m3 (u8)", "scales": "ue8m0 (u8)", "bf16_io": "bf16", "math": "fp32 (fp64 refine)"},
             "data": "synthetic (seeded, drawn on the device; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
             "frac_of_hbm_peak": round(value / world / peak, 3),
@@ -1234,6 +1248,49 @@ def main():
     D.barrier(device)
     if D.dist.is_initialized():
         D.dist.destroy_process_group()
+
+
+def emulate_scaling(device, args) -> dict:
+    """The N-GPU step of the chosen partition, emulated on this one GPU: every rank's workload
+    (experts, received tokens, padded rows of that rank) is built and timed alone, one rank after
+    the other, exactly as bench.py times a rank (graph replay of the faster schedule, L2 flushed,
+    K steps).  The hot path has no exchange step, so an N-GPU run's step time is the max over these
+    per-rank times and its value = all ranks' bytes / that max (identical GPUs assumed; NVLink and
+    the post-timing collectives are not involved).  Outputs are verified per rank like the real run
+    (checksums only: the oracle comparison is bench.py's normal leg)."""
+    peak = RL.measured_peaks(ROOT)["hbm_gbs"]
+    out = {"what": "per-rank step times of N = 1, 2, 4, 8 emulated on one B200, one rank after the other; "
+                   "value = sum of the ranks' algorithmic bytes / max over ranks of the step time",
+           "partition": args.partition, "peak_gbs": peak, "steps": args.steps, "curve": []}
+    for n in (1, 2, 4, 8):
+        ranks = []
+        for r in range(n):
+            wl = Workload(r, n, args.partition, device)
+            ds = DeviceStep(wl)
+            for _ in range(args.warmup):
+                ds.timed_step_concurrent()
+            trial = ds.choose_schedule()
+            for _ in range(args.warmup):
+                ds.timed_step_graph()
+            ms = statistics.mean(ds.timed_step_graph() for _ in range(args.steps))
+            nb = sum(wl.op_bytes().values())
+            ranks.append({"rank": r, "experts": [wl.e0, wl.e0 + wl.E_loc], "rows": wl.R, "recv_tokens": wl.T_recv,
+                          "bytes": nb, "ms": round(ms, 4), "gbs": round(nb / ms / 1e6, 1), "schedule": ds.schedule,
+                          "schedule_trial_ms": trial})
+            del ds, wl
+            torch.cuda.empty_cache()
+        t = max(x["ms"] for x in ranks)
+        total = sum(x["bytes"] for x in ranks)
+        mean_bytes = total / n
+        out["curve"].append({"n_gpus": n, "ms_per_step": t, "value_gbs": round(total / t / 1e6, 1),
+                             "per_gpu_gbs": round(total / t / 1e6 / n, 1),
+                             "frac_of_hbm_peak_per_gpu": round(total / t / 1e6 / n / peak, 3),
+                             "load_imbalance": round(max(x["bytes"] for x in ranks) / mean_bytes, 3),
+                             "ranks": ranks})
+    v1 = out["curve"][0]["value_gbs"]
+    for c in out["curve"]:
+        c["efficiency_vs_1"] = round(c["value_gbs"] / (c["n_gpus"] * v1), 3)
+    return out
 
 
 SWEEP_SHAPES = [(128, 128), (256, 256), (512, 512), (1024, 1024), (2048, 2048), (4096, 4096), (4096, 7168),
@@ -1373,7 +1430,7 @@ def run_reference(args, rank, world, cfg):
         return
     import oracle as O  # the reference arm IS the oracle (tier framing)
 
-    frac = 1.0 / 32 if args.partition == "strong" and world == 1 else 1.0 / 8
+    frac = 1.0 / 32 if args.partition != "weak" and world == 1 else 1.0 / 8
     for _ in range(args.warmup):
         oracle_sample(O, frac, None, 0, world, args.partition)
     nb, ts, desc = 0.0, 0.0, ""
@@ -1383,7 +1440,7 @@ def run_reference(args, rank, world, cfg):
     v = nb / ts / 1e9
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ts / args.steps * 1e3, 2), "higher_is_better": True,
-            "scaling": "strong" if args.partition == "strong" else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.partition == "weak" else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": cfg, "impl": "reference",
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": desc},

@@ -8,6 +8,10 @@ layer (256 experts, 16384 tokens):
   fixed; the per-rank load follows the routing skew (reported as load_imbalance).
 * weak: rank r owns DeepSeek-V3 expert group r mod 8 (32 experts, the EP8 partition) and 1/8 of
   the tokens, so per-GPU work is one expert group at every n.
+* balanced: like strong (256/n experts and 1/n of the tokens per GPU), but WHICH experts a GPU
+  owns is chosen by load, longest-processing-time first over the routed row counts (the expert
+  placement an expert-parallel load balancer makes); the experts are relabelled so that GPU g's
+  set is the id range [g*256/n, (g+1)*256/n) (balanced_relabel).
 
 torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests) is used only OUTSIDE
 the timed region: barriers around it, the max over ranks of the measured time, the sum of bytes,
@@ -57,6 +61,10 @@ def shard(rank: int, world: int, mode: str, num_experts: int = 256, num_tokens: 
         t0, t1 = rank * num_tokens // world, (rank + 1) * num_tokens // world
         return {"mode": mode, "expert_begin": rank * per, "num_local_experts": per, "token_begin": t0,
                 "token_end": t1}
+    if mode == "balanced":
+        sh = shard(rank, world, "strong", num_experts, num_tokens, num_groups)
+        sh["mode"] = mode
+        return sh
     if mode == "weak":
         g = expert_group(rank, num_groups)
         per = num_experts // num_groups
@@ -64,6 +72,34 @@ def shard(rank: int, world: int, mode: str, num_experts: int = 256, num_tokens: 
         return {"mode": mode, "expert_begin": g * per, "num_local_experts": per, "token_begin": t0,
                 "token_end": t1, "group": g}
     raise ValueError(f"unknown partition {mode!r}")
+
+
+def balanced_placement(counts, world: int) -> list[list[int]]:
+    """Expert sets of `world` GPUs with equal expert counts and near-equal padded rows: experts
+    sorted by padded row count (descending, ties by id), each to the least-loaded GPU that still
+    has room (ties by GPU index) -- the LPT rule.  Deterministic."""
+    n = len(counts)
+    if world < 1 or n % world:
+        raise ValueError(f"{n} experts do not split over {world} ranks")
+    per = n // world
+    padded = [(int(c) + 15) // 16 * 16 for c in counts]
+    order = sorted(range(n), key=lambda e: (-padded[e], e))
+    load, sets = [0] * world, [[] for _ in range(world)]
+    for e in order:
+        g = min((g for g in range(world) if len(sets[g]) < per), key=lambda g: (load[g], g))
+        sets[g].append(e)
+        load[g] += padded[e]
+    return [sorted(x) for x in sets]
+
+
+def balanced_relabel(counts, world: int):
+    """new_id[e] for every expert id e: GPU g's LPT set becomes [g*E/n, (g+1)*E/n), in id order."""
+    sets = balanced_placement(counts, world)
+    new_id = [0] * len(counts)
+    for g, experts in enumerate(sets):
+        for i, e in enumerate(experts):
+            new_id[e] = g * (len(counts) // world) + i
+    return new_id
 
 
 def gather_objects(obj, device=torch.device("cpu")) -> list:
