@@ -5,9 +5,12 @@ One STEP = one pass of the whole hot path over one
 layer (16384 tokens, top-8 of 256 experts, hidden 7168, expert FFN 2x2048), partitioned over the
 job's GPUs (paper_2511_02302_b200/dist.py):
 
-  --partition strong (default)  GPU g of n owns experts [g*256/n, (g+1)*256/n) and tokens
-                                [g*T/n, (g+1)*T/n) of the entry casts; n = 1 is the WHOLE layer
-                                (256 experts, ~133k padded rows) on one GPU; total work fixed.
+  --partition balanced (default) GPU g of n owns 256/n experts placed by load (LPT over the routed
+                                rows) and tokens [g*T/n, (g+1)*T/n) of the entry casts; n = 1 is
+                                the WHOLE layer (256 experts, ~133k padded rows) on one GPU; total
+                                work fixed.
+  --partition strong            the same with contiguous expert ranges [g*256/n, (g+1)*256/n)
+                                (SURVEY 8(e)); the ranks then inherit the routing skew.
   --partition weak              every GPU owns one EP8 expert group (32 experts, 1/8 of tokens).
 
 Per GPU and step:
@@ -1080,7 +1083,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--partition", choices=["strong", "balanced", "weak"], default="strong",
+    ap.add_argument("--partition", choices=["strong", "balanced", "weak"], default="balanced",
                     help="strong: the layer's 256 experts split over the GPUs in id ranges (N=1: whole layer); "
                          "balanced: 256/N experts per GPU placed by load (LPT); "
                          "weak: one EP8 expert group (32 experts) per GPU")

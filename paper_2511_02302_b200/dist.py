@@ -3,12 +3,12 @@
 The hot path shards with no exchange step.  Two partitions of the DeepSeek-V3
 layer (256 experts, 16384 tokens):
 
-* strong (the default): rank g of n owns experts [g*256/n, (g+1)*256/n) and the token shard
+* strong: rank g of n owns experts [g*256/n, (g+1)*256/n) and the token shard
   [g*T/n, (g+1)*T/n) of the two entry casts; n = 1 is the whole layer on one GPU.  Total work is
   fixed; the per-rank load follows the routing skew (reported as load_imbalance).
 * weak: rank r owns DeepSeek-V3 expert group r mod 8 (32 experts, the EP8 partition) and 1/8 of
   the tokens, so per-GPU work is one expert group at every n.
-* balanced: like strong (256/n experts and 1/n of the tokens per GPU), but WHICH experts a GPU
+* balanced (bench.py's default): like strong (256/n experts and 1/n of the tokens per GPU), but WHICH experts a GPU
   owns is chosen by load, longest-processing-time first over the routed row counts (the expert
   placement an expert-parallel load balancer makes); the experts are relabelled so that GPU g's
   set is the id range [g*256/n, (g+1)*256/n) (balanced_relabel).
