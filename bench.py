@@ -1055,7 +1055,8 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10, checks: list | None = None) -
     shT = torch.empty(hw.R // 128 + E, 2 * FFN, dtype=torch.uint8, device=dev)
     F.fp8flow_scaling_aware_transpose(qh, sh, hT, shT, seg_offsets=ds.off)
     dW = torch.empty(E, 2 * FFN, HIDDEN, dtype=torch.bfloat16, device=dev)
-    ms = timed(lambda: F.fp8flow_gemm_wgrad(hT, shT, ds.xT, ds.sxT, dW, ds.off))
+    wsw = torch.empty(F.fp8flow_gemm_wgrad_workspace_bytes(E), dtype=torch.uint8, device=dev)
+    ms = timed(lambda: F.fp8flow_gemm_wgrad(hT, shT, ds.xT, ds.sxT, dW, ds.off, workspace=wsw))
     flops = 2.0 * hw.R * 2 * FFN * HIDDEN
     tf = flops / ms / 1e9
     offs = ds.off.cpu().numpy()

@@ -268,10 +268,14 @@ FP8FLOW_API int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, in
  *     zero-padded); a group with no rows gets D_e = 0.
  *   D  [num_groups][Ma][Nb] fp32 (d_f32 != 0) or BF16.  Ma % 128 == 0, Nb % 256 == 0,
  *   1 <= num_groups <= 512, seg_offsets device int32 [num_groups + 1] (required).
+ *   workspace: caller-owned device memory, 128-byte aligned, >= fp8flow_gemm_wgrad_workspace_bytes
+ *     (num_groups) bytes (the per-group TMA descriptors, written by the call on `stream`; it must
+ *     not be shared with a concurrent call).  Too small -> FP8FLOW_ERR_WORKSPACE.
  * ========================================================================================== */
+FP8FLOW_API int64_t fp8flow_gemm_wgrad_workspace_bytes(int32_t num_groups);
 FP8FLOW_API int fp8flow_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT,
                                    const uint8_t* sbT, int64_t Nb, const int32_t* seg_offsets, int32_t num_groups,
-                                   void* D, int32_t d_f32, void* stream);
+                                   void* D, int32_t d_f32, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ==========================================================================================
  * NEXT-3  Expert-parallel FP8 dispatch / BF16 combine over peer memory (

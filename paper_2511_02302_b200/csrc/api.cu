@@ -283,16 +283,23 @@ int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa,
                                           static_cast<cudaStream_t>(stream), sms));
 }
 
+int64_t fp8flow_gemm_wgrad_workspace_bytes(int32_t num_groups) {
+  return num_groups < 1 ? 0 : static_cast<int64_t>(num_groups) * 256;  // two 128-byte TMA maps per group
+}
+
 int fp8flow_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT, const uint8_t* sbT,
                        int64_t Nb, const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
-                       void* stream) {
+                       void* workspace, int64_t workspace_bytes, void* stream) {
   if (Ma <= 0 || Nb <= 0 || Ma % 128 != 0 || Nb % 256 != 0 || Ma > (1 << 24) || Nb > (1 << 24)) return FP8FLOW_ERR_SHAPE;
   if (num_groups < 1 || num_groups > 512) return FP8FLOW_ERR_ARG;
-  if (!AT || !saT || !BT || !sbT || !D || !seg_offsets) return FP8FLOW_ERR_NULL;
-  if (!aligned16(AT) || !aligned16(saT) || !aligned16(BT) || !aligned16(sbT) || !aligned16(D)) return FP8FLOW_ERR_ALIGN;
+  if (!AT || !saT || !BT || !sbT || !D || !seg_offsets || !workspace) return FP8FLOW_ERR_NULL;
+  if (workspace_bytes < fp8flow_gemm_wgrad_workspace_bytes(num_groups)) return FP8FLOW_ERR_WORKSPACE;
+  if (!aligned16(AT) || !aligned16(saT) || !aligned16(BT) || !aligned16(sbT) || !aligned16(D) ||
+      reinterpret_cast<uintptr_t>(workspace) % 128 != 0)
+    return FP8FLOW_ERR_ALIGN;
   int sms = 0, st = device(&sms);
   if (st != FP8FLOW_OK) return st;
-  return launched(launch_gemm_wgrad(AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32,
+  return launched(launch_gemm_wgrad(AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32, workspace,
                                     static_cast<cudaStream_t>(stream), sms));
 }
 

@@ -212,6 +212,37 @@ __device__ __forceinline__ void epilogue_bf16_tma(const CUtensorMap* tmap_d, uin
   }
 }
 
+// BF16 epilogue of one warp through two 128-byte-swizzled 32 x 64 staging boxes (4 KB each; the
+// swizzle keeps the row-per-lane writes bank-conflict free): 128-byte row segments per TMA store.
+// Each buffer is rewritten only after the TMA engine has read it.
+__device__ __forceinline__ void epilogue_bf16_tma_sw(const CUtensorMap* tmap_d, uint8_t* stage, const uint32_t (&v)[4][32],
+                                                     int col0, int row0, int lane, int& pending) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint8_t* buf = stage + h * 4096;
+    if (pending >= 2) {
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 64h + 8j .. +7
+      const uint32_t* w = &v[2 * h + (j >> 2)][8 * (j & 3)];
+      *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+          make_uint4(pack_bf16x2(__uint_as_float(w[0]), __uint_as_float(w[1])),
+                     pack_bf16x2(__uint_as_float(w[2]), __uint_as_float(w[3])),
+                     pack_bf16x2(__uint_as_float(w[4]), __uint_as_float(w[5])),
+                     pack_bf16x2(__uint_as_float(w[6]), __uint_as_float(w[7])));
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmap_d, buf, col0 + 64 * h, row0);
+      bulk_commit();
+    }
+    pending = pending < 2 ? pending + 1 : 2;
+  }
+}
+
 // tile t -> (group, first row, valid rows, first column)
 struct GemmTile {
   int g, r0, rows, n0;
@@ -450,28 +481,30 @@ __global__ void __launch_bounds__(kGThreads, 1)
 // Wgrad: groups split K (the tokens of each expert), e.g. dW1_e = dH_e^T X_e.  Both operands are
 // A2's column-wise outputs: per segment e a [rows][m_e] K-major matrix at byte offset rows * o_e,
 // scales sT rows P_e .. P_e + ceil(m_e/128) - 1 (A2's layout).  The row stride m_e changes per
-// group (and m_e is only a multiple of 16), so the operand tiles are loaded with cp.async 16-byte
-// chunks written straight into the 128-byte-swizzled K-major layout (chunk c of row r lands at
-// r * 128 + ((c ^ (r % 8)) * 16), the pattern TMA's SWIZZLE_128B produces), zero-filled past the
-// segment's last token; a group with no tokens gets D_e = 0.
-// Warps: 0-1 cp.async producers (warp 0 also owns TMEM), 2 MMA issuer, 3 scale expansion,
-// 4-11 epilogue (as in the Fprop kernel).
+// group, so no single host-encoded TMA map addresses them: wgrad_maps_kernel writes two maps per
+// group into the caller's workspace (a host-encoded template with the base address, the K extent
+// m_e and the row stride m_e replaced by tensormap.replace, published by tensormap.cp_fenceproxy),
+// and the GEMM's producer acquires a group's maps when it reaches the group.  TMA zero-fills K past
+// the segment's last token; a group with no tokens gets D_e = 0.
+// CTA pairs (clusters of 2) take the two 128-row halves of a 256-row block of D_e with the same 256
+// columns: each loads its own A rows and half of the shared B tile, multicast into both (per SM a
+// K step issues 32 KB of loads instead of 48 KB; the stage is released by both CTAs' MMA commits).
+// An odd last 128-row block is paired with zero-filled rows past Ma that are not stored.
+// Warps: 0 TMEM + TMA producer, 1 MMA issuer, 2 scale expansion, 3-10 epilogue (BF16 through
+// 128-byte-swizzled 32 x 64 staging boxes).  At ~500 tokens per expert the operand loads bound
+// it (the L2 -> SM traffic of re-reading each operand tile once per output tile); r01/r02 loaded
+// them with 64 threads of 16-byte cp.async (1.25 ms at the EP8 shape, now 0.68 ms:
+// profiles/r02_gemm_wgrad.txt).
 // =============================================================================================
-constexpr int kWThreads = 384;
-constexpr int kWProd = 64;  // producer threads
-constexpr int kWStages = 3;  // (smem for two BF16 staging boxes per epilogue warp)
+constexpr int kWThreads = 352;
 
-__device__ __forceinline__ void cp_async_16(void* dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-
+template <int STAGES, int NBUF>
 struct WgradSmem {
-  GemmStage st[kWStages];
-  alignas(1024) uint8_t stg[8][4 * 2048];  // BF16 epilogue staging: four 32 x 32 boxes per epilogue warp
-  uint64_t full[kWStages];     // kWProd producer arrivals (after their copies landed + proxy fence)
-  uint64_t empty[kWStages];
-  uint64_t sfready[kWStages];
+  GemmStage st[STAGES];
+  alignas(1024) uint8_t stg[8][NBUF * 2048];  // BF16 epilogue staging: NBUF 32 x 32 boxes per warp
+  uint64_t full[STAGES];     // operand boxes + scale runs landed (TMA transaction bytes)
+  uint64_t empty[STAGES];    // the stage's MMAs completed (tcgen05.commit)
+  uint64_t sfready[STAGES];  // the stage's scale-factor chunks are expanded
   uint64_t tmem_full;
   uint64_t tmem_empty;
   uint32_t tmem_base;
@@ -481,20 +514,59 @@ struct WgradSmem {
   int32_t total_rb;
 };
 
+// maps[2g] (A operand of group g) and maps[2g + 1] (B operand): one warp per map
+__global__ void __launch_bounds__(256) wgrad_maps_kernel(const __grid_constant__ CUtensorMap tmpl_a,
+                                                         const __grid_constant__ CUtensorMap tmpl_b,
+                                                         const uint8_t* AT, int64_t Ma, const uint8_t* BT, int64_t Nb,
+                                                         const int32_t* __restrict__ seg_offsets, int32_t num_groups,
+                                                         CUtensorMap* __restrict__ maps) {
+  __shared__ alignas(128) CUtensorMap tm[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = static_cast<int>(blockIdx.x) * 8 + warp; i < 2 * num_groups; i += static_cast<int>(gridDim.x) * 8) {
+    const int g = i >> 1;
+    const bool is_b = (i & 1) != 0;
+    const int o = seg_offsets[g], me = seg_offsets[g + 1] - o;
+    const uint32_t ext = me > 0 ? static_cast<uint32_t>(me) : 16u;  // an empty group's maps are never used
+    const CUtensorMap* src = is_b ? &tmpl_b : &tmpl_a;
+    if (lane < 8) reinterpret_cast<uint4*>(&tm[warp])[lane] = reinterpret_cast<const uint4*>(src)[lane];
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t a = smem_u32(&tm[warp]);
+      const uint64_t base = reinterpret_cast<uint64_t>(is_b ? BT + Nb * o : AT + Ma * o);
+      asm volatile("tensormap.replace.tile.global_address.shared::cta.b1024.b64 [%0], %1;" ::"r"(a), "l"(base)
+                   : "memory");
+      asm volatile("tensormap.replace.tile.global_dim.shared::cta.b1024.b32 [%0], 0, %1;" ::"r"(a), "r"(ext)
+                   : "memory");
+      asm volatile("tensormap.replace.tile.global_stride.shared::cta.b1024.b64 [%0], 0, %1;" ::"r"(a),
+                   "l"(static_cast<uint64_t>(ext))
+                   : "memory");
+    }
+    __syncwarp();
+    asm volatile(
+        "tensormap.cp_fenceproxy.global.shared::cta.tensormap::generic.release.gpu.sync.aligned [%0], [%1], 128;" ::"l"(
+            reinterpret_cast<uint64_t>(maps + i)),
+        "r"(smem_u32(&tm[warp]))
+        : "memory");
+    __syncwarp();
+  }
+}
+
+template <int STAGES, int NBUF>
 __global__ void __launch_bounds__(kWThreads, 1)
-    gemm_wgrad_kernel(const __grid_constant__ CUtensorMap tmap_d, const uint8_t* __restrict__ AT, const uint8_t* __restrict__ saT, int64_t Ma,
-                      const uint8_t* __restrict__ BT, const uint8_t* __restrict__ sbT, int64_t Nb,
+    gemm_wgrad_kernel(const __grid_constant__ CUtensorMap tmap_d, const CUtensorMap* __restrict__ maps,
+                      const uint8_t* __restrict__ saT, int64_t Ma, const uint8_t* __restrict__ sbT, int64_t Nb,
                       const int32_t* __restrict__ seg_offsets, int32_t num_groups, void* __restrict__ D,
                       int32_t d_f32) {
   extern __shared__ __align__(1024) uint8_t smem_wg[];
-  WgradSmem& sm = *reinterpret_cast<WgradSmem*>((reinterpret_cast<uintptr_t>(smem_wg) + 1023) & ~uintptr_t(1023));
+  using Smem = WgradSmem<STAGES, NBUF>;
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_wg) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   if (tid == 32) {
-    for (int i = 0; i < kWStages; ++i) {
-      mbar_init(&sm.full[i], kWProd);
-      mbar_init(&sm.empty[i], 1);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 2);     // both CTAs' MMA commits (the peer multicasts half of B here)
       mbar_init(&sm.sfready[i], 32);  // every lane of the scale-expansion warp
     }
     mbar_init(&sm.tmem_full, 1);
@@ -503,67 +575,60 @@ __global__ void __launch_bounds__(kWThreads, 1)
   }
   tc_fence_before();
   load_segments<kWThreads>(sm, seg_offsets, num_groups, 0);  // blk_prefix[e] = P_e (scale-tile rows)
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const int n_mt = static_cast<int>(Ma / kGM), n_nt = static_cast<int>(Nb / kGN);
-  const int per_group = n_mt * n_nt;
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int n_mp = static_cast<int>((Ma / kGM + 1) / 2), n_nt = static_cast<int>(Nb / kGN);
+  const int per_group = n_mp * n_nt;
   const int total_tiles = num_groups * per_group;
-  auto tile_of = [&](int t, int& e, int& m0, int& n0) {
+  const int c0 = static_cast<int>(blockIdx.x) / 2, ncl = static_cast<int>(gridDim.x) / 2;
+  auto tile_of = [&](int t, int& e, int& m0, int& n0) {  // m0: this CTA's rows
     e = t / per_group;
     const int r = t - e * per_group;
-    m0 = (r / n_nt) * kGM;
+    m0 = (r / n_nt) * 2 * kGM + kGM * rank;
     n0 = (r % n_nt) * kGN;
   };
 
-  if (warp < 2) {  // ------------------------------------------------------- cp.async producers
-    int st = 0, n = 0;
-    uint32_t parity = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      int e, m0, n0;
-      tile_of(t, e, m0, n0);
-      const int o = sm.seg_off[e], me = sm.seg_off[e + 1] - o;
-      const int nk = (me + kGK - 1) / kGK;
-      const uint8_t* a_base = AT + Ma * o + static_cast<int64_t>(m0) * me;
-      const uint8_t* b_base = BT + Nb * o + static_cast<int64_t>(n0) * me;
-      for (int kb = 0; kb < nk; ++kb, ++n) {
-        if (n >= kWStages) mbar_wait(&sm.empty[st], parity ^ 1u);
-        GemmStage& S = sm.st[st];
-        const int kv = me - kb * kGK;  // valid K bytes in this step (>= 16)
-#pragma unroll 4
-        for (int q = tid; q < kGM * 8; q += kWProd) {
-          const int r = q >> 3, c = q & 7;
-          const uint32_t ok = 16 * c < kv ? 16u : 0u;
-          cp_async_16(&S.a[r * 128 + ((c ^ (r & 7)) * 16)], a_base + static_cast<int64_t>(r) * me + kb * kGK + (ok ? 16 * c : 0),
-                      ok);
+  if (warp == 0) {  // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int st = 0, n = 0, cur = -1;
+      uint32_t parity = 0;
+      for (int t = c0; t < total_tiles; t += ncl) {
+        int e, m0, n0;
+        tile_of(t, e, m0, n0);
+        const int nk = (sm.seg_off[e + 1] - sm.seg_off[e] + kGK - 1) / kGK;
+        if (nk == 0) continue;
+        const CUtensorMap* ma = maps + 2 * e;
+        const CUtensorMap* mb = ma + 1;
+        if (e != cur) {  // the group's maps, written by wgrad_maps_kernel (generic proxy)
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(ma))
+                       : "memory");
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(reinterpret_cast<uint64_t>(mb))
+                       : "memory");
+          cur = e;
         }
-#pragma unroll 4
-        for (int q = tid; q < kGN * 8; q += kWProd) {
-          const int r = q >> 3, c = q & 7;
-          const uint32_t ok = 16 * c < kv ? 16u : 0u;
-          cp_async_16(&S.b[r * 128 + ((c ^ (r & 7)) * 16)], b_base + static_cast<int64_t>(r) * me + kb * kGK + (ok ? 16 * c : 0),
-                      ok);
-        }
-        const int64_t srow = sm.blk_prefix[e] + kb;  // this K block's row of sT
-        if (tid < kGM / 16) cp_async_16(&S.sa[16 * tid], saT + srow * Ma + m0 + 16 * tid, 16);
-        else if (tid < kGM / 16 + kGN / 16) {
-          const int j = tid - kGM / 16;
-          cp_async_16(&S.sb[16 * j], sbT + srow * Nb + n0 + 16 * j, 16);
-        }
-        // this thread's copies arrive on the stage's barrier when they land (noinc: the 64
-        // producer arrivals are the barrier's expected count) -- no blocking wait, the producer
-        // runs ahead as far as the ring allows
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[st]))
-                     : "memory");
-        if (++st == kWStages) {
-          st = 0;
-          parity ^= 1u;
+        for (int kb = 0; kb < nk; ++kb, ++n) {
+          if (n >= STAGES) mbar_wait(&sm.empty[st], parity ^ 1u);
+          GemmStage& S = sm.st[st];
+          mbar_expect_tx(&sm.full[st], kGM * kGK + kGN * kGK + kGM + kGN);
+          tma_load_2d(S.a, ma, &sm.full[st], kb * kGK, m0);
+          // this CTA's half of the shared B tile, into both CTAs of the pair
+          tma_load_2d_mc(S.b + rank * (kGN / 2) * kGK, mb, &sm.full[st], kb * kGK, n0 + (kGN / 2) * rank, 0x3);
+          const int64_t srow = sm.blk_prefix[e] + kb;  // this K block's row of sT
+          bulk_load_1d(S.sa, saT + srow * Ma + min(static_cast<int64_t>(m0), Ma - kGM), kGM, &sm.full[st]);
+          bulk_load_1d(S.sb, sbT + srow * Nb + n0, kGN, &sm.full[st]);
+          if (++st == STAGES) {
+            st = 0;
+            parity ^= 1u;
+          }
         }
       }
     }
-  } else if (warp == 2) {  // ------------------------------------------------------ MMA issue
+  } else if (warp == 1) {  // ------------------------------------------------------ MMA issue
     int st = 0, step = 0;
     uint32_t parity = 0;
-    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+    for (int t = c0, i = 0; t < total_tiles; t += ncl, ++i) {
       int e, m0, n0;
       tile_of(t, e, m0, n0);
       const int me = sm.seg_off[e + 1] - sm.seg_off[e];
@@ -571,9 +636,8 @@ __global__ void __launch_bounds__(kWThreads, 1)
       if (i > 0) mbar_wait(&sm.tmem_empty, (i - 1) & 1);
       tc_fence_after();
       for (int kb = 0; kb < nk; ++kb, ++step) {
-        mbar_wait(&sm.sfready[st], parity);
+        mbar_wait(&sm.sfready[st], parity);  // implies full: the expansion warp waited for it
         tc_fence_after();
-        fence_proxy_async_smem();  // the operands were written by cp.async (generic proxy)
         if (lane == 0) {
           GemmStage& S = sm.st[st];
           const uint32_t sfa_t = tmem + kSfCol + 16u * (step & 1);
@@ -587,10 +651,10 @@ __global__ void __launch_bounds__(kWThreads, 1)
           for (int k = 0; k < slices; ++k)
             tc_mma_mxf8(tmem, adesc + 2u * k, bdesc + 2u * k, idesc_mxf8(static_cast<uint32_t>(k)),
                         (kb | k) != 0 ? 1u : 0u, sfa_t, sfb_t);
-          tc_commit(&sm.empty[st]);
+          tc_commit_mc(&sm.empty[st], 0x3);
         }
         __syncwarp();
-        if (++st == kWStages) {
+        if (++st == STAGES) {
           st = 0;
           parity ^= 1u;
         }
@@ -598,10 +662,10 @@ __global__ void __launch_bounds__(kWThreads, 1)
       if (lane == 0) tc_commit(&sm.tmem_full);
       __syncwarp();
     }
-  } else if (warp == 3) {  // --------------------------------------------- scale expansion
+  } else if (warp == 2) {  // --------------------------------------------- scale expansion
     int st = 0;
     uint32_t parity = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = c0; t < total_tiles; t += ncl) {
       int e, m0, n0;
       tile_of(t, e, m0, n0);
       const int nk = (sm.seg_off[e + 1] - sm.seg_off[e] + kGK - 1) / kGK;
@@ -621,7 +685,7 @@ __global__ void __launch_bounds__(kWThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         mbar_arrive(&sm.sfready[st]);
-        if (++st == kWStages) {
+        if (++st == STAGES) {
           st = 0;
           parity ^= 1u;
         }
@@ -629,9 +693,9 @@ __global__ void __launch_bounds__(kWThreads, 1)
     }
   } else {  // ------------------------------------------------------------------- epilogue
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int half = (warp - 3) >> 2;
     int pending = 0;
-    for (int t = blockIdx.x, i = 0; t < total_tiles; t += gridDim.x, ++i) {
+    for (int t = c0, i = 0; t < total_tiles; t += ncl, ++i) {
       int e, m0, n0;
       tile_of(t, e, m0, n0);
       const bool empty_group = sm.seg_off[e + 1] == sm.seg_off[e];
@@ -648,32 +712,24 @@ __global__ void __launch_bounds__(kWThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[c][j] = 0u;  // no tokens: dW_e = 0
       }
+      if (m0 >= Ma) continue;  // the zero-filled half of an odd last row pair
       const int64_t grow = static_cast<int64_t>(e) * Ma + m0 + 32 * q + lane;
       const int col0 = n0 + 128 * half;
       if (!d_f32) {
-        epilogue_bf16_tma<4>(&tmap_d, sm.stg[warp - 4], v, col0, static_cast<int>(grow - lane), lane, pending);
+        epilogue_bf16_tma_sw(&tmap_d, sm.stg[warp - 3], v, col0, static_cast<int>(grow - lane), lane, pending);
         continue;
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        if (d_f32) {
-          float* dp = static_cast<float*>(D) + grow * Nb + col0 + 32 * c;
+        float* dp = static_cast<float*>(D) + grow * Nb + col0 + 32 * c;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[c][j], v[c][j + 1], v[c][j + 2], v[c][j + 3]));
-        } else {
-          __nv_bfloat16* dp = static_cast<__nv_bfloat16*>(D) + grow * Nb + col0 + 32 * c;
-#pragma unroll
-          for (int j = 0; j < 32; j += 8)
-            st_v4(dp + j, make_uint4(pack_bf16x2(__uint_as_float(v[c][j]), __uint_as_float(v[c][j + 1])),
-                                     pack_bf16x2(__uint_as_float(v[c][j + 2]), __uint_as_float(v[c][j + 3])),
-                                     pack_bf16x2(__uint_as_float(v[c][j + 4]), __uint_as_float(v[c][j + 5])),
-                                     pack_bf16x2(__uint_as_float(v[c][j + 6]), __uint_as_float(v[c][j + 7]))));
-        }
+        for (int j = 0; j < 32; j += 4) st_v4(dp + j, make_uint4(v[c][j], v[c][j + 1], v[c][j + 2], v[c][j + 3]));
       }
     }
   }
-  if (warp >= 4 && lane == 0) bulk_wait_all();  // TMA stores of the epilogue
+  if (warp >= 3 && lane == 0) bulk_wait_all();  // TMA stores of the epilogue
   __syncthreads();
+  cluster_sync_all();
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -772,27 +828,54 @@ namespace fp8flow {
 
 cudaError_t launch_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT, const uint8_t* sbT,
                               int64_t Nb, const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
-                              cudaStream_t stream, int num_sms) {
+                              void* workspace, cudaStream_t stream, int num_sms) {
+  constexpr int kStages = 3, kNbuf = 4;
+  using Smem = WgradSmem<kStages, kNbuf>;
   static KernelSetup setup;
-  if (prepare_kernel(setup, gemm_wgrad_kernel, kWThreads, sizeof(WgradSmem) + 1024, sizeof(WgradSmem) + 1024) == 0)
+  if (prepare_kernel(setup, gemm_wgrad_kernel<kStages, kNbuf>, kWThreads, sizeof(Smem) + 1024, sizeof(Smem) + 1024) == 0)
     return cudaErrorInvalidValue;
   PFN_encodeTiled encode = tensor_map_encoder();
   if (!encode) return cudaErrorNotSupported;
-  CUtensorMap md;
+  const cuuint32_t es[2] = {1, 1};
+  CUtensorMap md, ta, tb;
   const cuuint64_t gdim_d[2] = {static_cast<cuuint64_t>(Nb), static_cast<cuuint64_t>(num_groups) * Ma};
   const cuuint64_t gstr_d[1] = {static_cast<cuuint64_t>(Nb) * 2};
-  const cuuint32_t box_d[2] = {32, 32};
-  const cuuint32_t es[2] = {1, 1};
+  const cuuint32_t box_d[2] = {64, 32};
+  // operand templates: K extent and row stride 128 (replaced per group on the device), 128-byte
+  // swizzled K-major boxes of 128 K x 128 rows (A; B: one CTA's half of the 256-row tile)
+  const cuuint64_t gdim_a[2] = {128, static_cast<cuuint64_t>(Ma)}, gdim_b[2] = {128, static_cast<cuuint64_t>(Nb)};
+  const cuuint64_t gstr_t[1] = {128};
+  const cuuint32_t box_a[2] = {kGK, kGM}, box_b[2] = {kGK, kGN / 2};
   if (encode(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, gdim_d, gstr_d, box_d, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS ||
+      encode(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(AT), gdim_a, gstr_t, box_a, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+      encode(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(BT), gdim_b, gstr_t, box_b, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const int64_t tiles = static_cast<int64_t>(num_groups) * (Ma / kGM) * (Nb / kGN);
-  const int64_t grid = tiles < num_sms ? tiles : num_sms;
-  if (grid < 1) return cudaSuccess;
-  gemm_wgrad_kernel<<<static_cast<unsigned>(grid), kWThreads, sizeof(WgradSmem) + 1024, stream>>>(
-      md, AT, saT, Ma, BT, sbT, Nb, seg_offsets, num_groups, D, d_f32);
-  return cudaGetLastError();
+  CUtensorMap* maps = static_cast<CUtensorMap*>(workspace);
+  wgrad_maps_kernel<<<(2 * num_groups + 7) / 8, 256, 0, stream>>>(ta, tb, AT, Ma, BT, Nb, seg_offsets, num_groups,
+                                                                  maps);
+  const int64_t pairs = static_cast<int64_t>(num_groups) * ((Ma / kGM + 1) / 2) * (Nb / kGN);
+  int64_t grid = (pairs < num_sms / 2 ? pairs : num_sms / 2) * 2;
+  if (grid < 2) grid = 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kWThreads);
+  cfg.dynamicSmemBytes = sizeof(Smem) + 1024;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_wgrad_kernel<kStages, kNbuf>, md, static_cast<const CUtensorMap*>(maps), saT,
+                            Ma, sbT, Nb, seg_offsets, num_groups, D, d_f32);
 }
 
 }  // namespace fp8flow

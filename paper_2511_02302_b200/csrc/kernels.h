@@ -95,7 +95,7 @@ cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t
                                     cudaStream_t stream, int num_sms);
 cudaError_t launch_gemm_wgrad(const uint8_t* AT, const uint8_t* saT, int64_t Ma, const uint8_t* BT, const uint8_t* sbT,
                               int64_t Nb, const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,
-                              cudaStream_t stream, int num_sms);
+                              void* workspace, cudaStream_t stream, int num_sms);
 cudaError_t launch_swiglu_bwd_quant(const void* h, const void* dA, int64_t rows_max, const int32_t* rows_dev,
                                     int64_t ffn, uint8_t* q, uint8_t* s, int64_t ld_s, cudaStream_t stream,
                                     int num_sms);

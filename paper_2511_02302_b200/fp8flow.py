@@ -47,7 +47,8 @@ SIGNATURES = {
     "fp8flow_quantize_dual": (ctypes.c_int, [_P, _I64, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
     "fp8flow_swiglu_quant_dual": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
     "fp8flow_gemm_blockscaled": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _P, _I32, _P]),
-    "fp8flow_gemm_wgrad": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _I32, _P, _I32, _P]),
+    "fp8flow_gemm_wgrad_workspace_bytes": (_I64, [_I32]),
+    "fp8flow_gemm_wgrad": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _I32, _P, _I32, _P, _I64, _P]),
     "fp8flow_ipc_get_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
     "fp8flow_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "fp8flow_ipc_close": (ctypes.c_int, [_P]),
@@ -270,14 +271,21 @@ def fp8flow_gemm_blockscaled(A: torch.Tensor, sa: torch.Tensor, B: torch.Tensor,
 
 
 def fp8flow_gemm_wgrad(AT: torch.Tensor, saT: torch.Tensor, BT: torch.Tensor, sbT: torch.Tensor, D: torch.Tensor,
-                       seg_offsets: torch.Tensor, stream=None) -> None:
+                       seg_offsets: torch.Tensor, workspace: torch.Tensor | None = None, stream=None) -> None:
     """NEXT-2 Wgrad: AT/BT flat uint8 (A2 outputs of [rows, Ma] / [rows, Nb]) + their sT [tiles, Ma/Nb];
-    D float32 or bfloat16 [G, Ma, Nb]; groups = the A2 segments."""
+    D float32 or bfloat16 [G, Ma, Nb]; groups = the A2 segments.  workspace: uint8 CUDA tensor of
+    >= fp8flow_gemm_wgrad_workspace_bytes(G) bytes (allocated here when None)."""
     G, Ma, Nb = D.shape
     assert seg_offsets.numel() == G + 1 and saT.shape[1] == Ma and sbT.shape[1] == Nb
+    if workspace is None:
+        workspace = torch.empty(fp8flow_gemm_wgrad_workspace_bytes(G), dtype=torch.uint8, device=D.device)
     _check(lib().fp8flow_gemm_wgrad(_ptr(_u8(AT)), _ptr(_u8(saT)), Ma, _ptr(_u8(BT)), _ptr(_u8(sbT)), Nb,
                                     _ptr(seg_offsets), G, _ptr(D), 1 if D.dtype == torch.float32 else 0,
-                                    _stream(stream)), "fp8flow_gemm_wgrad")
+                                    _ptr(workspace), workspace.numel(), _stream(stream)), "fp8flow_gemm_wgrad")
+
+
+def fp8flow_gemm_wgrad_workspace_bytes(num_groups: int) -> int:
+    return int(lib().fp8flow_gemm_wgrad_workspace_bytes(num_groups))
 
 
 def fp8flow_checksum64(buf: torch.Tensor, out: torch.Tensor, stream=None) -> None:

@@ -108,11 +108,16 @@ def test_validation_of_next_row_entry_points(L):
     assert L.fp8flow_gemm_blockscaled(None, a16, 32, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 1
     assert L.fp8flow_gemm_blockscaled(P(8), a16, 32, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 3
     assert L.fp8flow_gemm_blockscaled(None, None, 0, None, None, 256, 0, 256, 128, None, 0, None, 1, None) == 0
-    # Wgrad: Ma % 128, Nb % 256, groups required, NULL
-    assert L.fp8flow_gemm_wgrad(a16, a16, 100, a16, a16, 256, a16, 4, a16, 1, None) == 2
-    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 200, a16, 4, a16, 1, None) == 2
-    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, a16, 0, a16, 1, None) == 4
-    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, None, 4, a16, 1, None) == 1
+    # Wgrad: Ma % 128, Nb % 256, groups required, NULL, workspace size and alignment
+    a128 = P(128)
+    assert L.fp8flow_gemm_wgrad_workspace_bytes(4) == 1024
+    assert L.fp8flow_gemm_wgrad(a16, a16, 100, a16, a16, 256, a16, 4, a16, 1, a128, 1024, None) == 2
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 200, a16, 4, a16, 1, a128, 1024, None) == 2
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, a16, 0, a16, 1, a128, 1024, None) == 4
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, None, 4, a16, 1, a128, 1024, None) == 1
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, a16, 4, a16, 1, None, 1024, None) == 1
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, a16, 4, a16, 1, a128, 1023, None) == 5
+    assert L.fp8flow_gemm_wgrad(a16, a16, 128, a16, a16, 256, a16, 4, a16, 1, a16, 1024, None) == 3
 
 
 def test_validation_of_next3_entry_points(L):

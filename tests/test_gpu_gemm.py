@@ -158,12 +158,14 @@ def test_gemm_dgrad_on_transposed_weights(F, orc):
     assert np.max(np.abs(D - exact)) <= 0.1 * np.max(np.abs(exact))
 
 
-@pytest.mark.parametrize("m", [[128, 256], [16, 0, 144, 528, 48]])
-def test_gemm_wgrad_grouped_k(F, orc, m):
+@pytest.mark.parametrize("m,Ma,Nb,bf16", [([128, 256], 128, 256, False), ([16, 0, 144, 528, 48], 128, 256, False),
+                                          ([16, 0, 144, 528, 48], 384, 512, False), ([272, 0, 32], 512, 768, True)])
+def test_gemm_wgrad_grouped_k(F, orc, m, Ma, Nb, bf16):
     """Wgrad with groups over K (each expert's tokens, multiples of 16, an empty expert, partial K
-    blocks): dW_e = dH_e^T X_e straight from A2's column-wise outputs of dH and X_perm."""
+    blocks): dW_e = dH_e^T X_e straight from A2's column-wise outputs of dH and X_perm.  Ma = 128
+    and 384 leave the last CTA pair half outside Ma; fp32 and BF16 outputs."""
     seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
-    R, Ma, Nb = int(seg[-1]), 128, 256
+    R = int(seg[-1])
     dh = synth.normal_bf16(R, Ma, 91)
     x = synth.activations_bf16(R, Nb, 92)
     qd, sd = orc.quantize_rowwise_bf16(synth.bf16_bits(dh))
@@ -171,12 +173,12 @@ def test_gemm_wgrad_grouped_k(F, orc, m):
     dT, sdT = orc.scaling_aware_transpose(qd, sd, seg)
     xT, sxT = orc.scaling_aware_transpose(qx, sx, seg)
     G = len(m)
-    D = torch.full((G, Ma, Nb), float("nan"), dtype=torch.float32, device="cuda")
+    D = torch.full((G, Ma, Nb), float("nan"), dtype=torch.bfloat16 if bf16 else torch.float32, device="cuda")
     F.fp8flow_gemm_wgrad(torch.from_numpy(dT).cuda(), torch.from_numpy(np.ascontiguousarray(sdT)).cuda(),
                          torch.from_numpy(xT).cuda(), torch.from_numpy(np.ascontiguousarray(sxT)).cuda(), D,
                          torch.from_numpy(seg).cuda())
     torch.cuda.synchronize()
-    D = D.cpu().numpy()
+    D = D.float().cpu().numpy()
     P = np.concatenate([[0], np.cumsum((np.asarray(m) + 127) // 128)])
     for e in range(G):
         o, me = int(seg[e]), int(m[e])
@@ -187,4 +189,4 @@ def test_gemm_wgrad_grouped_k(F, orc, m):
         B = xT[Nb * o: Nb * (o + me)].reshape(Nb, me)
         sA, sB = sdT[P[e]:P[e + 1]], sxT[P[e]:P[e + 1]]
         check(D[e], orc.gemm_blockscaled(A, sA, B, sB), orc.gemm_blockscaled(A & 0x7F, sA, B & 0x7F, sB),
-              slice(0, Ma), what=f"wgrad e{e} m_e={me}")
+              slice(0, Ma), bf16=bf16, what=f"wgrad e{e} m_e={me}")
