@@ -132,4 +132,35 @@ __device__ __forceinline__ void st_v2(void* p, uint32_t a, uint32_t b) {
 __device__ __forceinline__ float bf16lo_to_f32(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi_to_f32(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
+// per bf16 half: max(|a|, |b|), sign bit = xor of the signs (callers mask it off)
+__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// A1's arithmetic (Eq. 2-3, power-of-two scales P:173-175) for one 1x128 tile row held
+// by 8 consecutive lanes (8k..8k+7), 16 BF16 per lane in w (any split of the row's columns): exact
+// |amax| by 7 packed max.xorsign.abs, 3 butterfly shuffles on the 15-bit magnitude, scale byte
+// T + 127 = max(((mag + 0x1F) >> 7) - 8, 0) (the +0x1F carries into the exponent exactly when the
+// 7-bit mantissa exceeds 0x60), codes RNE(x * 2^-T) (the product is exact).  c[j]: the two codes of
+// w[j] (low byte = low half).  Returns the scale byte (zero / subnormal amax -> 0, R11, R13).
+__device__ __forceinline__ uint32_t a1_quant16(const uint32_t (&w)[8], uint32_t (&c)[8]) {
+  const uint32_t m = absmax_bf16x2(absmax_bf16x2(absmax_bf16x2(w[0], w[1]), absmax_bf16x2(w[2], w[3])),
+                                   absmax_bf16x2(absmax_bf16x2(w[4], w[5]), absmax_bf16x2(w[6], w[7])));
+  uint32_t mag = max(m & 0x7FFFu, (m >> 16) & 0x7FFFu);
+  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 1));
+  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 2));
+  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 4));
+  const int sb = max(static_cast<int>((mag + 0x1Fu) >> 7) - 8, 0);
+  const float inv = __uint_as_float(static_cast<uint32_t>(254 - sb) << 23);
+  const float2 iv = make_float2(inv, inv);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 p = __fmul2_rn(make_float2(bf16lo_to_f32(w[j]), bf16hi_to_f32(w[j])), iv);
+    c[j] = cvt_e4m3x2_f32(p.x, p.y);
+  }
+  return static_cast<uint32_t>(sb);
+}
+
 }  // namespace fp8flow

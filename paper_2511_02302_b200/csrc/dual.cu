@@ -65,28 +65,6 @@ struct DualSmem {
 };
 
 
-// A1 on N rows (lane: 4 columns of each): exact integer amax over |bf16| bit patterns, scale byte
-// from the amax bits, codes = RNE(x * 2^-T) (the product is exact).  c[i]: the lane's 4 codes of
-// row i; returns the scale byte of row (lane % N).
-template <int N>
-__device__ __forceinline__ uint32_t quant_rows(const uint2 (&w)[N], uint32_t (&c)[N]) {
-  const int lane = threadIdx.x & 31;
-  uint32_t mine = 0;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const uint32_t m2 = __vmaxu2(w[i].x & 0x7FFF7FFFu, w[i].y & 0x7FFF7FFFu);  // packed 16-bit max
-    const uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
-    const uint32_t sb = scale_byte_from_bf16_mag(__reduce_max_sync(0xffffffffu, m));
-    const float inv = inv_scale_from_byte(sb);
-    const float2 iv = make_float2(inv, inv);
-    const float2 px = __fmul2_rn(make_float2(bf16lo_to_f32(w[i].x), bf16hi_to_f32(w[i].x)), iv);
-    const float2 py = __fmul2_rn(make_float2(bf16lo_to_f32(w[i].y), bf16hi_to_f32(w[i].y)), iv);
-    c[i] = cvt_e4m3x2_f32(px.x, px.y) | (cvt_e4m3x2_f32(py.x, py.y) << 16);
-    mine = (lane & (N - 1)) == i ? sb : mine;
-  }
-  return mine;
-}
-
 template <int OP, int STAGES>
 __global__ void __launch_bounds__(kDThreads, 1)
     dual_kernel(const __grid_constant__ CUtensorMap tmap, int64_t rows_max, const int32_t* __restrict__ rows_dev,
@@ -181,18 +159,66 @@ __global__ void __launch_bounds__(kDThreads, 1)
         parity ^= 1u;
       }
       mbar_wait(&sm.full[hs], hp);
+      if (OP == 0) {
+        // A1's lane layout (common.cuh a1_quant16): lanes 8k..8k+7 hold rows k and k + 4 of the
+        // warp's 8, lane chunk c8 = columns 8c8..8c8+7 and 64+8c8..+7 (conflict-free smem reads)
+        const int r_in = lane >> 3, c8 = lane & 7;
+        uint4 v[2][2];
+        if (active) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint8_t* rp = &sm.in[hs][0][(hr0 + r_in + 4 * h) * kDT * 2];
+            v[h][0] = *reinterpret_cast<const uint4*>(rp + 16 * c8);
+            v[h][1] = *reinterpret_cast<const uint4*>(rp + 128 + 16 * c8);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[hs]);
+        uint32_t cw[2][4], sb[2] = {0u, 0u};
+        if (active) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t w8[8] = {v[h][0].x, v[h][0].y, v[h][0].z, v[h][0].w,
+                                    v[h][1].x, v[h][1].y, v[h][1].z, v[h][1].w};
+            uint32_t c[8];
+            sb[h] = a1_quant16(w8, c);
+            cw[h][0] = c[0] | (c[1] << 16);
+            cw[h][1] = c[2] | (c[3] << 16);
+            cw[h][2] = c[4] | (c[5] << 16);
+            cw[h][3] = c[6] | (c[7] << 16);
+            const int64_t row = r0 + wr0 + r_in + 4 * h;
+            uint8_t* qrow = q + row * cols + jb * kDT + 8 * c8;
+            st_v2(qrow, cw[h][0], cw[h][1]);
+            st_v2(qrow + 64, cw[h][2], cw[h][3]);
+            if (c8 == 0) s[static_cast<int64_t>(jb) * ld_s + row] = static_cast<uint8_t>(sb[h]);
+          }
+        }
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, max(sb[0], sb[1]));  // 0 when inactive
+        if (i >= 2) mbar_wait(&sm.cempty[b], ((i >> 1) - 1) & 1);  // tile i-2's transpose is done with b
+        if (active) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = wr0 + r_in + 4 * h;
+            const int swz = (row >> 2) & 7;
+            uint32_t* crow = &sm.ctile[b][row * (kDT / 4) + (c8 & 1) * 2];
+            *reinterpret_cast<uint2*>(crow + (((c8 >> 1) ^ swz) << 2)) = make_uint2(cw[h][0], cw[h][1]);
+            *reinterpret_cast<uint2*>(crow + (((4 + (c8 >> 1)) ^ swz) << 2)) = make_uint2(cw[h][2], cw[h][3]);
+            if (c8 == 0) reinterpret_cast<uint8_t*>(sm.sc[b])[row] = static_cast<uint8_t>(sb[h]);
+          }
+        }
+        if (lane == 0) sm.wmax[b][warp] = wm;
+        __syncwarp();
+        mbar_arrive(&sm.cfull[b]);  // release (per lane): this lane's code-tile writes are visible
+        continue;
+      }
       uint32_t cw[kDRpw], sbyte = 0;
       if (active) {
         uint2 wa[kDRpw];
 #pragma unroll
         for (int r = 0; r < kDRpw; ++r)
           wa[r] = *reinterpret_cast<const uint2*>(&sm.in[hs][0][((hr0 + r) * kDT + 4 * lane) * 2]);
-        if (OP == 0) {
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.empty[hs]);
-          sbyte = quant_rows<kDRpw>(wa, cw);
-        } else {
+        {
           uint2 wb[kDRpw];
 #pragma unroll
           for (int r = 0; r < kDRpw; ++r)

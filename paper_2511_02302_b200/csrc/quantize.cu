@@ -29,30 +29,11 @@ namespace {
 
 constexpr int kA1Warps = 4;  // 128-thread CTAs (8-warp CTAs measured equal)
 
-__device__ __forceinline__ uint32_t absmax_bf16x2(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("max.xorsign.abs.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;  // per half: max(|a|, |b|) with the xor of the signs
-}
-
-// one 1x128 tile row held by 8 lanes (16 BF16 each): amax, scale byte, 16 codes, stores
+// one 1x128 tile row held by 8 lanes (16 BF16 each): common.cuh a1_quant16, then the stores
 __device__ __forceinline__ void a1_tile_row(const uint4 (&v)[2], int lane, bool ok, uint8_t* pq, uint8_t* ps) {
   const uint32_t w[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
-  const uint32_t m = absmax_bf16x2(absmax_bf16x2(absmax_bf16x2(w[0], w[1]), absmax_bf16x2(w[2], w[3])),
-                                   absmax_bf16x2(absmax_bf16x2(w[4], w[5]), absmax_bf16x2(w[6], w[7])));
-  uint32_t mag = max(m & 0x7FFFu, (m >> 16) & 0x7FFFu);
-  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 1));
-  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 2));
-  mag = max(mag, __shfl_xor_sync(0xffffffffu, mag, 4));
-  const int sb = max(static_cast<int>((mag + 0x1Fu) >> 7) - 8, 0);
-  const float inv = __uint_as_float(static_cast<uint32_t>(254 - sb) << 23);
-  const float2 iv = make_float2(inv, inv);
   uint32_t c[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float2 p = __fmul2_rn(make_float2(bf16lo_to_f32(w[j]), bf16hi_to_f32(w[j])), iv);
-    c[j] = cvt_e4m3x2_f32(p.x, p.y);
-  }
+  const uint32_t sb = a1_quant16(w, c);
   if (ok) {
     st_v4(pq, make_uint4(c[0] | (c[1] << 16), c[2] | (c[3] << 16), c[4] | (c[5] << 16), c[6] | (c[7] << 16)));
     if ((lane & 7) == 0) *ps = static_cast<uint8_t>(sb);
