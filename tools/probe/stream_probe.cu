@@ -82,3 +82,24 @@ extern "C" int probe_copy(const void* p, int64_t bytes, void* o, int grid, void*
   copy_kernel<4><<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)p, bytes / 16, (uint4*)o);
   return (int)cudaGetLastError();
 }
+
+// scatter-write probe: warp per row, rows in the order given (e.g. the permute plan's row_map
+// order), each row H bytes of a constant -- the DRAM write ceiling of the A3 move's pattern
+__global__ void __launch_bounds__(256) scatter_rows_kernel(const int32_t* __restrict__ order, int64_t nrows, int64_t H,
+                                                           uint4* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint4 v = make_uint4(0x3c3c3c3c, 0x3c3c3c3c, 0x3c3c3c3c, 0x3c3c3c3c);
+  for (int64_t i = w0; i < nrows; i += nw) {
+    const int32_t r = order[i];
+    if (r < 0) continue;
+    uint4* dst = out + static_cast<int64_t>(r) * (H / 16);
+    for (int64_t j = lane; j < H / 16; j += 32) dst[j] = v;
+  }
+}
+extern "C" int probe_scatter_rows(const void* order, int64_t nrows, int64_t H, void* out, int grid, void* stream) {
+  scatter_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const int32_t*>(order), nrows, H,
+                                                                           static_cast<uint4*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
