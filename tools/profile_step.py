@@ -1,7 +1,7 @@
 """Profiling driver (not product): warms up bench.py's step, then runs ONE serial pass of the
-step's 8 launches (whole DeepSeek-V3 layer on one GPU, bench.py's default strong partition) plus
+step's 8 launches (whole DeepSeek-V3 layer on one GPU, bench.py's default partition) plus
 the NEXT-row kernels on expert group 0 (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM,
-NEXT-3 dispatch and combine of rank 0 of 8 virtual EP ranks) between cudaProfilerStart/Stop, so
+fc1 Wgrad, dual-output quantize at 4096x7168, NEXT-3 dispatch and combine of rank 0 of 8 virtual EP ranks) between cudaProfilerStart/Stop, so
     ncu --set full --profile-from-start off ... python tools/profile_step.py [--partition weak]
 captures exactly one launch of each kernel, in this order."""
 import argparse
@@ -17,12 +17,13 @@ import synth  # noqa: E402
 
 ORDER = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
          "A2_transpose_xperm", "A2_transpose_a", "NEXT1_swiglu_bwd_quant", "NEXT1_swiglu_quant_dual",
-         "NEXT2_gemm_fc1_fprop", "NEXT3_dispatch_permute_pad", "NEXT3_combine_unpermute"]
+         "NEXT2_gemm_fc1_fprop", "NEXT2_gemm_fc1_wgrad (maps + GEMM)", "NEXT1_quantize_dual",
+         "NEXT3_dispatch_permute_pad", "NEXT3_combine_unpermute"]
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--partition", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--partition", choices=["strong", "balanced", "weak"], default="balanced")
     ap.add_argument("--no-next", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -41,12 +42,24 @@ def main():
         Dg = torch.empty(wl.R, 2 * bench.FFN, dtype=torch.bfloat16, device=dev)
         rows_dev = g0.off[E:]
         g0.launch_ops(record=False)
+        hT = torch.empty(wl.R * 2 * bench.FFN, dtype=torch.uint8, device=dev)
+        shT = torch.empty(wl.R // 128 + E, 2 * bench.FFN, dtype=torch.uint8, device=dev)
+        dW = torch.empty(E, 2 * bench.FFN, bench.HIDDEN, dtype=torch.bfloat16, device=dev)
+        wsw = torch.empty(F.fp8flow_gemm_wgrad_workspace_bytes(E), dtype=torch.uint8, device=dev)
+        xq = synth.activations_bf16_device(4096, bench.HIDDEN, synth.BASE_SEED + 9, dev)
+        qq = torch.empty(4096, bench.HIDDEN, dtype=torch.uint8, device=dev)
+        sq = torch.empty(bench.HIDDEN // 128, 4096, dtype=torch.uint8, device=dev)
+        qqT = torch.empty(4096 * bench.HIDDEN, dtype=torch.uint8, device=dev)
+        sqT = torch.empty(4096 // 128 + 1, bench.HIDDEN, dtype=torch.uint8, device=dev)
         st = bench.ep_setup(dev)  # NEXT-3: 8 virtual EP ranks on this device
 
         def extra():
             F.fp8flow_swiglu_bwd_quant(wl.h, dA, qb, sbw, rows_dev=rows_dev)
             F.fp8flow_swiglu_quant_dual(wl.h, g0.q_a, g0.s_a, g0.aT, g0.saT, seg_offsets=g0.off)
             F.fp8flow_gemm_blockscaled(g0.x_perm, g0.s_perm, W, sW, Dg, seg_offsets=g0.off)
+            F.fp8flow_scaling_aware_transpose(qb, sbw, hT, shT, seg_offsets=g0.off)
+            F.fp8flow_gemm_wgrad(hT, shT, g0.xT, g0.sxT, dW, g0.off, workspace=wsw)
+            F.fp8flow_quantize_dual(xq, qq, sq, qqT, sqT)
             st["receive"](0, kernel_only=True)
             st["ep"].combine(st["peers"], 0, st["tpr"], bench.HIDDEN, st["E"], st["ranks"][0]["topk"],
                              st["ranks"][0]["probs"], st["y"])
