@@ -17,7 +17,7 @@ import synth  # noqa: E402
 
 ORDER = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
          "A2_transpose_xperm", "A2_transpose_a", "NEXT1_swiglu_bwd_quant", "NEXT1_swiglu_quant_dual",
-         "NEXT2_gemm_fc1_fprop", "NEXT2_gemm_fc1_wgrad (maps + GEMM)", "NEXT1_quantize_dual",
+         "NEXT2_gemm_fc1_fprop", "A2_transpose_dH", "NEXT2_wgrad_maps", "NEXT2_gemm_fc1_wgrad", "NEXT1_quantize_dual",
          "NEXT3_dispatch_permute_pad", "NEXT3_combine_unpermute"]
 
 
