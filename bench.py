@@ -720,9 +720,50 @@ def next_ops_measure(device, peak: float, reps: int = 20, checks: list | None = 
                           F.fp8flow_scaling_aware_transpose(ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off)))
     ms = med(lambda: F.fp8flow_swiglu_quant_dual(wl.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off))
     out["NEXT1_swiglu_quant_dual"] = line(ms, nb, segments=len(segs), vs_A5_then_A2_us=round(ms_two * 1e3, 2))
+    out.update({"dual_" + k: v for k, v in dual_fusions_measure(ds, wl, peak).items()})
     out.update(gemm_measure(ds, reps=10, checks=checks))
     out.update(ep_measure(device, peak, reps))
     return out
+
+
+def dual_fusions_measure(ds, wl, peak: float) -> dict:
+    """NEXT-1 dual outputs on a workload's step buffers: the A3 move fused with A2 (one gather, X_perm
+    and X_perm^T) against the move then A2(X_perm), and SwiGLU + quant fused with A2 against A5 then
+    A2(A); marginal cold-L2 costs, and every defined output byte compared with the unfused launches'
+    (which the step's verification compares with the oracle)."""
+    F, fns = ds.F, ds.op_fns()
+    seg = [int(x) for x in wl.padded]
+    blocks = sum((x + 127) // 128 for x in seg)
+    R = sum(seg)
+    keys = {"x_perm": lambda t: t[:R], "s_perm": lambda t: t[:, :R], "xT": lambda t: t[: R * HIDDEN],
+            "sxT": lambda t: t[:blocks], "q_a": lambda t: t[:R], "s_a": lambda t: t[:, :R],
+            "aT": lambda t: t[: R * FFN], "saT": lambda t: t[:blocks]}
+    for op in ("A3_move", "A2_transpose_xperm", "A5_swiglu_quant", "A2_transpose_a"):
+        fns[op]()
+    torch.cuda.synchronize()
+    ref = {k: v(getattr(ds, k)).clone() for k, v in keys.items()}
+    pd = lambda: F.fp8flow_permute_pad_dual(wl.q_recv, wl.s_recv, ds.src, ds.off, ds.x_perm, ds.s_perm,  # noqa: E731
+                                            ds.xT, ds.sxT)
+    sd = lambda: F.fp8flow_swiglu_quant_dual(wl.h, ds.q_a, ds.s_a, ds.aT, ds.saT, seg_offsets=ds.off,  # noqa: E731
+                                             rows_dev=ds.off[wl.E_loc:])
+    for k in keys:
+        getattr(ds, k).fill_(0xEE)
+    pd()
+    sd()
+    torch.cuda.synchronize()
+    same = all(torch.equal(ref[k], v(getattr(ds, k))) for k, v in keys.items())
+    del ref
+    t = {"move": marginal_us(fns["A3_move"], ds.flush_l2), "a2x": marginal_us(fns["A2_transpose_xperm"], ds.flush_l2),
+         "pd": marginal_us(pd, ds.flush_l2), "a5": marginal_us(fns["A5_swiglu_quant"], ds.flush_l2),
+         "a2a": marginal_us(fns["A2_transpose_a"], ds.flush_l2), "sd": marginal_us(sd, ds.flush_l2)}
+
+    def line(us, nb, two_us):
+        return {"us": round(us, 2), "bytes": nb, "gbs": round(nb / us / 1e3, 1), "frac": round(nb / us / 1e3 / peak, 3),
+                "unfused_us": round(two_us, 2), "speedup_vs_unfused": round(two_us / us, 3)}
+    return {"NEXT1_permute_pad_dual": line(t["pd"], RL.permute_dual_bytes(wl.T_recv, seg, HIDDEN), t["move"] + t["a2x"]),
+            "NEXT1_swiglu_quant_dual": line(t["sd"], RL.swiglu_quant_dual_bytes(seg, FFN), t["a5"] + t["a2a"]),
+            "identical_to_unfused": same,
+            "note": "unfused_us = marginal(move) + marginal(A2 X_perm), resp. marginal(A5) + marginal(A2 A)"}
 
 
 def ep_setup(device) -> dict:
@@ -1248,6 +1289,7 @@ def main():
     checks: list = []
     extra = {}
     if rank == 0 and world == 1 and not args.no_next:
+        extra["dual_fusions"] = {"workload": cfg["workload"], **dual_fusions_measure(ds, wl, peak)}
         extra["cfg2"] = cfg2_measure(device, peak)
         extra["next_ops"] = next_ops_measure(device, peak, checks=checks)
     threads = max(1, cpu_cores() // world)

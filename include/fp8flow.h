@@ -238,6 +238,28 @@ FP8FLOW_API int fp8flow_swiglu_quant_dual(const void* h_bf16, int64_t rows_max, 
                                           int64_t ffn, const int32_t* seg_offsets, int32_t num_segs, uint8_t* q,
                                           uint8_t* s, int64_t ld_s, uint8_t* qT, uint8_t* sT, void* stream);
 
+/* fp8flow_permute_pad_dual -- the A3 move fused with A2 (NEXT-1 dual output, R37): one
+ *     gather of each 128 x 128 block of the padded expert-major tensor produces both the row-wise
+ *     output of fp8flow_permute_pad (X_perm, the Fprop operand) and its scaling-aware transpose per
+ *     expert (A2 with segments = expert_offsets, the Wgrad operand).  By
+ *     definition bit-identical to fp8flow_permute_pad followed by fp8flow_scaling_aware_transpose(
+ *     q_out, s_out, ld_s = max_rows, rows = R, seg_offsets = expert_offsets, num_segs = E_loc),
+ *     without the second pass over X_perm.
+ *   q_tok, s_tok, ld_s_tok, num_tokens, hidden: as fp8flow_permute_pad (row-wise FP8 tokens)
+ *   src_of_row, expert_offsets, num_local_experts, max_rows: the plan's (fp8flow_permute_plan), made
+ *                with align % 16 == 0 (A2's segment lengths are multiples of 16); offsets past
+ *                max_rows (an overflowed plan) are clamped to it
+ *   q_out [max_rows][hidden], s_out [hidden/128][max_rows]: as fp8flow_permute_pad
+ *   qT, sT: as fp8flow_scaling_aware_transpose (capacity hidden * max_rows and
+ *           hidden * (max_rows/128 + E_loc) bytes)
+ *   hidden % 128 == 0, max_rows % 16 == 0, ld_s_tok % 4 == 0 (scale bytes are fetched as the 4-byte
+ *   words holding them); q_tok, s_tok, q_out, s_out, qT, sT, src_of_row 16-byte aligned;
+ *   num_tokens == 0 is a no-op. */
+FP8FLOW_API int fp8flow_permute_pad_dual(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok,
+                                         int64_t num_tokens, int64_t hidden, const int32_t* src_of_row,
+                                         const int32_t* expert_offsets, int32_t num_local_experts, int64_t max_rows,
+                                         uint8_t* q_out, uint8_t* s_out, uint8_t* qT, uint8_t* sT, void* stream);
+
 /* ==========================================================================================
  * NEXT-2  Block-scaled FP8 GEMM, the consumer of the casting-free path (
  *     P:43): the row-wise (A1/A3/A5) or column-wise (A2) FP8 outputs with their

@@ -267,6 +267,27 @@ int fp8flow_swiglu_quant_dual(const void* h_bf16, int64_t rows_max, const int32_
                                            sT, static_cast<cudaStream_t>(stream), sms));
 }
 
+int fp8flow_permute_pad_dual(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t num_tokens,
+                             int64_t hidden, const int32_t* src_of_row, const int32_t* expert_offsets,
+                             int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out, uint8_t* qT,
+                             uint8_t* sT, void* stream) {
+  if (num_tokens < 0 || hidden <= 0 || hidden % 128 != 0 || max_rows < 0 || max_rows % 16 != 0)
+    return FP8FLOW_ERR_SHAPE;
+  if (ld_s_tok < num_tokens || ld_s_tok % 4 != 0 || num_tokens > INT32_MAX || max_rows > INT32_MAX - 128)
+    return FP8FLOW_ERR_SHAPE;
+  if (num_local_experts < 1 || num_local_experts > 1024) return FP8FLOW_ERR_ARG;
+  if (max_rows == 0 || num_tokens == 0) return FP8FLOW_OK;  // no tokens: every expert is empty
+  if (!q_tok || !s_tok || !src_of_row || !expert_offsets || !q_out || !s_out || !qT || !sT) return FP8FLOW_ERR_NULL;
+  if (!aligned16(q_tok) || !aligned16(s_tok) || !aligned16(q_out) || !aligned16(s_out) || !aligned16(qT) ||
+      !aligned16(sT) || !aligned16(src_of_row))
+    return FP8FLOW_ERR_ALIGN;
+  int sms = 0, st = device(&sms);
+  if (st != FP8FLOW_OK) return st;
+  return launched(launch_permute_pad_dual(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets,
+                                          num_local_experts, max_rows, q_out, s_out, qT, sT,
+                                          static_cast<cudaStream_t>(stream), sms));
+}
+
 int fp8flow_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B, const uint8_t* sb,
                              int64_t ld_sb, int64_t M, int64_t N, int64_t K, const int32_t* seg_offsets,
                              int32_t num_groups, void* D, int32_t d_f32, void* stream) {

@@ -89,6 +89,10 @@ cudaError_t launch_quantize_dual(const void* x, int64_t rows, int64_t cols, cons
 cudaError_t launch_swiglu_quant_dual(const void* h, int64_t rows_max, const int32_t* rows_dev, int64_t ffn,
                                      const int32_t* seg_offsets, int32_t num_segs, uint8_t* q, uint8_t* s,
                                      int64_t ld_s, uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms);
+cudaError_t launch_permute_pad_dual(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
+                                    const int32_t* src_of_row, const int32_t* expert_offsets,
+                                    int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
+                                    uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms);
 cudaError_t launch_gemm_blockscaled(const uint8_t* A, const uint8_t* sa, int64_t ld_sa, const uint8_t* B,
                                     const uint8_t* sb, int64_t ld_sb, int64_t M, int64_t N, int64_t K,
                                     const int32_t* seg_offsets, int32_t num_groups, void* D, int32_t d_f32,

@@ -4,6 +4,7 @@
 // tile index maps to (segment, row block) without any host synchronisation.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 
 namespace fp8flow {
@@ -35,9 +36,12 @@ __device__ __forceinline__ int block_exclusive_scan(int v, uint32_t* warp_tmp, i
 
 // Loads the segment offsets into seg_off[0..num_segs] and builds blk_prefix[e] = sum_{e'<e}
 // ceil(m_e'/128) in shared memory; *total_rb = blk_prefix[num_segs].  NT * 4 > num_segs.
+// clamp: every offset is first clamped to it (an overflowed permute plan reports its true padded
+// total past the buffer's capacity; its consumers see the rows that exist).
 template <int NT>
 __device__ __forceinline__ void load_segments(int32_t* seg_off, int32_t* blk_prefix, uint32_t* red, int32_t* total_rb,
-                                              const int32_t* seg_offsets, int32_t num_segs, int64_t rows) {
+                                              const int32_t* seg_offsets, int32_t num_segs, int64_t rows,
+                                              int32_t clamp = INT32_MAX) {
   const int tid = threadIdx.x;
   if (seg_offsets == nullptr) {  // one segment: no scan, one barrier
     if (tid == 0) {
@@ -51,7 +55,7 @@ __device__ __forceinline__ void load_segments(int32_t* seg_off, int32_t* blk_pre
     __syncthreads();
     return;
   }
-  for (int i = tid; i <= num_segs; i += NT) seg_off[i] = seg_offsets[i];
+  for (int i = tid; i <= num_segs; i += NT) seg_off[i] = min(seg_offsets[i], clamp);
   __syncthreads();
   // 4 consecutive segments per thread (num_segs <= 1024)
   int nb[4], tsum = 0;
@@ -97,6 +101,72 @@ __device__ __forceinline__ int find_segment(const int32_t* blk_prefix, int num_s
     else hi = mid;
   }
   return lo;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// A2's tile walk over 128x128 blocks of segmented rows (used by A2 and the permute dual kernel)
+// ------------------------------------------------------------------------------------------
+constexpr int kRowGroup = 8;  // row blocks of a segment walked together (tile order)
+
+struct TileCoord {
+  int32_t o, m;     // segment row offset and length
+  int32_t ib, jb;   // row block inside the segment, column block
+  int32_t rb;       // global row-block index of the output scales
+  int32_t rows_valid;
+  int32_t pad[2];
+};
+
+
+struct SegTables {
+  const int32_t* seg_off;
+  const int32_t* blk_prefix;
+};
+
+// Tile order (segment-major): for each segment e, its row blocks in groups of kRowGroup, and inside
+// a group column block jb, then row block ib fastest.  Consecutive tiles -- the ones the persistent
+// CTAs hold at the same time -- therefore read whole input rows of up to 1024 rows (contiguous) and
+// write, for each output row j, up to 1024 contiguous bytes: at the whole-layer size (256 experts,
+// output rows of ~520 bytes spread over 1 GB) a row-block-major order left the L2 evicting 128-byte
+// pieces of ~60 MB of scattered output (r02: 0.54 of peak).  Tile t -> (e, ib, jb):
+//   e = segment of virtual row block t / n_jb (segment tiles = n_jb * blocks, contiguous in t),
+//   t' = t - n_jb * blk_prefix[e], group g = t' / (n_jb * RG), gsz = min(RG, nblk - g * RG),
+//   u = t' - g * n_jb * RG, jb = u / gsz, ib = g * RG + u % gsz.
+__device__ __forceinline__ TileCoord tile_coord(const SegTables& sm, int nsegs, int n_jb, int t) {
+  const int rbv = t / n_jb;
+  const int e = find_segment(sm.blk_prefix, nsegs, rbv);
+  const int b0 = sm.blk_prefix[e];
+  const int nblk = sm.blk_prefix[e + 1] - b0;
+  const int tp = t - b0 * n_jb;
+  const int g = tp / (n_jb * kRowGroup);
+  const int gsz = min(kRowGroup, nblk - g * kRowGroup);
+  const int u = tp - g * n_jb * kRowGroup;
+  const int jb = u / gsz;
+  const int ib = g * kRowGroup + (u - jb * gsz);
+  TileCoord c;
+  c.o = sm.seg_off[e];
+  c.m = sm.seg_off[e + 1] - c.o;
+  c.ib = ib;
+  c.jb = jb;
+  c.rb = b0 + ib;
+  c.rows_valid = min(kTile, c.m - ib * kTile);
+  return c;
+}
+
+// The same walk split into column chunks of `ch` blocks: all segments' tiles of column blocks
+// [q*ch, q*ch + ch) before those of the next chunk (the last chunk may be narrower); inside a chunk
+// tile_coord's segment-major order over the chunk's columns.  A kernel that gathers its input rows
+// (the permute dual kernel) then reads only ch * 128 bytes of each source row per chunk.
+__device__ __forceinline__ TileCoord tile_coord_chunked(const SegTables& sm, int nsegs, int n_jb, int total_rb, int ch,
+                                                        int t) {
+  const int nq = (n_jb + ch - 1) / ch;
+  const int per_chunk = total_rb * ch;
+  const int q = min(t / per_chunk, nq - 1);
+  const int w = min(ch, n_jb - q * ch);
+  const int tc = t - q * per_chunk;
+  TileCoord c = tile_coord(sm, nsegs, w, tc);
+  c.jb += q * ch;
+  return c;
 }
 
 }  // namespace fp8flow

@@ -43,15 +43,6 @@ template <int WS>
 __host__ __device__ constexpr int a2_threads() { return kTConsumers + 32 * WS + 32; }  // + WS store warps + 1 producer
 constexpr int kMaxSegs = 1024;
 constexpr int kTileBytes = kTile * kTile;
-constexpr int kRowGroup = 8;                  // row blocks of a segment walked together (tile order)
-
-struct TileCoord {
-  int32_t o, m;     // segment row offset and length
-  int32_t ib, jb;   // row block inside the segment, column block
-  int32_t rb;       // global row-block index of the output scales
-  int32_t rows_valid;
-  int32_t pad[2];
-};
 
 template <int STAGES, int OUTBUF>
 struct TransposeSmem {
@@ -73,41 +64,6 @@ template <typename Smem>
 __host__ __device__ constexpr size_t a2_smem_bytes(int nsegs) {
   return (sizeof(Smem) + 15) / 16 * 16 + 8 * static_cast<size_t>(nsegs + 1);
 }
-struct SegTables {
-  const int32_t* seg_off;
-  const int32_t* blk_prefix;
-};
-
-// Tile order (segment-major): for each segment e, its row blocks in groups of kRowGroup, and inside
-// a group column block jb, then row block ib fastest.  Consecutive tiles -- the ones the persistent
-// CTAs hold at the same time -- therefore read whole input rows of up to 1024 rows (contiguous) and
-// write, for each output row j, up to 1024 contiguous bytes: at the whole-layer size (256 experts,
-// output rows of ~520 bytes spread over 1 GB) a row-block-major order left the L2 evicting 128-byte
-// pieces of ~60 MB of scattered output (r02: 0.54 of peak).  Tile t -> (e, ib, jb):
-//   e = segment of virtual row block t / n_jb (segment tiles = n_jb * blocks, contiguous in t),
-//   t' = t - n_jb * blk_prefix[e], group g = t' / (n_jb * RG), gsz = min(RG, nblk - g * RG),
-//   u = t' - g * n_jb * RG, jb = u / gsz, ib = g * RG + u % gsz.
-__device__ __forceinline__ TileCoord tile_coord(const SegTables& sm, int nsegs, int n_jb, int t) {
-  const int rbv = t / n_jb;
-  const int e = find_segment(sm.blk_prefix, nsegs, rbv);
-  const int b0 = sm.blk_prefix[e];
-  const int nblk = sm.blk_prefix[e + 1] - b0;
-  const int tp = t - b0 * n_jb;
-  const int g = tp / (n_jb * kRowGroup);
-  const int gsz = min(kRowGroup, nblk - g * kRowGroup);
-  const int u = tp - g * n_jb * kRowGroup;
-  const int jb = u / gsz;
-  const int ib = g * kRowGroup + (u - jb * gsz);
-  TileCoord c;
-  c.o = sm.seg_off[e];
-  c.m = sm.seg_off[e + 1] - c.o;
-  c.ib = ib;
-  c.jb = jb;
-  c.rb = b0 + ib;
-  c.rows_valid = min(kTile, c.m - ib * kTile);
-  return c;
-}
-
 // WS > 0 (store-warp mode, OUTBUF == 2): WS extra warps drain the staging buffers (read-out and
 // global stores) while the 8 consumer warps shift and transpose the next tile; buffers are handed
 // over on out_full / out_empty mbarriers instead of consumer-wide barriers.

@@ -46,6 +46,7 @@ SIGNATURES = {
     "fp8flow_swiglu_bwd_quant": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _I64, _P]),
     "fp8flow_quantize_dual": (ctypes.c_int, [_P, _I64, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
     "fp8flow_swiglu_quant_dual": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I32, _P, _P, _I64, _P, _P, _P]),
+    "fp8flow_permute_pad_dual": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _P, _I32, _I64, _P, _P, _P, _P, _P]),
     "fp8flow_gemm_blockscaled": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _P, _I32, _P]),
     "fp8flow_gemm_wgrad_workspace_bytes": (_I64, [_I32]),
     "fp8flow_gemm_wgrad": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _P, _I32, _P, _I32, _P, _I64, _P]),
@@ -252,6 +253,16 @@ def fp8flow_swiglu_quant_dual(h: torch.Tensor, q: torch.Tensor, s: torch.Tensor,
     _check(lib().fp8flow_swiglu_quant_dual(_ptr(h), rows_max, _ptr(rows_dev), F2 // 2, _ptr(seg_offsets), nseg,
                                            _ptr(_u8(q)), _ptr(_u8(s)), s.shape[1], _ptr(_u8(qT)), _ptr(_u8(sT)),
                                            _stream(stream)), "fp8flow_swiglu_quant_dual")
+
+
+def fp8flow_permute_pad_dual(q_tok, s_tok, src_of_row, expert_offsets, q_out, s_out, qT, sT, stream=None) -> None:
+    """NEXT-1 dual output of the A3 move: (q_out, s_out) as fp8flow_permute_pad and (qT, sT) as A2 of them
+    with the plan's expert offsets as segments."""
+    T, H = q_tok.shape
+    _check(lib().fp8flow_permute_pad_dual(_ptr(_u8(q_tok)), _ptr(_u8(s_tok)), s_tok.shape[1], T, H, _ptr(src_of_row),
+                                          _ptr(expert_offsets), expert_offsets.numel() - 1, q_out.shape[0],
+                                          _ptr(_u8(q_out)), _ptr(_u8(s_out)), _ptr(_u8(qT)), _ptr(_u8(sT)),
+                                          _stream(stream)), "fp8flow_permute_pad_dual")
 
 
 def fp8flow_gemm_blockscaled(A: torch.Tensor, sa: torch.Tensor, B: torch.Tensor, sb: torch.Tensor, D: torch.Tensor,

@@ -75,6 +75,16 @@ def swiglu_quant_dual_bytes(seg_lengths, ffn: int) -> int:
     return m * (4 * ffn + ffn + ffn) + m * (ffn // 128) + blocks * ffn
 
 
+def permute_dual_bytes(unique_src_rows: int, seg_lengths, hidden: int) -> int:
+    """NEXT-1 dual A3 move: each source token's codes + scales read once, every padded row written
+    row-wise (codes + scales) and column-wise (codes + one scale byte per (128-row block, column)),
+    src_of_row read."""
+    m = sum(seg_lengths)
+    blocks = sum((x + 127) // 128 for x in seg_lengths)
+    row = hidden + hidden // 128
+    return unique_src_rows * row + m * row + m * hidden + blocks * hidden + m * 4
+
+
 def dispatch_permute_bytes(unique_recv_tokens: int, padded_rows: int, total_tokens: int, top_k: int,
                            hidden: int) -> int:
     """NEXT-3 dispatch + permute (receive side): every routed token's codes + scales read once from
