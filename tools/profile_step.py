@@ -1,6 +1,6 @@
 """Profiling driver (not product): warms up bench.py's step, then runs ONE serial pass of the
 step's 8 launches (whole DeepSeek-V3 layer on one GPU, bench.py's default partition) plus
-the NEXT-row kernels on expert group 0 (SwiGLU backward, dual-output SwiGLU, grouped fc1 GEMM,
+the NEXT-row kernels on expert group 0 (SwiGLU backward, dual-output SwiGLU, dual-output move, grouped fc1 GEMM,
 fc1 Wgrad, dual-output quantize at 4096x7168, NEXT-3 dispatch and combine of rank 0 of 8 virtual EP ranks) between cudaProfilerStart/Stop, so
     ncu --set full --profile-from-start off ... python tools/profile_step.py [--partition weak]
 captures exactly one launch of each kernel, in this order."""
@@ -17,6 +17,7 @@ import synth  # noqa: E402
 
 ORDER = ["A1_quantize_x", "A3_plan", "A3_move", "A5_swiglu_quant", "A4_unpermute", "A1_quantize_dy",
          "A2_transpose_xperm", "A2_transpose_a", "NEXT1_swiglu_bwd_quant", "NEXT1_swiglu_quant_dual",
+         "NEXT1_permute_pad_dual",
          "NEXT2_gemm_fc1_fprop", "A2_transpose_dH", "NEXT2_wgrad_maps", "NEXT2_gemm_fc1_wgrad", "NEXT1_quantize_dual",
          "NEXT3_dispatch_permute_pad", "NEXT3_combine_unpermute"]
 
@@ -56,6 +57,7 @@ def main():
         def extra():
             F.fp8flow_swiglu_bwd_quant(wl.h, dA, qb, sbw, rows_dev=rows_dev)
             F.fp8flow_swiglu_quant_dual(wl.h, g0.q_a, g0.s_a, g0.aT, g0.saT, seg_offsets=g0.off)
+            F.fp8flow_permute_pad_dual(wl.q_recv, wl.s_recv, g0.src, g0.off, g0.x_perm, g0.s_perm, g0.xT, g0.sxT)
             F.fp8flow_gemm_blockscaled(g0.x_perm, g0.s_perm, W, sW, Dg, seg_offsets=g0.off)
             F.fp8flow_scaling_aware_transpose(qb, sbw, hT, shT, seg_offsets=g0.off)
             F.fp8flow_gemm_wgrad(hT, shT, g0.xT, g0.sxT, dW, g0.off, workspace=wsw)
