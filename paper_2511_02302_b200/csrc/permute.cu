@@ -8,16 +8,18 @@
 // the end of each expert; R17 PAD = code 0x00 + scale byte 0x00; R21 gates applied at unpermute,
 // fp32 fused multiply-add in k order, BF16 RNE output.
 //
-// Plan (deterministic, no CUB, no host sync), two kernels over 512-token chunks:
-//   K1 plan_count : per chunk, a shared-memory histogram over the local experts
-//   K2 plan_place : per chunk, the expert offsets (padded sizes, exclusive scan over experts) and
-//                   the chunk's per-expert base are derived from the small count table; an
-//                   (expert x token) bit matrix in shared memory gives each token's rank inside
-//                   its experts as a prefix popcount, so row = offset[e] + base[e] + rank is
-//                   stable in token order.  Chunk 0 also writes expert_offsets and the PAD rows.
-// Move: warp item = 4 consecutive output rows (balanced contiguous item ranges per warp, one wave
-// of CTAs); the 4 rows stream with 128-bit loads and stores (16 in flight per lane), their scale
-// bytes are gathered per 1x128 tile (all gathers issued before the stores).
+// Plan (deterministic, no CUB, no host sync) over 512-token chunks, one thread per token:
+//   plan_fused_kernel (one cooperative launch when every chunk CTA fits on the GPU at once, up to
+//   ~150k tokens): each CTA builds its chunk's shared-memory histogram over the local experts, a
+//   grid sync, then every CTA derives the expert offsets (padded sizes, exclusive scan over experts)
+//   and its chunk's per-expert base from the count table; an (expert x token) bit matrix in shared
+//   memory gives each token's rank inside its experts as a prefix popcount, so row = offset[e] +
+//   base[e] + rank is stable in token order; chunk 0 also writes expert_offsets and the PAD rows.
+//   Beyond that size the same two phases run as two kernels (plan_count_kernel, plan_place_kernel).
+// Move: fp8flow_permute_pad is the one-rank case of the fused dispatch engine (ep.cu): each token
+// read once by a 1D bulk copy and written to all of its local rows by bulk stores.
+// Unpermute (A4, below): warp per token, rows taken several at a time with 128-bit loads, fp32 FMA
+// in k order, BF16 RNE stores.
 #include <cooperative_groups.h>
 
 #include "async.cuh"
