@@ -18,8 +18,9 @@
 //   Beyond that size the same two phases run as two kernels (plan_count_kernel, plan_place_kernel).
 // Move: fp8flow_permute_pad is the one-rank case of the fused dispatch engine (ep.cu): each token
 // read once by a 1D bulk copy and written to all of its local rows by bulk stores.
-// Unpermute (A4, below): warp per token, rows taken several at a time with 128-bit loads, fp32 FMA
-// in k order, BF16 RNE stores.
+// Unpermute (A4, below): a bulk-copy engine -- one producer warp streams each token's local rows
+// into a shared-memory ring, 7 consumer warps accumulate them in fp32 FMA in k order and store
+// BF16 (RNE) with 128-bit stores.
 #include <cooperative_groups.h>
 
 #include "async.cuh"
