@@ -108,6 +108,19 @@ def test_validation_of_next_row_entry_points(L):
     assert L.fp8flow_gemm_blockscaled(None, a16, 32, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 1
     assert L.fp8flow_gemm_blockscaled(P(8), a16, 32, a16, a16, 256, 32, 256, 128, None, 0, a16, 1, None) == 3
     assert L.fp8flow_gemm_blockscaled(None, None, 0, None, None, 256, 0, 256, 128, None, 0, None, 1, None) == 0
+    # fused move + A2: hidden % 128, max_rows % 16, scale pitch (>= tokens, % 4), expert count, NULL,
+    # alignment; no tokens = no-op
+    pd = L.fp8flow_permute_pad_dual
+    assert pd(a16, a16, 64, 64, 100, a16, a16, 4, 64, a16, a16, a16, a16, None) == 2
+    assert pd(a16, a16, 64, 64, 128, a16, a16, 4, 60, a16, a16, a16, a16, None) == 2
+    assert pd(a16, a16, 32, 64, 128, a16, a16, 4, 64, a16, a16, a16, a16, None) == 2
+    assert pd(a16, a16, 66, 64, 128, a16, a16, 4, 64, a16, a16, a16, a16, None) == 2
+    assert pd(a16, a16, 64, 64, 128, a16, a16, 0, 64, a16, a16, a16, a16, None) == 4
+    assert pd(a16, a16, 64, 64, 128, a16, a16, 2000, 64, a16, a16, a16, a16, None) == 4
+    assert pd(a16, a16, 64, 64, 128, a16, a16, 4, 64, a16, a16, None, a16, None) == 1
+    assert pd(P(8), a16, 64, 64, 128, a16, a16, 4, 64, a16, a16, a16, a16, None) == 3
+    assert pd(a16, P(8), 64, 64, 128, a16, a16, 4, 64, a16, a16, a16, a16, None) == 3
+    assert pd(None, None, 0, 0, 128, None, None, 4, 64, None, None, None, None, None) == 0
     # Wgrad: Ma % 128, Nb % 256, groups required, NULL, workspace size and alignment
     a128 = P(128)
     assert L.fp8flow_gemm_wgrad_workspace_bytes(4) == 1024
