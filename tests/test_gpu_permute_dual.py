@@ -160,3 +160,16 @@ def test_permute_pad_dual_zero_tokens_is_noop(F):
     F.fp8flow_permute_pad_dual(q_tok, s_tok, src, off, q_out, s_out, qT, sT)
     torch.cuda.synchronize()
     assert torch.all(q_out == 0xEE) and torch.all(qT == 0xEE)
+
+
+@pytest.mark.parametrize("T,H,E,K,align", [(50, 128, 1024, 2, 16), (300, 384, 7, 3, 32), (1, 256, 4, 1, 16),
+                                           (129, 1152, 2, 2, 16)])
+def test_permute_pad_dual_edge_shapes(F, orc, T, H, E, K, align):
+    """One column block (H = 128), 1024 local experts (most empty: the largest segment table),
+    align 32, a single token (one expert of 16 rows, 15 of them PAD), an expert of 129 + PAD rows
+    (a full block and a 16-row partial one) with an odd number of column blocks."""
+    rng = np.random.default_rng(T + H)
+    q_tok = rng.integers(0, 256, (T, H), dtype=np.uint8)
+    s_tok = rng.integers(100, 135, (H // 128, T), dtype=np.uint8)
+    topk = np.stack([rng.permutation(E)[:K] for _ in range(T)]).astype(np.int32)
+    check(F, orc, q_tok, s_tok, topk, 0, E, align=align)
