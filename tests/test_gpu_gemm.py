@@ -159,11 +159,13 @@ def test_gemm_dgrad_on_transposed_weights(F, orc):
 
 
 @pytest.mark.parametrize("m,Ma,Nb,bf16", [([128, 256], 128, 256, False), ([16, 0, 144, 528, 48], 128, 256, False),
-                                          ([16, 0, 144, 528, 48], 384, 512, False), ([272, 0, 32], 512, 768, True)])
+                                          ([16, 0, 144, 528, 48], 384, 512, False), ([272, 0, 32], 512, 768, True),
+                                          ([16, 0, 144, 528, 48], 128, 1792, False), ([272, 0, 32], 256, 1792, True)])
 def test_gemm_wgrad_grouped_k(F, orc, m, Ma, Nb, bf16):
     """Wgrad with groups over K (each expert's tokens, multiples of 16, an empty expert, partial K
     blocks): dW_e = dH_e^T X_e straight from A2's column-wise outputs of dH and X_perm.  Ma = 128
-    and 384 leave the last CTA pair half outside Ma; fp32 and BF16 outputs."""
+    and 384 leave the last CTA pair half outside Ma; fp32 and BF16 outputs; Nb = 1792 (7 column
+    tiles: an odd count of 256-column tiles per 256-row block pair)."""
     seg = np.concatenate([[0], np.cumsum(m)]).astype(np.int32)
     R = int(seg[-1])
     dh = synth.normal_bf16(R, Ma, 91)
