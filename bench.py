@@ -1306,6 +1306,7 @@ def main():
             "dtypes": {"codes": "e4m3 (u8)", "scales": "ue8m0 (u8)", "bf16_io": "bf16", "math": "fp32 (fp64 refine)"},
             "data": "synthetic (seeded, drawn on the device; DeepSeek-V3 shapes, skewed routing)", "config": cfg,
             "frac_of_hbm_peak": round(value / world / peak, 3),
+            "frac_of_nominal_8000": round(value / world / 8000.0, 3),  # B200 HBM3e nominal
             "per_gpu_gbs": round(value / world, 1),
             "load_imbalance": round(imbalance, 3),
             "step_us_quantiles": {q: round(float(np.percentile(step_ms, p)) * 1e3, 1)
