@@ -79,6 +79,7 @@ class Workload:
 
         t0 = time.time()
         self.F, self.dev, self.mode = F, device, mode
+        self.rank, self.world = rank, world
         sh = D.shard(rank, world, mode, N_EXPERTS, T_GLOBAL)
         self.shard = sh
         self.e0, self.E_loc = sh["expert_begin"], sh["num_local_experts"]
@@ -510,6 +511,10 @@ def cpu_baseline_leg(wl: Workload, ds: DeviceStep, time_it: bool, verify: bool, 
                                 f"precision): A1 {wl.n_shard}x{HIDDEN} x2, A3 plan+move {wl.T_recv} tokens -> "
                                 f"{wl.R} rows over {wl.E_loc} experts, A5 {wl.R}x{2 * FFN}, A4 {wl.T_recv} "
                                 f"tokens, A2 {wl.R}x{HIDDEN} + {wl.R}x{FFN}"}
+        # also single-threaded, on the reference arm's bounded sample of the same step
+        b1, t1, d1 = oracle_sample(O, 1.0 / 32, 1, wl.rank, wl.world, wl.mode)
+        out["cpu"]["single_thread"] = {"value": round(b1 / t1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                                       "seconds": round(t1, 2), "sample": d1}
     if not verify:
         return out
     gpu = getattr(ds, "host_out", None)

@@ -129,6 +129,8 @@ def merge_rank_reports(reports: list[dict]) -> dict:
                                "sample": cpu[0]["sample"] + (f" (x{len(cpu)} ranks, each on its own shard, "
                                                             "concurrently)" if len(cpu) > 1 else ""),
                                "seconds": round(secs, 2)}
+        if cpu[0].get("single_thread"):  # rank 0's single-threaded timing of a bounded sample
+            out["cpu_baseline"]["single_thread"] = cpu[0]["single_thread"]
     return out
 
 
