@@ -1161,8 +1161,8 @@ def gemm_measure(ds: "DeviceStep", reps: int = 10, checks: list | None = None) -
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--partition", choices=["strong", "balanced", "weak"], default="balanced",
                     help="strong: the layer's 256 experts split over the GPUs in id ranges (N=1: whole layer); "
