@@ -692,6 +692,45 @@ def cfg2_measure(device, peak: float, reps: int = 20) -> dict:
     return out
 
 
+def cfg1_measure(device, reps: int = 20) -> dict:
+    """Config 1 (256 x 256, the oracle's correctness config): launch-latency bound on the GPU, so
+    per SURVEY 8(d) each op is timed inside a CUDA graph (50 launches per replay) to separate the
+    launch overhead; no GB/s claim.  A1, A2 and the round trip A1 -> A2 (its output checked against
+    A2 applied to A1's output by the oracle is part of the GPU tests, not repeated here)."""
+    from paper_2511_02302_b200 import fp8flow as F
+
+    rows = cols = 256
+    x = synth.activations_bf16_device(rows, cols, synth.BASE_SEED + 11, device)
+    q = torch.empty(rows, cols, dtype=torch.uint8, device=device)
+    s = torch.empty(cols // 128, rows, dtype=torch.uint8, device=device)
+    qT = torch.empty(rows * cols, dtype=torch.uint8, device=device)
+    sT = torch.empty(rows // 128 + 1, cols, dtype=torch.uint8, device=device)
+    ops = {"A1_quantize": lambda: F.fp8flow_quantize_rowwise(x, q, s),
+           "A2_transpose": lambda: F.fp8flow_scaling_aware_transpose(q, s, qT, sT),
+           "A1_then_A2": lambda: (F.fp8flow_quantize_rowwise(x, q, s), F.fp8flow_scaling_aware_transpose(q, s, qT, sT))}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    out = {"shape": [rows, cols], "timing": "CUDA graph of 50 back-to-back launches, replayed; us per launch "
+                                            "(median of replays); latency-bound, no GB/s claim"}
+    for name, fn in ops.items():
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(50):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            ev[0].record()
+            g.replay()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]) / 50)
+        out[name] = {"us": round(statistics.median(ts) * 1e3, 2)}
+    return out
+
+
 def next_ops_measure(device, peak: float, reps: int = 20, checks: list | None = None) -> dict:
     """NEXT rows on one EP8 expert group of the layer (group 0, 32 experts; not part of the
     headline step): NEXT-1 fused SwiGLU backward + quant and the dual-output SwiGLU + quant,
@@ -1295,6 +1334,7 @@ def main():
     extra = {}
     if rank == 0 and world == 1 and not args.no_next:
         extra["dual_fusions"] = {"workload": cfg["workload"], **dual_fusions_measure(ds, wl, peak)}
+        extra["cfg1"] = cfg1_measure(device)
         extra["cfg2"] = cfg2_measure(device, peak)
         extra["next_ops"] = next_ops_measure(device, peak, checks=checks)
     threads = max(1, cpu_cores() // world)
