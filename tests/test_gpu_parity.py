@@ -87,6 +87,22 @@ def test_quantize_edge_values(F, orc):
     assert np.array_equal(q, q_ref) and np.array_equal(s[:, :rows], s_ref[:, :rows])
 
 
+def test_quantize_idempotent_on_gpu(F, orc):
+    """AC2 / Eqs. 5-8 on the device: A1 of the dequantized codes reproduces the values
+    exactly; the codes bit for bit wherever the tile scale is unchanged, else the scale drops by one
+    binade (a tile max in (224, 232) * 2^T rounds onto 448 * 2^(T-1), R28)."""
+    x = synth.activations_bf16(1024, 7168, 17).cuda()
+    q, s = run_quantize(F, x)
+    d = orc.dequantize_rows(q, s)                                    # exact: <= 4 significant bits
+    d_bf16 = torch.from_numpy(d).to(torch.bfloat16)
+    assert np.array_equal(d_bf16.to(torch.float64).numpy(), d)       # representable in BF16
+    q2, s2 = run_quantize(F, d_bf16.cuda())
+    assert np.array_equal(orc.dequantize_rows(q2, s2), d)
+    same = (s2 == s).T
+    assert np.array_equal(q[np.repeat(same, 128, axis=1)], q2[np.repeat(same, 128, axis=1)])
+    assert np.all((s2 == s) | (s2.astype(int) == s.astype(int) - 1))
+
+
 def test_quantize_deterministic(F):
     x = synth.activations_bf16(512, 2048, 7).cuda()
     a = run_quantize(F, x)
