@@ -9,9 +9,12 @@
 // Kernel design (sm_100a, HBM-bound, 2.016 B/element):
 //   * persistent CTAs, warp-specialised: 8 consumer warps (shift + transpose), 2-4 store warps
 //     (read-out + global stores) and one producer warp; below 64 tiles per SM 3 CTAs per SM with
-//     2 TMA stages and 2 store warps, above 2 CTAs per SM with 3 stages and 4 store warps.  Tiles
-//     are walked in segment-major order (tile_coord below); the segment tables are built in shared
-//     memory from the DEVICE segment offsets (no host sync: CUDA-graph capturable).
+//     2 TMA stages and 2 store warps; above, W = 2 column blocks per staged unit (one 256-byte x
+//     128-row box: input rows read 256 contiguous bytes at a time), 1 CTA per SM with 3-4 stages
+//     and 4 store warps -- the consumers transpose the unit's two 128x128 blocks one after the other
+//     (each with its own T_max) into the staging buffers.  Units are walked in segment-major order
+//     (segments.cuh tile_coord); the segment tables are built in shared memory from the DEVICE
+//     segment offsets (no host sync: CUDA-graph capturable).
 //   * producer (one lane): per tile its coordinates, the 16 KB code tile by TMA (one 128x128 box,
 //     or 16-row boxes for a segment's partial last block, so no bytes of the next segment are
 //     read) and the block's run of row scales by a 1D bulk copy, all on one mbarrier of the stage
@@ -33,21 +36,22 @@
 #include "kernels.h"
 #include "segments.cuh"
 
+
 namespace fp8flow {
 
 // <STAGES, OUTBUF>: TMA stages of the input ring and staging buffers for the transposed tile
 constexpr int kTConsumers = 256;              // 8 consumer (shift + transpose) warps
-constexpr int kMaxThreadsA2 = kTConsumers + 32 * 4 + 32;
+constexpr int kMaxThreadsA2 = kTConsumers + 32 * 8 + 32;
 constexpr int kPrefixThreads = 288;             // 4 segments per thread: covers offsets[0..1024]
 template <int WS>
 __host__ __device__ constexpr int a2_threads() { return kTConsumers + 32 * WS + 32; }  // + WS store warps + 1 producer
 constexpr int kMaxSegs = 1024;
 constexpr int kTileBytes = kTile * kTile;
 
-template <int STAGES, int OUTBUF>
+template <int STAGES, int OUTBUF, int W = 1>
 struct TransposeSmem {
-  uint8_t in[STAGES][kTileBytes];
-  uint32_t sc[STAGES][kTile / 4];  // the 128 row-scale bytes of each staged tile
+  uint8_t in[STAGES][W * kTileBytes];  // W column blocks of 128 rows (rows W*128 bytes apart)
+  uint32_t sc[STAGES][W][kTile / 4];   // the 128 row-scale bytes of each of the W blocks
   uint32_t out[OUTBUF][kTile * kTile / 4];
   TileCoord tc[STAGES];            // coordinates of the staged tile (written by the producer)
   TileCoord out_tc[OUTBUF];        // coordinates (pad[0] = T_max) of the tile in each staging buffer
@@ -67,14 +71,14 @@ __host__ __device__ constexpr size_t a2_smem_bytes(int nsegs) {
 // WS > 0 (store-warp mode, OUTBUF == 2): WS extra warps drain the staging buffers (read-out and
 // global stores) while the 8 consumer warps shift and transpose the next tile; buffers are handed
 // over on out_full / out_empty mbarriers instead of consumer-wide barriers.
-template <int STAGES, int OUTBUF, int MINB, int WS>
+template <int STAGES, int OUTBUF, int MINB, int WS, int W>
 __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
     scaling_aware_transpose_kernel(const __grid_constant__ CUtensorMap tmap_q,
                                    const __grid_constant__ CUtensorMap tmap_q16, const uint8_t* __restrict__ s,
                                    int64_t ld_s, int64_t rows, int64_t cols, const int32_t* __restrict__ seg_offsets,
                                    int32_t num_segs, uint8_t* __restrict__ qT, uint8_t* __restrict__ sT) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  using Smem = TransposeSmem<STAGES, OUTBUF>;
+  using Smem = TransposeSmem<STAGES, OUTBUF, W>;
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -104,7 +108,7 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
   if (tid <= 32) sm.mult[tid] = shift_multiplier(static_cast<uint32_t>(tid));
   load_segments<kThreads>(seg_off, blk_prefix, sm.red, &sm.total_rb, seg_offsets, nsegs, rows);  // (+ barrier)
 
-  const int n_jb = static_cast<int>(cols / kTile);
+  const int n_jb = static_cast<int>(cols / (kTile * W));  // staged units: W column blocks each
   const int total_tiles = sm.total_rb * n_jb;  // < 2^31 (rows < 2^31, checked by the ABI)
   const int first = blockIdx.x;
   const int stride = gridDim.x;
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
     // thread per output-row chunk), then hand it back
     const int st_tid = tid - kTConsumers;
     const int c8 = st_tid & 7;
-    for (int i = 0; i < n_local; ++i) {
+    for (int i = 0; i < n_local * W; ++i) {  // one staged output per column block
       const int b = i & 1;
       mbar_wait(&sm.out_full[b], (i >> 1) & 1);
       const TileCoord tc = sm.out_tc[b];
@@ -147,17 +151,20 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
       uint32_t phase = 0;
       for (int i = 0; i < n_local; ++i) {
         if (i >= STAGES) mbar_wait_sleep(&sm.empty_bar[st], phase ^ 1u, 32);
-        const TileCoord c = tile_coord(segt, nsegs, n_jb, first + i * stride);
+        TileCoord c = tile_coord(segt, nsegs, n_jb, first + i * stride);
+        c.jb *= W;  // the first of the unit's W column blocks
         sm.tc[st] = c;
         const int r0 = c.o + c.ib * kTile;
-        mbar_expect_tx(&sm.full_bar[st], static_cast<uint32_t>(c.rows_valid * (kTile + 1)));
+        mbar_expect_tx(&sm.full_bar[st], static_cast<uint32_t>(c.rows_valid * W * (kTile + 1)));
         if (c.rows_valid == kTile) {
           tma_load_2d(sm.in[st], &tmap_q, &sm.full_bar[st], c.jb * kTile, r0);
         } else {
           for (int r = 0; r < c.rows_valid; r += 16)
-            tma_load_2d(sm.in[st] + r * kTile, &tmap_q16, &sm.full_bar[st], c.jb * kTile, r0 + r);
+            tma_load_2d(sm.in[st] + r * W * kTile, &tmap_q16, &sm.full_bar[st], c.jb * kTile, r0 + r);
         }
-        bulk_load_1d(sm.sc[st], s + static_cast<int64_t>(c.jb) * ld_s + r0, c.rows_valid, &sm.full_bar[st]);
+#pragma unroll
+        for (int h = 0; h < W; ++h)
+          bulk_load_1d(sm.sc[st][h], s + static_cast<int64_t>(c.jb + h) * ld_s + r0, c.rows_valid, &sm.full_bar[st]);
         if (++st == STAGES) {
           st = 0;
           phase ^= 1u;
@@ -175,75 +182,81 @@ __global__ void __launch_bounds__(a2_threads<WS>(), MINB)
   for (int i = 0; i < n_local; ++i) {
     mbar_wait(&sm.full_bar[st], phase);
     const TileCoord tc = sm.tc[st];
-    // ---- block scale max (Algorithm 1: S_max = max_i S_i^row), per warp, no CTA barrier:
-    // lane l reads the staged scale bytes of rows 4l..4l+3; rows beyond the segment count as 0
-    const uint32_t sw_l = (4 * lane < tc.rows_valid) ? sm.sc[st][lane] : 0u;
-    const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
-    const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
-    const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);  // this thread's rows 4g..4g+3
+#pragma unroll 1
+    for (int h = 0; h < W; ++h) {
+      const int o = i * W + h;  // staged output index
+      // ---- block scale max (Algorithm 1: S_max = max_i S_i^row), per warp, no CTA barrier:
+      // lane l reads the staged scale bytes of rows 4l..4l+3; rows beyond the segment count as 0
+      const uint32_t sw_l = (4 * lane < tc.rows_valid) ? sm.sc[st][h][lane] : 0u;
+      const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
+      const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
+      const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);  // this thread's rows 4g..4g+3
 
-    // ---- shift rows (rows past rows_valid hold stale bytes: shifted, never stored) -----------
-    uint4 v[4];
+      // ---- shift rows (rows past rows_valid hold stale bytes: shifted, never stored) ---------
+      uint4 v[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
-    mbar_arrive(&sm.empty_bar[st]);  // this thread is done with the stage (scales, coordinates, codes)
-    uint32_t R[4][4];
+      for (int r = 0; r < 4; ++r)
+        v[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * (W * kTile) + h * kTile + 16 * c]);
+      if (h == W - 1) mbar_arrive(&sm.empty_bar[st]);  // done with the stage (scales, coordinates, codes)
+      uint32_t R[4][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
-      const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v[r].x, m2);
-      R[r][1] = shift4(v[r].y, m2);
-      R[r][2] = shift4(v[r].z, m2);
-      R[r][3] = shift4(v[r].w, m2);
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);  // k = T_max - T_row >= 0
+        const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
+        R[r][0] = shift4(v[r].x, m2);
+        R[r][1] = shift4(v[r].y, m2);
+        R[r][2] = shift4(v[r].z, m2);
+        R[r][3] = shift4(v[r].w, m2);
+      }
+      // ---- 4x4 byte transposes into the swizzled staging buffer --------------------------------
+      const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
+      uint32_t* out = sm.out[o & 1];
+      if (o >= 2) mbar_wait(&sm.out_empty[o & 1], ((o >> 1) - 1) & 1);  // drained by the store warps
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
+        const uint32_t t1 = __byte_perm(R[0][w], R[1][w], 0x7362);
+        const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
+        const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
+        const int j0 = 16 * c + 4 * w;
+        out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
+        out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
+        out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
+        out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
+      }
+      // hand the buffer (and the block's coordinates) to the store warps
+      if (tid == 0) {
+        TileCoord ob = tc;
+        ob.jb = tc.jb + h;
+        ob.pad[0] = static_cast<int32_t>(tmax);
+        sm.out_tc[o & 1] = ob;
+      }
+      __syncwarp();  // (tid 0's out_tc write above, before warp 0's arrivals)
+      mbar_arrive(&sm.out_full[o & 1]);
     }
     if (++st == STAGES) {
       st = 0;
       phase ^= 1u;
     }
-    // ---- 4x4 byte transposes into the swizzled staging buffer ----------------------------------
-    const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);  // swizzled word position within an out row
-    uint32_t* out = sm.out[i & 1];
-    if (i >= 2) mbar_wait(&sm.out_empty[i & 1], ((i >> 1) - 1) & 1);  // drained by the store warps
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
-      const uint32_t t1 = __byte_perm(R[0][w], R[1][w], 0x7362);
-      const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
-      const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
-      const int j0 = 16 * c + 4 * w;
-      out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
-      out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
-      out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
-      out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
-    }
-    // hand the buffer (and the tile's coordinates) to the store warps
-    if (tid == 0) {
-      TileCoord o = tc;
-      o.pad[0] = static_cast<int32_t>(tmax);
-      sm.out_tc[i & 1] = o;
-    }
-    __syncwarp();  // (tid 0's out_tc write above, before warp 0's arrivals)
-    mbar_arrive(&sm.out_full[i & 1]);
   }
 }
 
 // ---------------------------------------------------------------------------------------------
 // host side: tensor map + launch
 // ---------------------------------------------------------------------------------------------
-template <int S, int O, int B, int WS>
+template <int S, int O, int B, int WS, int W>
 static cudaError_t launch_a2v(const CUtensorMap& map, const CUtensorMap& map16, const uint8_t* s, int64_t ld_s, int64_t rows, int64_t cols,
                               const int32_t* seg_offsets, int32_t num_segs, uint8_t* qT, uint8_t* sT,
                               cudaStream_t stream, int num_sms, int64_t ub_tiles) {
   static KernelSetup setup;
-  auto kernel = scaling_aware_transpose_kernel<S, O, B, WS>;
+  auto kernel = scaling_aware_transpose_kernel<S, O, B, WS, W>;
   constexpr int kThreads = a2_threads<WS>();
-  const size_t smem = a2_smem_bytes<TransposeSmem<S, O>>(seg_offsets ? num_segs : 1);
-  if (prepare_kernel(setup, kernel, kThreads, a2_smem_bytes<TransposeSmem<S, O>>(kMaxSegs), smem) == 0)
+  const size_t smem = a2_smem_bytes<TransposeSmem<S, O, W>>(seg_offsets ? num_segs : 1);
+  if (prepare_kernel(setup, kernel, kThreads, a2_smem_bytes<TransposeSmem<S, O, W>>(kMaxSegs), smem) == 0)
     return cudaErrorInvalidValue;
   int occ = 0;  // occupancy at this launch's shared memory (the segment tables vary with num_segs)
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
-  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
+  const int64_t grid = one_wave_grid(occ, num_sms, (ub_tiles + W - 1) / W);
   kernel<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(
       map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT);
   return cudaGetLastError();
@@ -252,21 +265,32 @@ static cudaError_t launch_a2v(const CUtensorMap& map, const CUtensorMap& map16, 
 cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, int64_t ld_s, int64_t rows,
                                            int64_t cols, const int32_t* seg_offsets, int32_t num_segs,
                                            uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
-  CUtensorMap map, map16;  // 128x128 boxes; 128x16 boxes for the partial last block of a segment
-  if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
-                 static_cast<uint64_t>(cols), kTile, kTile) ||
-      !encode_2d(&map16, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
-                 static_cast<uint64_t>(cols), kTile, 16))
-    return cudaErrorInvalidValue;
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  // Tiles held at once = SMs x CTAs x stages.  Launches with many tiles per SM stream better with a
-  // small window (fewer DRAM pages open at once) and more store warps; mid-size launches (~12 tiles
-  // per SM) need 3 CTAs per SM to ramp up (profiles/r02_a2_order_window.txt).
+  // Launches with >= 64 blocks per SM (the whole-layer X_perm and A) stage 2 column blocks per unit:
+  // one 256-byte x 128-row TMA box, so every input row is read 256 contiguous bytes at a time (half
+  // the DRAM page openings of 128-byte tile rows): X_perm 133056x7168 358 -> 313 us, A 99 -> 89 us
+  // (profiles/r02_a2_midsize.txt).  1 CTA per SM; 3 units in flight (4 for <= 2048 columns).
+  const bool wide = cols % (2 * kTile) == 0 && ub_tiles >= 64LL * num_sms;
+  const uint32_t bw = wide ? 2 * kTile : kTile;
+  CUtensorMap map, map16;  // (W x 128)-byte x 128-row boxes; 16-row boxes for the partial last block
+  if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
+                 static_cast<uint64_t>(cols), bw, kTile) ||
+      !encode_2d(&map16, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
+                 static_cast<uint64_t>(cols), bw, 16))
+    return cudaErrorInvalidValue;
+  if (wide && cols >= 4096)
+    return launch_a2v<3, 2, 1, 4, 2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                     ub_tiles);
+  if (wide)
+    return launch_a2v<4, 2, 1, 4, 2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                     ub_tiles);
+  // Below that, 128-column units.  Tiles held at once = SMs x CTAs x stages: mid-size launches
+  // (~12 tiles per SM) need 3 CTAs per SM to ramp up (profiles/r02_a2_order_window.txt).
   if (ub_tiles >= 64LL * num_sms)
-    return launch_a2v<3, 2, 2, 4>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
-                                  ub_tiles);
-  return launch_a2v<2, 2, 3, 2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
-                                ub_tiles);
+    return launch_a2v<3, 2, 2, 4, 1>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                     ub_tiles);
+  return launch_a2v<2, 2, 3, 2, 1>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                   ub_tiles);
 }
 
 // =============================================================================================
