@@ -266,11 +266,13 @@ cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, i
                                            int64_t cols, const int32_t* seg_offsets, int32_t num_segs,
                                            uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
   const int64_t ub_tiles = (rows / kTile + (seg_offsets ? num_segs : 1)) * (cols / kTile);
-  // Launches with >= 64 blocks per SM (the whole-layer X_perm and A) stage 2 column blocks per unit:
+  // Launches with >= 32 blocks per SM (the whole-layer X_perm and A, an EP8 shard's X_perm) stage 2
+  // column blocks per unit:
   // one 256-byte x 128-row TMA box, so every input row is read 256 contiguous bytes at a time (half
   // the DRAM page openings of 128-byte tile rows): X_perm 133056x7168 358 -> 313 us, A 99 -> 89 us
-  // (profiles/r02_a2_midsize.txt).  1 CTA per SM; 3 units in flight (4 for <= 2048 columns).
-  const bool wide = cols % (2 * kTile) == 0 && ub_tiles >= 64LL * num_sms;
+  // (profiles/r02_a2_midsize.txt); >= 64 blocks per SM: 1 CTA per SM with 3 units in flight (4 for
+  // <= 2048 columns); 32..64: 2 CTAs per SM with 2 (EP8 X_perm 40.8 -> 39.0 us).
+  const bool wide = cols % (2 * kTile) == 0 && ub_tiles >= 32LL * num_sms;
   const uint32_t bw = wide ? 2 * kTile : kTile;
   CUtensorMap map, map16;  // (W x 128)-byte x 128-row boxes; 16-row boxes for the partial last block
   if (!encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
@@ -278,6 +280,9 @@ cudaError_t launch_scaling_aware_transpose(const uint8_t* q, const uint8_t* s, i
       !encode_2d(&map16, CU_TENSOR_MAP_DATA_TYPE_UINT8, q, static_cast<uint64_t>(cols), static_cast<uint64_t>(rows),
                  static_cast<uint64_t>(cols), bw, 16))
     return cudaErrorInvalidValue;
+  if (wide && ub_tiles < 64LL * num_sms)  // 32..64 blocks per SM (an EP8 shard's X_perm): 2 CTAs/SM
+    return launch_a2v<2, 2, 2, 2, 2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
+                                     ub_tiles);
   if (wide && cols >= 4096)
     return launch_a2v<3, 2, 1, 4, 2>(map, map16, s, ld_s, rows, cols, seg_offsets, num_segs, qT, sT, stream, num_sms,
                                      ub_tiles);
