@@ -10,10 +10,11 @@
 // PAD rows code 0x00 / scale 0x00), (qT, sT) exactly A2 of them with segments = expert_offsets:
 //     T_max = max_i T[i][jb];  sT_e[ib][j] = T_max;  qT_e[j][i-o] = shift(q_out[i][j], T_max - T[i][jb]).
 //
-// Kernel: A2's persistent, warp-specialised structure (transpose.cu) with gathering producers, tiles
-// in A2's segment-major order but column block by column block (all experts' tiles of column block
-// jb before jb + 1: the 128-byte pieces of the tokens gathered meanwhile stay in L2 for the ~8
-// expert rows that read each):
+// Kernel: A2's persistent, warp-specialised structure (transpose.cu) with gathering producers, units
+// of W column blocks (W = 2 for launches with >= 32 blocks per SM: 256-byte pieces of every token
+// and X_perm row, as A2's two-block units) in A2's segment-major order but unit column by unit
+// column (all experts' units of one column before the next: the token pieces gathered meanwhile
+// stay in L2 for the ~8 expert rows that read each):
 //   * 4 producer warps: warp p gathers block rows 32p..32p+31 with 16-byte cp.async (each warp
 //     instruction = 4 rows x 128 bytes; PAD rows by zero-fill) and writes their scale bytes; a
 //     tile's two dependent global reads (src_of_row, then s_tok) are issued 4 and 2 tiles ahead as
@@ -42,6 +43,7 @@ constexpr int kPdProducers = 4;  // producer warps: 32 block rows each
 // tiles walked in column chunks of one block: all experts' tiles of column block jb before jb + 1,
 // so the token bytes gathered meanwhile (num_tokens x 128) stay in L2 for their ~8 expert rows
 constexpr int kPdChunk = 1;
+
 #ifndef PDDEPTH
 #define PDDEPTH 4
 #endif
@@ -51,10 +53,10 @@ template <int WS>
 __host__ __device__ constexpr int pd_threads() { return kPdCons + 32 * WS + 32 * kPdProducers; }  // + store warps + producers
 constexpr int kPdMaxThreads = pd_threads<4>();
 
-template <int STAGES>
+template <int STAGES, int W>
 struct PermDualSmem {
-  uint8_t in[STAGES][kTile * kTile];  // gathered block: row i = token src_of_row[r0 + i] (16 KB)
-  uint32_t sc[STAGES][kTile / 4];     // the block's 128 row-scale bytes
+  uint8_t in[STAGES][W * kTile * kTile];  // gathered unit: row i = token src_of_row[r0 + i], W*128 bytes
+  uint32_t sc[STAGES][W][kTile / 4];      // the 128 row-scale bytes of each of the W blocks
   uint32_t out[2][kTile * kTile / 4]; // transposed staging (A2's swizzle)
   TileCoord tc[STAGES];
   TileCoord out_tc[2];                // pad[0] = T_max
@@ -63,7 +65,7 @@ struct PermDualSmem {
   uint64_t out_full[2];
   uint64_t out_empty[2];
   int32_t psrc[kPdProducers][kPdDepth * 32];  // per producer warp: ring of source tokens
-  uint32_t psc[kPdProducers][kPdDepth * 32];  // ... and of the words holding their scale bytes
+  uint32_t psc[kPdProducers][kPdDepth * W * 32];  // ... and of the words holding their scale bytes
   uint32_t mult[33];
   uint32_t red[kPdMaxThreads / 32];
   int32_t total_rb;
@@ -109,7 +111,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int STAGES, int MINB, int WS>
+template <int STAGES, int MINB, int WS, int W>
 __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
     permute_dual_kernel(const uint8_t* __restrict__ q_tok, const uint8_t* __restrict__ s_tok, int64_t ld_s_tok,
                         int64_t hidden, const int32_t* __restrict__ src_of_row,
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
                         uint8_t* __restrict__ q_out, uint8_t* __restrict__ s_out, uint8_t* __restrict__ qT,
                         uint8_t* __restrict__ sT) {
   extern __shared__ __align__(1024) uint8_t smem_pd[];
-  using Smem = PermDualSmem<STAGES>;
+  using Smem = PermDualSmem<STAGES, W>;
   Smem& sm = *reinterpret_cast<Smem*>(smem_pd);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int32_t* seg_off = reinterpret_cast<int32_t*>(smem_pd + (sizeof(Smem) + 15) / 16 * 16);
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
   load_segments<kThreads>(seg_off, blk_prefix, sm.red, &sm.total_rb, expert_offsets, num_segs, max_rows,
                           static_cast<int32_t>(max_rows));  // (+ barrier)
 
-  const int n_jb = static_cast<int>(hidden / kTile);
+  const int n_jb = static_cast<int>(hidden / (W * kTile));  // units of W column blocks
   const int total_tiles = sm.total_rb * n_jb;
   const int first = blockIdx.x;
   const int stride = gridDim.x;
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
     const int st_tid = tid - kPdCons;
     const int c8 = st_tid & 7;
     const uint64_t pol_out = l2_policy_evict_first();  // streamed outputs
-    for (int i = 0; i < n_local; ++i) {
+    for (int i = 0; i < n_local * W; ++i) {  // one staged output per column block
       const int b = i & 1;
       mbar_wait(&sm.out_full[b], (i >> 1) & 1);
       const TileCoord tc = sm.out_tc[b];
@@ -188,7 +190,10 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
     uint32_t* rsc = sm.psc[pw];      // [kPdDepth][32] the 4-byte words holding their scale bytes
     const uint64_t pol_in = l2_policy_evict_last();
     auto coord = [&](int i) {
-      return i < n_local ? tile_coord_chunked(segt, num_segs, n_jb, sm.total_rb, kPdChunk, first + i * stride) : TileCoord{};
+      TileCoord c = i < n_local ? tile_coord_chunked(segt, num_segs, n_jb, sm.total_rb, kPdChunk, first + i * stride)
+                                : TileCoord{};
+      c.jb *= W;  // the unit's first column block
+      return c;
     };
     // tile coordinates, 32 at a time: lane k computes those of tiles base + k (cur) and
     // base + 32 + k (nxt); using one costs a shuffle per field
@@ -213,12 +218,16 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
       if (row < c.rows_valid) cp_async4(d, src_of_row + static_cast<int64_t>(c.o) + c.ib * kTile + row);
       else *d = -1;
     };
-    auto issue_scale = [&](int i) {  // the word of s_tok[jb] holding this row's scale byte -> rsc slot
+    auto issue_scale = [&](int i) {  // the words of s_tok[jb + h] holding this row's scale bytes -> rsc
       if (i >= n_local) return;
       const int sl = (i % kPdDepth) * 32 + lane;
       const int src = rsrc[sl];
       const int jb = get(i).jb;  // (shuffles: every lane)
-      if (src >= 0) cp_async4(&rsc[sl], s_tok + static_cast<int64_t>(jb) * ld_s_tok + (src & ~3));
+#pragma unroll
+      for (int h = 0; h < W; ++h)
+        if (src >= 0)
+          cp_async4(&rsc[((i % kPdDepth) * W + h) * 32 + lane],
+                    s_tok + static_cast<int64_t>(jb + h) * ld_s_tok + (src & ~3));
     };
 #pragma unroll 1
     for (int d = 0; d < kPdDepth; ++d) issue_src(d);
@@ -242,22 +251,28 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
       const int sl0 = (i % kPdDepth) * 32;
       if (i >= STAGES) mbar_wait_sleep(&sm.empty_bar[st], phase ^ 1u, 32);
       if (lane == 0 && pw == 0) sm.tc[st] = c0;
-      const int col = c0.jb * kTile + 16 * (lane & 7);
+      // a warp instruction copies 32 / (8 W) rows of W * 128 bytes (8 W lanes per row)
+      constexpr int kLpr = 8 * W, kRpi = 32 / kLpr;
+      const int col = c0.jb * kTile + 16 * (lane % kLpr);
       const int my_src = rsrc[sl0 + lane];  // this lane's own cp.async result (complete, visible to it)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = pw * 32 + 4 * k + (lane >> 3);
-        const int src = __shfl_sync(0xffffffffu, my_src, 4 * k + (lane >> 3));
+      for (int k = 0; k < 32 / kRpi; ++k) {
+        const int r = pw * 32 + kRpi * k + lane / kLpr;
+        const int src = __shfl_sync(0xffffffffu, my_src, kRpi * k + lane / kLpr);
         if (r < c0.rows_valid) {
-          cp_async16_zfill(sm.in[st] + r * kTile + 16 * (lane & 7),
+          cp_async16_zfill(sm.in[st] + r * (W * kTile) + 16 * (lane % kLpr),
                            q_tok + static_cast<int64_t>(src >= 0 ? src : 0) * hidden + col, src >= 0 ? 16u : 0u,
                            pol_in);
         }
       }
       cp_async_mbar_arrive(&sm.full_bar[st]);  // arrives once this lane's copies have landed
-      if (row < c0.rows_valid)
-        reinterpret_cast<uint8_t*>(sm.sc[st])[row] =
-            my_src >= 0 ? static_cast<uint8_t>(rsc[sl0 + lane] >> (8 * (my_src & 3))) : uint8_t{0};
+      if (row < c0.rows_valid) {
+#pragma unroll
+        for (int h = 0; h < W; ++h)
+          reinterpret_cast<uint8_t*>(sm.sc[st][h])[row] =
+              my_src >= 0 ? static_cast<uint8_t>(rsc[((i % kPdDepth) * W + h) * 32 + lane] >> (8 * (my_src & 3)))
+                          : uint8_t{0};
+      }
       mbar_arrive(&sm.full_bar[st]);  // releases this lane's scale / coordinate writes
       issue_src(i + kPdDepth);  // into slot i % kPdDepth (read above by this lane only)
       cp_async_commit();
@@ -280,76 +295,84 @@ __global__ void __launch_bounds__(pd_threads<WS>(), MINB)
     mbar_wait(&sm.full_bar[st], phase);
     const TileCoord tc = sm.tc[st];
     const int64_t r0 = static_cast<int64_t>(tc.o) + tc.ib * kTile;
-    // block scale max (Algorithm 1), per warp; rows beyond the segment count as 0
-    const uint32_t sw_l = (4 * lane < tc.rows_valid) ? sm.sc[st][lane] : 0u;
-    const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
-    const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
-    const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);
-    if (warp == 0 && 4 * lane < tc.rows_valid)  // row-wise scales: s_out[jb][r0 + 4l .. + 3]
-      *reinterpret_cast<uint32_t*>(s_out + static_cast<int64_t>(tc.jb) * max_rows + r0 + 4 * lane) = sw_l;
-    uint4 v[4];
+#pragma unroll 1
+    for (int h = 0; h < W; ++h) {
+      const int o = i * W + h;  // staged output index
+      const int jb = tc.jb + h;
+      // block scale max (Algorithm 1), per warp; rows beyond the segment count as 0
+      const uint32_t sw_l = (4 * lane < tc.rows_valid) ? sm.sc[st][h][lane] : 0u;
+      const uint32_t mx = max(max(sw_l & 0xFFu, (sw_l >> 8) & 0xFFu), max((sw_l >> 16) & 0xFFu, sw_l >> 24));
+      const uint32_t tmax = __reduce_max_sync(0xffffffffu, mx);
+      const uint32_t sw = __shfl_sync(0xffffffffu, sw_l, g);
+      if (warp == 0 && 4 * lane < tc.rows_valid)  // row-wise scales: s_out[jb][r0 + 4l .. + 3]
+        *reinterpret_cast<uint32_t*>(s_out + static_cast<int64_t>(jb) * max_rows + r0 + 4 * lane) = sw_l;
+      uint4 v[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * kTile + 16 * c]);
-    mbar_arrive(&sm.empty_bar[st]);
-    // row-wise output: the gathered codes unchanged (a warp store = 4 rows x 128 bytes)
+      for (int r = 0; r < 4; ++r)
+        v[r] = *reinterpret_cast<const uint4*>(&sm.in[st][(4 * g + r) * (W * kTile) + h * kTile + 16 * c]);
+      if (h == W - 1) mbar_arrive(&sm.empty_bar[st]);
+      // row-wise output: the gathered codes unchanged (a warp store = 4 rows x 128 bytes; the W
+      // blocks of a unit give each row W * 128 contiguous bytes)
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      if (4 * g + r < tc.rows_valid)
-        st_v4_hint(q_out + (r0 + 4 * g + r) * hidden + tc.jb * kTile + 16 * c, v[r], pol_out);
-    // A2's exponent shift (rows past rows_valid hold stale bytes: shifted, never stored)
-    uint32_t R[4][4];
+      for (int r = 0; r < 4; ++r)
+        if (4 * g + r < tc.rows_valid)
+          st_v4_hint(q_out + (r0 + 4 * g + r) * hidden + jb * kTile + 16 * c, v[r], pol_out);
+      // A2's exponent shift (rows past rows_valid hold stale bytes: shifted, never stored)
+      uint32_t R[4][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);
-      const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
-      R[r][0] = shift4(v[r].x, m2);
-      R[r][1] = shift4(v[r].y, m2);
-      R[r][2] = shift4(v[r].z, m2);
-      R[r][3] = shift4(v[r].w, m2);
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t k = tmax - ((sw >> (8 * r)) & 0xFFu);
+        const uint32_t m2 = sm.mult[k < 32u ? k : 32u];
+        R[r][0] = shift4(v[r].x, m2);
+        R[r][1] = shift4(v[r].y, m2);
+        R[r][2] = shift4(v[r].z, m2);
+        R[r][3] = shift4(v[r].w, m2);
+      }
+      const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);
+      uint32_t* out = sm.out[o & 1];
+      if (o >= 2) mbar_wait(&sm.out_empty[o & 1], ((o >> 1) - 1) & 1);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
+        const uint32_t t1 = __byte_perm(R[0][w], R[1][w], 0x7362);
+        const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
+        const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
+        const int j0 = 16 * c + 4 * w;
+        out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
+        out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
+        out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
+        out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
+      }
+      if (tid == 0) {
+        TileCoord ob = tc;
+        ob.jb = jb;
+        ob.pad[0] = static_cast<int32_t>(tmax);
+        sm.out_tc[o & 1] = ob;
+      }
+      __syncwarp();
+      mbar_arrive(&sm.out_full[o & 1]);
     }
     if (++st == STAGES) {
       st = 0;
       phase ^= 1u;
     }
-    const int wpos = 4 * ((g >> 2) ^ c) + (g & 3);
-    uint32_t* out = sm.out[i & 1];
-    if (i >= 2) mbar_wait(&sm.out_empty[i & 1], ((i >> 1) - 1) & 1);
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t t0 = __byte_perm(R[0][w], R[1][w], 0x5140);
-      const uint32_t t1 = __byte_perm(R[0][w], R[1][w], 0x7362);
-      const uint32_t t2 = __byte_perm(R[2][w], R[3][w], 0x5140);
-      const uint32_t t3 = __byte_perm(R[2][w], R[3][w], 0x7362);
-      const int j0 = 16 * c + 4 * w;
-      out[(j0 + 0) * 32 + wpos] = __byte_perm(t0, t2, 0x5410);
-      out[(j0 + 1) * 32 + wpos] = __byte_perm(t0, t2, 0x7632);
-      out[(j0 + 2) * 32 + wpos] = __byte_perm(t1, t3, 0x5410);
-      out[(j0 + 3) * 32 + wpos] = __byte_perm(t1, t3, 0x7632);
-    }
-    if (tid == 0) {
-      TileCoord o = tc;
-      o.pad[0] = static_cast<int32_t>(tmax);
-      sm.out_tc[i & 1] = o;
-    }
-    __syncwarp();
-    mbar_arrive(&sm.out_full[i & 1]);
   }
 }
 
-template <int S, int B, int WS>
+template <int S, int B, int WS, int W>
 cudaError_t launch_pd(const uint8_t* q_tok, const uint8_t* s_tok, int64_t ld_s_tok, int64_t hidden,
                       const int32_t* src_of_row, const int32_t* expert_offsets, int32_t num_segs, int64_t max_rows,
                       uint8_t* q_out, uint8_t* s_out, uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms,
                       int64_t ub_tiles) {
   static KernelSetup setup;
-  auto kernel = permute_dual_kernel<S, B, WS>;
+  auto kernel = permute_dual_kernel<S, B, WS, W>;
   constexpr int kThreads = pd_threads<WS>();
-  const size_t smem = pd_smem_bytes<PermDualSmem<S>>(num_segs);
-  if (prepare_kernel(setup, kernel, kThreads, pd_smem_bytes<PermDualSmem<S>>(kPdMaxSegs), smem) == 0)
+  const size_t smem = pd_smem_bytes<PermDualSmem<S, W>>(num_segs);
+  if (prepare_kernel(setup, kernel, kThreads, pd_smem_bytes<PermDualSmem<S, W>>(kPdMaxSegs), smem) == 0)
     return cudaErrorInvalidValue;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
-  const int64_t grid = one_wave_grid(occ, num_sms, ub_tiles);
+  const int64_t grid = one_wave_grid(occ, num_sms, (ub_tiles + W - 1) / W);
   kernel<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(q_tok, s_tok, ld_s_tok, hidden, src_of_row,
                                                                   expert_offsets, num_segs, max_rows, q_out, s_out,
                                                                   qT, sT);
@@ -363,9 +386,20 @@ cudaError_t launch_permute_pad_dual(const uint8_t* q_tok, const uint8_t* s_tok, 
                                     int32_t num_local_experts, int64_t max_rows, uint8_t* q_out, uint8_t* s_out,
                                     uint8_t* qT, uint8_t* sT, cudaStream_t stream, int num_sms) {
   const int64_t ub_tiles = (max_rows / kTile + num_local_experts) * (hidden / kTile);
+  // as A2: launches with >= 32 blocks per SM gather units of 2 column blocks (256 contiguous bytes
+  // of every token row and of every X_perm row per unit); 1 CTA per SM with 3 stages from 64 blocks
+  // per SM (whole layer 599 -> 561-564 us; 2 CTAs/SM there: 620), 2 CTAs per SM with 2 stages below
+  // (EP8 shard 61.4 -> 60.2 us)
+  const bool wide = hidden % (2 * kTile) == 0 && ub_tiles >= 32LL * num_sms;
+  if (wide && ub_tiles >= 64LL * num_sms)
+    return launch_pd<3, 1, 4, 2>(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts,
+                                 max_rows, q_out, s_out, qT, sT, stream, num_sms, ub_tiles);
+  if (wide)
+    return launch_pd<2, 2, 4, 2>(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts,
+                                 max_rows, q_out, s_out, qT, sT, stream, num_sms, ub_tiles);
   // 2 CTAs per SM (448-thread CTAs: 3 per SM would spill), 3 stages, 4 store warps
-  return launch_pd<3, 2, 4>(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts,
-                                   max_rows, q_out, s_out, qT, sT, stream, num_sms, ub_tiles);
+  return launch_pd<3, 2, 4, 1>(q_tok, s_tok, ld_s_tok, hidden, src_of_row, expert_offsets, num_local_experts,
+                               max_rows, q_out, s_out, qT, sT, stream, num_sms, ub_tiles);
 }
 
 }  // namespace fp8flow
