@@ -214,7 +214,8 @@ def _strong_worker(rank, world, port, q):
     rows = int(np.sum((per + 15) // 16 * 16))
     rep = {"parity": {"A1_quantize_x": True, "A2_transpose_xperm": rank == 0 or world == 1},
            "checksums_match": True,
-           "cpu": {"seconds": 2.0 + rank, "bytes": 1e9 * (rank + 1), "cores": 4, "sample": "shard"}}
+           "cpu": {"seconds": 2.0 + rank, "bytes": 1e9 * (rank + 1), "cores": 4, "sample": "shard",
+                   "single_thread": {"value": 0.1 + rank, "unit": "GB/s", "cores": 1}}}
     reports = D.gather_objects(rep)
     merged = D.merge_rank_reports(reports)
     D.barrier()
@@ -250,6 +251,7 @@ def test_two_rank_gloo_strong_partition_and_reports():
                             "rank1": {"A1_quantize_x": True, "A2_transpose_xperm": False}}
     assert m0["parity_all_ranks"] is False and m0["checksums_match"] is True
     assert m0["cpu_baseline"]["value"] == round(3e9 / 3.0 / 1e9, 4) and m0["cpu_baseline"]["cores"] == 8
+    assert m0["cpu_baseline"]["single_thread"]["value"] == 0.1         # rank 0's single-threaded timing
 
 
 def test_partition_modes_single_process():
